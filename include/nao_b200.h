@@ -1,0 +1,155 @@
+/*
+ * nao_b200.h -- C ABI of the B200-native NAO hot path (arXiv 2510.16028).
+ *
+ * libnao_b200.so (sm_100a) replaces the numpy inner loops of the reference
+ * package /root/reference/pkg/src/fpverify behind its own Python API
+ * (bounds.op_bound / co_execute, calibration.percentile_profile,
+ * dispute.observed_p_max / leaf check, commitments.build_tree / canon_tensor).
+ * Each entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Tensor pointers are DEVICE pointers
+ *     owned by the caller; small descriptor arrays (shapes, grids, headers,
+ *     thresholds) are HOST pointers read during the call.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*);
+ *     none synchronizes the host.  Scratch comes from a caller workspace
+ *     sized by the matching *_workspace() query.
+ *   - Return 0 (NAO_OK) or a status; nao_last_error() gives the message
+ *     (thread-local).  The Python layer maps NAO_EINVAL to ValueError as the
+ *     reference raises (bounds.py:57-58, :108-109; calibration.py:28-29;
+ *     commitments.py:116-117).
+ *   - No global mutable state; reentrant across streams.
+ */
+#ifndef NAO_B200_H
+#define NAO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum nao_status { NAO_OK = 0, NAO_EINVAL = 1, NAO_ECUDA = 2, NAO_ENONFINITE = 3 };
+
+enum nao_hash_alg { NAO_HASH_SHA256 = 0, NAO_HASH_KECCAK256 = 1 };
+
+/* how nao_check obtains the per-element bound */
+enum nao_eps_kind {
+    NAO_EPS_TENSOR_F32 = 0,   /* eps array, FP32 rounded up            */
+    NAO_EPS_TENSOR_F64 = 1,   /* eps array, FP64 (reference dtype)     */
+    NAO_EPS_SCALED_LOCAL = 2, /* eps = scale * |local| (u|y|, 2u|y|)   */
+    NAO_EPS_ZERO = 3          /* data movement / relu / max / min      */
+};
+
+enum nao_reduce_kind { NAO_RED_SUM = 0, NAO_RED_MEAN = 1, NAO_RED_MAX = 2, NAO_RED_MIN = 3 };
+enum nao_unary_kind {
+    NAO_UN_EXP = 0, NAO_UN_LOG = 1, NAO_UN_SQRT = 2, NAO_UN_RSQRT = 3,
+    NAO_UN_TANH = 4, NAO_UN_GELU = 5, NAO_UN_SILU = 6
+};
+enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1 };
+
+/* ------------------------------------------------------------ library */
+int nao_version(void);
+/* copies the calling thread's last error message; returns its length */
+int nao_last_error(char* buf, size_t buf_len);
+/* number of SMs / compute capability of the current device (sanity) */
+int nao_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------- commit */
+/* Replaces commitments.build_tree(leaves).root over the chunked leaves of
+ * every traced tensor (commitments.py:39-61 canon bytes, :112-142 tree):
+ *   leaves(t) = [canon_header(t)] + payload split into chunk_bytes pieces.
+ * n_tensors roots (32 B each) are written to roots_out (device).  If
+ * leaf_digests_out != NULL the level-0 digests are written there
+ * (sum_i (1 + ceil(bytes_i/chunk)) * 32 bytes) and the workspace may omit them.
+ * payloads: 16-byte aligned device pointers, byte sizes multiple of 4.
+ * headers: host pointers (<= 136 bytes each). */
+size_t nao_merkle_commit_workspace(int64_t n_tensors, const uint64_t* payload_bytes,
+                                   uint64_t chunk_bytes);
+int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
+                              const uint64_t* payload_bytes, const uint8_t* const* headers,
+                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                              uint8_t* roots_out, uint8_t* leaf_digests_out, void* workspace,
+                              size_t workspace_bytes, void* stream);
+/* leaf_digest(x) = H(0x00 || x) for n byte strings packed in device memory;
+ * offsets: device int64[n+1] (commitments.py:137-138). */
+int nao_merkle_hash_leaves(const uint8_t* data, const int64_t* offsets, int64_t n_leaves,
+                           int hash_alg, uint8_t* digests_out, void* stream);
+/* MerkleTree(leaf_digests).root (commitments.py:112-134).  levels_out (device,
+ * optional) receives every level concatenated, leaves first (MerkleTree.levels). */
+size_t nao_merkle_root_workspace(int64_t n_leaves);
+int nao_merkle_root_of(const uint8_t* leaf_digests, int64_t n_leaves, int hash_alg,
+                       uint8_t* root_out, uint8_t* levels_out, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* -------------------------------------------------------------- check */
+typedef struct nao_check_result {
+    uint64_t n;
+    uint64_t n_violations;   /* #{|claimed-local| > eps}   dispute.py:641-648 */
+    uint64_t n_borderline;   /* eps*lo_factor < diff <= eps (verdict-sensitive band) */
+    uint64_t n_nonfinite;
+    double max_ratio;        /* max diff/eps (inf if diff>0 where eps==0) */
+    int32_t threshold_exceeded; /* observed_p_max(...) > 1.0  dispute.py:130-150 */
+    int32_t first_exceeded;     /* grid index (abs: i, rel: G+i) or -1 */
+    int32_t n_ambiguous;        /* targets settled by the exact second pass */
+    int32_t reserved;
+} nao_check_result;
+
+/* One pass over (local, claimed[, eps]) per operator: bound violations and
+ * the exact p_max > 1 verdict of observed_p_max against (tau_abs, tau_rel) on
+ * the percentile grid (calibration.py:16, dispute.py:114-141).  grid/tau are
+ * host arrays of n_grid (<= 32) doubles; result is a device pointer. */
+size_t nao_check_workspace(void);
+int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind, const void* eps,
+              double eps_scale, double lo_factor, const double* grid, const double* tau_abs,
+              const double* tau_rel, int n_grid, double epsilon, nao_check_result* result,
+              void* workspace, size_t workspace_bytes, void* stream);
+/* Exact numpy method="linear" percentile profiles (calibration.py:33-37):
+ * of |local-claimed| and |local-claimed|/(|local|+epsilon) (calibration.py:40-49),
+ * or of an arbitrary FP64 array.  Outputs are device arrays of n_grid doubles. */
+size_t nao_percentile_workspace(int64_t n);
+int nao_error_profiles(const float* local, const float* claimed, int64_t n, double epsilon,
+                       const double* grid, int n_grid, double* abs_prof, double* rel_prof,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int nao_percentile_profile(const double* values, int64_t n, const double* grid, int n_grid,
+                           double* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------- bounds */
+/* All bounds: eps = template(...) * (1 + slack); eps_f64 selects FP64 output
+ * (reference dtype) or FP32 rounded toward +inf.  Rows are contiguous
+ * [rows, n] with the reduced axis last (the host moves it).  u = unit
+ * roundoff, rc = FpModel.reduction_const(n-1) (bounds.py:42-45). */
+/* softmax_bound_parts, bounds.py:114-135 (values: engine.py:185-194, sequential) */
+int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                      double u, double rc, double slack, void* stream);
+/* layernorm_bound_parts, bounds.py:143-169 (values: engine.py:197-213) */
+int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                        float ln_eps, double u, double rc, double slack, void* stream);
+/* op_bound sum/mean/max/min, bounds.py:194-208 (values: engine.py:240-251) */
+int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                     int kind, double u, double rc, double slack, void* stream);
+/* _unary_intrinsic values, engine.py:133-154 (FP64 evaluation, one rounding) */
+int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* stream);
+/* eps = scale*|y|: single-rounding (u) / intrinsic (2u) templates, bounds.py:196-199 */
+int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, double scale,
+                         void* stream);
+/* matmul_bound, bounds.py:100-111 (+ linear's u|y|, bounds.py:214-217):
+ *   eps[b,m,n] = gamma_const * sum_k |A[b,m,k]||B[b,k,n]| * (1+slack) [+ u|y|]
+ * B is [K,N] (ldb) or, with transpose_b, [N,K].  Batch strides may be 0. */
+int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, int64_t batch,
+                       int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
+                       int64_t stride_a, int64_t stride_b, int64_t stride_c, int transpose_b,
+                       double gamma_const, const float* y_or_null, double u, double slack,
+                       int path, void* stream);
+/* matmul_op values under the sequential profile (engine.py:157-182),
+ * C contiguous [batch, M, N]; fma selects the "+fma" FP64-step emulation. */
+int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, int64_t M,
+                       int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t stride_a,
+                       int64_t stride_b, int64_t stride_c, int transpose_b, int fma,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NAO_B200_H */

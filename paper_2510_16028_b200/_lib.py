@@ -1,0 +1,160 @@
+"""ctypes binding of the in-tree C-ABI library libnao_b200.so (include/nao_b200.h).
+
+There is no CPU fallback: if the library or a CUDA device is missing every
+entry point raises.  Device pointers come from torch tensors; the stream is
+torch's current stream on the tensors' device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "libnao_b200.so"
+_lib = None
+_lock = threading.Lock()
+
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_int = ctypes.c_int
+c_dbl = ctypes.c_double
+c_sz = ctypes.c_size_t
+c_vp = ctypes.c_void_p
+
+NAO_OK, NAO_EINVAL, NAO_ECUDA, NAO_ENONFINITE = 0, 1, 2, 3
+HASH_SHA256, HASH_KECCAK256 = 0, 1
+EPS_TENSOR_F32, EPS_TENSOR_F64, EPS_SCALED_LOCAL, EPS_ZERO = 0, 1, 2, 3
+RED_SUM, RED_MEAN, RED_MAX, RED_MIN = 0, 1, 2, 3
+UNARY = {"exp": 0, "log": 1, "sqrt": 2, "rsqrt": 3, "tanh": 4, "gelu": 5, "silu": 6}
+GEMM_FFMA_RU, GEMM_TC_TF32X3 = 0, 1
+
+
+class CheckResult(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("n_violations", ctypes.c_uint64),
+                ("n_borderline", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
+                ("max_ratio", ctypes.c_double), ("threshold_exceeded", ctypes.c_int32),
+                ("first_exceeded", ctypes.c_int32), ("n_ambiguous", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+CHECK_RESULT_BYTES = ctypes.sizeof(CheckResult)
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "nao_version": (c_int, []),
+    "nao_last_error": (c_int, [ctypes.c_char_p, c_sz]),
+    "nao_device_info": (c_int, [ctypes.POINTER(c_int)] * 3),
+    "nao_merkle_commit_workspace": (c_sz, [c_i64, ctypes.POINTER(c_u64), c_u64]),
+    "nao_merkle_commit_tensors": (c_int, [c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_u64),
+                                          ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_uint32),
+                                          c_u64, c_int, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "nao_merkle_hash_leaves": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),
+    "nao_merkle_root_workspace": (c_sz, [c_i64]),
+    "nao_merkle_root_of": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "nao_check_workspace": (c_sz, []),
+    "nao_check": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_dbl, c_dbl,
+                          ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
+                          c_int, c_dbl, c_vp, c_vp, c_sz, c_vp]),
+    "nao_percentile_workspace": (c_sz, [c_i64]),
+    "nao_error_profiles": (c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_dbl), c_int,
+                                   c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "nao_percentile_profile": (c_int, [c_vp, c_i64, ctypes.POINTER(c_dbl), c_int, c_vp, c_vp,
+                                       c_sz, c_vp]),
+    "nao_softmax_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_dbl, c_dbl, c_dbl,
+                                  c_vp]),
+    "nao_layernorm_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, ctypes.c_float,
+                                    c_dbl, c_dbl, c_dbl, c_vp]),
+    "nao_reduce_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_int, c_dbl, c_dbl,
+                                 c_dbl, c_vp]),
+    "nao_unary_fp64": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
+    "nao_scaled_abs_bound": (c_int, [c_vp, c_vp, c_int, c_i64, c_dbl, c_vp]),
+    "nao_abs_gemm_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64,
+                                   c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_dbl, c_vp, c_dbl,
+                                   c_dbl, c_int, c_vp]),
+    "nao_matmul_profile": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+                                   c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+class NaoError(RuntimeError):
+    pass
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(require_cuda: bool = True):
+    """Load the library (building it first if it is missing and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not _LIB_PATH.exists():
+            from . import _build
+            _build.build()
+        L = ctypes.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    if require_cuda and not torch.cuda.is_available():
+        raise NaoError("paper_2510_16028_b200 needs a CUDA device (no CPU fallback)")
+    return _lib
+
+
+def last_error() -> str:
+    L = load(require_cuda=False)
+    buf = ctypes.create_string_buffer(2048)
+    L.nao_last_error(buf, 2048)
+    return buf.value.decode(errors="replace")
+
+
+def check(rc: int, what: str = ""):
+    if rc == NAO_OK:
+        return
+    msg = last_error()
+    if rc == NAO_EINVAL:
+        raise ValueError(msg or what)
+    raise NaoError(f"{what}: {msg} (status {rc})")
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def dbl_array(values):
+    vals = [float(v) for v in values]
+    return (c_dbl * len(vals))(*vals)
+
+
+# ------------------------------------------------------------------ workspace
+_ws: dict = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Per (device, stream) growable scratch buffer."""
+    dev = torch.device(device)
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
+        _ws[key] = buf
+    return buf

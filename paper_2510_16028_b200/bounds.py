@@ -1,0 +1,410 @@
+"""Per-operator IEEE-754 bounds co-computed with FP32 execution on the B200 --
+drop-in for /root/reference/pkg/src/fpverify/bounds.py.
+
+Same API and semantics (FpModel, gamma, gamma_tilde, BoundTensor,
+matmul_bound, softmax_bound(_parts), layernorm_bound_parts, op_bound,
+co_execute, save_bounds); the arithmetic runs in libnao_b200.so:
+  * matmul / linear  -> nao_abs_gemm_bound   (bounds.py:100-111, :209-217)
+  * softmax          -> nao_softmax_bound    (bounds.py:114-135)
+  * layernorm        -> nao_layernorm_bound  (bounds.py:143-169)
+  * sum/mean/max/min -> nao_reduce_bound     (bounds.py:194-208)
+  * u|y|, 2u|y|      -> nao_scaled_abs_bound (bounds.py:196-199)
+Guarantee vs the reference (tests/test_bounds_gpu.py):
+  eps_ref <= eps_gpu <= eps_ref * (1 + 1e-5).
+numpy arrays in -> numpy arrays out (host sync, like the reference);
+CUDA tensors in -> CUDA tensors out (asynchronous).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import (ExecutionError, fma_of, matmul_value, parse_shape_attr, relu,
+                     require_supported, to_device, unary, _batch_view)
+from .graph import DATA_MOVEMENT_KINDS, parse_ref
+from .tensor import Tensor
+
+FP32_UNIT_ROUNDOFF = 2.0 ** -24
+SINGLE_ROUNDING_KINDS = frozenset({"add", "sub", "mul", "div", "neg"})
+INTRINSIC_KINDS = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})
+ZERO_BOUND_KINDS = DATA_MOVEMENT_KINDS | {"transpose", "relu", "max", "min"}
+
+
+@dataclass(frozen=True)
+class FpModel:
+    """bounds.py:26-49."""
+    u: float = FP32_UNIT_ROUNDOFF
+    lam: float = 4.0
+    mode: str = "probabilistic"
+
+    def __post_init__(self):
+        if self.u <= 0:
+            raise ValueError("unit roundoff must be positive")
+        if self.lam <= 0:
+            raise ValueError("lambda must be positive")
+        if self.mode not in ("deterministic", "probabilistic"):
+            raise ValueError(f"unknown bound mode {self.mode!r}")
+
+    def reduction_const(self, k: int) -> float:
+        if self.mode == "deterministic":
+            return gamma(k, self.u)
+        return gamma_tilde(k, self.lam, self.u)
+
+    def confidence(self) -> float:
+        return 1.0 - 2.0 * math.exp(-self.lam ** 2 * (1.0 - self.u) ** 2 / 2.0)
+
+
+def gamma(k: int, u: float = FP32_UNIT_ROUNDOFF) -> float:
+    """Deterministic k u / (1 - k u)  (bounds.py:52-59)."""
+    if k < 0:
+        raise ValueError("k must be nonnegative")
+    ku = k * u
+    if ku >= 1.0:
+        raise ValueError(f"gamma undefined: k*u = {ku} >= 1")
+    return ku / (1.0 - ku)
+
+
+def gamma_tilde(k: int, lam: float = 4.0, u: float = FP32_UNIT_ROUNDOFF) -> float:
+    """Probabilistic expm1(lam sqrt(k) u + k u^2/(1-u))  (bounds.py:62-66)."""
+    if k < 0:
+        raise ValueError("k must be nonnegative")
+    return math.expm1(lam * math.sqrt(k) * u + k * u * u / (1.0 - u))
+
+
+# Slack factors: eps_gpu = template * (1 + slack).  They cover only FP64
+# summation-order differences vs numpy (pairwise np.sum / BLAS), so they sit
+# ~1e-12 -- far inside rtol 1e-5 -- while keeping eps_gpu >= eps_ref.
+def sum_slack(n: int) -> float:
+    return 4.0 * max(int(n), 1) * 2.0 ** -53 + 2.0 ** -50
+
+
+def gemm_slack(k: int) -> float:
+    return (int(k) + int(k) // 32 + 16) * 2.0 ** -52
+
+
+class BoundTensor:
+    """Same-shape non-negative cap (bounds.py:69-93); eps is FP64, flat,
+    held on the GPU or the host."""
+
+    __slots__ = ("shape", "_eps_np", "_eps_dev")
+
+    def __init__(self, shape, eps):
+        self.shape = tuple(int(d) for d in shape)
+        if isinstance(eps, torch.Tensor):
+            self._eps_dev, self._eps_np = eps.reshape(-1), None
+        else:
+            arr = np.ascontiguousarray(np.asarray(eps, dtype=np.float64)).reshape(-1)
+            if arr.size and float(arr.min()) < 0.0:
+                raise ValueError("bound must be nonnegative")
+            self._eps_dev, self._eps_np = None, arr
+
+    @property
+    def eps(self) -> np.ndarray:
+        if self._eps_np is None:
+            self._eps_np = self._eps_dev.double().cpu().numpy()
+        return self._eps_np
+
+    @property
+    def array(self) -> np.ndarray:
+        return self.eps.reshape(self.shape)
+
+    def device_tensor(self) -> torch.Tensor:
+        if self._eps_dev is None:
+            self._eps_dev = torch.from_numpy(self._eps_np).cuda()
+        return self._eps_dev.reshape(self.shape)
+
+    @classmethod
+    def from_array(cls, arr) -> "BoundTensor":
+        if isinstance(arr, torch.Tensor):
+            return cls(tuple(arr.shape), arr.double())
+        arr = np.asarray(arr, dtype=np.float64)
+        return cls(arr.shape, arr)
+
+    @classmethod
+    def zeros(cls, shape) -> "BoundTensor":
+        n = int(np.prod(tuple(shape), dtype=np.int64)) if tuple(shape) else 1
+        return cls(tuple(shape), np.zeros(n, dtype=np.float64))
+
+
+def _eps_buffer(shape, device, f64: bool) -> torch.Tensor:
+    return torch.empty(shape, dtype=torch.float64 if f64 else torch.float32, device=device)
+
+
+# ---------------------------------------------------------------- kernels
+
+def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
+                   y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
+                   path: int = _lib.GEMM_FFMA_RU) -> torch.Tensor:
+    """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors)."""
+    a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
+    eps = _eps_buffer(out_shape, a.device, eps_f64)
+    yc = None
+    if y is not None:
+        yc = y.contiguous()
+        if tuple(yc.shape) != tuple(out_shape):
+            raise ValueError("linear bound: output shape mismatch")
+    ldb = K if transpose_b else N
+    _lib.call("nao_abs_gemm_bound", a3.data_ptr(), b3.data_ptr(), eps.data_ptr(), int(eps_f64), nb,
+              M, N, K, K, ldb, N, sa, sb, M * N, int(transpose_b), float(const), _lib.ptr(yc),
+              float(u), gemm_slack(K), int(path), _lib.stream_ptr(a.device))
+    return eps
+
+
+def _rows_last(x: torch.Tensor, axis: int):
+    ax = axis % x.dim()
+    xm = x.movedim(ax, -1).contiguous()
+    n = xm.shape[-1]
+    rows = xm.numel() // n if n else 0
+    return xm, ax, rows, n
+
+
+def softmax_device(x: torch.Tensor, axis: int, model: FpModel, eps_f64=True):
+    xm, ax, rows, n = _rows_last(x, axis)
+    if n == 0:
+        raise ValueError("cannot reduce an empty axis")
+    y = torch.empty_like(xm)
+    eps = _eps_buffer(xm.shape, x.device, eps_f64)
+    _lib.call("nao_softmax_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64), rows,
+              n, model.u, model.reduction_const(n - 1), sum_slack(n), _lib.stream_ptr(x.device))
+    return y.movedim(-1, ax), eps.movedim(-1, ax)
+
+
+def layernorm_device(x: torch.Tensor, axis: int, ln_eps: float, model: FpModel, eps_f64=True):
+    xm, ax, rows, n = _rows_last(x, axis)
+    if n == 0:
+        raise ValueError("cannot reduce an empty axis")
+    y = torch.empty_like(xm)
+    eps = _eps_buffer(xm.shape, x.device, eps_f64)
+    _lib.call("nao_layernorm_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64),
+              rows, n, float(np.float32(ln_eps)), model.u, model.reduction_const(n - 1),
+              sum_slack(n), _lib.stream_ptr(x.device))
+    return y.movedim(-1, ax), eps.movedim(-1, ax)
+
+
+_RED = {"sum": _lib.RED_SUM, "mean": _lib.RED_MEAN, "max": _lib.RED_MAX, "min": _lib.RED_MIN}
+
+
+def reduce_device(kind: str, x: torch.Tensor, axis: int, model: FpModel, eps_f64=True):
+    xm, ax, rows, n = _rows_last(x, axis)
+    if n == 0:
+        raise ValueError("cannot reduce an empty axis")
+    y = torch.empty(xm.shape[:-1], dtype=torch.float32, device=x.device)
+    eps = _eps_buffer(xm.shape[:-1], x.device, eps_f64)
+    _lib.call("nao_reduce_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64), rows,
+              n, _RED[kind], model.u, model.reduction_const(n - 1), sum_slack(n),
+              _lib.stream_ptr(x.device))
+    return y, eps
+
+
+def scaled_abs(y: torch.Tensor, scale: float, eps_f64=True) -> torch.Tensor:
+    yc = y.contiguous()
+    eps = _eps_buffer(yc.shape, y.device, eps_f64)
+    _lib.call("nao_scaled_abs_bound", yc.data_ptr(), eps.data_ptr(), int(eps_f64), yc.numel(),
+              float(scale), _lib.stream_ptr(y.device))
+    return eps
+
+
+# ------------------------------------------------------------ public API
+
+def _to_host_pair(y, eps):
+    return y.cpu().numpy(), eps.double().cpu().numpy()
+
+
+def matmul_bound(a, b, model: FpModel, fma: bool = False, transpose_b: bool = False) -> BoundTensor:
+    """bounds.py:100-111."""
+    host = not isinstance(a, torch.Tensor)
+    A, B = to_device(a), to_device(b)
+    k_dim = A.shape[-1]
+    kb = B.shape[-1] if transpose_b else B.shape[-2]
+    if k_dim != kb:
+        raise ValueError(f"matmul inner dims disagree: {tuple(A.shape)} @ {tuple(B.shape)}")
+    count = k_dim if fma else 2 * k_dim - 1
+    eps = abs_gemm_bound(A, B, model.reduction_const(count), transpose_b)
+    return BoundTensor.from_array(eps.cpu().numpy() if host else eps)
+
+
+def softmax_bound_parts(x, axis, model: FpModel, profile=None):
+    """bounds.py:114-135 -> (y float32, eps float64) on the original axis layout."""
+    require_supported(profile)
+    host = not isinstance(x, torch.Tensor)
+    y, eps = softmax_device(to_device(x), int(axis), model)
+    return _to_host_pair(y, eps) if host else (y, eps)
+
+
+def softmax_bound(x, axis, model: FpModel, profile=None) -> BoundTensor:
+    _, eps = softmax_bound_parts(x, axis, model, profile)
+    return BoundTensor.from_array(eps)
+
+
+def layernorm_bound_parts(x, axis, eps_attr, model: FpModel, profile=None):
+    """bounds.py:143-169."""
+    require_supported(profile)
+    host = not isinstance(x, torch.Tensor)
+    y, eps = layernorm_device(to_device(x), int(axis), float(eps_attr), model)
+    return _to_host_pair(y, eps) if host else (y, eps)
+
+
+def apply_value(node, xs, profile) -> torch.Tensor:
+    """FP32 value of one non-fused node on the GPU (engine.py:220-285)."""
+    kind = node.kind
+    if kind in ("add", "sub", "mul", "div"):
+        a, b = xs
+        return {"add": torch.add, "sub": torch.sub, "mul": torch.mul, "div": torch.div}[kind](a, b)
+    if kind == "neg":
+        return torch.neg(xs[0])
+    if kind == "relu":
+        return relu(xs[0])
+    if kind in INTRINSIC_KINDS:
+        return unary(kind, xs[0])
+    if kind == "matmul":
+        return matmul_value(xs[0], xs[1], profile, bool(node.attr("transpose_b", 0)))
+    if kind == "linear":
+        return torch.add(matmul_value(xs[0], xs[1], profile), xs[2])
+    if kind == "concat":
+        return torch.cat(list(xs), dim=int(node.attr("axis", 0)))
+    if kind == "slice":
+        x = xs[0]
+        ax = int(node.attr("axis", 0)) % x.dim()
+        start, stop = int(node.attr("start", 0)), int(node.attr("stop", 0))
+        idx = [slice(None)] * x.dim()
+        idx[ax] = slice(start, stop)
+        return x[tuple(idx)].contiguous()
+    if kind == "reshape":
+        return xs[0].reshape(parse_shape_attr(node.attr("shape")))
+    if kind == "transpose":  # extension: axis permutation
+        return xs[0].permute(parse_shape_attr(node.attr("perm"))).contiguous()
+    if kind == "embedding":
+        ids, table = xs
+        idx = ids.to(torch.int64)
+        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= table.shape[0]):
+            raise ValueError("embedding index out of range")
+        return table[idx]
+    raise ExecutionError(f"unsupported op kind {kind!r}")
+
+
+def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
+    """(y, eps) for one node on device tensors.  eps is a tensor, or a
+    ("scaled", c) / ("zero",) tag when eps_f64 is None (lazy: the check
+    kernel recomputes c|y| on the fly and nothing is materialised)."""
+    kind = node.kind
+    lazy = eps_f64 is None
+    f64 = bool(eps_f64) if not lazy else False
+    u = model.u
+    if kind == "softmax":
+        require_supported(profile)
+        return softmax_device(xs[0], int(node.attr("axis", -1)), model, f64)
+    if kind == "layernorm":
+        require_supported(profile)
+        return layernorm_device(xs[0], int(node.attr("axis", -1)), float(node.attr("eps", 1e-5)),
+                                model, f64)
+    if kind in ("sum", "mean", "max", "min"):
+        require_supported(profile)
+        y, eps = reduce_device(kind, xs[0], int(node.attr("axis", -1)), model, f64)
+        if lazy and kind in ("max", "min"):
+            return y, ("zero",)
+        return y, eps
+    y = apply_value(node, xs, profile)
+    if kind in ZERO_BOUND_KINDS:
+        return y, (("zero",) if lazy else torch.zeros(y.shape, dtype=torch.float64 if f64 else
+                                                      torch.float32, device=y.device))
+    if kind in SINGLE_ROUNDING_KINDS or kind in INTRINSIC_KINDS:
+        c = u if kind in SINGLE_ROUNDING_KINDS else 2.0 * u
+        return y, (("scaled", c) if lazy else scaled_abs(y, c, f64))
+    if kind in ("matmul", "linear"):
+        tb = bool(node.attr("transpose_b", 0)) if kind == "matmul" else False
+        k_dim = xs[0].shape[-1]
+        count = k_dim if fma_of(profile) else 2 * k_dim - 1
+        const = model.reduction_const(count)
+        if kind == "matmul":
+            return y, abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64)
+        return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64)
+    raise ValueError(f"no bound template for kind {kind!r}")
+
+
+def op_bound(node, arrays, model: FpModel, profile=None):
+    """bounds.py:176-218: co-compute (FP32 value, FP64 bound) for one operator."""
+    host = any(not isinstance(a, torch.Tensor) for a in arrays)
+    xs = [to_device(a) for a in arrays]
+    if node.kind == "embedding":
+        xs[0] = to_device(arrays[0])
+    y, eps = op_bound_device(node, xs, model, profile, eps_f64=True)
+    if host:
+        return _to_host_pair(y, eps)
+    return y, eps
+
+
+def _resolve(ref, g, inputs, values):
+    cat, key = parse_ref(ref)
+    if cat == "node":
+        return values[key]
+    if cat == "input":
+        return to_device(inputs[key])
+    return to_device(g.weights[key])
+
+
+def _check_declared_inputs(g, inputs):
+    """engine.py:312-321."""
+    declared = dict(g.inputs)
+    missing = set(declared) - set(inputs)
+    if missing:
+        raise ExecutionError(f"missing graph inputs: {sorted(missing)}")
+    for name, shape in declared.items():
+        if shape is not None and tuple(inputs[name].shape) != tuple(shape):
+            raise ExecutionError(f"input {name!r} has shape {inputs[name].shape}, declared {shape}")
+
+
+def co_execute(g, inputs, profile, model: FpModel, with_trace: bool = False):
+    """bounds.py:221-262 on the GPU: returns (outputs, bounds[, trace]) with
+    device-resident Tensors / BoundTensors (numpy views materialise lazily)."""
+    from .commitments import tensor_digest
+    from .engine_trace import Trace
+
+    _check_declared_inputs(g, inputs)
+    values, bounds = [], []
+    for node in g.nodes:
+        xs = [_resolve(r, g, inputs, values) for r in node.inputs]
+        try:
+            y, eps = op_bound_device(node, xs, model, profile, eps_f64=True)
+        except ExecutionError:
+            raise
+        except NotImplementedError:
+            raise
+        except Exception as exc:
+            raise ExecutionError(f"node {node.index} ({node.name!r}, {node.kind}): {exc}",
+                                 node_index=node.index, node_name=node.name) from exc
+        y = y.contiguous()
+        if y.numel() and not bool(torch.isfinite(y).all()):
+            raise ExecutionError(f"non-finite intermediate at node {node.index} ({node.name!r})",
+                                 node_index=node.index, node_name=node.name)
+        values.append(y)
+        bounds.append(BoundTensor(tuple(y.shape), eps))
+    outputs = [Tensor(values[parse_ref(r)[1]].shape, values[parse_ref(r)[1]]) for r in g.outputs]
+    if not with_trace:
+        return outputs, bounds
+    trace = Trace(tensors=[Tensor(v.shape, v) for v in values],
+                  profile_id=getattr(profile, "id", "seq"),
+                  input_digests={k: tensor_digest(v) for k, v in sorted(inputs.items())},
+                  weight_digests={k: tensor_digest(v) for k, v in sorted(g.weights.items())})
+    return outputs, bounds, trace
+
+
+def save_bounds(dirpath, bounds, model: FpModel, profile_id: str) -> None:
+    """bounds.py:265-282: FP64 NAOT files + manifest."""
+    import json
+    from pathlib import Path
+
+    from .tensor import write_tensor_file
+
+    dirpath = Path(dirpath)
+    dirpath.mkdir(parents=True, exist_ok=True)
+    for i, bt in enumerate(bounds):
+        write_tensor_file(dirpath / f"{i:06d}.naot", bt.array)
+    manifest = {"n_nodes": len(bounds), "profile_id": profile_id,
+                "fp_model": {"u": model.u, "lambda": model.lam, "mode": model.mode}}
+    with open(dirpath / "manifest.json", "w") as fh:
+        json.dump(manifest, fh, sort_keys=True, indent=1)

@@ -1,0 +1,168 @@
+"""Percentile thresholds on the GPU -- drop-in for the hot-path part of
+/root/reference/pkg/src/fpverify/calibration.py (PERCENTILE_GRID :16,
+percentile :23-30, percentile_profile :33-37, elementwise_errors :40-49,
+error_profiles :52-55, OpThresholds/ThresholdSet :117-191,
+build_thresholds :194-203).
+
+Percentiles are numpy's method="linear" computed exactly (full radix sort of
+the FP64 keys, numpy _lerp arithmetic) in nao_percentile_profile /
+nao_error_profiles.  Offline calibration (`calibrate`, stability reports)
+is SURVEY.md 8(f) row 1 ("next").
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import to_device
+
+PERCENTILE_GRID = (0.0, 1.0) + tuple(float(p) for p in range(5, 100, 5)) + (99.0, 100.0)
+THRESHOLD_FILE_VERSION = 1
+DEFAULT_EPSILON = 1e-12
+DEFAULT_ALPHA = 3.0
+
+
+def _flat_f64(values) -> torch.Tensor:
+    if isinstance(values, torch.Tensor):
+        t = values.reshape(-1)
+        return (t if t.is_cuda else t.cuda()).double().contiguous()
+    arr = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
+    return torch.from_numpy(arr).cuda()
+
+
+def percentile_profile_device(values: torch.Tensor, grid=PERCENTILE_GRID) -> torch.Tensor:
+    v = _flat_f64(values)
+    n = v.numel()
+    if n == 0:
+        raise ValueError("percentile profile of empty input")
+    out = torch.empty(len(grid), dtype=torch.float64, device=v.device)
+    ws = _lib.workspace(_lib.load().nao_percentile_workspace(n), v.device)
+    _lib.call("nao_percentile_profile", v.data_ptr(), n, _lib.dbl_array(grid), len(grid),
+              out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(v.device))
+    return out
+
+
+def percentile_profile(values, grid=PERCENTILE_GRID) -> np.ndarray:
+    """calibration.py:33-37 (exact numpy "linear")."""
+    return percentile_profile_device(values, grid).cpu().numpy()
+
+
+def percentile(values, p: float) -> float:
+    """calibration.py:23-30."""
+    return float(percentile_profile(values, (float(p),))[0])
+
+
+def error_profiles_device(local: torch.Tensor, claimed: torch.Tensor, grid=PERCENTILE_GRID,
+                          epsilon: float = DEFAULT_EPSILON):
+    """Exact percentile profiles of |a-b| and |a-b|/(|a|+eps) (calibration.py:40-55)."""
+    a = to_device(local).reshape(-1).contiguous()
+    b = to_device(claimed).reshape(-1).contiguous()
+    if a.numel() != b.numel():
+        raise ValueError(f"shape mismatch: {a.numel()} vs {b.numel()}")
+    n = a.numel()
+    if n == 0:
+        raise ValueError("percentile profile of empty input")
+    pa = torch.empty(len(grid), dtype=torch.float64, device=a.device)
+    pr = torch.empty(len(grid), dtype=torch.float64, device=a.device)
+    ws = _lib.workspace(_lib.load().nao_percentile_workspace(n), a.device)
+    _lib.call("nao_error_profiles", a.data_ptr(), b.data_ptr(), n, float(epsilon),
+              _lib.dbl_array(grid), len(grid), pa.data_ptr(), pr.data_ptr(), ws.data_ptr(),
+              ws.numel(), _lib.stream_ptr(a.device))
+    return pa, pr
+
+
+def elementwise_errors(y_a, y_b, epsilon: float = DEFAULT_EPSILON):
+    """calibration.py:40-49 (host arrays, exact FP64 like the reference)."""
+    if tuple(y_a.shape) != tuple(y_b.shape):
+        raise ValueError(f"shape mismatch: {y_a.shape} vs {y_b.shape}")
+    a = to_device(y_a.data if hasattr(y_a, "data") and not isinstance(y_a, torch.Tensor) else y_a)
+    b = to_device(y_b.data if hasattr(y_b, "data") and not isinstance(y_b, torch.Tensor) else y_b)
+    a64, b64 = a.reshape(-1).double(), b.reshape(-1).double()
+    abs_err = (a64 - b64).abs()
+    rel_err = abs_err / (a64.abs() + epsilon)
+    return abs_err.cpu().numpy(), rel_err.cpu().numpy()
+
+
+def error_profiles(y_a, y_b, grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON):
+    if tuple(y_a.shape) != tuple(y_b.shape):
+        raise ValueError(f"shape mismatch: {y_a.shape} vs {y_b.shape}")
+    pa, pr = error_profiles_device(_payload(y_a), _payload(y_b), grid, epsilon)
+    return pa.cpu().numpy(), pr.cpu().numpy()
+
+
+def _payload(t):
+    if isinstance(t, torch.Tensor) or isinstance(t, np.ndarray):
+        return t
+    if hasattr(t, "_dev") and t._dev is not None:
+        return t._dev
+    return np.asarray(t.data)
+
+
+@dataclass(frozen=True)
+class OpThresholds:
+    name: str
+    tau_abs: np.ndarray
+    tau_rel: np.ndarray
+
+
+@dataclass
+class ThresholdSet:
+    """calibration.py:124-191."""
+    alpha: float
+    epsilon: float
+    grid: tuple
+    ops: list
+
+    def __post_init__(self):
+        self._by_name = {op.name: op for op in self.ops}
+
+    def lookup(self, name: str) -> OpThresholds:
+        if name not in self._by_name:
+            raise KeyError(f"no thresholds for operator {name!r}")
+        return self._by_name[name]
+
+    def scaled(self, alpha: float) -> "ThresholdSet":
+        if alpha <= 0:
+            raise ValueError("alpha must be positive")
+        f = alpha / self.alpha
+        return ThresholdSet(alpha=alpha, epsilon=self.epsilon, grid=self.grid,
+                            ops=[OpThresholds(o.name, o.tau_abs * f, o.tau_rel * f)
+                                 for o in self.ops])
+
+    def to_json(self) -> dict:
+        return {"version": THRESHOLD_FILE_VERSION, "alpha": self.alpha, "epsilon": self.epsilon,
+                "grid": list(self.grid),
+                "ops": [{"name": o.name, "tau_abs": [float(v) for v in o.tau_abs],
+                         "tau_rel": [float(v) for v in o.tau_rel]} for o in self.ops]}
+
+    @classmethod
+    def from_json(cls, doc: dict) -> "ThresholdSet":
+        if doc.get("version") != THRESHOLD_FILE_VERSION:
+            raise ValueError(f"unsupported threshold file version {doc.get('version')}")
+        ops = [OpThresholds(e["name"], np.asarray(e["tau_abs"], dtype=np.float64),
+                            np.asarray(e["tau_rel"], dtype=np.float64)) for e in doc["ops"]]
+        return cls(alpha=doc["alpha"], epsilon=doc["epsilon"], grid=tuple(doc["grid"]), ops=ops)
+
+    def save(self, path) -> None:
+        with open(path, "w") as fh:
+            json.dump(self.to_json(), fh, sort_keys=True, indent=1)
+
+    @classmethod
+    def load(cls, path) -> "ThresholdSet":
+        with open(path) as fh:
+            return cls.from_json(json.load(fh))
+
+
+def build_thresholds(names, abs_env, rel_env, grid=PERCENTILE_GRID, alpha: float = DEFAULT_ALPHA,
+                     epsilon: float = DEFAULT_EPSILON) -> ThresholdSet:
+    """calibration.py:194-203 from per-node envelopes."""
+    if alpha <= 0:
+        raise ValueError("alpha must be positive")
+    ops = [OpThresholds(n, alpha * np.asarray(a, np.float64), alpha * np.asarray(r, np.float64))
+           for n, a, r in zip(names, abs_env, rel_env)]
+    return ThresholdSet(alpha=alpha, epsilon=epsilon, grid=tuple(grid), ops=ops)

@@ -1,0 +1,286 @@
+"""Merkle commitment of traced tensors on the GPU -- drop-in for
+/root/reference/pkg/src/fpverify/commitments.py (canon_tensor :39-61,
+leaf_digest :137-138, MerkleTree :112-134, build_tree :141-142,
+prove/verify :145-169).
+
+Hashing runs in libnao_b200.so (SHA-256 -- the reference's hash -- or
+Keccak-256, north_star (4)).  The chunked tensor commitment used by the hot
+path is
+
+    tensor_root(t) = build_tree([canon_header(t)] + chunks(payload(t), C)).root
+    trace_root     = build_tree([tensor_root(t_i) for i in node order]).root
+
+which in SHA-256 mode equals the reference build_tree over the same leaves
+bit for bit (tests/test_commit_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+SHA256 = "sha256"
+KECCAK256 = "keccak256"
+DEFAULT_CHUNK_BYTES = 4096
+PROOF_WIRE_VERSION = 1
+_LEAF_TAG = b"\x00"
+_NODE_TAG = b"\x01"
+
+
+def alg_id(alg) -> int:
+    if alg in (SHA256, _lib.HASH_SHA256):
+        return _lib.HASH_SHA256
+    if alg in (KECCAK256, _lib.HASH_KECCAK256):
+        return _lib.HASH_KECCAK256
+    raise ValueError(f"unknown hash algorithm {alg!r}")
+
+
+def sha256(data: bytes) -> bytes:
+    """Untagged whole-message SHA-256 (commitments.py:31-32); host hashlib,
+    used only for the reference's sequential whole-tensor digests."""
+    return hashlib.sha256(data).digest()
+
+
+def canonical_json_bytes(obj) -> bytes:
+    return json.dumps(obj, sort_keys=True, separators=(",", ":")).encode("utf-8")
+
+
+def canon_header(shape, dtype=np.float32) -> bytes:
+    """u8 dtype code || u32 rank || dims u64 || contiguous strides u64 (commitments.py:39-61)."""
+    dt = np.dtype(dtype) if not isinstance(dtype, torch.dtype) else (
+        np.dtype(np.float32) if dtype == torch.float32 else np.dtype(np.float64))
+    if dt == np.float32:
+        code = 0
+    elif dt == np.float64:
+        code = 1
+    else:
+        raise ValueError(f"unsupported dtype {dt}")
+    shape = tuple(int(d) for d in shape)
+    strides, acc = [], 1
+    for d in reversed(shape):
+        strides.append(acc)
+        acc *= d
+    strides.reverse()
+    return (struct.pack("<BI", code, len(shape)) + b"".join(struct.pack("<Q", d) for d in shape)
+            + b"".join(struct.pack("<Q", s) for s in strides))
+
+
+def canon_tensor(t) -> bytes:
+    arr = t.array if hasattr(t, "array") and not isinstance(t, np.ndarray) else np.asarray(t)
+    if arr.dtype not in (np.float32, np.float64):
+        raise ValueError(f"unsupported dtype {arr.dtype}")
+    dt = np.dtype("<f4") if arr.dtype == np.float32 else np.dtype("<f8")
+    return canon_header(arr.shape, arr.dtype) + np.ascontiguousarray(arr, dtype=dt).tobytes()
+
+
+def tensor_digest(t) -> str:
+    return sha256(canon_tensor(t)).hex()
+
+
+def _device(device=None):
+    return torch.device(device if device is not None else "cuda", torch.cuda.current_device()
+                        if device is None else torch.device(device).index)
+
+
+def hash_leaves(leaves, alg=SHA256, device=None) -> torch.Tensor:
+    """leaf_digest(x) for every byte string -> (n, 32) uint8 CUDA tensor."""
+    if len(leaves) == 0:
+        raise ValueError("merkle tree requires at least one leaf")
+    dev = _device(device)
+    offs = np.zeros(len(leaves) + 1, dtype=np.int64)
+    np.cumsum([len(x) for x in leaves], out=offs[1:])
+    blob = b"".join(leaves)
+    data = torch.frombuffer(bytearray(blob or b"\x00"), dtype=torch.uint8).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    out = torch.empty((len(leaves), 32), dtype=torch.uint8, device=dev)
+    _lib.call("nao_merkle_hash_leaves", data.data_ptr(), d_offs.data_ptr(), len(leaves),
+              alg_id(alg), out.data_ptr(), _lib.stream_ptr(dev))
+    return out
+
+
+def leaf_digest(data: bytes, alg=SHA256) -> bytes:
+    return bytes(hash_leaves([data], alg).cpu().numpy()[0])
+
+
+def node_digest(left: bytes, right: bytes, alg=SHA256) -> bytes:
+    """H(0x01 || L || R): the one-node tree over two 32-byte digests."""
+    leaves = torch.tensor(np.frombuffer(left + right, dtype=np.uint8).reshape(2, 32),
+                          device=_device())
+    return bytes(root_of_digests(leaves, alg).cpu().numpy())
+
+
+def root_of_digests(digests: torch.Tensor, alg=SHA256, with_levels: bool = False):
+    """MerkleTree over (n, 32) uint8 CUDA digests -> root (32,) [and levels]."""
+    n = int(digests.shape[0])
+    if n == 0:
+        raise ValueError("merkle tree requires at least one leaf")
+    dev = digests.device
+    digests = digests.contiguous()
+    root = torch.empty(32, dtype=torch.uint8, device=dev)
+    levels = None
+    sizes = [n]
+    while sizes[-1] > 1:
+        sizes.append((sizes[-1] + 1) // 2)
+    if with_levels:
+        levels = torch.empty((sum(sizes), 32), dtype=torch.uint8, device=dev)
+    wsb = _lib.load().nao_merkle_root_workspace(n)
+    ws = _lib.workspace(wsb, dev)
+    _lib.call("nao_merkle_root_of", digests.data_ptr(), n, alg_id(alg), root.data_ptr(),
+              _lib.ptr(levels), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev))
+    if with_levels:
+        out, off = [], 0
+        for s in sizes:
+            out.append(levels[off:off + s])
+            off += s
+        return root, out
+    return root
+
+
+class MerkleTree:
+    """Levels with odd-node self-pairing (commitments.py:112-134), hashed on the GPU."""
+
+    def __init__(self, leaf_digests, alg=SHA256):
+        if len(leaf_digests) == 0:
+            raise ValueError("merkle tree requires at least one leaf")
+        self.alg = alg
+        if isinstance(leaf_digests, torch.Tensor):
+            d = leaf_digests
+        else:
+            d = torch.tensor(np.frombuffer(b"".join(leaf_digests), dtype=np.uint8).reshape(-1, 32),
+                             device=_device())
+        _, lv = root_of_digests(d, alg, with_levels=True)
+        host = [x.cpu().numpy() for x in lv]
+        self.levels = [[bytes(row) for row in lvl] for lvl in host]
+
+    @property
+    def root(self) -> bytes:
+        return self.levels[-1][0]
+
+    @property
+    def n_leaves(self) -> int:
+        return len(self.levels[0])
+
+
+def build_tree(leaves, alg=SHA256) -> MerkleTree:
+    """commitments.py:141-142."""
+    return MerkleTree(hash_leaves(list(leaves), alg), alg)
+
+
+@dataclass(frozen=True)
+class MerkleProof:
+    """commitments.py:81-109 (wire: u8 version, u32 index, u8 depth, [dir, sibling]*)."""
+    leaf_index: int
+    siblings: tuple
+    directions: tuple
+
+    def to_wire(self) -> bytes:
+        out = [struct.pack("<BIB", PROOF_WIRE_VERSION, self.leaf_index, len(self.siblings))]
+        for d, s in zip(self.directions, self.siblings):
+            out.append(struct.pack("<B", d))
+            out.append(s)
+        return b"".join(out)
+
+    @classmethod
+    def from_wire(cls, data: bytes) -> "MerkleProof":
+        version, index, depth = struct.unpack_from("<BIB", data, 0)
+        if version != PROOF_WIRE_VERSION:
+            raise ValueError(f"unsupported proof version {version}")
+        off, sibs, dirs = 6, [], []
+        for _ in range(depth):
+            if data[off] not in (0, 1):
+                raise ValueError(f"invalid direction byte {data[off]}")
+            dirs.append(data[off])
+            sibs.append(data[off + 1:off + 33])
+            off += 33
+        if off != len(data):
+            raise ValueError("trailing bytes in proof wire")
+        return cls(leaf_index=index, siblings=tuple(sibs), directions=tuple(dirs))
+
+
+def prove(tree: MerkleTree, index: int) -> MerkleProof:
+    """commitments.py:145-157."""
+    if not (0 <= index < tree.n_leaves):
+        raise IndexError(f"leaf index {index} out of range")
+    sibs, dirs, idx = [], [], index
+    for level in tree.levels[:-1]:
+        sib = idx ^ 1
+        if sib >= len(level):
+            sib = idx
+        sibs.append(level[sib])
+        dirs.append(1 if sib >= idx else 0)
+        idx //= 2
+    return MerkleProof(leaf_index=index, siblings=tuple(sibs), directions=tuple(dirs))
+
+
+def verify(root: bytes, leaf: bytes, proof: MerkleProof, alg=SHA256) -> bool:
+    """commitments.py:160-169."""
+    node = leaf_digest(leaf, alg)
+    for d, sib in zip(proof.directions, proof.siblings):
+        if sib == node and d != 1:
+            return False
+        node = node_digest(node, sib, alg) if d else node_digest(sib, node, alg)
+    return node == root
+
+
+# ------------------------------------------------------- tensor commitments
+
+def _as_payload(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"unsupported dtype {t.dtype}")
+    t = t.contiguous()
+    if t.numel() and t.data_ptr() % 16 != 0:
+        t = t.clone()
+    return t
+
+
+def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
+                   out: torch.Tensor | None = None, leaf_digests: torch.Tensor | None = None):
+    """Chunked tensor roots for CUDA tensors, one batched launch set, no host
+    sync.  Returns an (n, 32) uint8 CUDA tensor (row i = root of tensors[i])."""
+    tensors = [_as_payload(t) for t in tensors]
+    n = len(tensors)
+    if n == 0:
+        raise ValueError("no tensors to commit")
+    dev = tensors[0].device
+    sizes = (ctypes.c_uint64 * n)(*[t.numel() * t.element_size() for t in tensors])
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() if t.numel() else 0 for t in tensors])
+    headers = [canon_header(t.shape, t.dtype) for t in tensors]
+    hbufs = [ctypes.create_string_buffer(h, len(h)) for h in headers]
+    hptrs = (ctypes.c_void_p * n)(*[ctypes.addressof(b) for b in hbufs])
+    hlens = (ctypes.c_uint32 * n)(*[len(h) for h in headers])
+    roots = out if out is not None else torch.empty((n, 32), dtype=torch.uint8, device=dev)
+    L = _lib.load()
+    wsb = L.nao_merkle_commit_workspace(n, sizes, chunk_bytes)
+    ws = _lib.workspace(wsb, dev)
+    _lib.call("nao_merkle_commit_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes, alg_id(alg),
+              roots.data_ptr(), _lib.ptr(leaf_digests), ws.data_ptr(), ws.numel(),
+              _lib.stream_ptr(dev))
+    # keep payload tensors alive until the kernels that read them have run
+    if torch.cuda.is_current_stream_capturing() is False:
+        for t in tensors:
+            t.record_stream(torch.cuda.current_stream(dev))
+    return roots
+
+
+def tensor_root(t, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256) -> bytes:
+    if not isinstance(t, torch.Tensor):
+        arr = np.asarray(t.array if hasattr(t, "array") else t)
+        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+    return bytes(commit_tensors([t], chunk_bytes, alg)[0].cpu().numpy())
+
+
+def trace_root(tensor_roots, alg=SHA256) -> bytes:
+    """Root over per-node tensor roots in canonical node order (leaf = H(0x00||root))."""
+    if isinstance(tensor_roots, torch.Tensor):
+        leaves = [bytes(r) for r in tensor_roots.cpu().numpy()]
+    else:
+        leaves = list(tensor_roots)
+    return build_tree(leaves, alg).root

@@ -1,0 +1,379 @@
+// Memory-bound operator values + IEEE-754 bounds (north_star (2)).
+//
+// FP32 parts follow the reference's default "sequential" DeviceProfile
+// bit for bit (engine.py:80-84 left fold per row, engine.py:133-154 FP64
+// intrinsic rounded once), and every FP64 bound expression is evaluated in
+// the same operation order as bounds.py with explicit __d*_rn intrinsics (no
+// FMA contraction).  Only the row sums of the FP64 templates differ in
+// association from numpy's pairwise np.sum; the caller's `slack` (>= 4 n 2^-53)
+// covers that, so eps_gpu >= eps_ref and eps_gpu <= eps_ref (1 + slack).
+//
+// Row kernels use one warp per 32 rows: 32x32 tiles are loaded coalesced
+// (lane = column), transposed through shared memory, and each lane then
+// folds its own row left to right -- 32 independent sequential folds per warp.
+#include <cmath>
+#include "common.cuh"
+
+namespace nao {
+
+constexpr int kRowWarps = 4;  // warps per CTA in row kernels
+
+struct RowTile {
+    float t[32][33];
+};
+
+// eps output: FP64 (API dtype) or FP32 rounded up (streaming pipeline)
+__device__ __forceinline__ void store_eps(void* eps, int f64, int64_t i, double v, double slack) {
+    double e = __dmul_rn(v, __dadd_rn(1.0, slack));
+    if (f64) static_cast<double*>(eps)[i] = e;
+    else static_cast<float*>(eps)[i] = __double2float_ru(e);
+}
+
+// ----------------------------------------------------------------- softmax
+
+// bounds.py:114-135 over engine.py:185-194 (axis already moved last by the host).
+__global__ void __launch_bounds__(32 * kRowWarps) k_softmax(
+    const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+    int64_t rows, int64_t n, double u, double rc, double slack) {
+    __shared__ RowTile tiles[kRowWarps][2];
+    __shared__ float s_m[kRowWarps][32], s_S[kRowWarps][32];
+    __shared__ double s_epsS[kRowWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + w) * 32;
+    if (r0 >= rows) return;
+    const int64_t my_row = r0 + lane;
+    const bool row_ok = my_row < rows;
+    float (*tx)[33] = tiles[w][0].t;
+    float (*te)[33] = tiles[w][1].t;
+
+    // phase 1: row max (order independent, exact)
+    float m = -INFINITY;
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+        const int64_t c = c0 + lane;
+        for (int rr = 0; rr < 32; rr++) {
+            const int64_t r = r0 + rr;
+            tx[rr][lane] = (r < rows && c < n) ? __ldg(x + r * n + c) : -INFINITY;
+        }
+        __syncwarp();
+        const int cm = (int)(n - c0 < 32 ? n - c0 : 32);
+        for (int cc = 0; cc < cm; cc++) m = fmaxf(m, tx[lane][cc]);
+        __syncwarp();
+    }
+    s_m[w][lane] = m;
+    __syncwarp();
+
+    // phase 2: z = x - m, e = fp32(exp64(z)), S = left fold (profile), FP64 sums
+    float S = 0.0f;
+    double se = 0.0, seps = 0.0;
+    const double two_u = __dmul_rn(2.0, u);
+    const double m64a = fabs((double)m);
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+        const int64_t c = c0 + lane;
+        for (int rr = 0; rr < 32; rr++) {
+            const int64_t r = r0 + rr;
+            float xv = 0.f, ev = 0.f;
+            if (r < rows && c < n) {
+                xv = __ldg(x + r * n + c);
+                float z = __fsub_rn(xv, s_m[w][rr]);
+                ev = (float)exp((double)z);
+                y[r * n + c] = ev;  // stash e in the output buffer
+            }
+            tx[rr][lane] = xv;
+            te[rr][lane] = ev;
+        }
+        __syncwarp();
+        const int cm = (int)(n - c0 < 32 ? n - c0 : 32);
+        for (int cc = 0; cc < cm; cc++) {
+            const float ev = te[lane][cc];
+            S = (c0 == 0 && cc == 0) ? ev : __fadd_rn(S, ev);
+            const double e64 = (double)ev;
+            const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)tx[lane][cc]), m64a));
+            const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+            se = __dadd_rn(se, e64);
+            seps = __dadd_rn(seps, eps_e);
+        }
+        __syncwarp();
+    }
+    s_S[w][lane] = S;
+    s_epsS[w][lane] = __dadd_rn(__dmul_rn(rc, se), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+    __syncwarp();
+    (void)row_ok;
+
+    // phase 3 (coalesced, elementwise): y = e / S ; eps_y
+    for (int rr = 0; rr < 32; rr++) {
+        const int64_t r = r0 + rr;
+        if (r >= rows) break;
+        const float Sr = s_S[w][rr];
+        const double S64 = (double)Sr, epsS = s_epsS[w][rr];
+        const double m64 = fabs((double)s_m[w][rr]);
+        const double S2 = __dmul_rn(S64, S64);
+        for (int64_t c = lane; c < n; c += 32) {
+            const int64_t i = r * n + c;
+            const float ev = y[i];
+            const float xv = __ldg(x + i);
+            const float yv = __fdiv_rn(ev, Sr);
+            y[i] = yv;
+            const double e64 = (double)ev;
+            const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64));
+            const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+            const double t1 = __ddiv_rn(eps_e, S64);
+            const double t2 = __ddiv_rn(__dmul_rn(e64, epsS), S2);
+            const double v = __dadd_rn(__dadd_rn(t1, t2), __dmul_rn(u, fabs((double)yv)));
+            store_eps(eps, eps_f64, i, v, slack);
+        }
+    }
+}
+
+// --------------------------------------------------------------- layernorm
+
+// bounds.py:143-169 over engine.py:197-213.
+__global__ void __launch_bounds__(32 * kRowWarps) k_layernorm(
+    const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+    int64_t rows, int64_t n, float ln_eps, double u, double rc, double slack) {
+    __shared__ RowTile tiles[kRowWarps];
+    __shared__ float s_mu[kRowWarps][32], s_sigma[kRowWarps][32];
+    __shared__ double s_epsmu[kRowWarps][32], s_epssig[kRowWarps][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + w) * 32;
+    if (r0 >= rows) return;
+    float (*tx)[33] = tiles[w].t;
+    const float nf = (float)n;
+    const double nd = (double)n;
+
+    // phase 1: mu = fold(x) / float32(n); sum |x| in FP64
+    float acc = 0.f;
+    double sabs = 0.0;
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+        const int64_t c = c0 + lane;
+        for (int rr = 0; rr < 32; rr++) {
+            const int64_t r = r0 + rr;
+            tx[rr][lane] = (r < rows && c < n) ? __ldg(x + r * n + c) : 0.f;
+        }
+        __syncwarp();
+        const int cm = (int)(n - c0 < 32 ? n - c0 : 32);
+        for (int cc = 0; cc < cm; cc++) {
+            const float v = tx[lane][cc];
+            acc = (c0 == 0 && cc == 0) ? v : __fadd_rn(acc, v);
+            sabs = __dadd_rn(sabs, fabs((double)v));
+        }
+        __syncwarp();
+    }
+    const float mu = __fdiv_rn(acc, nf);
+    const double eps_mu =
+        __dadd_rn(__ddiv_rn(__dmul_rn(rc, sabs), nd), __dmul_rn(u, fabs((double)mu)));
+    s_mu[w][lane] = mu;
+    s_epsmu[w][lane] = eps_mu;
+    __syncwarp();
+
+    // phase 2: xc = x - mu, sq = xc*xc, var = fold(sq)/n; FP64 sums of sq and eps_sq
+    float acc2 = 0.f;
+    double ssq = 0.0, seps = 0.0;
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+        const int64_t c = c0 + lane;
+        for (int rr = 0; rr < 32; rr++) {
+            const int64_t r = r0 + rr;
+            float v = 0.f;
+            if (r < rows && c < n) {
+                float xc = __fsub_rn(__ldg(x + r * n + c), s_mu[w][rr]);
+                v = xc;
+            }
+            tx[rr][lane] = v;
+        }
+        __syncwarp();
+        const int cm = (int)(n - c0 < 32 ? n - c0 : 32);
+        for (int cc = 0; cc < cm; cc++) {
+            const float xc = tx[lane][cc];
+            const float sq = __fmul_rn(xc, xc);
+            acc2 = (c0 == 0 && cc == 0) ? sq : __fadd_rn(acc2, sq);
+            const double xc64 = fabs((double)xc), sq64 = (double)sq;
+            const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
+            const double eps_sq =
+                __dadd_rn(__dmul_rn(__dmul_rn(2.0, xc64), eps_xc), __dmul_rn(u, sq64));
+            ssq = __dadd_rn(ssq, sq64);
+            seps = __dadd_rn(seps, eps_sq);
+        }
+        __syncwarp();
+    }
+    const float var = __fdiv_rn(acc2, nf);
+    const float sp = __fadd_rn(var, ln_eps);
+    const float sigma = __fsqrt_rn(sp);
+    const double eps_ssq = __dadd_rn(__dmul_rn(rc, ssq), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+    const double eps_var = __dadd_rn(__ddiv_rn(eps_ssq, nd), __dmul_rn(u, fabs((double)var)));
+    const double eps_sp = __dadd_rn(eps_var, __dmul_rn(u, fabs((double)sp)));
+    const double sig64 = fabs((double)sigma);
+    const double eps_sig = __dadd_rn(__ddiv_rn(eps_sp, __dmul_rn(2.0, sig64)), __dmul_rn(u, sig64));
+    s_sigma[w][lane] = sigma;
+    s_epssig[w][lane] = eps_sig;
+    __syncwarp();
+
+    // phase 3: y = xc / sigma ; eps_y
+    for (int rr = 0; rr < 32; rr++) {
+        const int64_t r = r0 + rr;
+        if (r >= rows) break;
+        const float mu_r = s_mu[w][rr], sg = s_sigma[w][rr];
+        const double sg64 = fabs((double)sg), sg2 = __dmul_rn(sg64, sg64);
+        const double emu = s_epsmu[w][rr], esg = s_epssig[w][rr];
+        for (int64_t c = lane; c < n; c += 32) {
+            const int64_t i = r * n + c;
+            const float xc = __fsub_rn(__ldg(x + i), mu_r);
+            const float yv = __fdiv_rn(xc, sg);
+            y[i] = yv;
+            const double xc64 = fabs((double)xc);
+            const double eps_xc = __dadd_rn(emu, __dmul_rn(u, xc64));
+            const double t1 = __ddiv_rn(eps_xc, sg64);
+            const double t2 = __ddiv_rn(__dmul_rn(xc64, esg), sg2);
+            const double v = __dadd_rn(__dadd_rn(t1, t2), __dmul_rn(u, fabs((double)yv)));
+            store_eps(eps, eps_f64, i, v, slack);
+        }
+    }
+}
+
+// ------------------------------------------------------ sum / mean / max / min
+
+// engine.py:240-251 values, bounds.py:194-208 templates.  kind: 0 sum 1 mean 2 max 3 min
+__global__ void __launch_bounds__(32 * kRowWarps) k_reduce_rows(
+    const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+    int64_t rows, int64_t n, int kind, double u, double rc, double slack) {
+    __shared__ RowTile tiles[kRowWarps];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + w) * 32;
+    if (r0 >= rows) return;
+    float (*tx)[33] = tiles[w].t;
+    float acc = 0.f;
+    double sabs = 0.0;
+    for (int64_t c0 = 0; c0 < n; c0 += 32) {
+        const int64_t c = c0 + lane;
+        for (int rr = 0; rr < 32; rr++) {
+            const int64_t r = r0 + rr;
+            tx[rr][lane] = (r < rows && c < n) ? __ldg(x + r * n + c) : 0.f;
+        }
+        __syncwarp();
+        const int cm = (int)(n - c0 < 32 ? n - c0 : 32);
+        for (int cc = 0; cc < cm; cc++) {
+            const float v = tx[lane][cc];
+            if (c0 == 0 && cc == 0) acc = v;
+            else if (kind == 2) acc = fmaxf(acc, v);
+            else if (kind == 3) acc = fminf(acc, v);
+            else acc = __fadd_rn(acc, v);
+            sabs = __dadd_rn(sabs, fabs((double)v));
+        }
+        __syncwarp();
+    }
+    const int64_t r = r0 + lane;
+    if (r < rows) {
+        float out = acc;
+        if (kind == 1) out = __fdiv_rn(acc, (float)n);
+        y[r] = out;
+        double e = 0.0;
+        if (kind <= 1) {
+            e = __dmul_rn(rc, sabs);
+            if (kind == 1) e = __dadd_rn(__ddiv_rn(e, (double)n), __dmul_rn(u, fabs((double)out)));
+        }
+        if (eps) store_eps(eps, eps_f64, r, e, kind <= 1 ? slack : 0.0);
+    }
+}
+
+// ------------------------------------------------------ elementwise pieces
+
+// engine.py:133-154: FP64 evaluation rounded once to FP32.
+// kind: 0 exp 1 log 2 sqrt 3 rsqrt 4 tanh 5 gelu 6 silu
+__global__ void k_unary(const float* __restrict__ x, float* __restrict__ y, int64_t n, int kind) {
+    const double kS = 0.7978845608028654;  // sqrt(2/pi)  (engine.py:23)
+    const double kC = 0.044715;            // engine.py:24
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = (double)__ldg(x + i);
+        double o;
+        switch (kind) {
+            case 0: o = exp(v); break;
+            case 1: o = log(v); break;
+            case 2: o = sqrt(v); break;
+            case 3: o = __ddiv_rn(1.0, sqrt(v)); break;
+            case 4: o = tanh(v); break;
+            case 5: {  // 0.5 * x * (1 + tanh(S * (x + C * x**3)))
+                const double x3 = __dmul_rn(__dmul_rn(v, v), v);
+                const double inner = __dmul_rn(kS, __dadd_rn(v, __dmul_rn(kC, x3)));
+                o = __dmul_rn(__dmul_rn(0.5, v), __dadd_rn(1.0, tanh(inner)));
+                break;
+            }
+            default: o = __ddiv_rn(v, __dadd_rn(1.0, exp(-v))); break;
+        }
+        y[i] = (float)o;
+    }
+}
+
+// eps = scale * |y|  (single-rounding u|y| / intrinsic 2u|y| templates, bounds.py:196-199)
+__global__ void k_scaled_abs(const float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+                             int64_t n, double scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double e = __dmul_rn(scale, fabs((double)__ldg(y + i)));
+        if (eps_f64) static_cast<double*>(eps)[i] = e;
+        else static_cast<float*>(eps)[i] = __double2float_ru(e);
+    }
+}
+
+static int ew_grid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    return (int)(b < kNumSMs * 16 ? (b < 1 ? 1 : b) : kNumSMs * 16);
+}
+
+static int row_grid(int64_t rows) { return (int)ceil_div(rows, 32 * kRowWarps); }
+
+}  // namespace nao
+
+using namespace nao;
+
+extern "C" {
+
+int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                      double u, double rc, double slack, void* stream) {
+    NAO_REQUIRE(rows >= 0 && n > 0, "softmax: cannot reduce an empty axis");
+    NAO_REQUIRE(x && y && eps, "softmax: null pointer");
+    if (rows == 0) return NAO_OK;
+    k_softmax<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, y, eps, eps_f64, rows, n, u, rc, slack);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                        float ln_eps, double u, double rc, double slack, void* stream) {
+    NAO_REQUIRE(rows >= 0 && n > 0, "layernorm: cannot reduce an empty axis");
+    NAO_REQUIRE(x && y && eps, "layernorm: null pointer");
+    if (rows == 0) return NAO_OK;
+    k_layernorm<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, y, eps, eps_f64, rows, n, ln_eps, u, rc, slack);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                     int kind, double u, double rc, double slack, void* stream) {
+    NAO_REQUIRE(rows >= 0 && n > 0, "cannot reduce an empty axis");
+    NAO_REQUIRE(kind >= NAO_RED_SUM && kind <= NAO_RED_MIN, "bad reduce kind %d", kind);
+    if (rows == 0) return NAO_OK;
+    k_reduce_rows<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, y, eps, eps_f64, rows, n, kind, u, rc, slack);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* stream) {
+    NAO_REQUIRE(kind >= NAO_UN_EXP && kind <= NAO_UN_SILU, "bad unary kind %d", kind);
+    if (n == 0) return NAO_OK;
+    k_unary<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n, kind);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, double scale,
+                         void* stream) {
+    if (n == 0) return NAO_OK;
+    k_scaled_abs<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(y, eps, eps_f64, n,
+                                                                            scale);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// Chunked Merkle commitment of traced tensors (north_star (4)).
+//
+// Per tensor:  leaves = [canon header] + [payload chunk_i]  (chunk = C bytes)
+//              root   = MerkleTree(H(0x00||leaf)).root     (commitments.py:112-142)
+// Kernels:
+//   k_chunk_leaves : one thread per payload chunk, batched over up to kMaxSegs
+//                    tensors per launch (a whole layer's node outputs), so the
+//                    grid fills 148 SMs even for 33 MB tensors.
+//   k_bytes_leaves : generic odd-length leaves (headers, JSON chunks).
+//   k_tree_reduce  : each CTA folds an aligned group of 2^lg nodes of one level
+//                    through lg levels in shared memory (odd node pairs with
+//                    itself; aligned groups reproduce the global tree exactly).
+#include <cstdio>
+#include <cstdarg>
+#include <vector>
+#include <algorithm>
+
+#include "common.cuh"
+#include "hash.cuh"
+
+namespace nao {
+
+constexpr int kMaxSegs = 128;
+constexpr int kTreeThreads = 256;  // a CTA folds up to 512 nodes
+
+struct ChunkTable {
+    int n;
+    uint32_t chunk_words;
+    const uint32_t* payload[kMaxSegs];
+    uint64_t nbytes[kMaxSegs];
+    uint64_t chunk_prefix[kMaxSegs + 1];  // cumulative chunk counts
+    uint64_t out_index[kMaxSegs];         // digest index of chunk 0
+};
+
+constexpr int kMaxHeader = 136;  // canon header of rank <= 8: 5 + 16*rank bytes
+
+struct HeaderTable {  // passed by value: no host->device staging, no sync
+    int n;
+    uint32_t len[kMaxSegs];
+    uint64_t out_index[kMaxSegs];
+    uint8_t bytes[kMaxSegs][kMaxHeader];
+};
+
+struct TreeTable {
+    int n;
+    int lg;                                // levels folded per CTA
+    int full_levels[kMaxSegs];             // 1: fold exactly lg levels (>1 group)
+    uint64_t in_index[kMaxSegs];
+    uint64_t n_in[kMaxSegs];
+    uint64_t out_index[kMaxSegs];
+    uint64_t group_prefix[kMaxSegs + 1];
+};
+
+__device__ __forceinline__ int find_seg(const uint64_t* prefix, int n, uint64_t t) {
+    int lo = 0, hi = n;  // prefix[lo] <= t < prefix[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (prefix[mid] <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void store_digest(uint32_t* dst, const uint32_t d[8]) {
+    uint4* p = reinterpret_cast<uint4*>(dst);
+    p[0] = make_uint4(d[0], d[1], d[2], d[3]);
+    p[1] = make_uint4(d[4], d[5], d[6], d[7]);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(128) k_chunk_leaves(const __grid_constant__ ChunkTable tab,
+                                                      uint32_t* __restrict__ digests) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tab.chunk_prefix[tab.n]) return;
+    const int s = find_seg(tab.chunk_prefix, tab.n, t);
+    const uint64_t c = t - tab.chunk_prefix[s];
+    const uint64_t off_w = c * tab.chunk_words;
+    const uint64_t total_w = tab.nbytes[s] >> 2;
+    const uint32_t nw = (uint32_t)(total_w - off_w < tab.chunk_words ? total_w - off_w : tab.chunk_words);
+    GlobalWords ld{tab.payload[s] + off_w};
+    uint32_t d[8];
+    hash_tagged_words<ALG>(ld, nw, 0u, d);
+    store_digest(digests + 8 * (tab.out_index[s] + c), d);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(64) k_header_leaves(const __grid_constant__ HeaderTable tab,
+                                                      uint32_t* __restrict__ digests) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= tab.n) return;
+    ByteMsg m{tab.bytes[s], tab.len[s], 0};
+    uint32_t d[8];
+    hash_bytes_generic<ALG>(m, d);
+    store_digest(digests + 8 * tab.out_index[s], d);
+}
+
+// Generic leaves laid out contiguously in device memory (offsets in device memory).
+template <int ALG>
+__global__ void __launch_bounds__(64) k_packed_leaves(const uint8_t* __restrict__ data,
+                                                      const int64_t* __restrict__ offsets,
+                                                      int64_t n, uint32_t* __restrict__ digests) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    ByteMsg m{data + offsets[s], (uint64_t)(offsets[s + 1] - offsets[s]), 0};
+    uint32_t d[8];
+    hash_bytes_generic<ALG>(m, d);
+    store_digest(digests + 8 * s, d);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kTreeThreads) k_tree_reduce(const __grid_constant__ TreeTable tab,
+                                                              const uint32_t* __restrict__ in,
+                                                              uint32_t* __restrict__ out) {
+    __shared__ uint4 sm[2 * kTreeThreads][2];  // up to 512 digests
+    const int s = find_seg(tab.group_prefix, tab.n, blockIdx.x);
+    const uint64_t g = blockIdx.x - tab.group_prefix[s];
+    const uint64_t group = 1ull << tab.lg;
+    const uint64_t first = g * group;
+    uint64_t m = (tab.n_in[s] - first < group ? tab.n_in[s] - first : group);  // live nodes in this group
+    const uint32_t* src = in + 8 * (tab.in_index[s] + first);
+    // level 0 -> smem
+    for (uint64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint4* p = reinterpret_cast<const uint4*>(src + 8 * i);
+        sm[i][0] = p[0];
+        sm[i][1] = p[1];
+    }
+    __syncthreads();
+    const int levels = tab.full_levels[s] ? tab.lg : 64;
+    for (int l = 0; l < levels; l++) {
+        if (!tab.full_levels[s] && m <= 1) break;
+        const uint64_t mo = (m + 1) >> 1;
+        uint32_t res[8];
+        const uint64_t j = threadIdx.x;
+        if (j < mo) {
+            uint32_t L[8], R[8];
+            uint4 a0 = sm[2 * j][0], a1 = sm[2 * j][1];
+            uint64_t r = (2 * j + 1 < m) ? 2 * j + 1 : 2 * j;  // odd node pairs with itself
+            uint4 b0 = sm[r][0], b1 = sm[r][1];
+            L[0] = a0.x; L[1] = a0.y; L[2] = a0.z; L[3] = a0.w;
+            L[4] = a1.x; L[5] = a1.y; L[6] = a1.z; L[7] = a1.w;
+            R[0] = b0.x; R[1] = b0.y; R[2] = b0.z; R[3] = b0.w;
+            R[4] = b1.x; R[5] = b1.y; R[6] = b1.z; R[7] = b1.w;
+            hash_node<ALG>(L, R, res);
+        }
+        __syncthreads();
+        if (j < mo) {
+            sm[j][0] = make_uint4(res[0], res[1], res[2], res[3]);
+            sm[j][1] = make_uint4(res[4], res[5], res[6], res[7]);
+        }
+        __syncthreads();
+        m = mo;
+    }
+    if (threadIdx.x == 0) {
+        uint4* p = reinterpret_cast<uint4*>(out + 8 * (tab.out_index[s] + g));
+        p[0] = sm[0][0];
+        p[1] = sm[0][1];
+    }
+}
+
+// ----------------------------------------------------------------- host side
+
+static int launch_chunk_leaves(int alg, ChunkTable& tab, uint32_t* digests, cudaStream_t st) {
+    uint64_t total = tab.chunk_prefix[tab.n];
+    if (total == 0) return NAO_OK;
+    const int threads = 128;
+    uint64_t blocks = (total + threads - 1) / threads;
+    if (alg == kSHA256) k_chunk_leaves<kSHA256><<<(unsigned)blocks, threads, 0, st>>>(tab, digests);
+    else k_chunk_leaves<kKECCAK256><<<(unsigned)blocks, threads, 0, st>>>(tab, digests);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+static int launch_header_leaves(int alg, HeaderTable& tab, uint32_t* digests, cudaStream_t st) {
+    if (tab.n == 0) return NAO_OK;
+    int blocks = (tab.n + 63) / 64;
+    if (alg == kSHA256) k_header_leaves<kSHA256><<<blocks, 64, 0, st>>>(tab, digests);
+    else k_header_leaves<kKECCAK256><<<blocks, 64, 0, st>>>(tab, digests);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+// Reduce `nseg` level-0 digest ranges to one root each.  Level arrays
+// ping-pong between two scratch buffers; roots land in roots_out[k].
+// If levels_out != nullptr (single segment only) every level is stored
+// consecutively there and lg is forced to 1.
+static int reduce_trees(int alg, int nseg, const uint64_t* in_index, const uint64_t* n_leaves,
+                        const uint32_t* level0, uint32_t* scratch_a, uint32_t* scratch_b,
+                        uint32_t* roots_out, uint32_t* levels_out, cudaStream_t st) {
+    std::vector<uint64_t> cur_n(n_leaves, n_leaves + nseg);
+    std::vector<uint64_t> cur_idx(in_index, in_index + nseg);
+    const uint32_t* cur = level0;
+    uint32_t* bufs[2] = {scratch_a, scratch_b};
+    int which = 0;
+    const int lg = levels_out ? 1 : 9;
+    uint64_t level_store_off = 0;
+    if (levels_out) {
+        NAO_CHECK_CUDA(cudaMemcpyAsync(levels_out, level0 + 8 * in_index[0], 32 * n_leaves[0],
+                                       cudaMemcpyDeviceToDevice, st));
+        level_store_off = n_leaves[0];
+    }
+    // segments with a single leaf: root == leaf digest
+    for (int k = 0; k < nseg; k++)
+        if (cur_n[k] == 1)
+            NAO_CHECK_CUDA(cudaMemcpyAsync(roots_out + 8 * k, level0 + 8 * in_index[k], 32,
+                                           cudaMemcpyDeviceToDevice, st));
+    for (int iter = 0; iter < 64; iter++) {
+        std::vector<int> live;
+        for (int k = 0; k < nseg; k++)
+            if (cur_n[k] > 1) live.push_back(k);
+        if (live.empty()) break;
+        uint32_t* dst = levels_out ? levels_out : bufs[which];
+        uint64_t dst_base = levels_out ? level_store_off : 0;
+        std::vector<uint64_t> next_n(nseg), next_idx(nseg);
+        for (size_t b0 = 0; b0 < live.size(); b0 += kMaxSegs) {
+            TreeTable tab;
+            memset(&tab, 0, sizeof tab);
+            tab.lg = lg;
+            int cnt = 0;
+            tab.group_prefix[0] = 0;
+            for (size_t q = b0; q < live.size() && cnt < kMaxSegs; q++, cnt++) {
+                int k = live[q];
+                uint64_t groups = (cur_n[k] + (1ull << lg) - 1) >> lg;
+                tab.full_levels[cnt] = groups > 1 ? 1 : 0;
+                tab.in_index[cnt] = cur_idx[k];
+                tab.n_in[cnt] = cur_n[k];
+                tab.out_index[cnt] = dst_base;
+                next_n[k] = groups;
+                next_idx[k] = dst_base;
+                dst_base += groups;
+                tab.group_prefix[cnt + 1] = tab.group_prefix[cnt] + groups;
+            }
+            tab.n = cnt;
+            uint64_t blocks = tab.group_prefix[cnt];
+            if (alg == kSHA256)
+                k_tree_reduce<kSHA256><<<(unsigned)blocks, kTreeThreads, 0, st>>>(tab, cur, dst);
+            else
+                k_tree_reduce<kKECCAK256><<<(unsigned)blocks, kTreeThreads, 0, st>>>(tab, cur, dst);
+            NAO_CHECK_LAUNCH();
+        }
+        for (int k : live) {
+            cur_n[k] = next_n[k];
+            cur_idx[k] = next_idx[k];
+            if (cur_n[k] == 1)
+                NAO_CHECK_CUDA(cudaMemcpyAsync(roots_out + 8 * k, dst + 8 * cur_idx[k], 32,
+                                               cudaMemcpyDeviceToDevice, st));
+        }
+        if (levels_out) level_store_off = dst_base;
+        cur = dst;
+        which ^= 1;
+    }
+    return NAO_OK;
+}
+
+static uint64_t seg_chunks(uint64_t nbytes, uint64_t chunk) { return (nbytes + chunk - 1) / chunk; }
+
+}  // namespace nao
+
+using namespace nao;
+
+extern "C" {
+
+size_t nao_merkle_commit_workspace(int64_t n_tensors, const uint64_t* payload_bytes,
+                                   uint64_t chunk_bytes) {
+    if (n_tensors <= 0 || chunk_bytes == 0) return 0;
+    uint64_t leaves = 0;
+    for (int64_t i = 0; i < n_tensors; i++) leaves += 1 + seg_chunks(payload_bytes[i], chunk_bytes);
+    // level-0 digests + two ping-pong level buffers (each <= leaves/512 + n)
+    uint64_t lvl = leaves / 256 + 2 * (uint64_t)n_tensors + 16;
+    return (size_t)(32 * (leaves + 2 * lvl) + 3 * 256);
+}
+
+int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
+                              const uint64_t* payload_bytes, const uint8_t* const* headers,
+                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                              uint8_t* roots_out, uint8_t* leaf_digests_out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    NAO_REQUIRE(n_tensors > 0, "n_tensors must be positive");
+    NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg %d",
+                hash_alg);
+    NAO_REQUIRE(chunk_bytes >= 64 && chunk_bytes % 64 == 0 && chunk_bytes <= (1ull << 30),
+                "chunk_bytes must be a positive multiple of 64 (got %llu)",
+                (unsigned long long)chunk_bytes);
+    NAO_REQUIRE(roots_out != nullptr, "roots_out is null");
+    std::vector<uint64_t> in_index(n_tensors), n_leaves(n_tensors);
+    uint64_t leaves = 0;
+    for (int64_t i = 0; i < n_tensors; i++) {
+        NAO_REQUIRE(payload_bytes[i] % 4 == 0, "payload %lld: byte size not a multiple of 4",
+                    (long long)i);
+        NAO_REQUIRE(payload_bytes[i] == 0 ||
+                        (reinterpret_cast<uintptr_t>(payloads[i]) % 16 == 0),
+                    "payload %lld: not 16-byte aligned", (long long)i);
+        NAO_REQUIRE(headers[i] != nullptr && header_lens[i] > 0 && header_lens[i] <= kMaxHeader,
+                    "header %lld missing or longer than %d bytes", (long long)i, kMaxHeader);
+        in_index[i] = leaves;
+        n_leaves[i] = 1 + seg_chunks(payload_bytes[i], chunk_bytes);
+        leaves += n_leaves[i];
+    }
+    Workspace ws(workspace, workspace_bytes);
+    uint32_t* lvl0 = leaf_digests_out ? reinterpret_cast<uint32_t*>(leaf_digests_out)
+                                      : ws.take<uint32_t>(8 * leaves);
+    uint64_t lvl = leaves / 256 + 2 * (uint64_t)n_tensors + 16;
+    uint32_t* sa = ws.take<uint32_t>(8 * lvl);
+    uint32_t* sb = ws.take<uint32_t>(8 * lvl);
+    NAO_REQUIRE(lvl0 && sa && sb, "workspace too small (%zu bytes)", workspace_bytes);
+    // header leaves: host bytes travel as kernel parameters (<= 136 B each)
+    for (int64_t b0 = 0; b0 < n_tensors; b0 += kMaxSegs) {
+        static thread_local HeaderTable ht;
+        ht.n = 0;
+        for (int64_t i = b0; i < n_tensors && ht.n < kMaxSegs; i++) {
+            memcpy(ht.bytes[ht.n], headers[i], header_lens[i]);
+            ht.len[ht.n] = header_lens[i];
+            ht.out_index[ht.n] = in_index[i];
+            ht.n++;
+        }
+        int rc = launch_header_leaves(hash_alg, ht, lvl0, st);
+        if (rc) return rc;
+    }
+    for (int64_t b0 = 0; b0 < n_tensors; b0 += kMaxSegs) {
+        ChunkTable ct;
+        memset(&ct, 0, sizeof ct);
+        ct.chunk_words = (uint32_t)(chunk_bytes / 4);
+        int cnt = 0;
+        ct.chunk_prefix[0] = 0;
+        for (int64_t i = b0; i < n_tensors && cnt < kMaxSegs; i++, cnt++) {
+            ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
+            ct.nbytes[cnt] = payload_bytes[i];
+            ct.out_index[cnt] = in_index[i] + 1;
+            ct.chunk_prefix[cnt + 1] = ct.chunk_prefix[cnt] + seg_chunks(payload_bytes[i], chunk_bytes);
+        }
+        ct.n = cnt;
+        int rc = launch_chunk_leaves(hash_alg, ct, lvl0, st);
+        if (rc) return rc;
+    }
+    return reduce_trees(hash_alg, (int)n_tensors, in_index.data(), n_leaves.data(), lvl0, sa, sb,
+                        reinterpret_cast<uint32_t*>(roots_out), nullptr, st);
+}
+
+int nao_merkle_hash_leaves(const uint8_t* data, const int64_t* offsets, int64_t n_leaves,
+                           int hash_alg, uint8_t* digests_out, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    NAO_REQUIRE(n_leaves > 0, "n_leaves must be positive");
+    NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg");
+    int64_t blocks = (n_leaves + 63) / 64;
+    if (hash_alg == kSHA256)
+        k_packed_leaves<kSHA256><<<(unsigned)blocks, 64, 0, st>>>(
+            data, offsets, n_leaves, reinterpret_cast<uint32_t*>(digests_out));
+    else
+        k_packed_leaves<kKECCAK256><<<(unsigned)blocks, 64, 0, st>>>(
+            data, offsets, n_leaves, reinterpret_cast<uint32_t*>(digests_out));
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+size_t nao_merkle_root_workspace(int64_t n_leaves) {
+    if (n_leaves <= 0) return 0;
+    return (size_t)(2 * 32 * ((uint64_t)n_leaves / 256 + 16) + 512);
+}
+
+int nao_merkle_root_of(const uint8_t* leaf_digests, int64_t n_leaves, int hash_alg,
+                       uint8_t* root_out, uint8_t* levels_out, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    NAO_REQUIRE(n_leaves > 0, "merkle tree requires at least one leaf");
+    NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg");
+    Workspace ws(workspace, workspace_bytes);
+    uint64_t lvl = (uint64_t)n_leaves / 256 + 16;
+    uint32_t* sa = ws.take<uint32_t>(8 * lvl);
+    uint32_t* sb = ws.take<uint32_t>(8 * lvl);
+    if (levels_out == nullptr) NAO_REQUIRE(sa && sb, "workspace too small");
+    uint64_t idx = 0, n = (uint64_t)n_leaves;
+    return reduce_trees(hash_alg, 1, &idx, &n, reinterpret_cast<const uint32_t*>(leaf_digests), sa,
+                        sb, reinterpret_cast<uint32_t*>(root_out),
+                        reinterpret_cast<uint32_t*>(levels_out), st);
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+"""Threshold check and leaf bound check on the GPU -- drop-in for the hot-path
+part of /root/reference/pkg/src/fpverify/dispute.py (p_max :114-127,
+observed_p_max :130-141, screen :144-150, select_offending :153-158, the leaf
+route of Challenger.leaf_payload :639-657).  The ledger / protocol state
+machine is the reference's control plane and out of scope.
+
+Two GPU entry points:
+  * observed_p_max: exact percentiles (sort) -> exact p_max value, as the
+    reference returns it.
+  * check_node (nao_check): ONE pass deciding the same verdict p_max > 1 plus
+    bound violations / max violation ratio -- the streaming hot-path check.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID, error_profiles_device
+from .engine import to_device
+
+
+def p_max(abs_profile, rel_profile, tau_abs, tau_rel) -> float:
+    """dispute.py:114-127 (0/0 -> 0, x/0 -> inf)."""
+    if len(abs_profile) != len(tau_abs) or len(rel_profile) != len(tau_rel):
+        raise ValueError("percentile grid mismatch between observation and thresholds")
+    worst = 0.0
+    for obs, tau in ((abs_profile, tau_abs), (rel_profile, tau_rel)):
+        obs = np.asarray(obs, dtype=np.float64)
+        tau = np.asarray(tau, dtype=np.float64)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ratio = np.where(tau > 0.0, obs / np.where(tau > 0.0, tau, 1.0),
+                             np.where(obs > 0.0, np.inf, 0.0))
+        worst = max(worst, float(np.max(ratio)) if ratio.size else 0.0)
+    return worst
+
+
+def _payload(t):
+    if isinstance(t, (torch.Tensor, np.ndarray)):
+        return t
+    if getattr(t, "_dev", None) is not None:
+        return t._dev
+    return np.asarray(t.data)
+
+
+def observed_p_max(local, claimed, thresholds, name: str) -> float:
+    """dispute.py:130-141: exact p_max (relative denominator = local magnitudes)."""
+    pa, pr = error_profiles_device(_payload(local), _payload(claimed), thresholds.grid,
+                                   thresholds.epsilon)
+    op = thresholds.lookup(name)
+    return p_max(pa.cpu().numpy(), pr.cpu().numpy(), op.tau_abs, op.tau_rel)
+
+
+def screen(local_outputs, claimed_outputs, output_names, thresholds):
+    """dispute.py:144-150."""
+    details = {}
+    for local, claimed, name in zip(local_outputs, claimed_outputs, output_names):
+        details[name] = observed_p_max(local, claimed, thresholds, name)
+    return any(v > 1.0 for v in details.values()), details
+
+
+def select_offending(offense_ratios):
+    """dispute.py:153-158."""
+    for j, ratio in enumerate(offense_ratios):
+        if ratio is not None and ratio > 1.0:
+            return j
+    return None
+
+
+# ----------------------------------------------------- streaming node check
+
+class CheckRecord:
+    """Device-side nao_check_result; `.host()` reads it (one small D2H)."""
+
+    def __init__(self, buf: torch.Tensor):
+        self.buf = buf
+
+    def host(self) -> dict:
+        raw = self.buf.cpu().numpy().tobytes()
+        r = _lib.CheckResult.from_buffer_copy(raw[:_lib.CHECK_RESULT_BYTES])
+        return {f: getattr(r, f) for f, _ in _lib.CheckResult._fields_ if f != "reserved"}
+
+
+def new_result_buffer(device, n: int = 1) -> torch.Tensor:
+    return torch.zeros((n, _lib.CHECK_RESULT_BYTES), dtype=torch.uint8, device=device)
+
+
+def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel,
+               grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON, lo_factor: float = 1.0,
+               out: torch.Tensor | None = None) -> CheckRecord:
+    """One-pass check of a node.  eps: FP32/FP64 CUDA tensor, ("scaled", c)
+    for c|local| templates, or ("zero",).  No host sync."""
+    a = to_device(local).reshape(-1).contiguous()
+    b = to_device(claimed).reshape(-1).contiguous()
+    if a.numel() != b.numel():
+        raise ValueError("shape mismatch between local and claimed")
+    n = a.numel()
+    if n == 0:
+        raise ValueError("percentile profile of empty input")
+    if len(tau_abs) != len(grid) or len(tau_rel) != len(grid):
+        raise ValueError("percentile grid mismatch between observation and thresholds")
+    eps_ptr, kind, scale = None, _lib.EPS_ZERO, 0.0
+    if isinstance(eps, tuple):
+        if eps[0] == "scaled":
+            kind, scale = _lib.EPS_SCALED_LOCAL, float(eps[1])
+    else:
+        e = eps.reshape(-1).contiguous()
+        if e.numel() != n:
+            raise ValueError("bound shape mismatch")
+        kind = _lib.EPS_TENSOR_F64 if e.dtype == torch.float64 else _lib.EPS_TENSOR_F32
+        if e.dtype == torch.float32 and lo_factor == 1.0:
+            lo_factor = 1.0 / (1.0 + 2.0 ** -22)
+        eps_ptr = e.data_ptr()
+    res = out if out is not None else new_result_buffer(a.device)
+    L = _lib.load()
+    ws = _lib.workspace(L.nao_check_workspace(), a.device)
+    _lib.call("nao_check", a.data_ptr(), b.data_ptr(), n, kind, eps_ptr, scale, float(lo_factor),
+              _lib.dbl_array(grid), _lib.dbl_array(tau_abs), _lib.dbl_array(tau_rel), len(grid),
+              float(epsilon), res.data_ptr(), ws.data_ptr(), ws.numel(),
+              _lib.stream_ptr(a.device))
+    return CheckRecord(res)
+
+
+def leaf_check(claimed, y_ref, eps) -> dict:
+    """dispute.py:641-648 on the GPU: any(|claimed - y_ref| > eps) and its count.
+    Thresholds are irrelevant here (grid of one point, tau = +inf)."""
+    e = eps if isinstance(eps, tuple) else to_device_eps(eps)
+    rec = check_node(y_ref, claimed, e, [np.inf], [np.inf], grid=(100.0,)).host()
+    return {"n_violations": int(rec["n_violations"]), "max_ratio": float(rec["max_ratio"]),
+            "any_violation": rec["n_violations"] > 0}
+
+
+def to_device_eps(eps) -> torch.Tensor:
+    if isinstance(eps, torch.Tensor):
+        return eps if eps.is_cuda else eps.cuda()
+    if hasattr(eps, "device_tensor"):
+        return eps.device_tensor()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(eps, dtype=np.float64))).cuda()
+
+
+__all__ = ["p_max", "observed_p_max", "screen", "select_offending", "check_node", "leaf_check",
+           "CheckRecord", "new_result_buffer"]
+_ = ctypes

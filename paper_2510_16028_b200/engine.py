@@ -1,0 +1,153 @@
+"""FP32 operator values on the GPU, mirroring the reference executor
+(/root/reference/pkg/src/fpverify/engine.py).
+
+Profiles: the reference simulates devices by reduction order (engine.py:29-65).
+This B200 build executes
+  * "sequential" (with/without "+fma") bit-exactly -- the reference's default
+    proposer profile (config.py:14) -- for every reduction (matmul via
+    nao_matmul_profile, softmax/layernorm/sum/mean via the fused bound kernels);
+  * "native": GEMMs on cuBLAS FP32 (TF32 off), the production forward whose
+    values are *not* any simulated profile (the B200 is its own device).
+Other reduction orders (pairwise / blocked / permuted) are SURVEY.md 8(f)
+row 3 ("next") and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+REDUCTIONS = ("sequential", "pairwise", "blocked", "permuted", "native")
+
+
+@dataclass(frozen=True)
+class DeviceProfile:
+    """engine.py:29-55 (plus the B200 "native" profile)."""
+    id: str
+    reduction: str = "sequential"
+    block_size: int = 32
+    perm_seed: int = 0
+    fma: bool = False
+
+    def __post_init__(self):
+        if self.reduction not in REDUCTIONS:
+            raise ValueError(f"unknown reduction strategy {self.reduction!r}")
+
+    @classmethod
+    def from_spec(cls, spec: str, id: str | None = None) -> "DeviceProfile":
+        fma = spec.endswith("+fma")
+        if fma:
+            spec = spec[: -len("+fma")]
+        head, _, arg = spec.partition(":")
+        kw = {}
+        if head == "blocked" and arg:
+            kw["block_size"] = int(arg)
+        elif head == "permuted" and arg:
+            kw["perm_seed"] = int(arg)
+        return cls(id=id or spec + ("+fma" if fma else ""), reduction=head, fma=fma, **kw)
+
+
+def default_profiles():
+    """engine.py:58-65."""
+    return [DeviceProfile("seq", "sequential"), DeviceProfile("pair", "pairwise"),
+            DeviceProfile("blk32", "blocked", block_size=32),
+            DeviceProfile("perm7+fma", "permuted", perm_seed=7, fma=True)]
+
+
+NATIVE = DeviceProfile("b200", "native")
+
+
+class ExecutionError(RuntimeError):
+    """engine.py:68-72."""
+
+    def __init__(self, message, node_index=None, node_name=None):
+        super().__init__(message)
+        self.node_index = node_index
+        self.node_name = node_name
+
+
+def require_supported(profile) -> str:
+    red = "sequential" if profile is None else profile.reduction
+    if red not in ("sequential", "native"):
+        raise NotImplementedError(
+            f"reduction order {red!r} is not emulated on the B200 path yet (SURVEY.md 8(f) row 3)")
+    return red
+
+
+def fma_of(profile) -> bool:
+    return bool(profile.fma) if profile is not None else False
+
+
+# ------------------------------------------------------------------ values
+
+def to_device(a, device=None) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        t = a if a.is_cuda else a.to(device or "cuda")
+        return t if t.dtype == torch.float32 else t.float()
+    if hasattr(a, "cuda") and hasattr(a, "shape") and not isinstance(a, np.ndarray):
+        return a.cuda(device).reshape(a.shape)
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    return torch.from_numpy(arr).to(device or "cuda")
+
+
+def unary(kind: str, x: torch.Tensor) -> torch.Tensor:
+    """engine.py:133-154 (FP64 evaluation rounded once)."""
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _lib.call("nao_unary_fp64", x.data_ptr(), y.data_ptr(), x.numel(), _lib.UNARY[kind],
+              _lib.stream_ptr(x.device))
+    return y
+
+
+def _batch_view(a: torch.Tensor, b: torch.Tensor, transpose_b: bool):
+    """numpy-@ broadcasting over leading dims.  Returns contiguous operands
+    A [nb,M,K], B [nb,K,N] (or [nb,N,K] with transpose_b), their batch strides
+    (0 = broadcast 2-D operand), nb, M, N, K and the output shape."""
+    if a.dim() < 2 or b.dim() < 2:
+        raise ValueError("matmul operands must be at least 2-D")
+    kb, nn = (b.shape[-1], b.shape[-2]) if transpose_b else (b.shape[-2], b.shape[-1])
+    M, K = a.shape[-2], a.shape[-1]
+    if K != kb:
+        raise ValueError(f"matmul inner dims disagree: {tuple(a.shape)} @ {tuple(b.shape)}"
+                         f"{' (transpose_b)' if transpose_b else ''}")
+    batch = tuple(torch.broadcast_shapes(a.shape[:-2], b.shape[:-2]))
+    nb = int(np.prod(batch, dtype=np.int64)) if batch else 1
+
+    def prep(t, inner):
+        if t.dim() == 2 or nb == 1:
+            return t.contiguous(), 0
+        if tuple(t.shape[:-2]) == batch:
+            return t.contiguous(), inner
+        return t.expand(*batch, *t.shape[-2:]).contiguous(), inner
+
+    a3, sa = prep(a, M * K)
+    b3, sb = prep(b, b.shape[-2] * b.shape[-1])
+    return a3, b3, sa, sb, nb, M, nn, K, batch + (M, nn)
+
+
+def matmul_value(a: torch.Tensor, b: torch.Tensor, profile, transpose_b=False) -> torch.Tensor:
+    """engine.py:157-182 under the sequential profile, or cuBLAS FP32 (native)."""
+    red = require_supported(profile)
+    if red == "native":
+        bb = b.transpose(-1, -2) if transpose_b else b
+        return torch.matmul(a, bb)
+    a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
+    out = torch.empty(out_shape, dtype=torch.float32, device=a.device)
+    ldb = K if transpose_b else N
+    _lib.call("nao_matmul_profile", a3.data_ptr(), b3.data_ptr(), out.data_ptr(), nb, M, N, K, K,
+              ldb, sa, sb, M * N, int(transpose_b), int(fma_of(profile)),
+              _lib.stream_ptr(a.device))
+    return out
+
+
+def relu(x: torch.Tensor) -> torch.Tensor:
+    # np.maximum(x, 0): keeps -0.0 (a >= b ? a : b)
+    return torch.where(x >= 0, x, torch.zeros((), dtype=x.dtype, device=x.device))
+
+
+def parse_shape_attr(spec) -> tuple:
+    return tuple(int(tok) for tok in str(spec).split(",") if tok != "")
