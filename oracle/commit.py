@@ -157,12 +157,14 @@ def tensor_leaves(arr, chunk_bytes: int) -> list[bytes]:
 
 def tensor_leaf_digests(arr, chunk_bytes: int, alg=SHA256, n_threads: int = 1) -> np.ndarray:
     """(1 + ceil(nbytes/C), 32) leaf digests: header leaf then payload chunks."""
-    arr = np.ascontiguousarray(np.asarray(arr))
+    arr = np.asarray(arr)
+    shape = arr.shape  # np.ascontiguousarray would turn a 0-d array into shape (1,)
+    arr = np.ascontiguousarray(arr)
     a = alg_id(alg)
     nbytes = arr.nbytes
     n_chunks = (nbytes + chunk_bytes - 1) // chunk_bytes
     out = np.empty((1 + n_chunks, 32), dtype=np.uint8)
-    out[0] = np.frombuffer(leaf_digest(canon_header(arr.shape, arr.dtype), a), dtype=np.uint8)
+    out[0] = np.frombuffer(leaf_digest(canon_header(shape, arr.dtype), a), dtype=np.uint8)
     if n_chunks:
         lib().oracle_chunk_leaves(a, arr.ctypes.data, nbytes, chunk_bytes,
                                   out[1:].ctypes.data, n_threads)

@@ -1,0 +1,170 @@
+"""GPU parity: per-operator values and bounds vs the reference goldens
+(tests/golden/ref_ops.npz, ref_mlp_784_256_10_b64.json; made by
+oracle/gen_golden.py from the unmodified reference).
+
+Tolerance (north_star): bounds within rtol 1e-5 of the reference and never
+below it:  eps_ref <= eps_gpu <= eps_ref * (1 + 1e-5).  Values under the
+sequential profile: bit-exact."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from _helpers import OP_SPECS, op_cases
+from oracle import bounds as OB
+from oracle import commit as OM
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+INTRINSIC_TRANSCENDENTAL = {"exp", "log", "tanh", "gelu", "silu"}
+
+
+def assert_bound(eps_gpu, eps_ref, what=""):
+    eps_gpu = np.asarray(eps_gpu, dtype=np.float64).reshape(-1)
+    eps_ref = np.asarray(eps_ref, dtype=np.float64).reshape(-1)
+    assert eps_gpu.shape == eps_ref.shape, what
+    below = eps_gpu < eps_ref
+    assert not below.any(), (what, int(below.sum()), float((eps_ref - eps_gpu)[below].max()))
+    over = eps_gpu > eps_ref * (1.0 + RTOL)
+    assert not over.any(), (what, int(over.sum()),
+                            float(np.max(eps_gpu[over] / eps_ref[over] - 1.0)))
+
+
+class _Node:
+    def __init__(self, kind, attrs):
+        self.kind, self.attrs, self.index, self.name, self.inputs = kind, attrs, 0, "op", ()
+
+    def attr(self, k, d=None):
+        return self.attrs.get(k, d)
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2510_16028_b200 import bounds
+    return bounds
+
+
+@pytest.mark.parametrize("tag", sorted(OP_SPECS))
+def test_op_bound_matches_reference(B, ref_ops, tag):
+    from paper_2510_16028_b200.engine import DeviceProfile
+    ins, y_ref, eps_ref = op_cases(ref_ops)[tag]
+    kind, attrs, mode, fma = OP_SPECS[tag]
+    model = B.FpModel(mode="deterministic" if mode == "det" else "probabilistic")
+    prof = DeviceProfile("seqf" if fma else "seq", "sequential", fma=fma)
+    y, eps = B.op_bound(_Node(kind, attrs), ins, model, prof)
+    assert y.dtype == np.float32 and eps.dtype == np.float64
+    assert y.shape == y_ref.shape and eps.shape == eps_ref.shape
+    yu, ru = y.view(np.int32).astype(np.int64), y_ref.astype(np.float32).view(np.int32)
+    same = yu == ru
+    if kind in INTRINSIC_TRANSCENDENTAL:
+        # FP64 exp/log/tanh differ from numpy's libm in the last FP64 ulp; after the
+        # single FP32 rounding that shows up as a rare 1-ulp value difference
+        # (engine.py:4-8 "2-ULP budget").  Bound = template on our own value.
+        if kind == "gelu":
+            # 0.5x(1+tanh(.)) cancels for x << 0: a 1-ulp FP64 tanh difference moves the
+            # result by ~|x| 2^-52 absolute -- the reference formula's own noise floor.
+            x64 = np.abs(ins[0].astype(np.float64))
+            ulp = np.spacing(np.abs(y_ref.astype(np.float32))).astype(np.float64)
+            tol = 2 * ulp + x64 * 2.0 ** -51
+            assert np.all(np.abs(y.astype(np.float64) - y_ref) <= tol), tag
+        else:
+            assert np.all(np.abs(yu - ru) <= 1), tag
+        assert same.mean() >= 0.95, (tag, same.mean())
+        np.testing.assert_array_equal(eps, 2 * 2.0 ** -24 * np.abs(y.astype(np.float64)))
+        assert_bound(eps.reshape(-1)[same.reshape(-1)], eps_ref.reshape(-1)[same.reshape(-1)], tag)
+    else:
+        assert same.all(), tag
+        assert_bound(eps, eps_ref, tag)
+
+
+def test_matmul_bound_api(B):
+    a = np.array([[2.0]], dtype=np.float32)
+    b = np.array([[3.0]], dtype=np.float32)
+    bt = B.matmul_bound(a, b, B.FpModel(mode="deterministic"))
+    ref = B.gamma(1) * 6.0
+    assert ref <= bt.array[0, 0] <= ref * (1 + RTOL)
+    with pytest.raises(ValueError):
+        B.matmul_bound(np.ones((2, 3), np.float32), np.ones((4, 2), np.float32), B.FpModel())
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 33, 5), (128, 128, 128), (129, 300, 131),
+                                   (64, 4096, 96), (300, 17, 1000)])
+@pytest.mark.parametrize("tb", [False, True])
+def test_abs_gemm_vs_fp64_blas(B, shape, tb):
+    M, K, N = shape
+    rng = np.random.default_rng(M * 7 + K)
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    model = B.FpModel()
+    ref = OB.matmul_bound(a, b, OB.FpModel(), transpose_b=tb)
+    got = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                           model.reduction_const(2 * K - 1), tb).cpu().numpy()
+    assert_bound(got, ref, str(shape))
+    got32 = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                             model.reduction_const(2 * K - 1), tb, eps_f64=False).cpu().numpy()
+    assert_bound(got32, ref, str(shape) + " f32")
+
+
+def test_abs_gemm_heterogeneous_rows(B):
+    """Softmax-like rows (one dominant entry, tiny rest) and wide dynamic range."""
+    rng = np.random.default_rng(5)
+    M, K, N = 64, 2048, 128
+    p = np.exp(rng.standard_normal((M, K)) * 8).astype(np.float32)
+    p /= p.sum(axis=1, keepdims=True)
+    v = (rng.standard_normal((K, N)) * 10.0 ** rng.integers(-20, 20, size=(K, N))).astype(
+        np.float32)
+    ref = OB.matmul_bound(p, v, OB.FpModel())
+    got = B.abs_gemm_bound(torch.from_numpy(p).cuda(), torch.from_numpy(v).cuda(),
+                           OB.FpModel().reduction_const(2 * K - 1)).cpu().numpy()
+    assert_bound(got, ref, "hetero")
+
+
+def test_batched_broadcast_matmul(B):
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((4, 3, 20, 33)).astype(np.float32)
+    b = rng.standard_normal((3, 18, 33)).astype(np.float32)
+    ref = OB.matmul_bound(a, b, OB.FpModel(), transpose_b=True)
+    got = B.matmul_bound(a, b, B.FpModel(), transpose_b=True).array
+    assert_bound(got, ref, "bcast")
+
+
+def test_softmax_layernorm_large_rows(B):
+    """Qwen-shaped rows: softmax over n=2048, layernorm over n=4096."""
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((96, 2048)) * 3).astype(np.float32)
+    y_ref, e_ref = OB.softmax_bound_parts(x, -1, OB.FpModel())
+    y, e = B.softmax_bound_parts(x, -1, B.FpModel())
+    assert np.array_equal(y.view(np.uint32), y_ref.view(np.uint32))
+    assert_bound(e, e_ref, "softmax")
+    x = (rng.standard_normal((40, 4096)) + 0.5).astype(np.float32)
+    y_ref, e_ref = OB.layernorm_bound_parts(x, -1, 1e-6, OB.FpModel())
+    y, e = B.layernorm_bound_parts(x, -1, 1e-6, B.FpModel())
+    assert np.array_equal(y.view(np.uint32), y_ref.view(np.uint32))
+    assert_bound(e, e_ref, "layernorm")
+
+
+def test_mlp_co_execute_matches_reference(B, ref_mlp):
+    """Full reference MLP (784-256-10, B=64) under the sequential profile:
+    every node value bit-exact (digest), bounds within [ref, ref(1+1e-5)]."""
+    from paper_2510_16028_b200 import commitments
+    from paper_2510_16028_b200.engine import DeviceProfile
+    from paper_2510_16028_b200.lowerings import build_mlp
+    from paper_2510_16028_b200.tensor import Rng
+    c = ref_mlp["config"]
+    spec = build_mlp(c["seed"], c["batch"], c["in_dim"], c["hidden"], c["n_classes"])
+    x = spec.make_inputs(Rng(*c["input_rng"]))
+    for run, fma in (("seq", False), ("seqf", True)):
+        for mode, mname in (("prob", "probabilistic"), ("det", "deterministic")):
+            prof = DeviceProfile(run, "sequential", fma=fma)
+            outs, bnds, trace = B.co_execute(spec.graph, x, prof, B.FpModel(mode=mname),
+                                             with_trace=True)
+            for i, (t, bt, ent) in enumerate(zip(trace.tensors, bnds, ref_mlp["runs"][f"{run}/{mode}"])):
+                node = spec.graph.nodes[i].name
+                assert commitments.tensor_digest(t) == ent["value_digest"], (run, mode, node)
+                flat = bt.eps
+                ref_s = np.asarray(ent["eps_sample"])
+                assert_bound(flat[ent["idx"]], ref_s, f"{run}/{mode}/{node}")
+                assert ent["eps_sum"] <= flat.sum() * (1 + 1e-12)
+                assert flat.sum() <= ent["eps_sum"] * (1 + RTOL)
