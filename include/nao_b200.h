@@ -149,6 +149,13 @@ int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, 
                        int64_t stride_b, int64_t stride_c, int transpose_b, int fma,
                        void* stream);
 
+/* Additive fault / drift hook on a node output (engine.py:325-351 `inject`):
+ * out = y with +-1-ulp flips on ~n/period elements and a relative fault
+ * `fault_scale` on ~n/fault_period elements (0 disables either).  Used to
+ * materialise claimed traces for tests and the benchmark harness. */
+int nao_inject_drift(const float* y, float* out, int64_t n, uint32_t seed, uint32_t period,
+                     float fault_scale, uint32_t fault_period, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,8 @@ _SIGS = {
                                    c_dbl, c_int, c_vp]),
     "nao_matmul_profile": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                                    c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
+    "nao_inject_drift": (c_int, [c_vp, c_vp, c_i64, ctypes.c_uint32, ctypes.c_uint32,
+                                 ctypes.c_float, ctypes.c_uint32, c_vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -127,9 +129,37 @@ def check(rc: int, what: str = ""):
     raise NaoError(f"{what}: {msg} (status {rc})")
 
 
+# optional per-entry-point CUDA-event timing (bench.py roofline): name -> events/units
+_timer = None
+
+
+def set_timer(store, units_fn, stream):
+    """Start (store=dict) or stop (None) event timing of every `call`.  On stop,
+    store[name] = {"ms": [...], "units": [...]} per launch (needs a prior sync)."""
+    global _timer
+    if store is None and _timer is not None:
+        d = _timer[0]
+        for name, ent in d.items():
+            ent["ms"] = [a.elapsed_time(b) for a, b in ent.pop("ev")]
+        _timer = None
+        return
+    _timer = (store, units_fn, stream) if store is not None else None
+
+
 def call(name: str, *args):
-    rc = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    if _timer is None:
+        check(fn(*args), name)
+        return
+    store, units_fn, stream = _timer
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rc = fn(*args)
+    e1.record(stream)
     check(rc, name)
+    ent = store.setdefault(name, {"ev": [], "units": []})
+    ent["ev"].append((e0, e1))
+    ent["units"].append(units_fn(name, args) if units_fn else 0.0)
 
 
 def stream_ptr(device=None) -> int:

@@ -377,3 +377,36 @@ int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, doub
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ fault / drift hook
+// Mirrors the reference's additive `inject` hook on node outputs
+// (engine.py:325-351): the claimed value of element i is y_i moved by
+// +-1 ulp with probability ~1/period (hash of (seed, i)) -- honest
+// cross-device drift -- plus an optional relative fault `scale` on every
+// element with (hash % fault_period == 0).
+namespace nao {
+__global__ void k_inject_drift(const float* __restrict__ y, float* __restrict__ out, int64_t n,
+                               uint32_t seed, uint32_t period, float fault_scale,
+                               uint32_t fault_period) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 0x9E3779B1u ^ seed;
+        h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+        float v = __ldg(y + i);
+        if (period && (h % period) == 0 && v != 0.0f && isfinite(v))
+            v = __int_as_float(__float_as_int(v) + ((h >> 20) & 1 ? 1 : -1));
+        if (fault_period && ((h >> 8) % fault_period) == 0) v = v * (1.0f + fault_scale);
+        out[i] = v;
+    }
+}
+}  // namespace nao
+
+extern "C" int nao_inject_drift(const float* y, float* out, int64_t n, uint32_t seed,
+                                uint32_t period, float fault_scale, uint32_t fault_period,
+                                void* stream) {
+    if (n == 0) return NAO_OK;
+    nao::k_inject_drift<<<nao::ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        y, out, n, seed, period, fault_scale, fault_period);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}

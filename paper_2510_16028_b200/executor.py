@@ -1,0 +1,264 @@
+"""Streaming co-execution on one B200: the NAO hot path at model scale.
+
+Trace-driven verification, the challenger's per-operator adjudication
+(dispute.py:605-657) applied to every node in canonical order (optionally a
+contiguous op slice, the reference's partition unit, graph.py:275-293):
+
+    y      = op(claimed inputs)            (re-execution from the committed trace)
+    eps    = bound template of that op     (fused where it needs FP32 parts)
+    check  = one pass over (y, claimed y', eps): bound violations |y'-y| > eps,
+             max violation ratio, exact p_max > 1 verdict (dispute.py:114-158)
+    commit = chunked Merkle root of the claimed tensor y' (batched per flush)
+
+Downstream nodes consume the claimed values, so an injected fault is flagged
+at its own node and nowhere else (the localisation property of the game).
+
+Only per-node roots (32 B) and check records (56 B) survive a node; the trace
+is never resident.  No host synchronisation happens
+until `finish()`.  Elementwise bounds are never materialised: the check
+kernel recomputes c|y| on the fly.
+
+`plain_forward` runs the same lowered graph with values only (cuBLAS FP32,
+TF32 off, torch eager ops) -- the baseline the overhead is measured against.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .bounds import FpModel, apply_value, op_bound_device
+from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID
+from .commitments import DEFAULT_CHUNK_BYTES, alg_id, commit_tensors, root_of_digests
+from .dispute import new_result_buffer
+from .engine import NATIVE, ExecutionError, to_device
+from .graph import parse_ref
+
+INF_TAU = np.full(len(PERCENTILE_GRID), np.inf)
+
+
+def last_uses(graph, start: int = 0, end: int | None = None) -> dict:
+    """node index -> last consumer index within [start, end) (outputs live to the end)."""
+    end = graph.n_nodes if end is None else end
+    last = {}
+    for node in graph.nodes[start:end]:
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            if cat == "node":
+                last[key] = node.index
+    for ref in graph.outputs:
+        last[parse_ref(ref)[1]] = end
+    return last
+
+
+REDUCTION_KINDS = frozenset({"matmul", "linear", "softmax", "layernorm", "sum", "mean"})
+
+
+def drift_claim(node, y: torch.Tensor, seed: int = 0, period: int = 16, fault_node=None,
+                fault_scale: float = 1e-3, fault_period: int = 64) -> torch.Tensor:
+    """Harness proposer: reduction ops drift by +-1 ulp on ~1/period elements
+    (a different device's summation order); deterministic ops are reproduced
+    exactly; `fault_node` additionally carries a relative fault."""
+    faulty = fault_node is not None and node.name == fault_node
+    if node.kind in REDUCTION_KINDS or faulty:
+        return inject_drift(y, seed * 7919 + node.index, period if node.kind in REDUCTION_KINDS
+                            else 0, fault_scale if faulty else 0.0, fault_period if faulty else 0)
+    return y.clone()
+
+
+def inject_drift(y: torch.Tensor, seed: int, period: int = 16, fault_scale: float = 0.0,
+                 fault_period: int = 0) -> torch.Tensor:
+    """Claimed tensor = y with honest +-1-ulp drift (+ optional fault); see nao_inject_drift."""
+    y = y.contiguous()
+    out = torch.empty_like(y)
+    _lib.call("nao_inject_drift", y.data_ptr(), out.data_ptr(), y.numel(), seed & 0xFFFFFFFF,
+              period, float(fault_scale), fault_period, _lib.stream_ptr(y.device))
+    return out
+
+
+@dataclass
+class NodeStats:
+    bytes_committed: int = 0
+    elements_checked: int = 0
+    gemm_flops: int = 0
+
+
+class StreamingVerifier:
+    def __init__(self, graph, model: FpModel | None = None, profile=NATIVE, thresholds=None,
+                 hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
+                 flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
+                 grid=PERCENTILE_GRID):
+        self.g = graph
+        self.model = model or FpModel()
+        self.profile = profile
+        self.thresholds = thresholds
+        self.alg = alg_id(hash_alg)
+        self.chunk = int(chunk_bytes)
+        self.flush_bytes = int(flush_bytes)
+        self.dev = torch.device(device)
+        self.epsilon = float(epsilon)
+        self.grid = tuple(grid)
+        self._tau_cache = {}
+
+    # ---------------------------------------------------------- thresholds
+    def _taus(self, name):
+        if self.thresholds is None:
+            return INF_TAU, INF_TAU
+        t = self._tau_cache.get(name)
+        if t is None:
+            try:
+                op = self.thresholds.lookup(name)
+                t = (op.tau_abs, op.tau_rel)
+            except KeyError:
+                t = (INF_TAU, INF_TAU)
+            self._tau_cache[name] = t
+        return t
+
+    # ----------------------------------------------------------------- run
+    def run(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
+            frontier: dict | None = None, stats: NodeStats | None = None):
+        """Verify nodes [start, end).  claimed_fn(node, y) -> the claimed CUDA tensor
+        of node (the proposer's trace; given the locally recomputed y for harnesses).
+        frontier maps external producer node index -> tensor (slice execution,
+        graph.py:244-272).  Returns (roots [n,32] uint8, records [n, R] uint8)."""
+        g = self.g
+        end = g.n_nodes if end is None else end
+        n = end - start
+        roots = torch.empty((n, 32), dtype=torch.uint8, device=self.dev)
+        records = new_result_buffer(self.dev, n)
+        last = last_uses(g, start, end)
+        values = dict(frontier or {})
+        pending, pend_idx, pend_bytes = [], [], 0
+        L = _lib.load()
+        ws_chk = _lib.workspace(L.nao_check_workspace(), self.dev)
+        stream = _lib.stream_ptr(self.dev)
+        grid_arr = _lib.dbl_array(self.grid)
+
+        def flush():
+            nonlocal pending, pend_idx, pend_bytes
+            if not pending:
+                return
+            r = commit_tensors(pending, self.chunk, self.alg)
+            idx = torch.as_tensor(pend_idx, device=self.dev)
+            roots.index_copy_(0, idx, r)
+            pending, pend_idx, pend_bytes = [], [], 0
+
+        for node in g.nodes[start:end]:
+            xs = []
+            for ref in node.inputs:
+                cat, key = parse_ref(ref)
+                if cat == "node":
+                    xs.append(values[key])
+                elif cat == "input":
+                    xs.append(to_device(inputs[key], self.dev))
+                else:
+                    xs.append(to_device(g.weights[key], self.dev))
+            try:
+                y, eps = op_bound_device(node, xs, self.model, self.profile, eps_f64=None)
+            except (ExecutionError, NotImplementedError):
+                raise
+            except Exception as exc:
+                raise ExecutionError(f"node {node.index} ({node.name!r}, {node.kind}): {exc}",
+                                     node_index=node.index, node_name=node.name) from exc
+            y = y.contiguous()
+            yc = claimed_fn(node, y)
+            tau_a, tau_r = self._taus(node.name)
+            kind, eps_ptr, scale, lo = _lib.EPS_ZERO, None, 0.0, 1.0
+            if isinstance(eps, tuple):
+                if eps[0] == "scaled":
+                    kind, scale = _lib.EPS_SCALED_LOCAL, float(eps[1])
+            else:
+                kind = _lib.EPS_TENSOR_F64 if eps.dtype == torch.float64 else _lib.EPS_TENSOR_F32
+                lo = 1.0 if eps.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
+                eps_ptr = eps.data_ptr()
+            i = node.index - start
+            if y.numel():
+                _lib.call("nao_check", y.data_ptr(), yc.data_ptr(), y.numel(), kind, eps_ptr,
+                          scale, lo, grid_arr, _lib.dbl_array(tau_a), _lib.dbl_array(tau_r),
+                          len(self.grid), self.epsilon, records[i].data_ptr(),
+                          ws_chk.data_ptr(), ws_chk.numel(), stream)
+            if stats is not None:
+                stats.elements_checked += y.numel()
+                stats.bytes_committed += y.numel() * 4
+                if node.kind in ("matmul", "linear"):
+                    stats.gemm_flops += 2 * y.numel() * xs[0].shape[-1]
+            del eps, y
+            yc = yc.contiguous()
+            values[node.index] = yc
+            pending.append(yc)
+            pend_idx.append(i)
+            pend_bytes += yc.numel() * 4
+            if pend_bytes >= self.flush_bytes or len(pending) >= 120:
+                flush()
+            for ref in node.inputs:
+                cat, key = parse_ref(ref)
+                if cat == "node" and last.get(key, -1) == node.index and key in values:
+                    del values[key]
+            if last.get(node.index, -1) <= node.index and node.index in values:
+                del values[node.index]
+        flush()
+        self.outputs = {k: v for k, v in values.items()}
+        return roots, records
+
+    def trace_root(self, roots: torch.Tensor) -> torch.Tensor:
+        """Merkle root over per-node roots (leaf = H(0x00||root)), on device."""
+        n = roots.shape[0]
+        offs = torch.arange(0, 32 * (n + 1), 32, dtype=torch.int64, device=roots.device)
+        leaves = torch.empty((n, 32), dtype=torch.uint8, device=roots.device)
+        _lib.call("nao_merkle_hash_leaves", roots.contiguous().data_ptr(), offs.data_ptr(), n,
+                  self.alg, leaves.data_ptr(), _lib.stream_ptr(roots.device))
+        return root_of_digests(leaves, self.alg)
+
+
+# ------------------------------------------------------------ plain forward
+
+def plain_value(node, xs, profile=NATIVE) -> torch.Tensor:
+    """Values only, torch eager FP32 (the baseline forward of the same graph)."""
+    k = node.kind
+    if k == "softmax":
+        return torch.softmax(xs[0], dim=int(node.attr("axis", -1)))
+    if k == "layernorm":
+        ax = int(node.attr("axis", -1)) % xs[0].dim()
+        x = xs[0].movedim(ax, -1)
+        y = F.layer_norm(x, (x.shape[-1],), eps=float(node.attr("eps", 1e-5)))
+        return y.movedim(-1, ax)
+    if k in ("sum", "mean", "max", "min"):
+        ax = int(node.attr("axis", -1))
+        return {"sum": torch.sum, "mean": torch.mean, "max": torch.amax,
+                "min": torch.amin}[k](xs[0], dim=ax)
+    if k in ("exp", "log", "sqrt", "rsqrt", "tanh"):
+        return getattr(torch, k)(xs[0])
+    if k == "gelu":
+        return F.gelu(xs[0], approximate="tanh")
+    if k == "silu":
+        return F.silu(xs[0])
+    return apply_value(node, xs, profile)
+
+
+def plain_forward(graph, inputs: dict, device="cuda", start: int = 0, end: int | None = None,
+                  frontier: dict | None = None):
+    g = graph
+    end = g.n_nodes if end is None else end
+    last = last_uses(g, start, end)
+    values = dict(frontier or {})
+    dev = torch.device(device)
+    for node in g.nodes[start:end]:
+        xs = []
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            if cat == "node":
+                xs.append(values[key])
+            elif cat == "input":
+                xs.append(to_device(inputs[key], dev))
+            else:
+                xs.append(to_device(g.weights[key], dev))
+        values[node.index] = plain_value(node, xs)
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            if cat == "node" and last.get(key, -1) == node.index and key in values:
+                del values[key]
+    return values

@@ -1,0 +1,116 @@
+"""GPU: the streaming hot path (executor.StreamingVerifier) end to end.
+
+MLP (reference graph, sequential profile): per-node roots equal the oracle's
+tensor roots of the reference values, check records equal the oracle's leaf
+check / observed_p_max verdicts.  Small Qwen3-shaped decoder (native profile):
+node-by-node bounds vs the oracle fed with the same GPU node inputs."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bounds as OB
+from oracle import check as OC
+from oracle import commit as OM
+
+pytestmark = pytest.mark.gpu
+
+
+def test_streaming_mlp_matches_oracle(ref_mlp):
+    from paper_2510_16028_b200 import calibration
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.engine import DeviceProfile
+    from paper_2510_16028_b200.executor import StreamingVerifier, drift_claim
+    from paper_2510_16028_b200.lowerings import build_mlp
+    from paper_2510_16028_b200.tensor import Rng
+    c = ref_mlp["config"]
+    spec = build_mlp(c["seed"], c["batch"], c["in_dim"], c["hidden"], c["n_classes"])
+    x = spec.make_inputs(Rng(*c["input_rng"]))
+    th = calibration.ThresholdSet.from_json(ref_mlp["thresholds"])
+    sv = StreamingVerifier(spec.graph, FpModel(), DeviceProfile("seq", "sequential"), th,
+                           hash_alg="sha256", chunk_bytes=4096)
+    claimed = {}
+
+    def claimed_fn(node, y):
+        yc = drift_claim(node, y, seed=1, period=8, fault_node="mm1")
+        claimed[node.index] = yc
+        return yc
+
+    roots, recs = sv.run(x, claimed_fn)
+    troot = sv.trace_root(roots)
+    torch.cuda.synchronize()
+    from paper_2510_16028_b200.dispute import CheckRecord
+    from paper_2510_16028_b200.graph import parse_ref
+    host_roots = roots.cpu().numpy()
+    cl = {i: t.cpu().numpy() for i, t in claimed.items()}
+    model = OB.FpModel()
+    tree_roots = []
+    for i, node in enumerate(spec.graph.nodes):
+        # oracle: the reference leaf adjudication from the claimed inputs
+        args = []
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            args.append(cl[key] if cat == "node" else (x[key].array if cat == "input"
+                                                        else spec.graph.weights[key].array))
+        y_ref, eps = OB.op_bound(node, args, model)
+        ref = OC.leaf_check(y_ref, cl[i], eps)
+        rec = CheckRecord(recs[i]).host()
+        # eps_gpu >= eps_ref: a GPU violation is a reference violation; any
+        # difference is confined to the reported borderline band
+        assert rec["n_violations"] <= ref["n_violations"] <= rec["n_violations"] + rec["n_borderline"], node.name
+        if node.name == "mm1":
+            assert ref["n_violations"] > 0 and rec["n_violations"] > 0
+        op = th.lookup(node.name)
+        pm = OC.observed_p_max(y_ref, cl[i], op.tau_abs, op.tau_rel, th.grid, th.epsilon)
+        assert bool(rec["threshold_exceeded"]) == (pm > 1.0), node.name
+        assert bytes(host_roots[i]) == OM.tensor_root(cl[i], 4096), node.name
+        tree_roots.append(bytes(host_roots[i]))
+    assert bytes(troot.cpu().numpy()) == OM.trace_root(tree_roots)
+
+
+def test_streaming_decoder_bounds_vs_oracle():
+    from paper_2510_16028_b200.bounds import FpModel, op_bound_device
+    from paper_2510_16028_b200.executor import StreamingVerifier, drift_claim, plain_forward
+    from paper_2510_16028_b200.graph import parse_ref
+    from paper_2510_16028_b200.lowerings import DecoderShape, build_decoder
+    from paper_2510_16028_b200.engine import NATIVE, to_device
+    from paper_2510_16028_b200.tensor import Rng
+    shape = DecoderShape("tiny-qwen", layers=2, hidden=128, heads=4, kv_heads=2, head_dim=32,
+                         inter=256, vocab=500, seq=64)
+    spec = build_decoder(shape, seed=3)
+    g = spec.graph
+    ids = spec.make_inputs(Rng(5))
+    # node-by-node: GPU bound on the GPU's own node inputs vs oracle op_bound on the same inputs
+    model = FpModel()
+    values = {}
+    for node in g.nodes:
+        xs = []
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            xs.append(values[key] if cat == "node" else to_device(
+                ids[key] if cat == "input" else g.weights[key]))
+        y, eps = op_bound_device(node, xs, model, NATIVE, eps_f64=True)
+        values[node.index] = y
+        ins = [a.cpu().numpy() for a in xs]
+        if node.kind == "embedding":
+            continue
+        if node.kind in ("matmul", "linear"):
+            tb = bool(node.attr("transpose_b", 0))
+            K = ins[0].shape[-1]
+            ref = OB.matmul_bound(ins[0], ins[1], OB.FpModel(), transpose_b=tb)
+            if node.kind == "linear":
+                ref = ref + 2.0 ** -24 * np.abs(y.cpu().numpy().astype(np.float64))
+        else:
+            yr, ref = OB.op_bound(node, ins, OB.FpModel())
+            assert np.array_equal(yr.view(np.uint32), y.cpu().numpy().view(np.uint32)) or \
+                node.kind in ("exp", "log", "tanh", "gelu", "silu"), node.name
+        e = eps.cpu().numpy()
+        assert np.all(e >= ref) and np.all(e <= ref * (1 + 1e-5)), node.name
+    # and the streaming pipeline runs end to end (native profile) with a planted fault
+    sv = StreamingVerifier(g, model, NATIVE, None, "keccak256", 4096)
+    roots, recs = sv.run(ids, lambda node, y: drift_claim(node, y, 3, 16, "l1_down", 0.05, 2))
+    from paper_2510_16028_b200.dispute import CheckRecord
+    viol = {node.name: CheckRecord(recs[i]).host()["n_violations"] for i, node in enumerate(g.nodes)}
+    assert viol["l1_down"] > 0
+    outs = plain_forward(g, ids)
+    assert set(outs) >= {g.n_nodes - 1}
