@@ -127,19 +127,25 @@ def calibrate_thresholds(g, sv_cls, ids, dev, model, args, start=0, end=None, fr
     from paper_2510_16028_b200.calibration import (PERCENTILE_GRID, OpThresholds, ThresholdSet,
                                                    error_profiles_device)
     from paper_2510_16028_b200.executor import drift_claim
-    prof = {}
+    env = {}  # max envelope over calibration samples (calibration.py:97-108)
 
-    def claimed_fn(node, y):
-        yc = drift_claim(node, y, seed=12345, period=args.drift_period)
-        if y.numel():
-            prof[node.name] = error_profiles_device(y, yc)
-        return yc
+    for seed in range(12345, 12345 + args.calib_samples):
+        def claimed_fn(node, y, seed=seed):
+            yc = drift_claim(node, y, seed=seed, period=args.drift_period)
+            if y.numel():
+                pa, pr = error_profiles_device(y, yc)
+                if node.name in env:
+                    torch.maximum(env[node.name][0], pa, out=env[node.name][0])
+                    torch.maximum(env[node.name][1], pr, out=env[node.name][1])
+                else:
+                    env[node.name] = (pa, pr)
+            return yc
 
-    sv = sv_cls(g, model, thresholds=None, hash_alg=args.hash, chunk_bytes=args.chunk)
-    sv.run(ids, claimed_fn, start, end, frontier)
+        sv = sv_cls(g, model, thresholds=None, hash_alg=args.hash, chunk_bytes=args.chunk)
+        sv.run(ids, claimed_fn, start, end, frontier)
     torch.cuda.synchronize()
     ops = [OpThresholds(n, 3.0 * a.cpu().numpy(), 3.0 * r.cpu().numpy())
-           for n, (a, r) in prof.items()]
+           for n, (a, r) in env.items()]
     return ThresholdSet(alpha=3.0, epsilon=1e-12, grid=PERCENTILE_GRID, ops=ops)
 
 
@@ -343,7 +349,7 @@ def run_ours(args):
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks
                     else "fallback", "traffic": None}
-        roof["share_of_step"] = round(shares[dom] / t_ver, 4)
+        roof["share_of_step"] = round(shares[dom] / args.steps / t_ver, 4)
         roof["kernel_ms_per_step"] = {k: round(v / args.steps, 2) for k, v in shares.items()}
 
     commit_ms = shares.get("nao_merkle_commit_tensors", 0.0) / args.steps
@@ -519,6 +525,7 @@ def main(argv=None):
     ap.add_argument("--drift-period", type=int, default=16)
     ap.add_argument("--fault-node", default="l3_down")
     ap.add_argument("--cpu-seq", type=int, default=512)
+    ap.add_argument("--calib-samples", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args(argv)
     if args.fault_node and args.layers <= int(args.fault_node.split("_")[0][1:] or 0):

@@ -142,6 +142,20 @@ int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, i
                        int64_t stride_a, int64_t stride_b, int64_t stride_c, int transpose_b,
                        double gamma_const, const float* y_or_null, double u, double slack,
                        int path, void* stream);
+/* tcgen05 path of matmul_bound: |x| -> TF32 (hi, lo) parts, K-major
+ * [batch, rows, Kp] with Kp = nao_tf32_split_cols(K) (x is [rows, K] row-major
+ * with leading dim ld, or [K, rows] when transpose).  hi <= |x| <= hi + lo. */
+int64_t nao_tf32_split_cols(int64_t K);
+int nao_tf32_split(const float* x, float* hi, float* lo, int64_t batch, int64_t rows, int64_t K,
+                   int64_t ld, int64_t stride_batch, int transpose, void* stream);
+/* eps >= gamma_const * sum_k |A||B| from the split parts on tcgen05.mma.kind::tf32
+ * (3 products, outward-compensated, within rtol 1e-5 of the FP64 reference);
+ * batch_a / batch_b are `batch` or 1 (broadcast).  Output [batch, M, N], ldc. */
+int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
+                    void* eps, int eps_f64, int64_t batch, int64_t batch_a, int64_t batch_b,
+                    int64_t M, int64_t N, int64_t K, int64_t ldc, int64_t stride_c,
+                    double gamma_const, const float* y_or_null, double u, double slack,
+                    void* stream);
 /* matmul_op values under the sequential profile (engine.py:157-182),
  * C contiguous [batch, M, N]; fma selects the "+fma" FP64-step emulation. */
 int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, int64_t M,

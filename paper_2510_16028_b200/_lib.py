@@ -76,6 +76,10 @@ _SIGS = {
                                    c_dbl, c_int, c_vp]),
     "nao_matmul_profile": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                                    c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
+    "nao_tf32_split_cols": (c_i64, [c_i64]),
+    "nao_tf32_split": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]),
+    "nao_abs_gemm_tc": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64,
+                                c_i64, c_i64, c_i64, c_i64, c_dbl, c_vp, c_dbl, c_dbl, c_vp]),
     "nao_inject_drift": (c_int, [c_vp, c_vp, c_i64, ctypes.c_uint32, ctypes.c_uint32,
                                  ctypes.c_float, ctypes.c_uint32, c_vp]),
 }

@@ -18,6 +18,8 @@ CUDA tensors in -> CUDA tensors out (asynchronous).
 from __future__ import annotations
 
 import math
+import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -137,10 +139,42 @@ def _eps_buffer(shape, device, f64: bool) -> torch.Tensor:
 
 # ---------------------------------------------------------------- kernels
 
+def default_gemm_path() -> int:
+    """tcgen05 3xTF32 unless NAO_GEMM_PATH=ffma (both are sound)."""
+    env = os.environ.get("NAO_GEMM_PATH", "tc").lower()
+    return _lib.GEMM_FFMA_RU if env in ("ffma", "simt", "0") else _lib.GEMM_TC_TF32X3
+
+
+# hi/lo TF32 splits of operands that outlive a call (weights), keyed by the
+# identity of the torch tensor object; dropped when that object dies.
+_SPLITS: dict = {}
+
+
+def tf32_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool):
+    """|x| -> (hi, lo) K-major [batch, rows, Kp] TF32 parts (nao_tf32_split)."""
+    key = id(x3)
+    if cache:
+        hit = _SPLITS.get(key)
+        if hit is not None and hit[0]() is x3 and hit[1] == x3._version:
+            return hit[2], hit[3]
+    batch = x3.numel() // (rows * K) if rows * K else 1
+    Kp = (K + 3) // 4 * 4
+    hi = torch.empty((batch, rows, Kp), dtype=torch.float32, device=x3.device)
+    lo = torch.empty_like(hi)
+    ld = rows if transpose else K
+    _lib.call("nao_tf32_split", x3.data_ptr(), hi.data_ptr(), lo.data_ptr(), batch, rows, K, ld,
+              rows * K, int(transpose), _lib.stream_ptr(x3.device))
+    if cache:
+        _SPLITS[key] = (weakref.ref(x3, lambda _r, k=key: _SPLITS.pop(k, None)), x3._version,
+                        hi, lo)
+    return hi, lo
+
+
 def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
                    y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
-                   path: int = _lib.GEMM_FFMA_RU) -> torch.Tensor:
+                   path: int | None = None, cache_b: bool = False) -> torch.Tensor:
     """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors)."""
+    path = default_gemm_path() if path is None else path
     a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
     eps = _eps_buffer(out_shape, a.device, eps_f64)
     yc = None
@@ -148,6 +182,15 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
         yc = y.contiguous()
         if tuple(yc.shape) != tuple(out_shape):
             raise ValueError("linear bound: output shape mismatch")
+    if path == _lib.GEMM_TC_TF32X3:
+        ahi, alo = tf32_split(a3, M, K, False, False)
+        bhi, blo = tf32_split(b if (cache_b and b3.data_ptr() == b.data_ptr()) else b3,
+                              N, K, not transpose_b, cache_b and b3.data_ptr() == b.data_ptr())
+        _lib.call("nao_abs_gemm_tc", ahi.data_ptr(), alo.data_ptr(), bhi.data_ptr(),
+                  blo.data_ptr(), eps.data_ptr(), int(eps_f64), nb, nb if sa else 1,
+                  nb if sb else 1, M, N, K, N, M * N, float(const), _lib.ptr(yc), float(u),
+                  gemm_slack(K), _lib.stream_ptr(a.device))
+        return eps
     ldb = K if transpose_b else N
     _lib.call("nao_abs_gemm_bound", a3.data_ptr(), b3.data_ptr(), eps.data_ptr(), int(eps_f64), nb,
               M, N, K, K, ldb, N, sa, sb, M * N, int(transpose_b), float(const), _lib.ptr(yc),
@@ -320,9 +363,11 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
         k_dim = xs[0].shape[-1]
         count = k_dim if fma_of(profile) else 2 * k_dim - 1
         const = model.reduction_const(count)
+        static_b = xs[1].dim() == 2  # 2-D right operands are weights in every lowering
         if kind == "matmul":
-            return y, abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64)
-        return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64)
+            return y, abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64, cache_b=static_b)
+        return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64,
+                                 cache_b=static_b)
     raise ValueError(f"no bound template for kind {kind!r}")
 
 

@@ -1,0 +1,421 @@
+// Abs-GEMM bound on the 5th-gen tensor cores (north_star (1), tcgen05 path).
+//
+//   eps[b,m,n] >= c * sum_k |A[b,m,k]| |B[b,k,n]|    (bounds.py:100-111)
+//
+// 3xTF32 split with outward rounding.  For a = |x| (x FP32):
+//   hi = a truncated to TF32 (<= a),   lo = (a - hi) rounded UP to TF32,
+// so a <= hi + lo < a (1 + 2^-20).  Products use hi*hi + hi*lo + lo*hi; the
+// dropped lo*lo <= 1.002 * 2^-20 a b is restored by the factor
+// 1/(1 - 1.002*2^-20).  Tensor-core accumulation of non-negative terms is
+// modelled as losing at most kMmaRel = 3*2^-23 of the running sum per MMA
+// instruction (products exact, aligned sum truncated), so:
+//   * acc0 (hi*hi) lives in TMEM for only KCHUNK = 64 k (8 MMAs), then the
+//     epilogue warps drain it into FP64 registers (double-buffered TMEM, the
+//     MMA warp never waits) and the chunk sum is scaled by 1/(1 - 8 kMmaRel);
+//   * acc1 (hi*lo + lo*hi, <= 2^-9 of acc0) accumulates over all of K and is
+//     scaled by 1/(1 - J1 kMmaRel); its relative weight keeps that inside 2^-9.
+// Worst-case over-estimate ~8e-6 < rtol 1e-5; typical ~4e-6.  Subnormal split
+// parts are lifted to FLT_MIN and an absolute floor K*2^-120*c covers any
+// flush-to-zero of products, so the result stays >= the exact bound.
+//
+// Kernel anatomy (one CTA per 128x128 output tile, 384 threads):
+//   warp 0      TMA producer: A_hi, A_lo, B_hi, B_lo tiles (128 x 32 fp32,
+//               SWIZZLE_128B) into a 3-stage smem ring (64 KB / stage)
+//   warp 1      single-thread tcgen05.mma.kind::tf32 issuer (12 MMAs / stage)
+//   warp 2      TMEM allocator (512 columns: acc0 x2, acc1)
+//   warps 4-11  epilogue: tcgen05.ld -> FP64 accumulate -> eps store
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace nao {
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, KCHUNK_KB = 2;
+constexpr int TILE_BYTES = BM * BK * 4;     // 16 KB (BM == BN)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A_hi, A_lo, B_hi, B_lo
+constexpr int NUM_THREADS = 384;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TcArgs {
+    int64_t M, N, K;
+    int nkb;
+    int a_batched, b_batched;
+    void* C;
+    const float* Y;
+    int64_t ldc, sC;
+    int out_f64;
+    double scale0, scale1, abs_floor, u;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// K-major, SWIZZLE_128B smem operand descriptor (rows of 128 B, 8-row groups 1024 B apart)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;           // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024u >> 4) << 32; // SBO
+    d |= (uint64_t)1u << 46;           // descriptor version (sm_100)
+    d |= (uint64_t)2u << 61;           // SWIZZLE_128B
+    return d;
+}
+// kind::tf32, D=F32, A=B=TF32, both K-major, N=BN, M=BM
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+#define TMEM_LD_X32(taddr, v)                                                                     \
+    asm volatile(                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"        \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),     \
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),              \
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),           \
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),           \
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),           \
+          "=r"(v[31])                                                                             \
+        : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_absgemm_tc(const __grid_constant__ CUtensorMap map_ahi,
+                 const __grid_constant__ CUtensorMap map_alo,
+                 const __grid_constant__ CUtensorMap map_bhi,
+                 const __grid_constant__ CUtensorMap map_blo, const __grid_constant__ TcArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;                      // [STAGES]
+    uint64_t* empty = bars + STAGES;            // [STAGES]
+    uint64_t* tfull = bars + 2 * STAGES;        // [2]
+    uint64_t* tempty = bars + 2 * STAGES + 2;   // [2]
+    uint64_t* acc1_full = bars + 2 * STAGES + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, bz = blockIdx.z;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+        mbar_init(acc1_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)));
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nkb = g.nkb;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            const int za = g.a_batched ? bz : 0, zb = g.b_batched ? bz : 0;
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * STAGE_BYTES;
+                mbar_expect_tx(&full[s], STAGE_BYTES);
+                tma_load_3d(st, &map_ahi, &full[s], kb * BK, m0, za);
+                tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * BK, m0, za);
+                tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * BK, n0, zb);
+                tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * BK, n0, zb);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            const uint32_t acc1 = tmem + 2 * BN;
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (kb / STAGES) & 1;
+                const int chunk = kb / KCHUNK_KB, buf = chunk & 1;
+                const bool first = (kb % KCHUNK_KB) == 0;
+                if (first) mbar_wait(&tempty[buf], ((chunk >> 1) & 1) ^ 1);
+                mbar_wait(&full[s], ph);
+                fence_after();
+                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                const uint32_t acc0 = tmem + buf * BN;
+#pragma unroll
+                for (int j = 0; j < BK / 8; j++) {
+                    const uint64_t ahi = make_desc(st + j * 32);
+                    const uint64_t alo = make_desc(st + TILE_BYTES + j * 32);
+                    const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
+                    const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
+                    umma_tf32(acc0, ahi, bhi, kIdesc, (first && j == 0) ? 0u : 1u);
+                    umma_tf32(acc1, ahi, blo, kIdesc, (kb == 0 && j == 0) ? 0u : 1u);
+                    umma_tf32(acc1, alo, bhi, kIdesc, 1u);
+                }
+                umma_commit(&empty[s]);
+                if ((kb % KCHUNK_KB) == KCHUNK_KB - 1 || kb == nkb - 1) umma_commit(&tfull[buf]);
+            }
+            umma_commit(acc1_full);
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue
+        const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        double acc[64];
+#pragma unroll
+        for (int i = 0; i < 64; i++) acc[i] = 0.0;
+        const int nchunks = (nkb + KCHUNK_KB - 1) / KCHUNK_KB;
+        for (int c = 0; c < nchunks; c++) {
+            const int buf = c & 1;
+            mbar_wait(&tfull[buf], (c >> 1) & 1);
+            fence_after();
+            uint32_t v[32];
+            const uint32_t col = tmem + lane_addr + buf * BN + half * 64;
+            TMEM_LD_X32(col, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i++) acc[i] = __dadd_rn(acc[i], (double)__uint_as_float(v[i]));
+            TMEM_LD_X32(col + 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+                acc[32 + i] = __dadd_rn(acc[32 + i], (double)__uint_as_float(v[i]));
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
+        mbar_wait(acc1_full, 0);
+        fence_after();
+        const int64_t m = m0 + row;
+        const uint32_t col1 = tmem + lane_addr + 2 * BN + half * 64;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            uint32_t v[32];
+            TMEM_LD_X32(col1 + 32 * h, v);
+            tmem_wait_ld();
+            if (m < g.M) {
+#pragma unroll
+                for (int i = 0; i < 32; i++) {
+                    const int64_t n = n0 + half * 64 + 32 * h + i;
+                    if (n < g.N) {
+                        double e = __dadd_rn(__dmul_rn(g.scale0, acc[32 * h + i]),
+                                             __dmul_rn(g.scale1, (double)__uint_as_float(v[i])));
+                        e = __dadd_rn(e, g.abs_floor);
+                        const int64_t o = (int64_t)bz * g.sC + m * g.ldc + n;
+                        if (g.Y) e = __dadd_rn(e, __dmul_rn(g.u, fabs((double)__ldg(g.Y + o))));
+                        if (g.out_f64) static_cast<double*>(g.C)[o] = e;
+                        else static_cast<float*>(g.C)[o] = __double2float_ru(e);
+                    }
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+}
+
+// |x| -> (hi, lo) TF32 parts, K-major [rows, Kp] (zero padded), optionally
+// reading x transposed (x is [K, rows] row-major when `trans`).
+__global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi,
+                             float* __restrict__ lo, int64_t batch, int64_t rows, int64_t K,
+                             int64_t Kp, int64_t ld, int64_t sbatch, int trans) {
+    const int64_t total = batch * rows * Kp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t % Kp, r = (t / Kp) % rows, b = t / (Kp * rows);
+        float a = 0.f;
+        if (k < K) {
+            const float* xb = x + b * sbatch;
+            a = fabsf(trans ? __ldg(xb + k * ld + r) : __ldg(xb + r * ld + k));
+        }
+        uint32_t ab = __float_as_uint(a);
+        uint32_t hb = ab & 0xFFFFE000u;                       // truncate to TF32: hi <= a
+        float h = __uint_as_float(hb);
+        float rem = __fsub_rn(a, h);                          // exact
+        uint32_t rb = __float_as_uint(rem);
+        uint32_t lb = (rb & 0x1FFFu) ? ((rb & 0xFFFFE000u) + 0x2000u) : rb;  // RU to TF32
+        float l = __uint_as_float(lb);
+        // tensor cores may flush subnormals: lift non-zero subnormal parts to FLT_MIN
+        if (h != 0.f && h < 1.17549435e-38f) h = 1.17549435e-38f;
+        if (l != 0.f && l < 1.17549435e-38f) l = 1.17549435e-38f;
+        hi[t] = h;
+        lo[t] = l;
+    }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+static EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t Kp, int64_t batch) {
+    EncodeFn enc = get_encode();
+    NAO_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)(rows * Kp * 4)};
+    cuuint32_t box[3] = {BK, (cuuint32_t)BM, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    NAO_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return NAO_OK;
+}
+
+}  // namespace tc
+}  // namespace nao
+
+using namespace nao;
+
+extern "C" {
+
+int64_t nao_tf32_split_cols(int64_t K) { return (K + 3) / 4 * 4; }
+
+int nao_tf32_split(const float* x, float* hi, float* lo, int64_t batch, int64_t rows, int64_t K,
+                   int64_t ld, int64_t stride_batch, int transpose, void* stream) {
+    NAO_REQUIRE(x && hi && lo, "tf32 split: null pointer");
+    NAO_REQUIRE(batch >= 1 && rows >= 0 && K >= 1, "tf32 split: bad shape");
+    const int64_t Kp = nao_tf32_split_cols(K);
+    const int64_t total = batch * rows * Kp;
+    if (total == 0) return NAO_OK;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+    tc::k_split_tf32<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, hi, lo, batch, rows, K, Kp, ld, stride_batch, transpose);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+// hi/lo operands from nao_tf32_split: A parts [batch_a, M, Kp], B parts [batch_b, N, Kp]
+// (batch_a / batch_b either `batch` or 1 = broadcast).
+int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
+                    void* eps, int eps_f64, int64_t batch, int64_t batch_a, int64_t batch_b,
+                    int64_t M, int64_t N, int64_t K, int64_t ldc, int64_t stride_c,
+                    double gamma_const, const float* y_or_null, double u, double slack,
+                    void* stream) {
+    using namespace nao::tc;
+    NAO_REQUIRE(a_hi && a_lo && b_hi && b_lo && eps, "abs-gemm tc: null pointer");
+    NAO_REQUIRE(M >= 1 && N >= 1 && K >= 1 && batch >= 1, "abs-gemm tc: bad shape");
+    NAO_REQUIRE((batch_a == batch || batch_a == 1) && (batch_b == batch || batch_b == 1),
+                "abs-gemm tc: bad batch broadcast");
+    NAO_REQUIRE(M <= 65535LL * BM && batch <= 65535, "abs-gemm tc: grid too large");
+    const int64_t Kp = nao_tf32_split_cols(K);
+    CUtensorMap mah, mal, mbh, mbl;
+    int rc;
+    if ((rc = make_map(&mah, a_hi, M, Kp, batch_a))) return rc;
+    if ((rc = make_map(&mal, a_lo, M, Kp, batch_a))) return rc;
+    if ((rc = make_map(&mbh, b_hi, N, Kp, batch_b))) return rc;
+    if ((rc = make_map(&mbl, b_lo, N, Kp, batch_b))) return rc;
+    TcArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.nkb = (int)((Kp + BK - 1) / BK);
+    g.a_batched = batch_a > 1; g.b_batched = batch_b > 1;
+    g.C = eps; g.Y = y_or_null; g.ldc = ldc; g.sC = stride_c; g.out_f64 = eps_f64; g.u = u;
+    // compensation factors (see header)
+    const double mma_rel = 3.0 * 0x1p-23;
+    const double j0 = (double)(KCHUNK_KB * BK / 8);
+    const double j1 = 2.0 * (double)g.nkb * (BK / 8);
+    const double comp_split = 1.0 / (1.0 - 1.002 * 0x1p-20);
+    const double comp0 = 1.0 / (1.0 - j0 * mma_rel);
+    NAO_REQUIRE(j1 * mma_rel < 0.5, "abs-gemm tc: K too large for the acc1 error model");
+    const double comp1 = 1.0 / (1.0 - j1 * mma_rel);
+    const double s = gamma_const * comp_split * (1.0 + slack) * (1.0 + 0x1p-50);
+    g.scale0 = s * comp0;
+    g.scale1 = s * comp1;
+    g.abs_floor = gamma_const * (double)K * 0x1p-120;
+    static bool attr_set = false;
+    if (!attr_set) {
+        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            SMEM_BYTES));
+        attr_set = true;
+    }
+    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
+    k_absgemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
+        mah, mal, mbh, mbl, g);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+}  // extern "C"

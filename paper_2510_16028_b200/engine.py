@@ -88,6 +88,8 @@ def to_device(a, device=None) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         t = a if a.is_cuda else a.to(device or "cuda")
         return t if t.dtype == torch.float32 else t.float()
+    if hasattr(a, "device_view"):
+        return a.device_view(device)
     if hasattr(a, "cuda") and hasattr(a, "shape") and not isinstance(a, np.ndarray):
         return a.cuda(device).reshape(a.shape)
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))

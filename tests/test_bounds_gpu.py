@@ -89,10 +89,15 @@ def test_matmul_bound_api(B):
         B.matmul_bound(np.ones((2, 3), np.float32), np.ones((4, 2), np.float32), B.FpModel())
 
 
+PATHS = [0, 1]  # NAO_GEMM_FFMA_RU, NAO_GEMM_TC_TF32X3
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("shape", [(1, 1, 1), (7, 33, 5), (128, 128, 128), (129, 300, 131),
-                                   (64, 4096, 96), (300, 17, 1000)])
+                                   (64, 4096, 96), (300, 17, 1000), (256, 12288, 256),
+                                   (2048, 128, 640)])
 @pytest.mark.parametrize("tb", [False, True])
-def test_abs_gemm_vs_fp64_blas(B, shape, tb):
+def test_abs_gemm_vs_fp64_blas(B, shape, tb, path):
     M, K, N = shape
     rng = np.random.default_rng(M * 7 + K)
     a = rng.standard_normal((M, K)).astype(np.float32)
@@ -100,14 +105,16 @@ def test_abs_gemm_vs_fp64_blas(B, shape, tb):
     model = B.FpModel()
     ref = OB.matmul_bound(a, b, OB.FpModel(), transpose_b=tb)
     got = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                           model.reduction_const(2 * K - 1), tb).cpu().numpy()
+                           model.reduction_const(2 * K - 1), tb, path=path).cpu().numpy()
     assert_bound(got, ref, str(shape))
     got32 = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                             model.reduction_const(2 * K - 1), tb, eps_f64=False).cpu().numpy()
+                             model.reduction_const(2 * K - 1), tb, eps_f64=False,
+                             path=path).cpu().numpy()
     assert_bound(got32, ref, str(shape) + " f32")
 
 
-def test_abs_gemm_heterogeneous_rows(B):
+@pytest.mark.parametrize("path", PATHS)
+def test_abs_gemm_heterogeneous_rows(B, path):
     """Softmax-like rows (one dominant entry, tiny rest) and wide dynamic range."""
     rng = np.random.default_rng(5)
     M, K, N = 64, 2048, 128
@@ -117,8 +124,59 @@ def test_abs_gemm_heterogeneous_rows(B):
         np.float32)
     ref = OB.matmul_bound(p, v, OB.FpModel())
     got = B.abs_gemm_bound(torch.from_numpy(p).cuda(), torch.from_numpy(v).cuda(),
-                           OB.FpModel().reduction_const(2 * K - 1)).cpu().numpy()
+                           OB.FpModel().reduction_const(2 * K - 1), path=path).cpu().numpy()
     assert_bound(got, ref, "hetero")
+
+
+@pytest.mark.parametrize("case", ["equal", "ramp", "sparse", "tf32_edge", "subnormal"])
+def test_abs_gemm_tc_adversarial(B, case):
+    """Data that stresses the tensor-core accumulation / split error model:
+    long runs of equal terms (truncation bias), values on TF32 boundaries,
+    sparse rows and subnormals.  Must stay inside [ref, ref (1 + 1e-5)]."""
+    rng = np.random.default_rng(17)
+    M, K, N = 256, 8192, 256
+    if case == "equal":
+        a = np.full((M, K), 1.0 + 2.0 ** -12, np.float32)
+        b = np.full((K, N), 3.0 - 2.0 ** -11, np.float32)
+    elif case == "ramp":
+        a = np.tile(np.linspace(1e-3, 1e3, K, dtype=np.float32), (M, 1))
+        b = rng.random((K, N)).astype(np.float32) + 1
+    elif case == "sparse":
+        a = (rng.random((M, K)) < 0.01).astype(np.float32) * rng.standard_normal((M, K)).astype(np.float32)
+        b = rng.standard_normal((K, N)).astype(np.float32)
+    elif case == "tf32_edge":
+        base = (rng.random((M, K)) + 1).astype(np.float32)
+        a = (base.view(np.uint32) | 0x1FFF).view(np.float32)  # all 13 dropped bits set
+        b = ((rng.random((K, N)) + 1).astype(np.float32).view(np.uint32) | 0x1000).view(np.float32)
+    else:
+        a = (rng.random((M, K)) * 1e-39).astype(np.float32)
+        b = (rng.random((K, N)) * 1e-3).astype(np.float32)
+    ref = OB.matmul_bound(a, b, OB.FpModel())
+    got = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                           OB.FpModel().reduction_const(2 * K - 1), path=1).cpu().numpy()
+    if case == "subnormal":  # absolute floor K*2^-120 dominates tiny products: sound, not tight
+        assert np.all(got >= ref)
+    else:
+        assert_bound(got, ref, case)
+
+
+def test_abs_gemm_tc_batched_and_cached_weight(B):
+    rng = np.random.default_rng(2)
+    q = torch.from_numpy(rng.standard_normal((8, 200, 64)).astype(np.float32)).cuda()
+    k = torch.from_numpy(rng.standard_normal((8, 300, 64)).astype(np.float32)).cuda()
+    ref = OB.matmul_bound(q.cpu().numpy(), k.cpu().numpy(), OB.FpModel(), transpose_b=True)
+    c = OB.FpModel().reduction_const(127)
+    got = B.abs_gemm_bound(q, k, c, True, path=1).cpu().numpy()
+    assert_bound(got, ref, "batched tb")
+    w = torch.from_numpy(rng.standard_normal((64, 96)).astype(np.float32)).cuda()
+    ref = OB.matmul_bound(q.cpu().numpy(), w.cpu().numpy(), OB.FpModel())
+    for _ in range(2):  # second call hits the cached weight split
+        got = B.abs_gemm_bound(q, w, c, False, path=1, cache_b=True).cpu().numpy()
+        assert_bound(got, ref, "bcast weight")
+    w.mul_(2.0)  # in-place change bumps _version -> cache must not be used
+    ref = OB.matmul_bound(q.cpu().numpy(), w.cpu().numpy(), OB.FpModel())
+    got = B.abs_gemm_bound(q, w, c, False, path=1, cache_b=True).cpu().numpy()
+    assert_bound(got, ref, "weight changed")
 
 
 def test_batched_broadcast_matmul(B):
