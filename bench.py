@@ -37,6 +37,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 METRIC = "bounds+check+commit overhead % vs FP32 fwd (Qwen3-8B shape); Merkle GB/s"
 UNIT = "%"
+PCT = (0.0, 1.0) + tuple(float(p) for p in range(5, 100, 5)) + (99.0, 100.0)
 
 
 def _peaks():
@@ -320,7 +321,9 @@ def run_ours(args):
         if r.n_violations:
             viol_nodes.append(names[i] if i < len(names) else i)
         if r.threshold_exceeded:
-            exceed_nodes.append(names[i] if i < len(names) else i)
+            g_idx = r.first_exceeded
+            where = (f"abs@p{PCT[g_idx]}" if g_idx < len(PCT) else f"rel@p{PCT[g_idx - len(PCT)]}")
+            exceed_nodes.append(f"{names[i] if i < len(names) else i}:{where}")
 
     overhead = 100.0 * (t_ver - t_plain) / t_plain
     peaks = _peaks()

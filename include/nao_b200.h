@@ -99,7 +99,10 @@ typedef struct nao_check_result {
 /* One pass over (local, claimed[, eps]) per operator: bound violations and
  * the exact p_max > 1 verdict of observed_p_max against (tau_abs, tau_rel) on
  * the percentile grid (calibration.py:16, dispute.py:114-141).  grid/tau are
- * host arrays of n_grid (<= 32) doubles; result is a device pointer. */
+ * host arrays of n_grid (<= 32) doubles; result is a device pointer.  Single
+ * launch: the last CTA finalizes.  The workspace (nao_check_workspace() bytes)
+ * is a dedicated accumulator that must be zero before its first use; every
+ * call leaves it zeroed again (do not share it with other entry points). */
 size_t nao_check_workspace(void);
 int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind, const void* eps,
               double eps_scale, double lo_factor, const double* grid, const double* tau_abs,

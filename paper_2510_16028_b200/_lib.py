@@ -192,3 +192,15 @@ def workspace(nbytes: int, device) -> torch.Tensor:
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
         _ws[key] = buf
     return buf
+
+
+def check_accumulator(device) -> torch.Tensor:
+    """Dedicated zero-initialised nao_check accumulator per (device, stream);
+    every nao_check call leaves it zeroed (include/nao_b200.h)."""
+    dev = torch.device(device)
+    key = ("check", dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws.get(key)
+    if buf is None:
+        buf = torch.zeros(int(load().nao_check_workspace()), dtype=torch.uint8, device=dev)
+        _ws[key] = buf
+    return buf

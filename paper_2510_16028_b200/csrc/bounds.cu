@@ -322,6 +322,11 @@ static int row_grid(int64_t rows) { return (int)ceil_div(rows, 32 * kRowWarps); 
 
 }  // namespace nao
 
+namespace nao { namespace rowb {
+static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                  int kind, float ln_eps, double u, double rc, double slack, cudaStream_t st);
+} }
+
 using namespace nao;
 
 extern "C" {
@@ -331,6 +336,11 @@ int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t 
     NAO_REQUIRE(rows >= 0 && n > 0, "softmax: cannot reduce an empty axis");
     NAO_REQUIRE(x && y && eps, "softmax: null pointer");
     if (rows == 0) return NAO_OK;
+    {
+        int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 0, 0.f, u, rc, slack,
+                                static_cast<cudaStream_t>(stream));
+        if (rc_b >= 0) return rc_b;
+    }
     k_softmax<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
         x, y, eps, eps_f64, rows, n, u, rc, slack);
     NAO_CHECK_LAUNCH();
@@ -342,6 +352,11 @@ int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_
     NAO_REQUIRE(rows >= 0 && n > 0, "layernorm: cannot reduce an empty axis");
     NAO_REQUIRE(x && y && eps, "layernorm: null pointer");
     if (rows == 0) return NAO_OK;
+    {
+        int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 1, ln_eps, u, rc, slack,
+                                static_cast<cudaStream_t>(stream));
+        if (rc_b >= 0) return rc_b;
+    }
     k_layernorm<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
         x, y, eps, eps_f64, rows, n, ln_eps, u, rc, slack);
     NAO_CHECK_LAUNCH();
@@ -353,6 +368,11 @@ int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t r
     NAO_REQUIRE(rows >= 0 && n > 0, "cannot reduce an empty axis");
     NAO_REQUIRE(kind >= NAO_RED_SUM && kind <= NAO_RED_MIN, "bad reduce kind %d", kind);
     if (rows == 0) return NAO_OK;
+    {
+        int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 2 + kind, 0.f, u, rc, slack,
+                                static_cast<cudaStream_t>(stream));
+        if (rc_b >= 0) return rc_b;
+    }
     k_reduce_rows<<<row_grid(rows), 32 * kRowWarps, 0, static_cast<cudaStream_t>(stream)>>>(
         x, y, eps, eps_f64, rows, n, kind, u, rc, slack);
     NAO_CHECK_LAUNCH();
@@ -410,3 +430,239 @@ extern "C" int nao_inject_drift(const float* y, float* out, int64_t n, uint32_t 
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }
+
+// ------------------------------------------------------------------------
+// Row kernels, design B (few rows / long rows): a CTA stages R whole rows in
+// shared memory (one DRAM read of x), one thread per row runs the profile's
+// left fold (the only serial part), and every order-free piece -- max, FP64
+// template sums, the elementwise value/bound epilogue -- is spread over all
+// 256 threads.  DRAM traffic = read x + write y + write eps.
+namespace nao {
+namespace rowb {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (kThreads / 32) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+    }
+    if (threadIdx.x == 0) red[0] = t;
+    __syncthreads();
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// kind: 0 softmax, 1 layernorm, 2 sum, 3 mean, 4 max, 5 min
+__global__ void __launch_bounds__(kThreads) k_rows_smem(
+    const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+    int64_t rows, int64_t n, int R, int kind, float ln_eps, double u, double rc, double slack) {
+    extern __shared__ __align__(16) float sx[];       // [R][n] x, then [R][n] e (softmax)
+    __shared__ double red[kThreads / 32];
+    __shared__ float s_a[32], s_b[32];                // per-row FP32 scalars
+    __shared__ double s_d0[32], s_d1[32];             // per-row FP64 scalars
+    const int64_t r0 = (int64_t)blockIdx.x * R;
+    const int nr = (int)((rows - r0) < R ? (rows - r0) : R);
+    float* se = sx + (size_t)R * n;
+    // stage rows (coalesced, vectorised when aligned)
+    const int64_t total = (int64_t)nr * n;
+    const float* xb = x + r0 * n;
+    if (((reinterpret_cast<uintptr_t>(xb) | (n * 4)) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(xb);
+        float4* s4 = reinterpret_cast<float4*>(sx);
+        for (int64_t i = threadIdx.x; i < total / 4; i += kThreads) s4[i] = __ldg(x4 + i);
+    } else {
+        for (int64_t i = threadIdx.x; i < total; i += kThreads) sx[i] = __ldg(xb + i);
+    }
+    __syncthreads();
+    const double two_u = __dmul_rn(2.0, u);
+    for (int r = 0; r < nr; r++) {
+        const float* row = sx + (size_t)r * n;
+        if (kind == 0) {  // ---- softmax: max (order free), e = fp32(exp64(x-m))
+            float m = -INFINITY;
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) m = fmaxf(m, row[c]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = (double)m;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float mm = -INFINITY;
+                for (int i = 0; i < kThreads / 32; i++) mm = fmaxf(mm, (float)red[i]);
+                s_a[r] = mm;
+                s_b[r] = mm;  // kept for the epilogue (s_a is reused by the fold)
+            }
+            __syncthreads();
+            m = s_a[r];
+            const double m64a = fabs((double)m);
+            double se_part = 0.0, seps_part = 0.0;
+            float* erow = se + (size_t)r * n;
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) {
+                const float xv = row[c];
+                const float ev = (float)exp((double)__fsub_rn(xv, m));
+                erow[c] = ev;
+                const double e64 = (double)ev;
+                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
+                se_part = __dadd_rn(se_part, e64);
+                seps_part = __dadd_rn(seps_part, __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64)));
+            }
+            const double s_e = block_sum(se_part, red);
+            const double s_eps = block_sum(seps_part, red);
+            if (threadIdx.x == 0) s_d0[r] = __dadd_rn(__dmul_rn(rc, s_e), __dmul_rn(__dadd_rn(rc, 1.0), s_eps));
+        } else if (kind == 1) {  // ---- layernorm: FP64 sum |x| (order free)
+            double sa = 0.0;
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) sa = __dadd_rn(sa, fabs((double)row[c]));
+            sa = block_sum(sa, red);
+            if (threadIdx.x == 0) s_d0[r] = sa;
+        } else if (kind <= 3) {
+            double sa = 0.0;
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) sa = __dadd_rn(sa, fabs((double)row[c]));
+            sa = block_sum(sa, red);
+            if (threadIdx.x == 0) s_d0[r] = sa;
+        }
+    }
+    __syncthreads();
+    // serial profile folds: thread r owns row r
+    if (threadIdx.x < nr) {
+        const int r = threadIdx.x;
+        const float* row = (kind == 0 ? se : sx) + (size_t)r * n;
+        float acc = row[0];
+        if (kind == 4) { for (int64_t c = 1; c < n; c++) acc = fmaxf(acc, row[c]); }
+        else if (kind == 5) { for (int64_t c = 1; c < n; c++) acc = fminf(acc, row[c]); }
+        else {
+#pragma unroll 8
+            for (int64_t c = 1; c < n; c++) acc = __fadd_rn(acc, row[c]);
+        }
+        if (kind == 1) {  // mu, then the second fold over sq = (x - mu)^2
+            const float mu = __fdiv_rn(acc, (float)n);
+            float xc0 = __fsub_rn(row[0], mu);
+            float acc2 = __fmul_rn(xc0, xc0);
+#pragma unroll 8
+            for (int64_t c = 1; c < n; c++) {
+                const float xc = __fsub_rn(row[c], mu);
+                acc2 = __fadd_rn(acc2, __fmul_rn(xc, xc));
+            }
+            s_a[r] = mu;
+            s_b[r] = acc2;
+        } else {
+            s_a[r] = acc;
+        }
+    }
+    __syncthreads();
+    if (kind >= 2) {  // reductions: one output per row
+        if (threadIdx.x < nr) {
+            const int r = threadIdx.x;
+            float out = s_a[r];
+            if (kind == 3) out = __fdiv_rn(out, (float)n);
+            y[r0 + r] = out;
+            double e = 0.0;
+            if (kind <= 3) {
+                e = __dmul_rn(rc, s_d0[r]);
+                if (kind == 3) e = __dadd_rn(__ddiv_rn(e, (double)n), __dmul_rn(u, fabs((double)out)));
+            }
+            if (eps) store_eps(eps, eps_f64, r0 + r, e, kind <= 3 ? slack : 0.0);
+        }
+        return;
+    }
+    const double nd = (double)n;
+    for (int r = 0; r < nr; r++) {
+        const float* row = sx + (size_t)r * n;
+        float* yrow = y + (r0 + r) * n;
+        const int64_t ob = (r0 + r) * n;
+        if (kind == 0) {
+            const float S = s_a[r];
+            const double S64 = (double)S, S2 = __dmul_rn(S64, S64), epsS = s_d0[r];
+            const float* erow = se + (size_t)r * n;
+            const double m64a = fabs((double)s_b[r]);
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) {
+                const float ev = erow[c];
+                const float yv = __fdiv_rn(ev, S);
+                yrow[c] = yv;
+                const double e64 = (double)ev;
+                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)row[c]), m64a));
+                const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+                const double v = __dadd_rn(__dadd_rn(__ddiv_rn(eps_e, S64),
+                                                     __ddiv_rn(__dmul_rn(e64, epsS), S2)),
+                                           __dmul_rn(u, fabs((double)yv)));
+                store_eps(eps, eps_f64, ob + c, v, slack);
+            }
+        } else {
+            // layernorm: FP64 chain (bounds.py:159-168), order-free sums over sq, eps_sq
+            const float mu = s_a[r];
+            const double eps_mu = __dadd_rn(__ddiv_rn(__dmul_rn(rc, s_d0[r]), nd),
+                                            __dmul_rn(u, fabs((double)mu)));
+            double ssq = 0.0, seps = 0.0;
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) {
+                const float xc = __fsub_rn(row[c], mu);
+                const float sq = __fmul_rn(xc, xc);
+                const double xc64 = fabs((double)xc), sq64 = (double)sq;
+                const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
+                ssq = __dadd_rn(ssq, sq64);
+                seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(__dmul_rn(2.0, xc64), eps_xc),
+                                                 __dmul_rn(u, sq64)));
+            }
+            ssq = block_sum(ssq, red);
+            seps = block_sum(seps, red);
+            const float var = __fdiv_rn(s_b[r], (float)n);
+            const float sp = __fadd_rn(var, ln_eps);
+            const float sigma = __fsqrt_rn(sp);
+            const double eps_ssq = __dadd_rn(__dmul_rn(rc, ssq), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+            const double eps_var = __dadd_rn(__ddiv_rn(eps_ssq, nd), __dmul_rn(u, fabs((double)var)));
+            const double eps_sp = __dadd_rn(eps_var, __dmul_rn(u, fabs((double)sp)));
+            const double sg64 = fabs((double)sigma), sg2 = __dmul_rn(sg64, sg64);
+            const double esg = __dadd_rn(__ddiv_rn(eps_sp, __dmul_rn(2.0, sg64)), __dmul_rn(u, sg64));
+            for (int64_t c = threadIdx.x; c < n; c += kThreads) {
+                const float xc = __fsub_rn(row[c], mu);
+                const float yv = __fdiv_rn(xc, sigma);
+                yrow[c] = yv;
+                const double xc64 = fabs((double)xc);
+                const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
+                const double v = __dadd_rn(__dadd_rn(__ddiv_rn(eps_xc, sg64),
+                                                     __ddiv_rn(__dmul_rn(xc64, esg), sg2)),
+                                           __dmul_rn(u, fabs((double)yv)));
+                store_eps(eps, eps_f64, ob + c, v, slack);
+            }
+        }
+    }
+}
+
+// rows per CTA for design B (0 = use the transposed-tile kernels)
+static int rows_per_cta(int64_t rows, int64_t n, int kind) {
+    const int64_t bufs = kind == 0 ? 2 : 1;
+    const int64_t per_row = bufs * n * 4;
+    const int64_t budget = 96 * 1024;
+    if (per_row > budget) return 0;
+    int64_t R = budget / per_row;
+    if (R > 32) R = 32;
+    // transposed-tile kernels win when there are enough rows to fill the GPU with warps
+    if (rows >= (int64_t)kNumSMs * 4 * 32 * 8 && n <= 2048 && kind != 1) return 0;
+    // keep >= 2 CTAs per SM worth of work when rows are few
+    while (R > 1 && ceil_div(rows, R) < 2 * kNumSMs) R >>= 1;
+    return (int)R;
+}
+
+static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                  int kind, float ln_eps, double u, double rc, double slack, cudaStream_t st) {
+    const int R = rows_per_cta(rows, n, kind);
+    if (R == 0) return -1;
+    const size_t smem = (size_t)(kind == 0 ? 2 : 1) * R * n * 4;
+    static bool attr = false;
+    if (!attr) {
+        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024));
+        attr = true;
+    }
+    k_rows_smem<<<(unsigned)ceil_div(rows, R), kThreads, smem, st>>>(x, y, eps, eps_f64, rows, n, R,
+                                                                     kind, ln_eps, u, rc, slack);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+}  // namespace rowb
+}  // namespace nao

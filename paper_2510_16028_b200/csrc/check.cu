@@ -28,14 +28,14 @@ namespace nao {
 
 constexpr int kMaxGrid = 32;
 
-struct CheckAccum {  // device scratch, zeroed per call
-    unsigned long long n_viol, n_border, n_nonfinite, n_amb_flag;
+struct CheckAccum {  // device scratch: zero on first use, left zeroed by every call
+    unsigned long long n_viol, n_border, n_nonfinite;
     unsigned long long hist_abs[kMaxGrid + 1];
     unsigned long long hist_rel[kMaxGrid + 1];
     unsigned long long max_ratio_bits;       // non-negative double
     unsigned long long amb_lo[2 * kMaxGrid];  // max key <= tau (double bits)
     unsigned long long amb_hi[2 * kMaxGrid];  // min key >  tau (double bits)
-    int amb_target[2 * kMaxGrid];             // 1 if target needs pass 2
+    unsigned int blocks_done;
 };
 
 struct CheckParams {
@@ -48,17 +48,13 @@ struct CheckParams {
     double lo_factor;   // borderline band
     double epsilon;     // relative-error guard (calibration.py:19)
     int G;
-    double t_abs[kMaxGrid];  // thresholds sorted ascending (host)
+    double t_abs[kMaxGrid];   // thresholds sorted ascending (host)
     double t_rel[kMaxGrid];
-};
-
-struct FinalParams {
-    int G;
-    int64_t n;
-    double grid[kMaxGrid];       // percentile grid (original order)
-    double tau_abs[kMaxGrid];    // effective thresholds, original order
+    // finalize (original grid order)
+    double grid[kMaxGrid];
+    double tau_abs[kMaxGrid];  // effective thresholds
     double tau_rel[kMaxGrid];
-    int lpos_abs[kMaxGrid];      // #{sorted t < tau_i}
+    int lpos_abs[kMaxGrid];    // #{sorted t < tau_i}
     int lpos_rel[kMaxGrid];
 };
 
@@ -85,168 +81,6 @@ __device__ __forceinline__ double rel_key(double diff, float y, double epsilon) 
     return __ddiv_rn(diff, __dadd_rn(fabs((double)y), epsilon));
 }
 
-struct SmemT {
-    double t_abs[kMaxGrid], t_rel[kMaxGrid];
-    float f_rel[kMaxGrid];
-    float f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];  // guard band edges
-    unsigned long long hist_abs[kMaxGrid + 1], hist_rel[kMaxGrid + 1];
-    unsigned long long viol, border, nonfin;
-    double maxr;
-};
-
-constexpr float kGuard = 1.0f / 524288.0f;  // 2^-19 relative guard for the FP32 fast path
-
-template <int EPSK>
-__device__ __forceinline__ double load_eps(const CheckParams& p, int64_t i, float y) {
-    if (EPSK == NAO_EPS_TENSOR_F32) return (double)__ldg(static_cast<const float*>(p.eps) + i);
-    if (EPSK == NAO_EPS_TENSOR_F64) return __ldg(static_cast<const double*>(p.eps) + i);
-    if (EPSK == NAO_EPS_SCALED_LOCAL) return __dmul_rn(p.eps_scale, fabs((double)y));
-    return 0.0;
-}
-
-template <int EPSK>
-__global__ void __launch_bounds__(256) k_check(const __grid_constant__ CheckParams p,
-                                               CheckAccum* __restrict__ acc) {
-    __shared__ SmemT sm;
-    const int G = p.G;
-    if (threadIdx.x < kMaxGrid) {
-        int i = threadIdx.x;
-        double ta = i < G ? p.t_abs[i] : INFINITY;
-        double tr = i < G ? p.t_rel[i] : INFINITY;
-        sm.t_abs[i] = ta;
-        sm.t_rel[i] = tr;
-        float fr = (float)tr;
-        sm.f_rel[i] = fr;
-        sm.f_rel_lo[i] = fr * (1.0f - kGuard);
-        sm.f_rel_hi[i] = fr * (1.0f + kGuard);
-    }
-    if (threadIdx.x <= kMaxGrid) { sm.hist_abs[threadIdx.x] = 0; sm.hist_rel[threadIdx.x] = 0; }
-    if (threadIdx.x == 0) { sm.viol = sm.border = sm.nonfin = 0; sm.maxr = 0.0; }
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    // warp-private interval counters (no atomics: one leader per distinct bucket)
-    __shared__ uint32_t wc[8][2][kMaxGrid + 1];
-    for (int b = lane; b <= kMaxGrid; b += 32) { wc[warp][0][b] = 0; wc[warp][1][b] = 0; }
-    __syncwarp();
-    unsigned long long viol = 0, border = 0, nonfin = 0;
-    double best_num = 0.0, best_den = 1.0;  // max ratio as a fraction
-    bool best_inf = false;
-
-    auto process = [&](bool valid, float y, float yc, double eps, int& pa, int& pr) {
-        pa = -1; pr = -1;
-        if (!valid) return;
-        if (!isfinite(y) || !isfinite(yc)) { nonfin++; viol++; pa = G; pr = G; return; }
-        const double diff = abs_key(y, yc);
-        if (diff > eps) viol++;
-        else if (diff > eps * p.lo_factor) border++;
-        // running max of diff/eps without a division per element
-        if (eps > 0.0) {
-            if (!best_inf && diff * best_den > best_num * eps) { best_num = diff; best_den = eps; }
-        } else if (diff > 0.0) {
-            best_inf = true;
-        }
-        if (diff == 0.0) { pa = 0; pr = 0; return; }
-        pa = bsearch_pos(sm.t_abs, G, diff);
-        // relative key: FP32 estimate, exact FP64 only inside the guard band
-        const float d32 = (float)diff;
-        const float den32 = __fadd_rn(fabsf(y), (float)p.epsilon);
-        const float r32 = __fdiv_rn(d32, den32);
-        int q = bsearch_pos32(sm.f_rel, G, r32);
-        bool safe = (d32 >= 1e-30f) && (r32 >= 1e-30f) && isfinite(r32) &&
-                    (q == G || r32 < sm.f_rel_lo[q]) && (q == 0 || r32 > sm.f_rel_hi[q - 1]);
-        if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, p.epsilon));
-        pr = q;
-    };
-
-    auto tally = [&](int pa, int pr) {
-        // common case: the whole warp lands in one bucket (e.g. all diffs zero)
-        const int a0 = __shfl_sync(0xffffffffu, pa, 0), r0 = __shfl_sync(0xffffffffu, pr, 0);
-        if (__all_sync(0xffffffffu, pa == a0 && pr == r0)) {
-            if (lane == 0 && a0 >= 0) { wc[warp][0][a0] += 32; wc[warp][1][r0] += 32; }
-        } else {
-            unsigned ma = __match_any_sync(0xffffffffu, pa);
-            unsigned mr = __match_any_sync(0xffffffffu, pr);
-            if (pa >= 0 && (__ffs(ma) - 1) == lane) wc[warp][0][pa] += __popc(ma);
-            __syncwarp();
-            if (pr >= 0 && (__ffs(mr) - 1) == lane) wc[warp][1][pr] += __popc(mr);
-            __syncwarp();
-        }
-        __syncwarp();
-    };
-
-    const int64_t n = p.n;
-    const int64_t nvec = n >> 2;
-    const float4* yl = reinterpret_cast<const float4*>(p.local);
-    const float4* yc = reinterpret_cast<const float4*>(p.claimed);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // warp-uniform trip count so every lane joins the ballots
-    const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
-    for (int64_t wb = base0; wb < nvec; wb += stride) {
-        const int64_t v = wb + lane;
-        const bool ok = v < nvec;
-        float4 a = ok ? __ldg(yl + v) : make_float4(0, 0, 0, 0);
-        float4 c = ok ? __ldg(yc + v) : make_float4(0, 0, 0, 0);
-        double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
-        if (ok) {
-            if (EPSK == NAO_EPS_TENSOR_F32) {
-                float4 e = __ldg(reinterpret_cast<const float4*>(p.eps) + v);
-                e0 = e.x; e1 = e.y; e2 = e.z; e3 = e.w;
-            } else if (EPSK == NAO_EPS_TENSOR_F64) {
-                const double2* ep = reinterpret_cast<const double2*>(p.eps);
-                double2 u0 = __ldg(ep + 2 * v), u1 = __ldg(ep + 2 * v + 1);
-                e0 = u0.x; e1 = u0.y; e2 = u1.x; e3 = u1.y;
-            } else if (EPSK == NAO_EPS_SCALED_LOCAL) {
-                e0 = __dmul_rn(p.eps_scale, fabs((double)a.x));
-                e1 = __dmul_rn(p.eps_scale, fabs((double)a.y));
-                e2 = __dmul_rn(p.eps_scale, fabs((double)a.z));
-                e3 = __dmul_rn(p.eps_scale, fabs((double)a.w));
-            }
-        }
-        int pa, pr;
-        process(ok, a.x, c.x, e0, pa, pr); tally(pa, pr);
-        process(ok, a.y, c.y, e1, pa, pr); tally(pa, pr);
-        process(ok, a.z, c.z, e2, pa, pr); tally(pa, pr);
-        process(ok, a.w, c.w, e3, pa, pr); tally(pa, pr);
-    }
-    // scalar tail (n % 4) handled by the first warp of block 0
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const int64_t i = (nvec << 2) + lane;
-        const bool ok = i < n;
-        float y = ok ? p.local[i] : 0.f, c = ok ? p.claimed[i] : 0.f;
-        double e = ok ? load_eps<EPSK>(p, i, y) : 0.0;
-        int pa, pr;
-        process(ok, y, c, e, pa, pr);
-        tally(pa, pr);
-    }
-    // reduce
-    viol = warp_sum(viol); border = warp_sum(border); nonfin = warp_sum(nonfin);
-    double r = best_inf ? INFINITY : (best_num > 0.0 ? best_num / best_den : 0.0);
-    r = warp_max(r);
-    for (int b = lane; b <= G; b += 32) {
-        if (wc[warp][0][b]) atomicAdd(&sm.hist_abs[b], (unsigned long long)wc[warp][0][b]);
-        if (wc[warp][1][b]) atomicAdd(&sm.hist_rel[b], (unsigned long long)wc[warp][1][b]);
-    }
-    if (lane == 0) {
-        atomicAdd(&sm.viol, viol);
-        atomicAdd(&sm.border, border);
-        atomicAdd(&sm.nonfin, nonfin);
-        atomic_max_nonneg(&sm.maxr, r);
-    }
-    __syncthreads();
-    if (threadIdx.x <= G) {
-        if (sm.hist_abs[threadIdx.x]) atomicAdd(&acc->hist_abs[threadIdx.x], sm.hist_abs[threadIdx.x]);
-        if (sm.hist_rel[threadIdx.x]) atomicAdd(&acc->hist_rel[threadIdx.x], sm.hist_rel[threadIdx.x]);
-    }
-    if (threadIdx.x == 0) {
-        if (sm.viol) atomicAdd(&acc->n_viol, sm.viol);
-        if (sm.border) atomicAdd(&acc->n_border, sm.border);
-        if (sm.nonfin) atomicAdd(&acc->n_nonfinite, sm.nonfin);
-        atomicMax(&acc->max_ratio_bits, (unsigned long long)__double_as_longlong(sm.maxr));
-    }
-}
-
 // numpy _lerp (_function_base_impl.py:4657-4679), no FMA contraction.
 __device__ __forceinline__ double np_lerp(double a, double b, double t) {
     double d = __dsub_rn(b, a);
@@ -270,94 +104,282 @@ __device__ __forceinline__ VIdx virtual_index(int64_t n, double p) {
     return v;
 }
 
-// phase: 0 = after pass 1 (decide / flag ambiguous), 1 = after pass 2.
-__global__ void k_check_finalize(const __grid_constant__ FinalParams fp, CheckAccum* acc,
-                                 nao_check_result* out, int phase) {
-    if (threadIdx.x != 0) return;
-    const int G = fp.G;
-    int exceeded = 0, first = -1, n_amb = 0;
-    for (int arr = 0; arr < 2; arr++) {
-        const unsigned long long* hist = arr == 0 ? acc->hist_abs : acc->hist_rel;
-        for (int i = 0; i < G; i++) {
-            const double tau = arr == 0 ? fp.tau_abs[i] : fp.tau_rel[i];
-            const int L = arr == 0 ? fp.lpos_abs[i] : fp.lpos_rel[i];
-            unsigned long long cle = 0;
-            for (int b = 0; b <= L; b++) cle += hist[b];
-            VIdx v = virtual_index(fp.n, fp.grid[i]);
-            bool ex;
-            if (v.last) {
-                ex = cle < (unsigned long long)fp.n;
-            } else if (cle <= (unsigned long long)v.prev) {
-                ex = true;
-            } else if (cle >= (unsigned long long)v.prev + 2) {
-                ex = false;
-            } else {  // x_(k) <= tau < x_(k+1): interpolate exactly
-                const int t = arr * kMaxGrid + i;
-                if (phase == 0) {
-                    acc->amb_target[t] = 1;
-                    acc->amb_lo[t] = 0ull;
-                    acc->amb_hi[t] = 0x7ff0000000000000ull;  // +inf
-                    n_amb++;
-                    ex = false;
-                } else {
-                    double a = __longlong_as_double((long long)acc->amb_lo[t]);
-                    double b = __longlong_as_double((long long)acc->amb_hi[t]);
-                    ex = np_lerp(a, b, v.g) > tau;
-                }
-            }
-            if (ex) {
-                exceeded = 1;
-                if (first < 0) first = arr * G + i;
-            }
-        }
-    }
-    if (phase == 0) acc->n_amb_flag = (unsigned long long)n_amb;
-    if (phase == 0 && n_amb > 0) return;  // pass 2 + phase-1 finalize complete the result
-    out->n = (uint64_t)fp.n;
-    out->n_violations = acc->n_viol;
-    out->n_borderline = acc->n_border;
-    out->n_nonfinite = acc->n_nonfinite;
-    out->max_ratio = __longlong_as_double((long long)acc->max_ratio_bits);
-    out->threshold_exceeded = exceeded;
-    out->first_exceeded = first;
-    out->n_ambiguous = (int32_t)acc->n_amb_flag;
+constexpr int kCheckThreads = 256, kCheckWarps = kCheckThreads / 32, kQ = 64;
+constexpr float kGuard = 1.0f / 524288.0f;  // 2^-19 relative guard for the FP32 fast path
+
+struct CheckSmem {
+    double t_abs[kMaxGrid], t_rel[kMaxGrid];
+    float f_rel[kMaxGrid], f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];
+    uint32_t wc[kCheckWarps][2][kMaxGrid + 1];   // warp-private interval counters
+    float qy[kCheckWarps][kQ], qc[kCheckWarps][kQ];  // warp compaction queue of
+    double qe[kCheckWarps][kQ];                      // non-zero differences
+    unsigned long long viol, border, nonfin;
+    double maxr;
+    // finalize
+    int amb[2 * kMaxGrid];
+    int n_amb, exceeded, first, is_last;
+    unsigned long long amb_lo[2 * kMaxGrid], amb_hi[2 * kMaxGrid];
+};
+
+template <int EPSK>
+__device__ __forceinline__ double load_eps(const CheckParams& p, int64_t i, float y) {
+    if (EPSK == NAO_EPS_TENSOR_F32) return (double)__ldg(static_cast<const float*>(p.eps) + i);
+    if (EPSK == NAO_EPS_TENSOR_F64) return __ldg(static_cast<const double*>(p.eps) + i);
+    if (EPSK == NAO_EPS_SCALED_LOCAL) return __dmul_rn(p.eps_scale, fabs((double)y));
+    return 0.0;
 }
 
-// Pass 2 (rare): for each ambiguous target, max key <= tau and min key > tau.
-__global__ void __launch_bounds__(256) k_check_pass2(const __grid_constant__ CheckParams p,
-                                                     const __grid_constant__ FinalParams fp,
-                                                     CheckAccum* __restrict__ acc) {
-    if (acc->n_amb_flag == 0) return;
-    __shared__ int targets[2 * kMaxGrid];
-    __shared__ double taus[2 * kMaxGrid];
-    __shared__ int nt;
-    if (threadIdx.x == 0) {
-        int c = 0;
-        for (int t = 0; t < 2 * kMaxGrid; t++)
-            if (acc->amb_target[t]) {
-                targets[c] = t;
-                taus[c] = (t < kMaxGrid) ? fp.tau_abs[t] : fp.tau_rel[t - kMaxGrid];
-                c++;
-            }
-        nt = c;
+// Decide every (array, grid point) from the interval histograms; returns the
+// number of ambiguous targets (k+1 keys <= tau) -- those need amb_lo / amb_hi.
+__device__ void finalize_targets(const CheckParams& p, CheckAccum* acc, CheckSmem& sm, bool phase2) {
+    const int G = p.G;
+    const int t = threadIdx.x;
+    if (t == 0) { sm.n_amb = 0; sm.exceeded = 0; sm.first = 0x7fffffff; }
+    __syncthreads();
+    if (t < 2 * G) {
+        const int arr = t / G, i = t % G;
+        const volatile unsigned long long* hist = arr == 0 ? acc->hist_abs : acc->hist_rel;
+        const double tau = arr == 0 ? p.tau_abs[i] : p.tau_rel[i];
+        const int L = arr == 0 ? p.lpos_abs[i] : p.lpos_rel[i];
+        unsigned long long cle = 0;
+        for (int b = 0; b <= L; b++) cle += hist[b];
+        const VIdx v = virtual_index(p.n, p.grid[i]);
+        bool ex;
+        if (v.last) ex = cle < (unsigned long long)p.n;
+        else if (cle <= (unsigned long long)v.prev) ex = true;
+        else if (cle >= (unsigned long long)v.prev + 2) ex = false;
+        else if (!phase2) { sm.amb[arr * kMaxGrid + i] = 1; atomicAdd(&sm.n_amb, 1); ex = false; }
+        else {
+            const double a = __longlong_as_double((long long)sm.amb_lo[arr * kMaxGrid + i]);
+            const double b = __longlong_as_double((long long)sm.amb_hi[arr * kMaxGrid + i]);
+            ex = np_lerp(a, b, v.g) > tau;
+        }
+        if (ex) { atomicOr(&sm.exceeded, 1); atomicMin(&sm.first, arr * G + i); }
     }
     __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float y = p.local[i], c = p.claimed[i];
-        double diff = abs_key(y, c);
-        double rel = rel_key(diff, y, p.epsilon);
-        for (int k = 0; k < nt; k++) {
-            int t = targets[k];
-            double key = t < kMaxGrid ? diff : rel;
-            unsigned long long bits = (unsigned long long)__double_as_longlong(key);
-            if (key <= taus[k]) atomicMax(&acc->amb_lo[t], bits);
-            else atomicMin(&acc->amb_hi[t], bits);
-        }
+}
+
+template <int EPSK>
+__global__ void __launch_bounds__(kCheckThreads) k_check(const __grid_constant__ CheckParams p,
+                                                         CheckAccum* __restrict__ acc,
+                                                         nao_check_result* __restrict__ out) {
+    __shared__ CheckSmem sm;
+    const int G = p.G;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < kMaxGrid) {
+        const int i = threadIdx.x;
+        const double ta = i < G ? p.t_abs[i] : INFINITY;
+        const double tr = i < G ? p.t_rel[i] : INFINITY;
+        sm.t_abs[i] = ta;
+        sm.t_rel[i] = tr;
+        const float fr = (float)tr;
+        sm.f_rel[i] = fr;
+        sm.f_rel_lo[i] = fr * (1.0f - kGuard);
+        sm.f_rel_hi[i] = fr * (1.0f + kGuard);
     }
+    if (threadIdx.x < 2 * kMaxGrid) { sm.amb[threadIdx.x] = 0; }
+    for (int b = lane; b <= kMaxGrid; b += 32) { sm.wc[w][0][b] = 0; sm.wc[w][1][b] = 0; }
+    if (threadIdx.x == 0) { sm.viol = sm.border = sm.nonfin = 0; sm.maxr = 0.0; sm.is_last = 0; }
+    __syncthreads();
+
+    unsigned long long viol = 0, border = 0, nonfin = 0;
+    double best_num = 0.0, best_den = 1.0;  // running max of diff/eps as a fraction
+    bool best_inf = false;
+    uint32_t nzero = 0;  // y' == y exactly: diff 0 -> bucket 0, never a violation
+
+    // exact processing of one non-zero difference (all lanes busy: no divergence)
+    auto process = [&](float y, float yc, double eps) {
+        if (!isfinite(y) || !isfinite(yc)) {
+            nonfin++; viol++;
+            atomicAdd(&sm.wc[w][0][G], 1u); atomicAdd(&sm.wc[w][1][G], 1u);
+            return;
+        }
+        const double diff = abs_key(y, yc);
+        if (diff > eps) viol++;
+        else if (diff > eps * p.lo_factor) border++;
+        if (eps > 0.0) {
+            if (!best_inf && diff * best_den > best_num * eps) { best_num = diff; best_den = eps; }
+        } else if (diff > 0.0) {
+            best_inf = true;
+        }
+        int pa = 0, q = 0;
+        if (diff != 0.0) {
+            pa = bsearch_pos(sm.t_abs, G, diff);
+            const float d32 = (float)diff;
+            const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)p.epsilon));
+            q = bsearch_pos32(sm.f_rel, G, r32);
+            const bool safe = (d32 >= 1e-30f) && (r32 >= 1e-30f) && isfinite(r32) &&
+                              (q == G || r32 < sm.f_rel_lo[q]) &&
+                              (q == 0 || r32 > sm.f_rel_hi[q - 1]);
+            if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, p.epsilon));
+        }
+        atomicAdd(&sm.wc[w][0][pa], 1u);
+        atomicAdd(&sm.wc[w][1][q], 1u);
+    };
+    int qn = 0;  // warp-uniform queue length
+    auto push = [&](bool flag, float y, float yc, double e) {
+        const unsigned m = __ballot_sync(0xffffffffu, flag);
+        if (m == 0) return;
+        if (flag) {
+            const int pos = qn + __popc(m & ((1u << lane) - 1u));
+            sm.qy[w][pos] = y; sm.qc[w][pos] = yc; sm.qe[w][pos] = e;
+        }
+        qn += __popc(m);
+        if (qn >= 32) {
+            __syncwarp();
+            process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane]);
+            __syncwarp();
+            if (lane < qn - 32) {
+                sm.qy[w][lane] = sm.qy[w][32 + lane];
+                sm.qc[w][lane] = sm.qc[w][32 + lane];
+                sm.qe[w][lane] = sm.qe[w][32 + lane];
+            }
+            __syncwarp();
+            qn -= 32;
+        }
+    };
+
+    const int64_t n = p.n;
+    const int64_t nvec = n >> 2;
+    const float4* yl = reinterpret_cast<const float4*>(p.local);
+    const float4* ycl = reinterpret_cast<const float4*>(p.claimed);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < nvec;
+         wb += stride) {  // warp-uniform trip count (ballots)
+        const int64_t v = wb + lane;
+        const bool ok = v < nvec;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+        if (ok) { a = __ldg(yl + v); c = __ldg(ycl + v); }
+        const bool z0 = (a.x == c.x) & isfinite(a.x), z1 = (a.y == c.y) & isfinite(a.y);
+        const bool z2 = (a.z == c.z) & isfinite(a.z), z3 = (a.w == c.w) & isfinite(a.w);
+        const bool all_eq = z0 & z1 & z2 & z3;
+        if (ok && all_eq) nzero += 4;
+        if (__all_sync(0xffffffffu, all_eq || !ok)) continue;
+        double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+        if (ok && !all_eq) {  // eps is only read where a difference exists
+            if (EPSK == NAO_EPS_TENSOR_F32) {
+                const float4 e = __ldg(reinterpret_cast<const float4*>(p.eps) + v);
+                e0 = e.x; e1 = e.y; e2 = e.z; e3 = e.w;
+            } else if (EPSK == NAO_EPS_TENSOR_F64) {
+                const double2* ep = reinterpret_cast<const double2*>(p.eps);
+                const double2 u0 = __ldg(ep + 2 * v), u1 = __ldg(ep + 2 * v + 1);
+                e0 = u0.x; e1 = u0.y; e2 = u1.x; e3 = u1.y;
+            } else if (EPSK == NAO_EPS_SCALED_LOCAL) {
+                e0 = __dmul_rn(p.eps_scale, fabs((double)a.x));
+                e1 = __dmul_rn(p.eps_scale, fabs((double)a.y));
+                e2 = __dmul_rn(p.eps_scale, fabs((double)a.z));
+                e3 = __dmul_rn(p.eps_scale, fabs((double)a.w));
+            }
+            if (z0) nzero++;
+            if (z1) nzero++;
+            if (z2) nzero++;
+            if (z3) nzero++;
+        }
+        const bool live = ok && !all_eq;
+        push(live && !z0, a.x, c.x, e0);
+        push(live && !z1, a.y, c.y, e1);
+        push(live && !z2, a.z, c.z, e2);
+        push(live && !z3, a.w, c.w, e3);
+    }
+    // scalar tail (n % 4): first warp of block 0
+    if (blockIdx.x == 0 && w == 0) {
+        const int64_t i = (nvec << 2) + lane;
+        const bool ok = i < n;
+        float y = 0.f, c = 0.f;
+        double e = 0.0;
+        if (ok) { y = p.local[i]; c = p.claimed[i]; e = load_eps<EPSK>(p, i, y); }
+        const bool z = (y == c) && isfinite(y);
+        if (ok && z) nzero++;
+        push(ok && !z, y, c, e);
+    }
+    __syncwarp();
+    if (lane < qn) process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane]);
+    __syncwarp();
+    if (nzero) { atomicAdd(&sm.wc[w][0][0], nzero); atomicAdd(&sm.wc[w][1][0], nzero); }
+
+    // ---- block reduction -> global accumulator
+    viol = warp_sum(viol); border = warp_sum(border); nonfin = warp_sum(nonfin);
+    double r = best_inf ? INFINITY : (best_num > 0.0 ? best_num / best_den : 0.0);
+    r = warp_max(r);
+    __syncwarp();
+    if (lane == 0) {
+        atomicAdd(&sm.viol, viol);
+        atomicAdd(&sm.border, border);
+        atomicAdd(&sm.nonfin, nonfin);
+        atomic_max_nonneg(&sm.maxr, r);
+    }
+    __syncthreads();
+    if (threadIdx.x <= G) {
+        unsigned long long ha = 0, hr = 0;
+        for (int ww = 0; ww < kCheckWarps; ww++) {
+            ha += sm.wc[ww][0][threadIdx.x];
+            hr += sm.wc[ww][1][threadIdx.x];
+        }
+        if (ha) atomicAdd(&acc->hist_abs[threadIdx.x], ha);
+        if (hr) atomicAdd(&acc->hist_rel[threadIdx.x], hr);
+    }
+    if (threadIdx.x == 0) {
+        if (sm.viol) atomicAdd(&acc->n_viol, sm.viol);
+        if (sm.border) atomicAdd(&acc->n_border, sm.border);
+        if (sm.nonfin) atomicAdd(&acc->n_nonfinite, sm.nonfin);
+        if (sm.maxr > 0.0)
+            atomicMax(&acc->max_ratio_bits, (unsigned long long)__double_as_longlong(sm.maxr));
+        __threadfence();
+        sm.is_last = atomicAdd(&acc->blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!sm.is_last) return;
+
+    // ---- last block: decide all 2G targets, settle ambiguous ones exactly
+    __threadfence();
+    finalize_targets(p, acc, sm, false);
+    if (sm.n_amb > 0) {
+        if (threadIdx.x < 2 * kMaxGrid) {
+            sm.amb_lo[threadIdx.x] = 0ull;
+            sm.amb_hi[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
+        }
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const float y = p.local[i], c = p.claimed[i];
+            const double diff = abs_key(y, c);
+            const double rel = rel_key(diff, y, p.epsilon);
+            for (int t = 0; t < 2 * G; t++) {
+                const int arr = t / G, gi = t % G;
+                if (!sm.amb[arr * kMaxGrid + gi]) continue;
+                const double key = arr == 0 ? diff : rel;
+                const double tau = arr == 0 ? p.tau_abs[gi] : p.tau_rel[gi];
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(key);
+                if (key <= tau) atomicMax(&sm.amb_lo[arr * kMaxGrid + gi], bits);
+                else atomicMin(&sm.amb_hi[arr * kMaxGrid + gi], bits);
+            }
+        }
+        __syncthreads();
+        finalize_targets(p, acc, sm, true);
+    }
+    if (threadIdx.x == 0) {
+        out->n = (uint64_t)n;
+        out->n_violations = acc->n_viol;
+        out->n_borderline = acc->n_border;
+        out->n_nonfinite = acc->n_nonfinite;
+        out->max_ratio = __longlong_as_double((long long)acc->max_ratio_bits);
+        out->threshold_exceeded = sm.exceeded;
+        out->first_exceeded = sm.exceeded ? sm.first : -1;
+        out->n_ambiguous = sm.n_amb;
+        out->reserved = 0;
+    }
+    __syncthreads();
+    // leave the accumulator zeroed for the next call on this stream
+    unsigned long long* z = reinterpret_cast<unsigned long long*>(acc);
+    for (int i = threadIdx.x; i < (int)(sizeof(CheckAccum) / 8); i += blockDim.x) z[i] = 0ull;
 }
 
 // ------------------------------------------------------- exact percentiles
+
+struct FinalParams {
+    int G;
+    int64_t n;
+    double grid[kMaxGrid];
+};
 
 __global__ void k_error_keys(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
                              double epsilon, unsigned long long* __restrict__ kabs,
@@ -449,50 +471,47 @@ int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind,
                 "local/claimed must be 16-byte aligned");
     NAO_REQUIRE(eps == nullptr || reinterpret_cast<uintptr_t>(eps) % 16 == 0,
                 "eps must be 16-byte aligned");
+    NAO_REQUIRE(n_grid > 0 && n_grid <= kMaxGrid, "grid size %d out of range (1..%d)", n_grid,
+                kMaxGrid);
     Workspace ws(workspace, workspace_bytes);
     CheckAccum* acc = ws.take<CheckAccum>(1);
     NAO_REQUIRE(acc != nullptr, "workspace too small");
-    FinalParams fp;
-    int rc = fill_grid(fp, grid, n_grid);
-    if (rc) return rc;
-    fp.n = n;
-    CheckParams p;
+    static thread_local CheckParams p;
     memset(&p, 0, sizeof p);
     p.local = local; p.claimed = claimed; p.eps = eps; p.n = n; p.eps_kind = eps_kind;
     p.eps_scale = eps_scale; p.lo_factor = lo_factor; p.epsilon = epsilon; p.G = n_grid;
     // effective thresholds: ratio obs/tau > 1  <=>  obs > tau (tau > 0) or obs > 0 (tau <= 0)
-    std::vector<double> ea(n_grid), er(n_grid);
+    double ea[kMaxGrid], er[kMaxGrid], sa[kMaxGrid], sr[kMaxGrid];
     for (int i = 0; i < n_grid; i++) {
-        ea[i] = tau_abs[i] > 0.0 ? tau_abs[i] : 0.0;
-        er[i] = tau_rel[i] > 0.0 ? tau_rel[i] : 0.0;
-        fp.tau_abs[i] = ea[i];
-        fp.tau_rel[i] = er[i];
+        NAO_REQUIRE(std::isfinite(grid[i]) && grid[i] >= 0.0 && grid[i] <= 100.0,
+                    "Percentiles must be in the range [0, 100]");
+        p.grid[i] = grid[i];
+        ea[i] = sa[i] = tau_abs[i] > 0.0 ? tau_abs[i] : 0.0;
+        er[i] = sr[i] = tau_rel[i] > 0.0 ? tau_rel[i] : 0.0;
+        p.tau_abs[i] = ea[i];
+        p.tau_rel[i] = er[i];
     }
-    std::vector<double> sa = ea, sr = er;
-    std::sort(sa.begin(), sa.end());
-    std::sort(sr.begin(), sr.end());
+    std::sort(sa, sa + n_grid);
+    std::sort(sr, sr + n_grid);
     for (int i = 0; i < n_grid; i++) {
         p.t_abs[i] = sa[i];
         p.t_rel[i] = sr[i];
-        fp.lpos_abs[i] = (int)(std::lower_bound(sa.begin(), sa.end(), ea[i]) - sa.begin());
-        fp.lpos_rel[i] = (int)(std::lower_bound(sr.begin(), sr.end(), er[i]) - sr.begin());
+        p.lpos_abs[i] = (int)(std::lower_bound(sa, sa + n_grid, ea[i]) - sa);
+        p.lpos_rel[i] = (int)(std::lower_bound(sr, sr + n_grid, er[i]) - sr);
     }
-    NAO_CHECK_CUDA(cudaMemsetAsync(acc, 0, sizeof(CheckAccum), st));
-    const int threads = 256;
-    int64_t warps_needed = ((n >> 2) + 31) / 32;
-    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((warps_needed + 7) / 8, kNumSMs * 8));
+    const int64_t warps_needed = ((n >> 2) + 31) / 32;
+    const int blocks = (int)std::max<int64_t>(
+        1, std::min<int64_t>((warps_needed + kCheckWarps - 1) / kCheckWarps, kNumSMs * 6));
     switch (eps_kind) {
-        case NAO_EPS_TENSOR_F32: k_check<NAO_EPS_TENSOR_F32><<<blocks, threads, 0, st>>>(p, acc); break;
-        case NAO_EPS_TENSOR_F64: k_check<NAO_EPS_TENSOR_F64><<<blocks, threads, 0, st>>>(p, acc); break;
-        case NAO_EPS_SCALED_LOCAL: k_check<NAO_EPS_SCALED_LOCAL><<<blocks, threads, 0, st>>>(p, acc); break;
-        default: k_check<NAO_EPS_ZERO><<<blocks, threads, 0, st>>>(p, acc); break;
+        case NAO_EPS_TENSOR_F32:
+            k_check<NAO_EPS_TENSOR_F32><<<blocks, kCheckThreads, 0, st>>>(p, acc, result); break;
+        case NAO_EPS_TENSOR_F64:
+            k_check<NAO_EPS_TENSOR_F64><<<blocks, kCheckThreads, 0, st>>>(p, acc, result); break;
+        case NAO_EPS_SCALED_LOCAL:
+            k_check<NAO_EPS_SCALED_LOCAL><<<blocks, kCheckThreads, 0, st>>>(p, acc, result); break;
+        default:
+            k_check<NAO_EPS_ZERO><<<blocks, kCheckThreads, 0, st>>>(p, acc, result); break;
     }
-    NAO_CHECK_LAUNCH();
-    k_check_finalize<<<1, 32, 0, st>>>(fp, acc, result, 0);
-    NAO_CHECK_LAUNCH();
-    k_check_pass2<<<grid_for(n, 256), 256, 0, st>>>(p, fp, acc);
-    NAO_CHECK_LAUNCH();
-    k_check_finalize<<<1, 32, 0, st>>>(fp, acc, result, 1);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

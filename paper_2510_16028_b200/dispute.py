@@ -116,7 +116,7 @@ def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel
         eps_ptr = e.data_ptr()
     res = out if out is not None else new_result_buffer(a.device)
     L = _lib.load()
-    ws = _lib.workspace(L.nao_check_workspace(), a.device)
+    ws = _lib.check_accumulator(a.device)
     _lib.call("nao_check", a.data_ptr(), b.data_ptr(), n, kind, eps_ptr, scale, float(lo_factor),
               _lib.dbl_array(grid), _lib.dbl_array(tau_abs), _lib.dbl_array(tau_rel), len(grid),
               float(epsilon), res.data_ptr(), ws.data_ptr(), ws.numel(),

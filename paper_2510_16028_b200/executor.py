@@ -134,7 +134,7 @@ class StreamingVerifier:
         values = dict(frontier or {})
         pending, pend_idx, pend_bytes = [], [], 0
         L = _lib.load()
-        ws_chk = _lib.workspace(L.nao_check_workspace(), self.dev)
+        ws_chk = _lib.check_accumulator(self.dev)
         stream = _lib.stream_ptr(self.dev)
         grid_arr = _lib.dbl_array(self.grid)
 

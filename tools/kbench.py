@@ -1,0 +1,118 @@
+"""Per-kernel microbenchmarks at Qwen3-8B shapes (CUDA events, warm L2 excluded by
+using tensors >> L2).  Prints one JSON line per kernel with achieved GB/s or TFLOP/s.
+
+    python tools/kbench.py [--only check,commit,softmax,gemm_tc,gemm_ffma,split,layernorm]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2510_16028_b200 import _lib  # noqa: E402
+from paper_2510_16028_b200.bounds import (FpModel, abs_gemm_bound, layernorm_device,  # noqa: E402
+                                          softmax_device, tf32_split)
+from paper_2510_16028_b200.commitments import commit_tensors  # noqa: E402
+from paper_2510_16028_b200.dispute import check_node  # noqa: E402
+from paper_2510_16028_b200.executor import inject_drift  # noqa: E402
+
+PEAK_HBM = json.load(open(Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json")).get(
+    "hbm_gbs", 6650.0) if (Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").exists() else 6650.0
+
+
+def timeit(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def report(name, ms, bytes_=None, flops=None, **kw):
+    d = {"kernel": name, "ms": round(ms, 4)}
+    if bytes_:
+        d["GB/s"] = round(bytes_ / ms / 1e6, 1)
+        d["frac_hbm"] = round(bytes_ / ms / 1e6 / PEAK_HBM, 3)
+    if flops:
+        d["TFLOP/s"] = round(flops / ms / 1e9, 2)
+    d.update(kw)
+    print(json.dumps(d), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--reps", type=int, default=10)
+    a = ap.parse_args()
+    only = set(a.only.split(",")) if a.only else None
+    want = lambda k: only is None or k in only  # noqa: E731
+    dev = torch.device("cuda")
+    torch.manual_seed(0)
+    S, H, I, NH = 2048, 4096, 12288, 32
+    model = FpModel()
+
+    if want("check"):
+        for shape in ((NH, S, S), (S, I), (S, H)):
+            y = torch.randn(shape, device=dev)
+            yc = inject_drift(y, 1, 16)
+            eps = torch.rand(shape, device=dev)
+            tau = np.linspace(1e-9, 1e-3, 23)
+            n = y.numel()
+            report("check_scaled", timeit(lambda: check_node(y, yc, ("scaled", 2 ** -24), tau, tau),
+                                          a.reps), 8 * n, shape=list(shape))
+            report("check_f32eps", timeit(lambda: check_node(y, yc, eps, tau, tau), a.reps),
+                   12 * n, shape=list(shape))
+    if want("commit"):
+        for alg in ("keccak256", "sha256"):
+            ts = [torch.randn((NH, S, S), device=dev)]
+            nb = sum(t.numel() * 4 for t in ts)
+            report(f"commit_{alg}", timeit(lambda: commit_tensors(ts, 4096, alg), a.reps), nb,
+                   bytes_committed=nb)
+            ts = [torch.randn((S, H), device=dev) for _ in range(20)]
+            nb = sum(t.numel() * 4 for t in ts)
+            report(f"commit_{alg}_batch20x33MB", timeit(lambda: commit_tensors(ts, 4096, alg),
+                                                        a.reps), nb)
+    if want("softmax"):
+        x = torch.randn((NH, S, S), device=dev) * 3
+        n = x.numel()
+        report("softmax_bound_f32eps", timeit(lambda: softmax_device(x, -1, model, False), a.reps),
+               12 * n)
+    if want("layernorm"):
+        x = torch.randn((S, H), device=dev)
+        report("layernorm_bound_f32eps", timeit(lambda: layernorm_device(x, -1, 1e-6, model, False),
+                                                a.reps), 12 * x.numel())
+    if want("split"):
+        x = torch.randn((S, I), device=dev)
+        report("tf32_split", timeit(lambda: tf32_split(x, S, I, False, False), a.reps),
+               12 * x.numel())
+    for path, tag in ((1, "gemm_tc"), (0, "gemm_ffma")):
+        if want(tag):
+            for (M, K, N) in ((S, H, H), (S, H, I), (S, I, H)):
+                A = torch.randn((M, K), device=dev)
+                B = torch.randn((K, N), device=dev)
+                c = model.reduction_const(2 * K - 1)
+                abs_gemm_bound(A, B, c, False, eps_f64=False, path=path, cache_b=True)
+                ms = timeit(lambda: abs_gemm_bound(A, B, c, False, eps_f64=False, path=path,
+                                                   cache_b=True), a.reps)
+                report(tag, ms, flops=2.0 * M * N * K, shape=[M, K, N])
+            if want("sgemm") or only is None:
+                A = torch.randn((S, H), device=dev)
+                B = torch.randn((H, I), device=dev)
+                torch.backends.cuda.matmul.allow_tf32 = False
+                report("cublas_sgemm_fp32", timeit(lambda: A @ B, a.reps), flops=2.0 * S * H * I)
+
+
+if __name__ == "__main__":
+    main()
