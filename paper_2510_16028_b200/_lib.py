@@ -155,7 +155,8 @@ def call(name: str, *args):
     if _timer is None:
         check(fn(*args), name)
         return
-    store, units_fn, stream = _timer
+    store, units_fn, _ = _timer
+    stream = torch.cuda.current_stream()  # the stream this entry point launches on
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     rc = fn(*args)

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_softmax(
         const double S64 = (double)Sr, epsS = s_epsS[w][rr];
         const double m64 = fabs((double)s_m[w][rr]);
         const double S2 = __dmul_rn(S64, S64);
+        const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(epsS, S2);
         for (int64_t c = lane; c < n; c += 32) {
             const int64_t i = r * n + c;
             const float ev = y[i];
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_softmax(
             const double e64 = (double)ev;
             const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64));
             const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
-            const double t1 = __ddiv_rn(eps_e, S64);
-            const double t2 = __ddiv_rn(__dmul_rn(e64, epsS), S2);
+            const double t1 = __dmul_rn(eps_e, invS);
+            const double t2 = __dmul_rn(e64, kS2);
             const double v = __dadd_rn(__dadd_rn(t1, t2), __dmul_rn(u, fabs((double)yv)));
             store_eps(eps, eps_f64, i, v, slack);
         }
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_layernorm(
         const float mu_r = s_mu[w][rr], sg = s_sigma[w][rr];
         const double sg64 = fabs((double)sg), sg2 = __dmul_rn(sg64, sg64);
         const double emu = s_epsmu[w][rr], esg = s_epssig[w][rr];
+        const double inv_sg = __ddiv_rn(1.0, sg64), k_sg2 = __ddiv_rn(esg, sg2);
         for (int64_t c = lane; c < n; c += 32) {
             const int64_t i = r * n + c;
             const float xc = __fsub_rn(__ldg(x + i), mu_r);
@@ -220,8 +222,8 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_layernorm(
             y[i] = yv;
             const double xc64 = fabs((double)xc);
             const double eps_xc = __dadd_rn(emu, __dmul_rn(u, xc64));
-            const double t1 = __ddiv_rn(eps_xc, sg64);
-            const double t2 = __ddiv_rn(__dmul_rn(xc64, esg), sg2);
+            const double t1 = __dmul_rn(eps_xc, inv_sg);
+            const double t2 = __dmul_rn(xc64, k_sg2);
             const double v = __dadd_rn(__dadd_rn(t1, t2), __dmul_rn(u, fabs((double)yv)));
             store_eps(eps, eps_f64, i, v, slack);
         }
@@ -578,6 +580,9 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
         if (kind == 0) {
             const float S = s_a[r];
             const double S64 = (double)S, S2 = __dmul_rn(S64, S64), epsS = s_d0[r];
+            // divisions by per-row constants as reciprocal multiplies: <= 2 ulp FP64,
+            // covered by `slack` (>= 2^-50)
+            const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(epsS, S2);
             const float* erow = se + (size_t)r * n;
             const double m64a = fabs((double)s_b[r]);
             for (int64_t c = threadIdx.x; c < n; c += kThreads) {
@@ -587,8 +592,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
                 const double e64 = (double)ev;
                 const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)row[c]), m64a));
                 const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
-                const double v = __dadd_rn(__dadd_rn(__ddiv_rn(eps_e, S64),
-                                                     __ddiv_rn(__dmul_rn(e64, epsS), S2)),
+                const double v = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
                                            __dmul_rn(u, fabs((double)yv)));
                 store_eps(eps, eps_f64, ob + c, v, slack);
             }
@@ -617,14 +621,15 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
             const double eps_sp = __dadd_rn(eps_var, __dmul_rn(u, fabs((double)sp)));
             const double sg64 = fabs((double)sigma), sg2 = __dmul_rn(sg64, sg64);
             const double esg = __dadd_rn(__ddiv_rn(eps_sp, __dmul_rn(2.0, sg64)), __dmul_rn(u, sg64));
+            const double inv_sg = __ddiv_rn(1.0, sg64), k_sg2 = __ddiv_rn(esg, sg2);
             for (int64_t c = threadIdx.x; c < n; c += kThreads) {
                 const float xc = __fsub_rn(row[c], mu);
                 const float yv = __fdiv_rn(xc, sigma);
                 yrow[c] = yv;
                 const double xc64 = fabs((double)xc);
                 const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
-                const double v = __dadd_rn(__dadd_rn(__ddiv_rn(eps_xc, sg64),
-                                                     __ddiv_rn(__dmul_rn(xc64, esg), sg2)),
+                const double v = __dadd_rn(__dadd_rn(__dmul_rn(eps_xc, inv_sg),
+                                                     __dmul_rn(xc64, k_sg2)),
                                            __dmul_rn(u, fabs((double)yv)));
                 store_eps(eps, eps_f64, ob + c, v, slack);
             }

@@ -91,7 +91,7 @@ class StreamingVerifier:
     def __init__(self, graph, model: FpModel | None = None, profile=NATIVE, thresholds=None,
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
-                 grid=PERCENTILE_GRID):
+                 grid=PERCENTILE_GRID, overlap: bool = True):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -103,6 +103,11 @@ class StreamingVerifier:
         self.epsilon = float(epsilon)
         self.grid = tuple(grid)
         self._tau_cache = {}
+        # side streams: the memory-bound check and the ALU-bound hashing run
+        # concurrently with the next nodes' GEMMs / bound kernels
+        self.overlap = bool(overlap)
+        self._s_chk = torch.cuda.Stream(self.dev) if overlap else None
+        self._s_com = torch.cuda.Stream(self.dev) if overlap else None
 
     # ---------------------------------------------------------- thresholds
     def _taus(self, name):
@@ -133,18 +138,35 @@ class StreamingVerifier:
         last = last_uses(g, start, end)
         values = dict(frontier or {})
         pending, pend_idx, pend_bytes = [], [], 0
-        L = _lib.load()
-        ws_chk = _lib.check_accumulator(self.dev)
-        stream = _lib.stream_ptr(self.dev)
+        _lib.load()
+        main = torch.cuda.current_stream(self.dev)
+        s_chk = self._s_chk or main
+        s_com = self._s_com or main
+        if self.overlap:  # side streams start after everything already queued on main
+            s_chk.wait_stream(main)
+            s_com.wait_stream(main)
+        with torch.cuda.stream(s_chk):
+            ws_chk = _lib.check_accumulator(self.dev)
+        chk_ptr = s_chk.cuda_stream
         grid_arr = _lib.dbl_array(self.grid)
+        all_idx = torch.arange(n, device=self.dev)
 
         def flush():
             nonlocal pending, pend_idx, pend_bytes
             if not pending:
                 return
-            r = commit_tensors(pending, self.chunk, self.alg)
-            idx = torch.as_tensor(pend_idx, device=self.dev)
-            roots.index_copy_(0, idx, r)
+            if self.overlap:
+                s_com.wait_stream(main)
+            with torch.cuda.stream(s_com):
+                r = commit_tensors(pending, self.chunk, self.alg)
+                lo, hi = pend_idx[0], pend_idx[-1] + 1
+                if hi - lo == len(pend_idx):
+                    roots[lo:hi].copy_(r)
+                else:
+                    roots.index_copy_(0, all_idx[torch.as_tensor(pend_idx)], r)
+            if self.overlap:
+                for t in pending:
+                    t.record_stream(s_com)
             pending, pend_idx, pend_bytes = [], [], 0
 
         for node in g.nodes[start:end]:
@@ -177,10 +199,17 @@ class StreamingVerifier:
                 eps_ptr = eps.data_ptr()
             i = node.index - start
             if y.numel():
-                _lib.call("nao_check", y.data_ptr(), yc.data_ptr(), y.numel(), kind, eps_ptr,
-                          scale, lo, grid_arr, _lib.dbl_array(tau_a), _lib.dbl_array(tau_r),
-                          len(self.grid), self.epsilon, records[i].data_ptr(),
-                          ws_chk.data_ptr(), ws_chk.numel(), stream)
+                if self.overlap:
+                    s_chk.wait_stream(main)
+                    y.record_stream(s_chk)
+                    yc.record_stream(s_chk)
+                    if not isinstance(eps, tuple):
+                        eps.record_stream(s_chk)
+                with torch.cuda.stream(s_chk):
+                    _lib.call("nao_check", y.data_ptr(), yc.data_ptr(), y.numel(), kind, eps_ptr,
+                              scale, lo, grid_arr, _lib.dbl_array(tau_a), _lib.dbl_array(tau_r),
+                              len(self.grid), self.epsilon, records[i].data_ptr(),
+                              ws_chk.data_ptr(), ws_chk.numel(), chk_ptr)
             if stats is not None:
                 stats.elements_checked += y.numel()
                 stats.bytes_committed += y.numel() * 4
@@ -201,6 +230,9 @@ class StreamingVerifier:
             if last.get(node.index, -1) <= node.index and node.index in values:
                 del values[node.index]
         flush()
+        if self.overlap:
+            main.wait_stream(s_chk)
+            main.wait_stream(s_com)
         self.outputs = {k: v for k, v in values.items()}
         return roots, records
 
