@@ -132,7 +132,9 @@ def calibrate_thresholds(g, sv_cls, ids, dev, model, args, start=0, end=None, fr
 
     for seed in range(12345, 12345 + args.calib_samples):
         def claimed_fn(node, y, seed=seed):
-            yc = drift_claim(node, y, seed=seed, period=args.drift_period)
+            # denser drift than the run (period/4): the envelope must cover the
+            # rare large-magnitude element at p100 that a sparse sample misses
+            yc = drift_claim(node, y, seed=seed, period=max(1, args.drift_period // 4))
             if y.numel():
                 pa, pr = error_profiles_device(y, yc)
                 if node.name in env:
@@ -261,16 +263,32 @@ def run_ours(args):
     def units(name, a):
         if name == "nao_abs_gemm_bound":
             return 2.0 * a[4] * a[5] * a[6] * a[7]
+        if name == "nao_abs_gemm_tc":
+            return 2.0 * a[6] * a[9] * a[10] * a[11]
+        if name == "nao_tf32_split":
+            return 12.0 * a[3] * a[4] * a[5]
+        if name in ("nao_softmax_bound", "nao_layernorm_bound"):
+            return 12.0 * a[4] * a[5]
+        if name == "nao_inject_drift":
+            return 8.0 * a[2]
         if name == "nao_merkle_commit_tensors":
             return float(sum(a[2][i] for i in range(a[0])))
         if name == "nao_check":
             return 8.0 * a[2] + (4.0 if a[3] == 0 else 8.0 if a[3] == 1 else 0.0) * a[2]
         return 0.0
 
-    _lib.set_timer(timers, units, stream)
     with ClockSampler(local) as clocks:
         t_ver = timed(verified_step, args.steps)
+
+    # decomposition pass (not the headline): same step with the side streams
+    # off so CUDA events around each launch measure that kernel alone
+    sv.overlap, keep = False, (sv._s_chk, sv._s_com)
+    sv._s_chk = sv._s_com = None
+    torch.cuda.synchronize()
+    _lib.set_timer(timers, units, stream)
+    t_serial = timed(verified_step, 1)
     _lib.set_timer(None, None, None)
+    sv.overlap, (sv._s_chk, sv._s_com) = True, keep
 
     # end to end: ids H2D from pinned host + verified forward + D2H of roots/records/root
     def e2e_step():
@@ -325,6 +343,23 @@ def run_ours(args):
             where = (f"abs@p{PCT[g_idx]}" if g_idx < len(PCT) else f"rel@p{PCT[g_idx - len(PCT)]}")
             exceed_nodes.append(f"{names[i] if i < len(names) else i}:{where}")
 
+    if args.debug_exceed and exceed_nodes:
+        from paper_2510_16028_b200.calibration import error_profiles_device
+        dbg = {}
+
+        def dbg_fn(node, y):
+            yc = drift_claim(node, y, 1, args.drift_period, fault)
+            if any(e.startswith(node.name + ":") for e in exceed_nodes):
+                pa, pr = error_profiles_device(y, yc)
+                op = thresholds.lookup(node.name)
+                dbg[node.name] = {"abs": pa.cpu().tolist(), "tau_abs": list(op.tau_abs),
+                                  "rel": pr.cpu().tolist(), "tau_rel": list(op.tau_rel),
+                                  "n": y.numel()}
+            return yc
+        sv.run(ids, dbg_fn, start, end, frontier)
+        torch.cuda.synchronize()
+        print(json.dumps({"debug_exceeded": dbg}), file=sys.stderr)
+
     overhead = 100.0 * (t_ver - t_plain) / t_plain
     peaks = _peaks()
     commit_bytes_per_step = stats.bytes_committed * (world if world > 1 else 1)
@@ -337,7 +372,17 @@ def run_ours(args):
         d = timers[dom]
         per_launch_ms = sum(d["ms"]) / len(d["ms"])
         per_launch_units = sum(d["units"]) / len(d["units"])
-        if dom == "nao_abs_gemm_bound":
+        if dom == "nao_abs_gemm_tc":
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
+            tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
+            peak = tf32 / 3.0
+            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
+                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = TF32 dense, / 3 "
+                                   "MMAs per product (3xTF32 split): algorithmic ceiling",
+                    "mma_tflops": round(3 * achieved, 1), "tf32_peak": round(tf32, 1),
+                    "traffic": None}
+        elif dom == "nao_abs_gemm_bound":
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
             peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 SIMT peak (derived, not measured)
             roof = {"kernel": dom, "bound": "fp32-simt", "achieved": round(achieved, 2),
@@ -352,10 +397,12 @@ def run_ours(args):
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks
                     else "fallback", "traffic": None}
-        roof["share_of_step"] = round(shares[dom] / args.steps / t_ver, 4)
-        roof["kernel_ms_per_step"] = {k: round(v / args.steps, 2) for k, v in shares.items()}
+        roof["share_of_serial_step"] = round(shares[dom] / t_serial, 4)
+        roof["serial_step_ms"] = round(t_serial, 2)
+        roof["kernel_ms_per_step"] = {k: round(v, 2) for k, v in sorted(
+            shares.items(), key=lambda kv: -kv[1])}
 
-    commit_ms = shares.get("nao_merkle_commit_tensors", 0.0) / args.steps
+    commit_ms = shares.get("nao_merkle_commit_tensors", 0.0)
     merkle_gbs = (stats.bytes_committed / (commit_ms * 1e-3) / 1e9) if commit_ms else None
 
     if rank != 0:
@@ -387,7 +434,7 @@ def run_ours(args):
         "e2e": {"value": round(100.0 * (e2e_ms - t_plain) / t_plain, 2), "unit": UNIT,
                 "ms_per_step": round(e2e_ms, 2), "h2d_bytes_per_step": int(ids_host.numel() * 4),
                 "d2h_bytes_per_step": int(n_nodes * (32 + _lib.CHECK_RESULT_BYTES) + 32)},
-        "gpu_launches": n_launch // max(args.steps, 1),
+        "gpu_launches": n_launch,
         "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
     }
     print(json.dumps(line))
@@ -529,6 +576,7 @@ def main(argv=None):
     ap.add_argument("--fault-node", default="l3_down")
     ap.add_argument("--cpu-seq", type=int, default=512)
     ap.add_argument("--calib-samples", type=int, default=4)
+    ap.add_argument("--debug-exceed", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args(argv)
     if args.fault_node and args.layers <= int(args.fault_node.split("_")[0][1:] or 0):
