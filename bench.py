@@ -98,28 +98,6 @@ def build_model(args, device):
     return build_decoder(shape, device=device, seed=0, layers=args.layers), shape
 
 
-def layer_bounds(g, n_layers):
-    """node index where each layer starts (+ head start), from node names."""
-    starts = []
-    for i, n in enumerate(g.nodes):
-        if n.name.startswith("l") and n.name.split("_")[0][1:].isdigit():
-            layer = int(n.name.split("_")[0][1:])
-            if len(starts) == layer:
-                starts.append(i)
-    return starts
-
-
-def rank_slice(g, n_layers, rank, world):
-    """Contiguous layer-aligned op slice for `rank` (partition sizes differ by <= 1 layer)."""
-    starts = layer_bounds(g, n_layers)
-    base, extra = divmod(n_layers, world)
-    lo = rank * base + min(rank, extra)
-    hi = lo + base + (1 if rank < extra else 0)
-    start = 0 if rank == 0 else starts[lo]
-    end = g.n_nodes if rank == world - 1 else starts[hi]
-    return start, end
-
-
 def calibrate_thresholds(g, sv_cls, ids, dev, model, args, start=0, end=None, frontier=None):
     """Offline calibration (calibration.py:70-114 restated for the device fleet
     {this B200, a drifting proposer}): exact error profiles of one honest
@@ -175,24 +153,17 @@ def run_ours(args):
 
     spec, shape = build_model(args, dev)
     g = spec.graph
-    start, end = rank_slice(g, args.layers, rank, world)
+    from paper_2510_16028_b200 import shard
+    start, end = shard.rank_slice(g, args.layers, rank, world)
     ids = spec.make_inputs(Rng(2024))
     ids_host = torch.from_numpy(np.array(ids["ids"].array)).pin_memory()
     model = FpModel()
 
     # frontier (residual stream entering the slice): synthetic claimed values
     frontier = {}
-    if start > 0:
-        from paper_2510_16028_b200.graph import parse_ref
-        need = set()
-        for node in g.nodes[start:end]:
-            for ref in node.inputs:
-                cat, key = parse_ref(ref)
-                if cat == "node" and key < start:
-                    need.add(key)
-        gen = torch.Generator(device=dev).manual_seed(77 + rank)
-        for k in need:
-            frontier[k] = torch.randn((shape.seq, shape.hidden), generator=gen, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(77 + rank)
+    for k in shard.frontier_refs(g, start, end):
+        frontier[k] = torch.randn((shape.seq, shape.hidden), generator=gen, device=dev)
 
     # materialise the slice's weights before timing (32.8 GB for the full model)
     from paper_2510_16028_b200.graph import parse_ref
@@ -283,7 +254,7 @@ def run_ours(args):
     # decomposition pass (not the headline): same step with the side streams
     # off so CUDA events around each launch measure that kernel alone
     sv.overlap, keep = False, (sv._s_chk, sv._s_com)
-    sv._s_chk = sv._s_com = None
+    sv._s_chk = sv._s_com = None  # serial: everything on the caller's stream
     torch.cuda.synchronize()
     _lib.set_timer(timers, units, stream)
     t_serial = timed(verified_step, 1)
@@ -303,21 +274,8 @@ def run_ours(args):
     for _ in range(args.steps):
         roots, recs, troot = verified_step(e2e=True)
         if world > 1:
-            n_local = roots.shape[0]
-            sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-            dist.all_gather(sizes, torch.tensor([n_local], device=dev))
-            mx = int(max(s.item() for s in sizes))
-            pad_r = torch.zeros((mx, 32), dtype=torch.uint8, device=dev)
-            pad_r[:n_local] = roots
-            pad_c = torch.zeros((mx, recs.shape[1]), dtype=torch.uint8, device=dev)
-            pad_c[:n_local] = recs
-            gr = [torch.empty_like(pad_r) for _ in range(world)]
-            gc = [torch.empty_like(pad_c) for _ in range(world)]
-            dist.all_gather(gr, pad_r)
-            dist.all_gather(gc, pad_c)
+            roots, recs = shard.gather_node_records(roots, recs)
             if rank == 0:
-                roots = torch.cat([gr[i][:int(sizes[i].item())] for i in range(world)])
-                recs = torch.cat([gc[i][:int(sizes[i].item())] for i in range(world)])
                 troot = sv.trace_root(roots)
         host_roots, host_recs = roots.cpu(), recs.cpu()
         host_troot = troot.cpu() if troot is not None else None
