@@ -153,7 +153,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 5);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, bz = blockIdx.z;
+    // grouped rasterization: consecutive CTAs sweep GROUP_M row tiles per column
+    // tile, so the B tiles in flight are shared by GROUP_M CTAs through L2
+    const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+    constexpr int GROUP_M = 8;
+    const int pid = blockIdx.x;
+    const int group = pid / (GROUP_M * tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gm = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
+    const int tm = first_m + (pid % (GROUP_M * tiles_n)) % gm;
+    const int tn = (pid % (GROUP_M * tiles_n)) / gm;
+    const int n0 = tn * BN, m0 = tm * BM, bz = blockIdx.z;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -286,6 +296,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // |x| -> (hi, lo) TF32 parts, K-major [rows, Kp] (zero padded), optionally
 // reading x transposed (x is [K, rows] row-major when `trans`).
+__device__ __forceinline__ void split_one(float x, float& h, float& l) {
+    const float a = fabsf(x);
+    const uint32_t hb = __float_as_uint(a) & 0xFFFFE000u;  // truncate to TF32: hi <= a
+    h = __uint_as_float(hb);
+    const uint32_t rb = __float_as_uint(__fsub_rn(a, h));  // exact remainder
+    l = __uint_as_float((rb & 0x1FFFu) ? ((rb & 0xFFFFE000u) + 0x2000u) : rb);  // RU to TF32
+    if (h != 0.f && h < 1.17549435e-38f) h = 1.17549435e-38f;  // no subnormal operands
+    if (l != 0.f && l < 1.17549435e-38f) l = 1.17549435e-38f;
+}
+
+// Fast path: x is [batch*rows, K] contiguous with K % 4 == 0 (so Kp == K).
+__global__ void k_split_tf32_vec(const float4* __restrict__ x, float4* __restrict__ hi,
+                                 float4* __restrict__ lo, int64_t n4) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n4;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(x + t);
+        float4 h, l;
+        split_one(v.x, h.x, l.x); split_one(v.y, h.y, l.y);
+        split_one(v.z, h.z, l.z); split_one(v.w, h.w, l.w);
+        hi[t] = h;
+        lo[t] = l;
+    }
+}
+
 __global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi,
                              float* __restrict__ lo, int64_t batch, int64_t rows, int64_t K,
                              int64_t Kp, int64_t ld, int64_t sbatch, int trans) {
@@ -359,6 +393,17 @@ int nao_tf32_split(const float* x, float* hi, float* lo, int64_t batch, int64_t 
     const int64_t Kp = nao_tf32_split_cols(K);
     const int64_t total = batch * rows * Kp;
     if (total == 0) return NAO_OK;
+    if (!transpose && Kp == K && ld == K && stride_batch == rows * K &&
+        (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
+        const int64_t n4 = total / 4;
+        int64_t b4 = (n4 + 255) / 256;
+        if (b4 > kNumSMs * 16) b4 = kNumSMs * 16;
+        tc::k_split_tf32_vec<<<(unsigned)b4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(hi),
+            reinterpret_cast<float4*>(lo), n4);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     int64_t blocks = (total + 255) / 256;
     if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
     tc::k_split_tf32<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
@@ -379,7 +424,8 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
     NAO_REQUIRE(M >= 1 && N >= 1 && K >= 1 && batch >= 1, "abs-gemm tc: bad shape");
     NAO_REQUIRE((batch_a == batch || batch_a == 1) && (batch_b == batch || batch_b == 1),
                 "abs-gemm tc: bad batch broadcast");
-    NAO_REQUIRE(M <= 65535LL * BM && batch <= 65535, "abs-gemm tc: grid too large");
+    NAO_REQUIRE(ceil_div(N, BN) * ceil_div(M, BM) < (1LL << 31) && batch <= 65535,
+                "abs-gemm tc: grid too large");
     const int64_t Kp = nao_tf32_split_cols(K);
     CUtensorMap mah, mal, mbh, mbl;
     int rc;
@@ -411,7 +457,7 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
                                             SMEM_BYTES));
         attr_set = true;
     }
-    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
+    dim3 grid((unsigned)(ceil_div(N, BN) * ceil_div(M, BM)), 1, (unsigned)batch);
     k_absgemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
         mah, mal, mbh, mbl, g);
     NAO_CHECK_LAUNCH();

@@ -105,12 +105,12 @@ class StreamingVerifier:
         self._tau_cache = {}
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
-        # (lowest priority: the block scheduler favours the critical path's CTAs and
-        # fills the remaining SM resources with hashing / checking)
+        # (equal priorities: a low-priority side stream starves and the memory its
+        # pending work pins via record_stream balloons -- measured 2x slower)
         self.overlap = bool(overlap)
-        self._s_chk = torch.cuda.Stream(self.dev, priority=0) if overlap else None
-        self._s_com = torch.cuda.Stream(self.dev, priority=0) if overlap else None
-        self._s_main = torch.cuda.Stream(self.dev, priority=-1) if overlap else None
+        self._s_chk = torch.cuda.Stream(self.dev) if overlap else None
+        self._s_com = torch.cuda.Stream(self.dev) if overlap else None
+        self._s_main = None
 
     # ---------------------------------------------------------- thresholds
     def _taus(self, name):
@@ -129,16 +129,7 @@ class StreamingVerifier:
     # ----------------------------------------------------------------- run
     def run(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
             frontier: dict | None = None, stats: NodeStats | None = None):
-        if not self.overlap:
-            return self._run(inputs, claimed_fn, start, end, frontier, stats)
-        caller = torch.cuda.current_stream(self.dev)
-        self._s_main.wait_stream(caller)
-        with torch.cuda.stream(self._s_main):
-            out = self._run(inputs, claimed_fn, start, end, frontier, stats)
-        caller.wait_stream(self._s_main)
-        for t in out:
-            t.record_stream(caller)
-        return out
+        return self._run(inputs, claimed_fn, start, end, frontier, stats)
 
     def _run(self, inputs, claimed_fn, start, end, frontier, stats):
         """Verify nodes [start, end).  claimed_fn(node, y) -> the claimed CUDA tensor

@@ -1,0 +1,61 @@
+"""GPU: empirical check of the tcgen05 accumulation error model behind
+nao_abs_gemm_tc (csrc/absgemm_tc.cu header): with TF32-exact operands the lo
+parts vanish, every product is exact, and the output is
+    eps = scale0 * sum_chunks acc0_chunk   (scale0 known)
+so the accumulator's relative loss per 64-k chunk (8 MMAs) can be measured
+exactly against an FP64 sum and compared with the modelled bound 8 * 3 * 2^-23.
+The runs are built to maximise truncation loss: long runs of equal terms
+(every addition aligns the same low bits away) and growing partial sums."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+MMA_REL = 3.0 * 2.0 ** -23
+J0 = 8
+
+
+def _scale0(c, K):
+    from paper_2510_16028_b200.bounds import gemm_slack
+    comp_split = 1.0 / (1.0 - 1.002 * 2.0 ** -20)
+    comp0 = 1.0 / (1.0 - J0 * MMA_REL)
+    return c * comp_split * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -50) * comp0, comp0
+
+
+def _tf32_exact(x):
+    return (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+@pytest.mark.parametrize("case", ["equal", "equal_big", "random_tf32", "ramp"])
+def test_tc_accumulation_loss_within_model(case):
+    from paper_2510_16028_b200.bounds import abs_gemm_bound
+    rng = np.random.default_rng(3)
+    M, K, N = 128, 8192, 128
+    if case == "equal":
+        a = np.full((M, K), 1.0 + 2.0 ** -10, np.float32)
+        b = np.full((K, N), 1.0 + 2.0 ** -9, np.float32)
+    elif case == "equal_big":
+        a = np.full((M, K), 1.9990234375, np.float32)  # 11 significant bits
+        b = np.full((K, N), 1.9990234375, np.float32)
+    elif case == "random_tf32":
+        a = _tf32_exact((rng.random((M, K)) + 0.5).astype(np.float32))
+        b = _tf32_exact((rng.random((K, N)) + 0.5).astype(np.float32))
+    else:
+        a = _tf32_exact(np.tile(np.linspace(1.0, 2.0, K, dtype=np.float32), (M, 1)))
+        b = _tf32_exact((rng.random((K, N)) + 1.0).astype(np.float32))
+    exact = np.abs(a.astype(np.float64)) @ np.abs(b.astype(np.float64))
+    c = 1.0
+    got = abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), c, path=1)
+    got = got.cpu().numpy()
+    scale0, comp0 = _scale0(c, K)
+    raw = got / scale0  # = sum of the per-chunk TMEM sums (lo parts are exactly zero)
+    loss = 1.0 - raw / exact  # relative loss of the tensor-core accumulation
+    worst = float(loss.max())
+    print(f"{case}: worst relative accumulation loss {worst:.3e} "
+          f"(model per chunk {J0 * MMA_REL:.3e})")
+    assert worst <= J0 * MMA_REL
+    assert np.all(got >= exact)  # the compensated bound stays sound
