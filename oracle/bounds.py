@@ -19,7 +19,7 @@ _SQRT_2_OVER_PI = math.sqrt(2.0 / math.pi)  # engine.py:23
 _GELU_COEFF = 0.044715  # engine.py:24
 
 DATA_MOVEMENT_KINDS = frozenset({"concat", "slice", "reshape", "embedding"})  # graph.py:27
-EXT_DATA_MOVEMENT_KINDS = frozenset({"transpose"})  # extension
+EXT_DATA_MOVEMENT_KINDS = frozenset({"transpose", "maxpool2d"})  # extensions
 SINGLE_ROUNDING_KINDS = frozenset({"add", "sub", "mul", "div", "neg"})  # bounds.py:172
 INTRINSIC_KINDS = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})  # :173
 
@@ -195,7 +195,37 @@ def apply_op(node, arrays, fma=False) -> np.ndarray:
         return table[idx]
     if kind == "transpose":  # extension: permutation of axes, pure data movement
         return np.transpose(arrays[0], _parse_shape(node.attr("perm")))
+    if kind == "conv2d":  # extension: sequential matmul over im2col, K order (c, kh, kw)
+        x, w = arrays
+        col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
+                                  int(node.attr("pad", 0)))
+        out = matmul_value(col, w.reshape(w.shape[0], -1), True, fma)
+        return np.ascontiguousarray(out.reshape(B, OH, OW, w.shape[0]).transpose(0, 3, 1, 2))
+    if kind == "maxpool2d":  # extension: exact max over windows (padding = -inf)
+        x = arrays[0]
+        k, st, pd = int(node.attr("k", 2)), int(node.attr("stride", 2)), int(node.attr("pad", 0))
+        xp = np.pad(x, ((0, 0), (0, 0), (pd, pd), (pd, pd)), constant_values=-np.inf)
+        B, C, H, W = xp.shape
+        OH, OW = (H - k) // st + 1, (W - k) // st + 1
+        out = np.full((B, C, OH, OW), -np.inf, dtype=np.float32)
+        for i in range(k):
+            for j in range(k):
+                out = np.maximum(out, xp[:, :, i:i + st * OH:st, j:j + st * OW:st])
+        return out
     raise ValueError(f"unsupported op kind {kind!r}")
+
+
+def im2col(x, k: int, stride: int, pad: int):
+    """[B, C, H, W] -> ([B, OH*OW, C*k*k], (B, OH, OW)); K ordered (c, kh, kw)."""
+    x = np.asarray(x, dtype=np.float32)
+    B, C, H, W = x.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    OH, OW = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    cols = np.empty((B, C, k, k, OH, OW), dtype=np.float32)
+    for i in range(k):
+        for j in range(k):
+            cols[:, :, i, j] = xp[:, :, i:i + stride * OH:stride, j:j + stride * OW:stride]
+    return cols.reshape(B, C * k * k, OH * OW).transpose(0, 2, 1), (B, OH, OW)
 
 
 # --------------------------------------------------------------- templates
@@ -296,6 +326,12 @@ def op_bound(node, arrays, model: FpModel, fma=False):
                                  bool(node.attr("transpose_b", 0)))
     if kind == "linear":
         return out, matmul_bound(arrays[0], arrays[1], model, fma) + u * _abs64(out)
+    if kind == "conv2d":  # extension: matmul_bound over the implicit im2col
+        x, w = arrays
+        col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
+                                  int(node.attr("pad", 0)))
+        eps = matmul_bound(col, w.reshape(w.shape[0], -1), model, fma, transpose_b=True)
+        return out, np.ascontiguousarray(eps.reshape(B, OH, OW, w.shape[0]).transpose(0, 3, 1, 2))
     raise ValueError(f"no bound template for kind {kind!r}")
 
 

@@ -34,7 +34,7 @@ from .tensor import Tensor
 FP32_UNIT_ROUNDOFF = 2.0 ** -24
 SINGLE_ROUNDING_KINDS = frozenset({"add", "sub", "mul", "div", "neg"})
 INTRINSIC_KINDS = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})
-ZERO_BOUND_KINDS = DATA_MOVEMENT_KINDS | {"transpose", "relu", "max", "min"}
+ZERO_BOUND_KINDS = DATA_MOVEMENT_KINDS | {"transpose", "relu", "max", "min", "maxpool2d"}
 
 
 @dataclass(frozen=True)
@@ -321,6 +321,18 @@ def apply_value(node, xs, profile) -> torch.Tensor:
         return xs[0].reshape(parse_shape_attr(node.attr("shape")))
     if kind == "transpose":  # extension: axis permutation
         return xs[0].permute(parse_shape_attr(node.attr("perm"))).contiguous()
+    if kind == "conv2d":  # extension: value = cuDNN (native) or im2col + profile matmul
+        x, w = xs
+        st, pd = int(node.attr("stride", 1)), int(node.attr("pad", 0))
+        if (profile is None or profile.reduction != "native"):
+            col, (B, OH, OW) = im2col(x, w.shape[-1], st, pd)
+            out = matmul_value(col, w.reshape(w.shape[0], -1), profile, transpose_b=True)
+            return out.reshape(B, OH, OW, w.shape[0]).permute(0, 3, 1, 2).contiguous()
+        return torch.nn.functional.conv2d(x, w, stride=st, padding=pd)
+    if kind == "maxpool2d":
+        return torch.nn.functional.max_pool2d(xs[0], int(node.attr("k", 2)),
+                                              int(node.attr("stride", 2)),
+                                              int(node.attr("pad", 0)))
     if kind == "embedding":
         ids, table = xs
         idx = ids.to(torch.int64)
@@ -368,7 +380,26 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
             return y, abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64, cache_b=static_b)
         return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64,
                                  cache_b=static_b)
+    if kind == "conv2d":
+        x, w = xs
+        col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
+                                  int(node.attr("pad", 0)))
+        K = col.shape[-1]
+        count = K if fma_of(profile) else 2 * K - 1
+        eps = abs_gemm_bound(col, w.reshape(w.shape[0], -1), model.reduction_const(count), True,
+                             eps_f64=f64, cache_b=True)
+        return y, eps.reshape(B, OH, OW, w.shape[0]).permute(0, 3, 1, 2).contiguous()
     raise ValueError(f"no bound template for kind {kind!r}")
+
+
+def im2col(x: torch.Tensor, k: int, stride: int, pad: int):
+    """[B, C, H, W] -> [B, OH*OW, C*k*k] patches (zero padding included in K,
+    SURVEY.md 2.3), K ordered (c, kh, kw) as torch.nn.functional.unfold."""
+    B, C, H, W = x.shape
+    col = torch.nn.functional.unfold(x, k, padding=pad, stride=stride)  # [B, C*k*k, L]
+    OH = (H + 2 * pad - k) // stride + 1
+    OW = (W + 2 * pad - k) // stride + 1
+    return col.transpose(1, 2).contiguous(), (B, OH, OW)
 
 
 def op_bound(node, arrays, model: FpModel, profile=None):

@@ -319,3 +319,70 @@ def build_decoder(shape: DecoderShape, device: str = "cuda", seed: int = 0,
     g = build_graph(nodes, [("ids", (B, S))], weights, [out])
     return ModelSpec(shape.name, g, {"ids": ("tokens", shape.vocab)},
                      meta={"shape": shape, "layers": L})
+
+
+# --------------------------------------------------------------- ResNet-18
+
+def build_resnet18(batch: int = 32, side: int = 224, n_classes: int = 1000, width: int = 64,
+                   device: str = "cuda", seed: int = 0) -> ModelSpec:
+    """ResNet-18 (eval) lowered onto reference kinds + conv2d / maxpool2d
+    extensions: conv -> BN as sub / mul / add with per-channel
+    constants (single-rounding templates) -> relu; maxpool; global average
+    pool = reshape + mean; fc = linear.  Kaiming-normal convs, randomised BN
+    running statistics, images U(-1, 1) (BASELINE config 2)."""
+    specs, nodes = {}, []
+
+    def add(name, kind, inputs, attrs=None):
+        nodes.append(make_node(name, kind, inputs, attrs))
+        return node_ref(len(nodes) - 1)
+
+    def conv(name, x, cin, cout, k, stride, pad):
+        specs[f"{name}.w"] = ((cout, cin, k, k), "normal", math.sqrt(2.0 / (cin * k * k)))
+        return add(name, "conv2d", [x, weight_ref(f"{name}.w")], {"stride": stride, "pad": pad})
+
+    def bn(name, x, c):
+        rng = np.random.default_rng(zlib.crc32(name.encode()) + seed)
+        mean = rng.uniform(-0.1, 0.1, c)
+        var = rng.uniform(0.5, 1.5, c)
+        gamma = rng.uniform(0.8, 1.2, c)
+        beta = rng.uniform(-0.1, 0.1, c)
+        scale = (gamma / np.sqrt(var + 1e-5)).astype(np.float32)
+        specs[f"{name}.mean"] = ((1, c, 1, 1), "const", mean.astype(np.float32))
+        specs[f"{name}.scale"] = ((1, c, 1, 1), "const", scale)
+        specs[f"{name}.beta"] = ((1, c, 1, 1), "const", beta.astype(np.float32))
+        y = add(f"{name}_sub", "sub", [x, weight_ref(f"{name}.mean")])
+        y = add(f"{name}_mul", "mul", [y, weight_ref(f"{name}.scale")])
+        return add(f"{name}_add", "add", [y, weight_ref(f"{name}.beta")])
+
+    x = input_ref("img")
+    h = conv("conv1", x, 3, width, 7, 2, 3)
+    h = bn("bn1", h, width)
+    h = add("relu1", "relu", [h])
+    h = add("maxpool", "maxpool2d", [h], {"k": 3, "stride": 2, "pad": 1})
+    cin, sp = width, side // 4
+    for li, (cout, stride) in enumerate([(width, 1), (2 * width, 2), (4 * width, 2),
+                                         (8 * width, 2)]):
+        for bi in range(2):
+            p = f"layer{li + 1}.{bi}"
+            s = stride if bi == 0 else 1
+            idn = h
+            y = conv(f"{p}.conv1", h, cin, cout, 3, s, 1)
+            y = bn(f"{p}.bn1", y, cout)
+            y = add(f"{p}.relu1", "relu", [y])
+            y = conv(f"{p}.conv2", y, cout, cout, 3, 1, 1)
+            y = bn(f"{p}.bn2", y, cout)
+            if s != 1 or cin != cout:
+                idn = conv(f"{p}.down", h, cin, cout, 1, s, 0)
+                idn = bn(f"{p}.downbn", idn, cout)
+            y = add(f"{p}.res", "add", [y, idn])
+            h = add(f"{p}.relu2", "relu", [y])
+            cin = cout
+        sp = sp if li == 0 else sp // 2
+    h = add("pool_flat", "reshape", [h], {"shape": f"{batch},{cin},{sp * sp}"})
+    h = add("avgpool", "mean", [h], {"axis": -1})
+    specs["fc.w"] = ((cin, n_classes), "uniform", 1.0 / math.sqrt(cin))
+    specs["fc.b"] = ((n_classes,), "uniform", 1.0 / math.sqrt(cin))
+    out = add("fc", "linear", [h, weight_ref("fc.w"), weight_ref("fc.b")])
+    g = build_graph(nodes, [("img", (batch, 3, side, side))], _LazyWeights(specs, device, seed),
+                    [out])
+    return ModelSpec("resnet18", g, {"img": ("uniform", -1.0, 1.0)}, n_classes)
