@@ -33,7 +33,14 @@
 namespace nao {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, KCHUNK_KB = 2;
+#ifndef NAO_TC_BK
+#define NAO_TC_BK 16
+#endif
+// BK = 16: 64 B rows (SWIZZLE_64B), 32 KB stages, 6 in flight;  BK = 32: 128 B
+// rows (SWIZZLE_128B), 64 KB stages, 3 in flight.  Same bytes in flight.
+constexpr int BM = 128, BN = 128, BK = NAO_TC_BK;
+constexpr int STAGES = BK == 16 ? 6 : 3;
+constexpr int KCHUNK_KB = 64 / BK;  // k-blocks per 64-k TMEM chunk
 constexpr int TILE_BYTES = BM * BK * 4;     // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A_hi, A_lo, B_hi, B_lo
 constexpr int NUM_THREADS = 384;
@@ -106,14 +113,15 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
-// K-major, SWIZZLE_128B smem operand descriptor (rows of 128 B, 8-row groups 1024 B apart)
+// K-major swizzled smem operand descriptor: rows of BK*4 bytes, 8-row groups
+// 8*BK*4 bytes apart (SWIZZLE_128B for 128 B rows, SWIZZLE_64B for 64 B rows)
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)1u << 16;           // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024u >> 4) << 32; // SBO
-    d |= (uint64_t)1u << 46;           // descriptor version (sm_100)
-    d |= (uint64_t)2u << 61;           // SWIZZLE_128B
+    d |= (uint64_t)1u << 16;                        // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8u * BK * 4u) >> 4) << 32;     // SBO
+    d |= (uint64_t)1u << 46;                        // descriptor version (sm_100)
+    d |= (uint64_t)(BK == 32 ? 2u : 4u) << 61;      // SWIZZLE_128B / SWIZZLE_64B
     return d;
 }
 // kind::tf32, D=F32, A=B=TF32, both K-major, N=BN, M=BM
@@ -371,7 +379,8 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K
     cuuint32_t box[3] = {BK, (cuuint32_t)BM, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     NAO_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return NAO_OK;
