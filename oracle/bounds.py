@@ -19,7 +19,7 @@ _SQRT_2_OVER_PI = math.sqrt(2.0 / math.pi)  # engine.py:23
 _GELU_COEFF = 0.044715  # engine.py:24
 
 DATA_MOVEMENT_KINDS = frozenset({"concat", "slice", "reshape", "embedding"})  # graph.py:27
-EXT_DATA_MOVEMENT_KINDS = frozenset({"transpose", "maxpool2d"})  # extensions
+EXT_DATA_MOVEMENT_KINDS = frozenset({"transpose", "maxpool2d", "upsample2x"})  # extensions
 SINGLE_ROUNDING_KINDS = frozenset({"add", "sub", "mul", "div", "neg"})  # bounds.py:172
 INTRINSIC_KINDS = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})  # :173
 
@@ -201,6 +201,8 @@ def apply_op(node, arrays, fma=False) -> np.ndarray:
                                   int(node.attr("pad", 0)))
         out = matmul_value(col, w.reshape(w.shape[0], -1), True, fma)
         return np.ascontiguousarray(out.reshape(B, OH, OW, w.shape[0]).transpose(0, 3, 1, 2))
+    if kind == "upsample2x":  # extension: nearest-neighbour 2x
+        return np.repeat(np.repeat(arrays[0], 2, axis=-2), 2, axis=-1)
     if kind == "maxpool2d":  # extension: exact max over windows (padding = -inf)
         x = arrays[0]
         k, st, pd = int(node.attr("k", 2)), int(node.attr("stride", 2)), int(node.attr("pad", 0))

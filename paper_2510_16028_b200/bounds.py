@@ -34,7 +34,8 @@ from .tensor import Tensor
 FP32_UNIT_ROUNDOFF = 2.0 ** -24
 SINGLE_ROUNDING_KINDS = frozenset({"add", "sub", "mul", "div", "neg"})
 INTRINSIC_KINDS = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})
-ZERO_BOUND_KINDS = DATA_MOVEMENT_KINDS | {"transpose", "relu", "max", "min", "maxpool2d"}
+ZERO_BOUND_KINDS = DATA_MOVEMENT_KINDS | {"transpose", "relu", "max", "min", "maxpool2d",
+                                          "upsample2x"}
 
 
 @dataclass(frozen=True)
@@ -329,6 +330,8 @@ def apply_value(node, xs, profile) -> torch.Tensor:
             out = matmul_value(col, w.reshape(w.shape[0], -1), profile, transpose_b=True)
             return out.reshape(B, OH, OW, w.shape[0]).permute(0, 3, 1, 2).contiguous()
         return torch.nn.functional.conv2d(x, w, stride=st, padding=pd)
+    if kind == "upsample2x":  # extension: nearest-neighbour, pure data movement
+        return xs[0].repeat_interleave(2, dim=-2).repeat_interleave(2, dim=-1).contiguous()
     if kind == "maxpool2d":
         return torch.nn.functional.max_pool2d(xs[0], int(node.attr("k", 2)),
                                               int(node.attr("stride", 2)),

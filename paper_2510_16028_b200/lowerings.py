@@ -386,3 +386,170 @@ def build_resnet18(batch: int = 32, side: int = 224, n_classes: int = 1000, widt
     g = build_graph(nodes, [("img", (batch, 3, side, side))], _LazyWeights(specs, device, seed),
                     [out])
     return ModelSpec("resnet18", g, {"img": ("uniform", -1.0, 1.0)}, n_classes)
+
+
+# ------------------------------------------------------------ SD-UNet
+
+@dataclass(frozen=True)
+class UNetShape:
+    name: str = "sd15-unet"
+    batch: int = 8
+    latent: int = 64
+    in_ch: int = 4
+    channels: tuple = (320, 640, 1280, 1280)
+    attn_levels: tuple = (True, True, True, False)
+    heads: int = 8
+    ctx_len: int = 77
+    ctx_dim: int = 768
+    groups: int = 32
+    temb: int = 1280
+    layers_per_block: int = 2
+
+
+SD15_UNET = UNetShape()
+
+
+def build_unet(shape: UNetShape = SD15_UNET, device: str = "cuda", seed: int = 0) -> ModelSpec:
+    """SD-1.5-shaped UNet denoising step (BASELINE config 5) on reference kinds
+    + conv2d / upsample2x extensions: GroupNorm = reshape + layernorm + reshape +
+    mul + add; SiLU; ResBlocks with the time-embedding projection broadcast-added;
+    transformer blocks (LayerNorm, self-attention, cross-attention to the text
+    context, tanh-GELU GEGLU feed-forward); skip concats; nearest 2x upsampling.
+    The sinusoidal timestep embedding (t = 500) is a constant input feature."""
+    B, C0 = shape.batch, shape.channels[0]
+    specs, nodes = {}, []
+
+    def add(name, kind, inputs, attrs=None):
+        nodes.append(make_node(name, kind, inputs, attrs))
+        return node_ref(len(nodes) - 1)
+
+    def W(name, shp, kind="uniform", a=None):
+        if a is None:
+            fan = int(np.prod(shp[1:])) if len(shp) == 4 else shp[0]
+            a = 1.0 / math.sqrt(fan)
+        specs[name] = (tuple(shp), kind, a)
+        return weight_ref(name)
+
+    def conv(name, x, cin, cout, k=3, stride=1):
+        y = add(name, "conv2d", [x, W(f"{name}.w", (cout, cin, k, k))],
+                {"stride": stride, "pad": k // 2})
+        return add(f"{name}_b", "add", [y, W(f"{name}.b", (1, cout, 1, 1), "uniform", 0.02)])
+
+    def groupnorm(name, x, c, hw):
+        g = shape.groups
+        y = add(f"{name}_g", "reshape", [x], {"shape": f"{B},{g},{(c // g) * hw}"})
+        y = add(f"{name}_ln", "layernorm", [y], {"axis": -1, "eps": 1e-5})
+        y = add(f"{name}_r", "reshape", [y], {"shape": f"{B},{c},{int(math.isqrt(hw))},{int(math.isqrt(hw))}"})
+        y = add(f"{name}_s", "mul", [y, W(f"{name}.g", (1, c, 1, 1), "uniform", 1.0)])
+        return add(f"{name}_t", "add", [y, W(f"{name}.bt", (1, c, 1, 1), "uniform", 0.1)])
+
+    def resblock(name, x, cin, cout, side, temb):
+        h = groupnorm(f"{name}.gn1", x, cin, side * side)
+        h = add(f"{name}.act1", "silu", [h])
+        h = conv(f"{name}.conv1", h, cin, cout)
+        t = add(f"{name}.tact", "silu", [temb])
+        t = add(f"{name}.tproj", "linear", [t, W(f"{name}.tw", (shape.temb, cout)),
+                                           W(f"{name}.tb", (cout,), "uniform", 0.02)])
+        t = add(f"{name}.t4", "reshape", [t], {"shape": f"{B},{cout},1,1"})
+        h = add(f"{name}.tadd", "add", [h, t])
+        h = groupnorm(f"{name}.gn2", h, cout, side * side)
+        h = add(f"{name}.act2", "silu", [h])
+        h = conv(f"{name}.conv2", h, cout, cout)
+        skip = x if cin == cout else conv(f"{name}.skip", x, cin, cout, k=1)
+        return add(f"{name}.res", "add", [h, skip])
+
+    def attention(name, xq, xkv, c, n_q, n_kv, kv_dim):
+        hd = c // shape.heads
+        q = add(f"{name}.q", "matmul", [xq, W(f"{name}.wq", (c, c))])
+        k = add(f"{name}.k", "matmul", [xkv, W(f"{name}.wk", (kv_dim, c))])
+        v = add(f"{name}.v", "matmul", [xkv, W(f"{name}.wv", (kv_dim, c))])
+        q = add(f"{name}.q4", "reshape", [q], {"shape": f"{B},{n_q},{shape.heads},{hd}"})
+        k = add(f"{name}.k4", "reshape", [k], {"shape": f"{B},{n_kv},{shape.heads},{hd}"})
+        v = add(f"{name}.v4", "reshape", [v], {"shape": f"{B},{n_kv},{shape.heads},{hd}"})
+        q = add(f"{name}.qt", "transpose", [q], {"perm": "0,2,1,3"})
+        k = add(f"{name}.kt", "transpose", [k], {"perm": "0,2,1,3"})
+        v = add(f"{name}.vt", "transpose", [v], {"perm": "0,2,1,3"})
+        s = add(f"{name}.scores", "matmul", [q, k], {"transpose_b": 1})
+        s = add(f"{name}.scaled", "mul", [s, W(f"{name}.scale", (1,), "const", [1.0 / math.sqrt(hd)])])
+        p = add(f"{name}.probs", "softmax", [s], {"axis": -1})
+        o = add(f"{name}.ctx", "matmul", [p, v])
+        o = add(f"{name}.ctxt", "transpose", [o], {"perm": "0,2,1,3"})
+        o = add(f"{name}.ctx2", "reshape", [o], {"shape": f"{B},{n_q},{c}"})
+        o = add(f"{name}.o", "matmul", [o, W(f"{name}.wo", (c, c))])
+        return add(f"{name}.ob", "add", [o, W(f"{name}.bo", (c,), "uniform", 0.02)])
+
+    def transformer(name, x, c, side):
+        n = side * side
+        h = groupnorm(f"{name}.gn", x, c, n)
+        h = add(f"{name}.flat", "reshape", [h], {"shape": f"{B},{c},{n}"})
+        h = add(f"{name}.tok", "transpose", [h], {"perm": "0,2,1"})
+        h = add(f"{name}.pin", "matmul", [h, W(f"{name}.pin.w", (c, c))])
+        a = add(f"{name}.ln1", "layernorm", [h], {"axis": -1, "eps": 1e-5})
+        h = add(f"{name}.r1", "add", [h, attention(f"{name}.sa", a, a, c, n, n, c)])
+        a = add(f"{name}.ln2", "layernorm", [h], {"axis": -1, "eps": 1e-5})
+        h = add(f"{name}.r2", "add", [h, attention(f"{name}.ca", a, input_ref("context"), c, n,
+                                                     shape.ctx_len, shape.ctx_dim)])
+        a = add(f"{name}.ln3", "layernorm", [h], {"axis": -1, "eps": 1e-5})
+        ff = add(f"{name}.ff1", "linear", [a, W(f"{name}.ff1.w", (c, 8 * c)),
+                                          W(f"{name}.ff1.b", (8 * c,), "uniform", 0.02)])
+        xg = add(f"{name}.ffx", "slice", [ff], {"axis": -1, "start": 0, "stop": 4 * c})
+        gt = add(f"{name}.ffg", "slice", [ff], {"axis": -1, "start": 4 * c, "stop": 8 * c})
+        gt = add(f"{name}.ffact", "gelu", [gt])
+        ff = add(f"{name}.geglu", "mul", [xg, gt])
+        ff = add(f"{name}.ff2", "linear", [ff, W(f"{name}.ff2.w", (4 * c, c)),
+                                          W(f"{name}.ff2.b", (c,), "uniform", 0.02)])
+        h = add(f"{name}.r3", "add", [h, ff])
+        h = add(f"{name}.pout", "matmul", [h, W(f"{name}.pout.w", (c, c))])
+        h = add(f"{name}.untok", "transpose", [h], {"perm": "0,2,1"})
+        h = add(f"{name}.unflat", "reshape", [h], {"shape": f"{B},{c},{side},{side}"})
+        return add(f"{name}.res", "add", [h, x])
+
+    # timestep embedding: sinusoid(t) is a constant feature, then MLP
+    half = C0 // 2
+    freqs = np.exp(-math.log(10000.0) * np.arange(half) / half)
+    sin = np.concatenate([np.cos(500.0 * freqs), np.sin(500.0 * freqs)]).astype(np.float32)
+    specs["tsin"] = ((B, C0), "const", np.tile(sin, B))
+    temb = add("temb1", "linear", [weight_ref("tsin"), W("temb1.w", (C0, shape.temb)),
+                                   W("temb1.b", (shape.temb,), "uniform", 0.02)])
+    temb = add("temb_act", "silu", [temb])
+    temb = add("temb2", "linear", [temb, W("temb2.w", (shape.temb, shape.temb)),
+                                   W("temb2.b", (shape.temb,), "uniform", 0.02)])
+    h = conv("conv_in", input_ref("latent"), shape.in_ch, C0)
+    side, cin = shape.latent, C0
+    skips = [(h, cin, side)]
+    for lvl, (c, attn) in enumerate(zip(shape.channels, shape.attn_levels)):
+        for j in range(shape.layers_per_block):
+            h = resblock(f"down{lvl}.res{j}", h, cin, c, side, temb)
+            cin = c
+            if attn:
+                h = transformer(f"down{lvl}.tf{j}", h, c, side)
+            skips.append((h, c, side))
+        if lvl < len(shape.channels) - 1:
+            h = conv(f"down{lvl}.ds", h, c, c, k=3, stride=2)
+            side //= 2
+            skips.append((h, c, side))
+    c = shape.channels[-1]
+    h = resblock("mid.res0", h, c, c, side, temb)
+    h = transformer("mid.tf", h, c, side)
+    h = resblock("mid.res1", h, c, c, side, temb)
+    for lvl in reversed(range(len(shape.channels))):
+        c = shape.channels[lvl]
+        for j in range(shape.layers_per_block + 1):
+            s_ref, s_c, _ = skips.pop()
+            h = add(f"up{lvl}.cat{j}", "concat", [h, s_ref], {"axis": 1})
+            h = resblock(f"up{lvl}.res{j}", h, cin + s_c, c, side, temb)
+            cin = c
+            if shape.attn_levels[lvl]:
+                h = transformer(f"up{lvl}.tf{j}", h, c, side)
+        if lvl > 0:
+            h = add(f"up{lvl}.us", "upsample2x", [h])
+            side *= 2
+            h = conv(f"up{lvl}.usconv", h, c, c)
+    h = groupnorm("out.gn", h, cin, side * side)
+    h = add("out.act", "silu", [h])
+    out = conv("conv_out", h, cin, shape.in_ch)
+    weights = _LazyWeights(specs, device, seed)
+    g = build_graph(nodes, [("latent", (B, shape.in_ch, shape.latent, shape.latent)),
+                            ("context", (B, shape.ctx_len, shape.ctx_dim))], weights, [out])
+    return ModelSpec(shape.name, g, {"latent": ("uniform", -1.0, 1.0),
+                                     "context": ("uniform", -1.0, 1.0)}, meta={"shape": shape})

@@ -97,3 +97,25 @@ def test_gpt2_small_full_config_flags_only_the_fault():
     from paper_2510_16028_b200.lowerings import GPT2_SMALL, build_decoder
     spec = build_decoder(GPT2_SMALL)
     assert _flagged(spec, "l5_fc") == ["l5_fc"]
+
+
+def test_unet_small_node_by_node():
+    from paper_2510_16028_b200.engine import NATIVE
+    from paper_2510_16028_b200.lowerings import UNetShape, build_unet
+    from paper_2510_16028_b200.tensor import Rng
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    shape = UNetShape(batch=1, latent=16, channels=(32, 64, 64, 64), heads=2, ctx_len=7,
+                      ctx_dim=24, groups=8, temb=64)
+    spec = build_unet(shape, seed=3)
+    _node_by_node(spec.graph, spec.make_inputs(Rng(6)), NATIVE)
+
+
+def test_unet_sd15_shape_flags_only_the_fault():
+    """SD-1.5-shaped UNet at the BASELINE width (320/640/1280/1280, 8 heads,
+    GroupNorm 32, 77x768 context) on a 32x32 latent, batch 1 (the 64x64 B=8
+    config is the 8-GPU batch-sharded bench shape; per-sample work is the same graph)."""
+    import dataclasses
+    from paper_2510_16028_b200.lowerings import SD15_UNET, build_unet
+    spec = build_unet(dataclasses.replace(SD15_UNET, batch=1, latent=32))
+    assert _flagged(spec, "down1.res0.conv2") == ["down1.res0.conv2"]
