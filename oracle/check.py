@@ -102,3 +102,28 @@ def leaf_check(local, claimed, eps) -> dict:
     return {"n_violations": int(np.count_nonzero(viol)),
             "max_ratio": float(ratio.max()) if ratio.size else 0.0,
             "any_violation": bool(viol.any())}
+
+
+def calibrate(graph, dataset, fmas, grid=PERCENTILE_GRID, epsilon=DEFAULT_EPSILON):
+    """calibration.py:70-114 restated for the sequential profile family
+    (fmas: list of bool, one simulated device each): max envelope over
+    (input, pair) of abs profiles and of rel profiles in both orientations."""
+    from . import bounds as OB
+    n_nodes = len(graph.nodes)
+    G = len(grid)
+    abs_env = [np.zeros(G) for _ in range(n_nodes)]
+    rel_env = [np.zeros(G) for _ in range(n_nodes)]
+    for sample in dataset:
+        traces = [OB.co_execute(graph, sample, OB.FpModel(), fma=f)[0] for f in fmas]
+        for i in range(n_nodes):
+            flats = [t[i].reshape(-1).astype(np.float64) for t in traces]
+            for j in range(len(fmas)):
+                for k in range(j + 1, len(fmas)):
+                    diff = np.abs(flats[j] - flats[k])
+                    stacked = np.stack([diff, diff / (np.abs(flats[j]) + epsilon),
+                                        diff / (np.abs(flats[k]) + epsilon)])
+                    profs = np.percentile(stacked, list(grid), axis=1, method="linear")
+                    np.maximum(abs_env[i], profs[:, 0], out=abs_env[i])
+                    np.maximum(rel_env[i], profs[:, 1], out=rel_env[i])
+                    np.maximum(rel_env[i], profs[:, 2], out=rel_env[i])
+    return abs_env, rel_env

@@ -166,3 +166,93 @@ def build_thresholds(names, abs_env, rel_env, grid=PERCENTILE_GRID, alpha: float
     ops = [OpThresholds(n, alpha * np.asarray(a, np.float64), alpha * np.asarray(r, np.float64))
            for n, a, r in zip(names, abs_env, rel_env)]
     return ThresholdSet(alpha=alpha, epsilon=epsilon, grid=tuple(grid), ops=ops)
+
+
+# ------------------------------------------------------------ calibration
+# calibrate / build_thresholds on the GPU.
+
+@dataclass
+class EnvelopeSet:
+    """calibration.py:58-67."""
+    grid: tuple
+    abs_env: list
+    rel_env: list
+    node_names: list
+    per_sample_abs: list
+
+
+def calibrate(g, dataset, profiles, grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON,
+              device="cuda") -> EnvelopeSet:
+    """calibration.py:70-114: every input under every profile; per node the
+    pointwise max over (input, profile pair) of the exact abs percentile
+    profile and of the rel profile in BOTH orientations.  The profiles run in
+    lockstep node by node, so only one node's values per profile are live
+    beyond their last use (no full traces)."""
+    from .bounds import apply_value, reduce_device, softmax_device, layernorm_device, FpModel
+    from .engine import require_supported
+    from .executor import last_uses
+    from .graph import parse_ref
+    if len(profiles) < 2:
+        raise ValueError("calibration requires at least 2 device profiles")
+    if not dataset:
+        raise ValueError("calibration requires at least 1 input")
+    for p in profiles:
+        require_supported(p)
+    n_nodes, G = g.n_nodes, len(grid)
+    dev = torch.device(device)
+    abs_env = [torch.zeros(G, dtype=torch.float64, device=dev) for _ in range(n_nodes)]
+    rel_env = [torch.zeros(G, dtype=torch.float64, device=dev) for _ in range(n_nodes)]
+    per_sample_abs = [[] for _ in range(n_nodes)]
+    last = last_uses(g)
+    model = FpModel()
+
+    def value(node, xs, prof):
+        k = node.kind
+        if k == "softmax":
+            return softmax_device(xs[0], int(node.attr("axis", -1)), model, False)[0]
+        if k == "layernorm":
+            return layernorm_device(xs[0], int(node.attr("axis", -1)),
+                                    float(node.attr("eps", 1e-5)), model, False)[0]
+        if k in ("sum", "mean", "max", "min"):
+            return reduce_device(k, xs[0], int(node.attr("axis", -1)), model, False)[0]
+        return apply_value(node, xs, prof)
+
+    for sample in dataset:
+        vals = [dict() for _ in profiles]
+        for node in g.nodes:
+            outs = []
+            for pi, prof in enumerate(profiles):
+                xs = []
+                for ref in node.inputs:
+                    cat, key = parse_ref(ref)
+                    xs.append(vals[pi][key] if cat == "node" else to_device(
+                        sample[key] if cat == "input" else g.weights[key], dev))
+                y = value(node, xs, prof).contiguous()
+                vals[pi][node.index] = y
+                outs.append(y.reshape(-1))
+            i = node.index
+            sample_abs = torch.zeros(G, dtype=torch.float64, device=dev)
+            for j in range(len(profiles)):
+                for k in range(j + 1, len(profiles)):
+                    pa, pr_j = error_profiles_device(outs[j], outs[k], grid, epsilon)
+                    _, pr_k = error_profiles_device(outs[k], outs[j], grid, epsilon)
+                    torch.maximum(abs_env[i], pa, out=abs_env[i])
+                    torch.maximum(rel_env[i], pr_j, out=rel_env[i])
+                    torch.maximum(rel_env[i], pr_k, out=rel_env[i])
+                    torch.maximum(sample_abs, pa, out=sample_abs)
+            per_sample_abs[i].append(sample_abs)
+            for pi in range(len(profiles)):
+                for ref in node.inputs:
+                    cat, key = parse_ref(ref)
+                    if cat == "node" and last.get(key, -1) == node.index:
+                        vals[pi].pop(key, None)
+    return EnvelopeSet(grid=tuple(grid), abs_env=[e.cpu().numpy() for e in abs_env],
+                       rel_env=[e.cpu().numpy() for e in rel_env],
+                       node_names=[n.name for n in g.nodes],
+                       per_sample_abs=[[s.cpu().numpy() for s in row] for row in per_sample_abs])
+
+
+def build_thresholds_from_envelopes(env: EnvelopeSet, alpha: float = DEFAULT_ALPHA,
+                                    epsilon: float = DEFAULT_EPSILON) -> ThresholdSet:
+    """calibration.py:194-203."""
+    return build_thresholds(env.node_names, env.abs_env, env.rel_env, env.grid, alpha, epsilon)

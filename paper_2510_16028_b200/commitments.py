@@ -284,3 +284,80 @@ def trace_root(tensor_roots, alg=SHA256) -> bytes:
     else:
         leaves = list(tensor_roots)
     return build_tree(leaves, alg).root
+
+
+# ------------------------------------------- dispute-time commitments
+# SURVEY.md 8(f) row 2.  Whole-tensor SHA-256 is one sequential Merkle-Damgard
+# stream per tensor, so it parallelises across tensors only: host hashlib
+# (releases the GIL) on a thread pool, exactly the reference's algorithm.
+
+def _digests(tensors) -> list:
+    from concurrent.futures import ThreadPoolExecutor
+    blobs = [canon_tensor(t) for t in tensors]
+    if len(blobs) <= 1:
+        return [sha256(b) for b in blobs]
+    with ThreadPoolExecutor(max_workers=min(16, len(blobs))) as ex:
+        return list(ex.map(sha256, blobs))
+
+
+def interface_hash(tensors) -> bytes:
+    """H over the concatenated per-tensor digests (commitments.py:172-174)."""
+    return sha256(b"".join(_digests(list(tensors))))
+
+
+def op_signature(node) -> bytes:
+    """commitments.py:68-78."""
+    return canonical_json_bytes({"name": node.name, "op": "call", "target": node.kind,
+                                 "args": list(node.inputs),
+                                 "kwargs": {k: v for k, v in node.attrs}})
+
+
+def weight_tree(weights: dict, alg=SHA256):
+    """commitments.py:177-181 (leaves = whole canon tensors, lexicographic names)."""
+    names = sorted(weights)
+    return build_tree([canon_tensor(weights[n]) for n in names], alg), names
+
+
+def graph_tree(g, alg=SHA256):
+    """commitments.py:184-185."""
+    return build_tree([op_signature(n) for n in g.nodes], alg)
+
+
+@dataclass(frozen=True)
+class Commitment:
+    """commitments.py:188-219."""
+    c0: bytes
+    r_w: bytes
+    r_g: bytes
+    r_e: bytes
+    input_digest: bytes
+    output_digest: bytes
+    meta: dict
+
+
+def _meta_bytes(meta: dict) -> bytes:
+    for k, v in meta.items():
+        if not isinstance(k, str) or not isinstance(v, (str, int, float, bool)):
+            raise ValueError(f"malformed meta entry {k!r}: {v!r}")
+    return canonical_json_bytes(meta)
+
+
+def make_commitment(r_w, r_g, r_e, input_tensors, output_tensors, meta) -> Commitment:
+    """commitments.py:229-235: c0 = H(r_w || r_g || h_x || h_y || meta)."""
+    h_x = interface_hash(input_tensors)
+    h_y = interface_hash(output_tensors)
+    c0 = sha256(r_w + r_g + h_x + h_y + _meta_bytes(meta))
+    return Commitment(c0=c0, r_w=r_w, r_g=r_g, r_e=r_e, input_digest=h_x, output_digest=h_y,
+                      meta=meta)
+
+
+def verify_commitment(c: Commitment, input_tensors=None, output_tensors=None) -> bool:
+    """commitments.py:238-247."""
+    h_x = interface_hash(input_tensors) if input_tensors is not None else c.input_digest
+    h_y = interface_hash(output_tensors) if output_tensors is not None else c.output_digest
+    if h_x != c.input_digest or h_y != c.output_digest:
+        return False
+    try:
+        return sha256(c.r_w + c.r_g + h_x + h_y + _meta_bytes(c.meta)) == c.c0
+    except ValueError:
+        return False
