@@ -199,6 +199,7 @@ def run_ours(args):
         return plain_forward(g, ids, dev, start, end, frontier)
 
     stream = torch.cuda.current_stream(dev)
+    host_ms = {}  # host enqueue time per step (< ms_per_step: the GPU is the bound)
 
     def timed(fn, k):
         if world > 1:
@@ -206,10 +207,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(k):
             out = fn()
             del out
         e1.record(stream)
+        host_ms[fn.__name__] = (time.perf_counter() - h0) * 1000.0 / k
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -383,6 +386,7 @@ def run_ours(args):
                    "parallelism": f"layer-sharded x{world}" if world > 1 else "single",
                    "l2": "inputs/weights (32.8 GB) far larger than L2 (126 MB)"},
         "plain_fwd_ms": round(t_plain, 2), "verified_fwd_ms": round(t_ver, 2),
+        "host_enqueue_ms": {k: round(v, 2) for k, v in host_ms.items()},
         "merkle_gbs": round(merkle_gbs, 1) if merkle_gbs else None,
         "committed_gb_per_step": round(commit_bytes_per_step / 1e9, 2),
         "gemm_tflop_per_step": round(stats.gemm_flops / 1e12, 2),

@@ -160,7 +160,7 @@ __device__ void finalize_targets(const CheckParams& p, CheckAccum* acc, CheckSme
 }
 
 template <int EPSK>
-__global__ void __launch_bounds__(kCheckThreads) k_check(const __grid_constant__ CheckParams p,
+__global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constant__ CheckParams p,
                                                          CheckAccum* __restrict__ acc,
                                                          nao_check_result* __restrict__ out) {
     __shared__ CheckSmem sm;
@@ -243,18 +243,22 @@ __global__ void __launch_bounds__(kCheckThreads) k_check(const __grid_constant__
     const int64_t nvec = n >> 2;
     const float4* yl = reinterpret_cast<const float4*>(p.local);
     const float4* ycl = reinterpret_cast<const float4*>(p.claimed);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t wb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wb < nvec;
-         wb += stride) {  // warp-uniform trip count (ballots)
-        const int64_t v = wb + lane;
+    // Each warp walks 64 consecutive float4 pairs per step (lanes take v and
+    // v + 32) and prefetches the next step's pairs before compacting the
+    // current ones, so ~128 B per lane stay in flight while the queue drains.
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
+    int64_t wb = (int64_t)blockIdx.x * blockDim.x * 2 + (int64_t)w * 64;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 na0 = zero4, nc0 = zero4, na1 = zero4, nc1 = zero4;
+    if (wb + lane < nvec) { na0 = __ldg(yl + wb + lane); nc0 = __ldg(ycl + wb + lane); }
+    if (wb + 32 + lane < nvec) { na1 = __ldg(yl + wb + 32 + lane); nc1 = __ldg(ycl + wb + 32 + lane); }
+    auto group = [&](const float4 a, const float4 c, const int64_t v) {
         const bool ok = v < nvec;
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
-        if (ok) { a = __ldg(yl + v); c = __ldg(ycl + v); }
         const bool z0 = (a.x == c.x) & isfinite(a.x), z1 = (a.y == c.y) & isfinite(a.y);
         const bool z2 = (a.z == c.z) & isfinite(a.z), z3 = (a.w == c.w) & isfinite(a.w);
         const bool all_eq = z0 & z1 & z2 & z3;
         if (ok && all_eq) nzero += 4;
-        if (__all_sync(0xffffffffu, all_eq || !ok)) continue;
+        if (__all_sync(0xffffffffu, all_eq || !ok)) return;
         double e0 = 0, e1 = 0, e2 = 0, e3 = 0;
         if (ok && !all_eq) {  // eps is only read where a difference exists
             if (EPSK == NAO_EPS_TENSOR_F32) {
@@ -280,6 +284,14 @@ __global__ void __launch_bounds__(kCheckThreads) k_check(const __grid_constant__
         push(live && !z1, a.y, c.y, e1);
         push(live && !z2, a.z, c.z, e2);
         push(live && !z3, a.w, c.w, e3);
+    };
+    for (; wb < nvec; wb += stride) {  // warp-uniform trip count (ballots)
+        const float4 a0 = na0, c0 = nc0, a1 = na1, c1 = nc1;
+        const int64_t wn = wb + stride;
+        if (wn + lane < nvec) { na0 = __ldg(yl + wn + lane); nc0 = __ldg(ycl + wn + lane); }
+        if (wn + 32 + lane < nvec) { na1 = __ldg(yl + wn + 32 + lane); nc1 = __ldg(ycl + wn + 32 + lane); }
+        group(a0, c0, wb + lane);
+        group(a1, c1, wb + 32 + lane);
     }
     // scalar tail (n % 4): first warp of block 0
     if (blockIdx.x == 0 && w == 0) {
@@ -499,9 +511,10 @@ int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind,
         p.lpos_abs[i] = (int)(std::lower_bound(sa, sa + n_grid, ea[i]) - sa);
         p.lpos_rel[i] = (int)(std::lower_bound(sr, sr + n_grid, er[i]) - sr);
     }
-    const int64_t warps_needed = ((n >> 2) + 31) / 32;
+    // one resident wave: 3 CTAs per SM (launch bounds), each warp 64 float4 per step
+    const int64_t warps_needed = ((n >> 2) + 63) / 64;
     const int blocks = (int)std::max<int64_t>(
-        1, std::min<int64_t>((warps_needed + kCheckWarps - 1) / kCheckWarps, kNumSMs * 6));
+        1, std::min<int64_t>((warps_needed + kCheckWarps - 1) / kCheckWarps, kNumSMs * 3));
     switch (eps_kind) {
         case NAO_EPS_TENSOR_F32:
             k_check<NAO_EPS_TENSOR_F32><<<blocks, kCheckThreads, 0, st>>>(p, acc, result); break;

@@ -128,9 +128,6 @@ __device__ __forceinline__ void sha256_tagged(const Load& ld, uint32_t nw, uint3
 
 // ---------------------------------------------------------------- Keccak-f
 
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int n) {
-    return (x << n) | (x >> (64 - n));
-}
 
 __constant__ uint64_t c_keccak_rc[24] = {
     0x0000000000000001ull, 0x0000000000008082ull, 0x800000000000808aull,
@@ -142,58 +139,149 @@ __constant__ uint64_t c_keccak_rc[24] = {
     0x000000000000800aull, 0x800000008000000aull, 0x8000000080008081ull,
     0x8000000000008080ull, 0x0000000080000001ull, 0x8000000080008008ull};
 
-__device__ __forceinline__ uint64_t chi(uint64_t a, uint64_t b, uint64_t c) { return a ^ (~b & c); }
 
-// Keccak-f[1600]; A[x + 5y].
-__device__ __forceinline__ void keccak_f1600(uint64_t A[25]) {
+// Keccak-f[1600]; A[x + 5y].  The permutation runs on 32-bit halves: a 64-bit
+// rotation is two funnel shifts (SHF.L.W) -- or a free half swap -- and the
+// 3-input XOR / chi terms map to one LOP3 per half (~180 ALU ops per round).
+struct Lane { uint32_t lo, hi; };
+__device__ __forceinline__ Lane lxor(Lane a, Lane b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
+
+template <int N>
+__device__ __forceinline__ Lane lrot(Lane x) {
+    static_assert(N > 0 && N < 64, "rotation");
+    if constexpr (N == 32) {
+        return {x.hi, x.lo};
+    } else if constexpr (N < 32) {
+        return {__funnelshift_l(x.hi, x.lo, N), __funnelshift_l(x.lo, x.hi, N)};
+    } else {
+        return {__funnelshift_l(x.lo, x.hi, N - 32), __funnelshift_l(x.hi, x.lo, N - 32)};
+    }
+}
+// The same rotation on the FMA pipe (the ALU pipe is the Keccak bound):
+// IMAD.WIDE by 2^M from constant memory (opaque to ptxas, so it is not
+// strength-reduced back to ALU shifts); the two halves never overlap, so the
+// ORs are additions and fold into the multiply-adds.
+__constant__ uint32_t c_pow2[32] = {
+    1u << 0,  1u << 1,  1u << 2,  1u << 3,  1u << 4,  1u << 5,  1u << 6,  1u << 7,
+    1u << 8,  1u << 9,  1u << 10, 1u << 11, 1u << 12, 1u << 13, 1u << 14, 1u << 15,
+    1u << 16, 1u << 17, 1u << 18, 1u << 19, 1u << 20, 1u << 21, 1u << 22, 1u << 23,
+    1u << 24, 1u << 25, 1u << 26, 1u << 27, 1u << 28, 1u << 29, 1u << 30, 1u << 31};
+template <int N>
+__device__ __forceinline__ Lane lrot_fma(Lane x) {
+    static_assert(N > 0 && N < 64 && N != 32, "rotation");
+    constexpr int M = N < 32 ? N : N - 32;
+    const uint32_t L = N < 32 ? x.lo : x.hi, H = N < 32 ? x.hi : x.lo;
+    const uint32_t p = c_pow2[M];
+    const uint64_t P = (uint64_t)L * p;                 // {L << M, L >> (32-M)}
+    const uint64_t Q = (uint64_t)H * p + (P >> 32);     // {(H << M) | (L >> (32-M)), H >> (32-M)}
+    uint32_t lo;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lo) : "r"((uint32_t)(Q >> 32)), "r"(c_pow2[0]),
+        "r"((uint32_t)P));
+    return {lo, (uint32_t)Q};
+}
+// 32-bit form: (H << M) | (L >> (32-M)) = H * 2^M + umulhi(L, 2^M), no register pairs
+template <int N>
+__device__ __forceinline__ Lane lrot_fma32(Lane x) {
+    static_assert(N > 0 && N < 64 && N != 32, "rotation");
+    constexpr int M = N < 32 ? N : N - 32;
+    const uint32_t L = N < 32 ? x.lo : x.hi, H = N < 32 ? x.hi : x.lo;
+    const uint32_t p = c_pow2[M];
+    return {L * p + __umulhi(H, p), H * p + __umulhi(L, p)};
+}
+template <int N, int FMA>  // 0 ALU funnel shifts, 1 IMAD.WIDE form, 2 32-bit IMAD form
+__device__ __forceinline__ Lane lrot_sel(Lane x) {
+    if constexpr (FMA == 1 && N != 32) return lrot_fma<N>(x);
+    else if constexpr (FMA == 2 && N != 32) return lrot_fma32<N>(x);
+    else return lrot<N>(x);
+}
+#ifndef NAO_KECCAK_FMA_MASK
+#define NAO_KECCAK_FMA_MASK 0u
+#endif
+
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// a ^ c ^ r as one LOP3 per half (theta's D = c ^ r is never materialised)
+__device__ __forceinline__ Lane lxor3(Lane a, Lane c, Lane r) {
+    return {xor3(a.lo, c.lo, r.lo), xor3(a.hi, c.hi, r.hi)};
+}
+__device__ __forceinline__ Lane lxor5(Lane a, Lane b, Lane c, Lane d, Lane e) {
+    return {xor3(xor3(a.lo, b.lo, c.lo), d.lo, e.lo), xor3(xor3(a.hi, b.hi, c.hi), d.hi, e.hi)};
+}
+__device__ __forceinline__ Lane lchi(Lane a, Lane b, Lane c) {
+    return {a.lo ^ (~b.lo & c.lo), a.hi ^ (~b.hi & c.hi)};
+}
+
+// MASK bit j moves rotation j (0..23: rho in the order below, 24..28: theta)
+// to the FMA pipe; bit 31 picks the 32-bit IMAD form over IMAD.WIDE.
+template <uint32_t MASK>
+__device__ __forceinline__ void keccak_f1600_m(uint64_t Aw[25]) {
+    Lane A[25];
+#pragma unroll
+    for (int i = 0; i < 25; i++) A[i] = {(uint32_t)Aw[i], (uint32_t)(Aw[i] >> 32)};
 #pragma unroll 1
     for (int r = 0; r < 24; r++) {
-        uint64_t C0 = A[0] ^ A[5] ^ A[10] ^ A[15] ^ A[20];
-        uint64_t C1 = A[1] ^ A[6] ^ A[11] ^ A[16] ^ A[21];
-        uint64_t C2 = A[2] ^ A[7] ^ A[12] ^ A[17] ^ A[22];
-        uint64_t C3 = A[3] ^ A[8] ^ A[13] ^ A[18] ^ A[23];
-        uint64_t C4 = A[4] ^ A[9] ^ A[14] ^ A[19] ^ A[24];
-        uint64_t D0 = C4 ^ rotl64(C1, 1), D1 = C0 ^ rotl64(C2, 1), D2 = C1 ^ rotl64(C3, 1);
-        uint64_t D3 = C2 ^ rotl64(C4, 1), D4 = C3 ^ rotl64(C0, 1);
-        // theta + rho + pi:  B[y + 5*((2x+3y)%5)] = rotl(A[x+5y] ^ D[x], r[x][y])
-        uint64_t B00 = A[0] ^ D0;
-        uint64_t B10 = rotl64(A[6] ^ D1, 44);
-        uint64_t B20 = rotl64(A[12] ^ D2, 43);
-        uint64_t B30 = rotl64(A[18] ^ D3, 21);
-        uint64_t B40 = rotl64(A[24] ^ D4, 14);
-        uint64_t B01 = rotl64(A[3] ^ D3, 28);
-        uint64_t B11 = rotl64(A[9] ^ D4, 20);
-        uint64_t B21 = rotl64(A[10] ^ D0, 3);
-        uint64_t B31 = rotl64(A[16] ^ D1, 45);
-        uint64_t B41 = rotl64(A[22] ^ D2, 61);
-        uint64_t B02 = rotl64(A[1] ^ D1, 1);
-        uint64_t B12 = rotl64(A[7] ^ D2, 6);
-        uint64_t B22 = rotl64(A[13] ^ D3, 25);
-        uint64_t B32 = rotl64(A[19] ^ D4, 8);
-        uint64_t B42 = rotl64(A[20] ^ D0, 18);
-        uint64_t B03 = rotl64(A[4] ^ D4, 27);
-        uint64_t B13 = rotl64(A[5] ^ D0, 36);
-        uint64_t B23 = rotl64(A[11] ^ D1, 10);
-        uint64_t B33 = rotl64(A[17] ^ D2, 15);
-        uint64_t B43 = rotl64(A[23] ^ D3, 56);
-        uint64_t B04 = rotl64(A[2] ^ D2, 62);
-        uint64_t B14 = rotl64(A[8] ^ D3, 55);
-        uint64_t B24 = rotl64(A[14] ^ D4, 39);
-        uint64_t B34 = rotl64(A[15] ^ D0, 41);
-        uint64_t B44 = rotl64(A[21] ^ D1, 2);
+        const Lane C0 = lxor5(A[0], A[5], A[10], A[15], A[20]);
+        const Lane C1 = lxor5(A[1], A[6], A[11], A[16], A[21]);
+        const Lane C2 = lxor5(A[2], A[7], A[12], A[17], A[22]);
+        const Lane C3 = lxor5(A[3], A[8], A[13], A[18], A[23]);
+        const Lane C4 = lxor5(A[4], A[9], A[14], A[19], A[24]);
+        // theta + rho + pi:  B[y + 5*((2x+3y)%5)] = rotl(A[x+5y] ^ D[x], r[x][y]),
+        // D[x] = C[x-1] ^ rotl(C[x+1], 1)
+#define NAO_R(N, j) lrot_sel<N, ((MASK >> (j)) & 1u) ? ((MASK >> 31) ? 2 : 1) : 0>
+        const Lane R0 = NAO_R(1, 24)(C1), R1 = NAO_R(1, 25)(C2), R2 = NAO_R(1, 26)(C3),
+                   R3 = NAO_R(1, 27)(C4), R4 = NAO_R(1, 28)(C0);
+#define NAO_TH(i, x) lxor3(A[i], C##x##m, R##x)
+        const Lane C0m = C4, C1m = C0, C2m = C1, C3m = C2, C4m = C3;
+        const Lane B00 = NAO_TH(0, 0);
+        const Lane B10 = NAO_R(44, 0)(NAO_TH(6, 1));
+        const Lane B20 = NAO_R(43, 1)(NAO_TH(12, 2));
+        const Lane B30 = NAO_R(21, 2)(NAO_TH(18, 3));
+        const Lane B40 = NAO_R(14, 3)(NAO_TH(24, 4));
+        const Lane B01 = NAO_R(28, 4)(NAO_TH(3, 3));
+        const Lane B11 = NAO_R(20, 5)(NAO_TH(9, 4));
+        const Lane B21 = NAO_R(3, 6)(NAO_TH(10, 0));
+        const Lane B31 = NAO_R(45, 7)(NAO_TH(16, 1));
+        const Lane B41 = NAO_R(61, 8)(NAO_TH(22, 2));
+        const Lane B02 = NAO_R(1, 9)(NAO_TH(1, 1));
+        const Lane B12 = NAO_R(6, 10)(NAO_TH(7, 2));
+        const Lane B22 = NAO_R(25, 11)(NAO_TH(13, 3));
+        const Lane B32 = NAO_R(8, 12)(NAO_TH(19, 4));
+        const Lane B42 = NAO_R(18, 13)(NAO_TH(20, 0));
+        const Lane B03 = NAO_R(27, 14)(NAO_TH(4, 4));
+        const Lane B13 = NAO_R(36, 15)(NAO_TH(5, 0));
+        const Lane B23 = NAO_R(10, 16)(NAO_TH(11, 1));
+        const Lane B33 = NAO_R(15, 17)(NAO_TH(17, 2));
+        const Lane B43 = NAO_R(56, 18)(NAO_TH(23, 3));
+        const Lane B04 = NAO_R(62, 19)(NAO_TH(2, 2));
+        const Lane B14 = NAO_R(55, 20)(NAO_TH(8, 3));
+        const Lane B24 = NAO_R(39, 21)(NAO_TH(14, 4));
+        const Lane B34 = NAO_R(41, 22)(NAO_TH(15, 0));
+        const Lane B44 = NAO_R(2, 23)(NAO_TH(21, 1));
+#undef NAO_TH
+#undef NAO_R
         // chi (row y: lanes Bxy for x=0..4) + iota
-        A[0] = chi(B00, B10, B20) ^ c_keccak_rc[r];
-        A[1] = chi(B10, B20, B30); A[2] = chi(B20, B30, B40);
-        A[3] = chi(B30, B40, B00); A[4] = chi(B40, B00, B10);
-        A[5] = chi(B01, B11, B21); A[6] = chi(B11, B21, B31); A[7] = chi(B21, B31, B41);
-        A[8] = chi(B31, B41, B01); A[9] = chi(B41, B01, B11);
-        A[10] = chi(B02, B12, B22); A[11] = chi(B12, B22, B32); A[12] = chi(B22, B32, B42);
-        A[13] = chi(B32, B42, B02); A[14] = chi(B42, B02, B12);
-        A[15] = chi(B03, B13, B23); A[16] = chi(B13, B23, B33); A[17] = chi(B23, B33, B43);
-        A[18] = chi(B33, B43, B03); A[19] = chi(B43, B03, B13);
-        A[20] = chi(B04, B14, B24); A[21] = chi(B14, B24, B34); A[22] = chi(B24, B34, B44);
-        A[23] = chi(B34, B44, B04); A[24] = chi(B44, B04, B14);
+        const uint64_t rc = c_keccak_rc[r];
+        A[0] = lchi(B00, B10, B20);
+        A[0].lo ^= (uint32_t)rc; A[0].hi ^= (uint32_t)(rc >> 32);
+        A[1] = lchi(B10, B20, B30); A[2] = lchi(B20, B30, B40);
+        A[3] = lchi(B30, B40, B00); A[4] = lchi(B40, B00, B10);
+        A[5] = lchi(B01, B11, B21); A[6] = lchi(B11, B21, B31); A[7] = lchi(B21, B31, B41);
+        A[8] = lchi(B31, B41, B01); A[9] = lchi(B41, B01, B11);
+        A[10] = lchi(B02, B12, B22); A[11] = lchi(B12, B22, B32); A[12] = lchi(B22, B32, B42);
+        A[13] = lchi(B32, B42, B02); A[14] = lchi(B42, B02, B12);
+        A[15] = lchi(B03, B13, B23); A[16] = lchi(B13, B23, B33); A[17] = lchi(B23, B33, B43);
+        A[18] = lchi(B33, B43, B03); A[19] = lchi(B43, B03, B13);
+        A[20] = lchi(B04, B14, B24); A[21] = lchi(B14, B24, B34); A[22] = lchi(B24, B34, B44);
+        A[23] = lchi(B34, B44, B04); A[24] = lchi(B44, B04, B14);
     }
+#pragma unroll
+    for (int i = 0; i < 25; i++) Aw[i] = ((uint64_t)A[i].hi << 32) | A[i].lo;
+}
+__device__ __forceinline__ void keccak_f1600(uint64_t Aw[25]) {
+    keccak_f1600_m<NAO_KECCAK_FMA_MASK>(Aw);
 }
 
 // lane bytes (prev.b3, cur.b0..b2, nxt.b3?) : lo32 = bytes (p.b3,c.b0,c.b1,c.b2)

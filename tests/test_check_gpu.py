@@ -143,3 +143,69 @@ def test_mlp_golden_checks(D, ref_mlp):
         op = th.lookup(node.name)
         rec = dsp.check_node(a, b, ("zero",), op.tau_abs, op.tau_rel, th.grid, th.epsilon).host()
         assert bool(rec["threshold_exceeded"]) == (ent["p_max"] > 1.0), node.name
+
+
+def _heavy_claims(y, rng):
+    """Every element drifts: ulp noise, some sign flips, some large faults,
+    some tiny values (FP32 fast path must hand these to the FP64 keys)."""
+    yc = _drift(y, 1.0, 6, rng)
+    n = y.size
+    k = rng.integers(0, n, size=max(1, n // 50))
+    yc[k] = -yc[k]
+    k = rng.integers(0, n, size=max(1, n // 100))
+    yc[k] = yc[k] * np.float32(37.0) + np.float32(1e3)
+    k = rng.integers(0, n, size=max(1, n // 100))
+    yc[k] = np.float32(1e-38) * rng.standard_normal(k.size).astype(np.float32)
+    return yc
+
+
+@pytest.mark.parametrize("n", [4, 1001, 262147])
+def test_threshold_verdict_heavy_drift_edges(D, n):
+    """Thresholds exactly at the true percentiles (not exceeded) and one FP64
+    ulp below them, per grid point (exceeded) -- the FP32 interval search
+    must fall back to the exact keys inside its guard band."""
+    dsp, _ = D
+    rng = np.random.default_rng(n + 99)
+    y = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 3, size=n)).astype(np.float32)
+    y[rng.integers(0, n, size=max(1, n // 100))] = 1e-39
+    yc = _heavy_claims(y, rng)
+    a, r = OC.elementwise_errors(y, yc)
+    pa, pr = OC.percentile_profile(a), OC.percentile_profile(r)
+    gy, gc = torch.from_numpy(y).cuda(), torch.from_numpy(yc).cuda()
+    rec = dsp.check_node(gy, gc, ("zero",), pa, pr).host()
+    assert rec["threshold_exceeded"] == 0
+    for arr in (0, 1):
+        for i in range(0, len(GRID), 3):
+            ta, tr = pa.copy(), pr.copy()
+            t = ta if arr == 0 else tr
+            if t[i] == 0.0:
+                continue
+            t[i] = np.nextafter(t[i], -np.inf)
+            ref = OC.observed_p_max(y, yc, ta, tr)
+            assert ref > 1.0
+            rec = dsp.check_node(gy, gc, ("zero",), ta, tr).host()
+            assert rec["threshold_exceeded"] == 1, (arr, i)
+            assert rec["first_exceeded"] == arr * len(GRID) + i
+
+
+@pytest.mark.parametrize("kind", ["scaled", "f32", "f64"])
+def test_bound_violations_heavy_drift(D, kind):
+    dsp, _ = D
+    rng = np.random.default_rng(5)
+    n = 200003
+    y = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 3, size=n)).astype(np.float32)
+    yc = _heavy_claims(y, rng)
+    c = 3.3 * 2.0 ** -24  # not a power of two: FP32 and FP64 products differ
+    eps64 = c * np.abs(y.astype(np.float64))
+    if kind == "scaled":
+        eps, ref_eps = ("scaled", c), eps64
+    elif kind == "f64":
+        eps, ref_eps = torch.from_numpy(eps64).cuda(), eps64
+    else:
+        e32 = eps64.astype(np.float32)
+        eps, ref_eps = torch.from_numpy(e32).cuda(), e32.astype(np.float64)
+    ref = OC.leaf_check(y, yc, ref_eps)
+    rec = dsp.check_node(torch.from_numpy(y).cuda(), torch.from_numpy(yc).cuda(), eps,
+                         np.full(len(GRID), np.inf), np.full(len(GRID), np.inf)).host()
+    assert rec["n_violations"] == ref["n_violations"]
+    assert rec["max_ratio"] == pytest.approx(ref["max_ratio"], rel=1e-12)
