@@ -245,6 +245,10 @@ def run_ours(args):
             return 12.0 * a[4] * a[5]
         if name == "nao_inject_drift":
             return 8.0 * a[2]
+        if name == "nao_reduce_bound":  # read x, write y + eps (f32/f64) per row
+            return 4.0 * a[4] * a[5] + (4.0 + (8.0 if a[3] else 4.0)) * a[4]
+        if name == "nao_unary_fp64":
+            return 8.0 * a[2]
         if name == "nao_merkle_commit_tensors":
             return float(sum(a[2][i] for i in range(a[0])))
         if name == "nao_check":
@@ -351,6 +355,19 @@ def run_ours(args):
                     "peak_source": "derived FP32 FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz "
                                    "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
                     "traffic": None}
+        elif dom == "nao_merkle_commit_tensors" and args.hash == "keccak256":
+            # Keccak-f[1600] is integer-ALU bound, not HBM bound: 24 rounds x 180
+            # ALU ops (122 LOP3 + 58 SHF.L.W, cuobjdump) per 136-byte block on a
+            # 64-lane/clk/SM ALU pipe (profiles/r1_keccak_pipe_balance.md)
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
+            sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+            peak = 148 * 64 * sm_mhz * 1e6 / (24 * 180 / 136.0) / 1e9
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
+                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "derived integer-ALU roofline of Keccak-256: 148 SM x 64 "
+                                   "lanes/clk x SM clock / (24 x 180 ops per 136 B block)",
+                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
         else:
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
             peak = peaks.get("hbm_gbs", 6650.0)
@@ -362,6 +379,16 @@ def run_ours(args):
         roof["serial_step_ms"] = round(t_serial, 2)
         roof["kernel_ms_per_step"] = {k: round(v, 2) for k, v in sorted(
             shares.items(), key=lambda kv: -kv[1])}
+        # algorithmic rate of every timed kernel family (TFLOP/s for the GEMMs,
+        # GB/s otherwise; units as in `units` above)
+        rates = {}
+        for k, v in timers.items():
+            t = sum(v["ms"]) * 1e-3
+            if t > 0 and sum(v["units"]) > 0:
+                flops = k in ("nao_abs_gemm_tc", "nao_abs_gemm_bound")
+                rates[k] = (f"{sum(v['units']) / t / 1e12:.1f} TFLOP/s" if flops
+                            else f"{sum(v['units']) / t / 1e9:.0f} GB/s")
+        roof["kernel_rates"] = rates
 
     commit_ms = shares.get("nao_merkle_commit_tensors", 0.0)
     merkle_gbs = (stats.bytes_committed / (commit_ms * 1e-3) / 1e9) if commit_ms else None

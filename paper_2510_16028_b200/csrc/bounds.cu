@@ -327,6 +327,8 @@ static int row_grid(int64_t rows) { return (int)ceil_div(rows, 32 * kRowWarps); 
 namespace nao { namespace rowb {
 static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                   int kind, float ln_eps, double u, double rc, double slack, cudaStream_t st);
+static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                     double u, double rc, double slack, cudaStream_t st);
 } }
 
 using namespace nao;
@@ -339,6 +341,9 @@ int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t 
     NAO_REQUIRE(x && y && eps, "softmax: null pointer");
     if (rows == 0) return NAO_OK;
     {
+        int rc_c = rowb::softmax_c(x, y, eps, eps_f64, rows, n, u, rc, slack,
+                                   static_cast<cudaStream_t>(stream));
+        if (rc_c >= 0) return rc_c;
         int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 0, 0.f, u, rc, slack,
                                 static_cast<cudaStream_t>(stream));
         if (rc_b >= 0) return rc_b;
@@ -635,6 +640,210 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Softmax, design C (many long rows): three launches, each at full occupancy.
+//   K1 warp per row : m = max, e = fp32(exp64(x - m)) -> y, FP64 eps sums
+//   K2 lane per row : the profile's sequential FP32 fold S of e (32 rows per
+//                     warp instruction: the only serial part, no idle CTA)
+//   K3 warp per row : y = e / S and the eps epilogue
+// Per-row stats (epsS f64, m f32, S f32) live in the first 16 bytes of the
+// row's own eps slot until K3 reads them (all lanes, then __syncwarp) and
+// overwrites that slot with the bound.
+struct RowStats { uint32_t w[4]; };  // [0..1] epsS bits, [2] m bits, [3] S bits
+__device__ __forceinline__ uint32_t* stats_ptr(void* eps, int f64, int64_t r, int64_t n) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(eps) + (size_t)r * n * (f64 ? 8 : 4));
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_smc_rows(const float* __restrict__ x, float* __restrict__ y,
+                                                  void* __restrict__ eps, int eps_f64, int64_t rows,
+                                                  int64_t n, double u, double rc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const double two_u = __dmul_rn(2.0, u);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+         r += nwarps) {
+        const float* xr = x + r * n;
+        float* er = y + r * n;
+        float m = -INFINITY;
+        if (VEC) {
+            const float4* x4 = reinterpret_cast<const float4*>(xr);
+            for (int64_t c = lane; c < (n >> 2); c += 32) {
+                const float4 v = __ldg(x4 + c);
+                m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            }
+        } else {
+            for (int64_t c = lane; c < n; c += 32) m = fmaxf(m, __ldg(xr + c));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const double m64a = fabs((double)m);
+        double se = 0.0, seps = 0.0;
+        auto one = [&](float xv) -> float {
+            const float ev = (float)exp((double)__fsub_rn(xv, m));
+            const double e64 = (double)ev;
+            const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
+            se = __dadd_rn(se, e64);
+            seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64)));
+            return ev;
+        };
+        if (VEC) {
+            const float4* x4 = reinterpret_cast<const float4*>(xr);
+            float4* e4 = reinterpret_cast<float4*>(er);
+            for (int64_t c = lane; c < (n >> 2); c += 32) {
+                const float4 v = __ldg(x4 + c);
+                float4 e;
+                e.x = one(v.x); e.y = one(v.y); e.z = one(v.z); e.w = one(v.w);
+                e4[c] = e;
+            }
+        } else {
+            for (int64_t c = lane; c < n; c += 32) er[c] = one(__ldg(xr + c));
+        }
+        se = warp_sum(se);
+        seps = warp_sum(seps);
+        if (lane == 0) {
+            const double epsS = __dadd_rn(__dmul_rn(rc, se), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+            uint32_t* st = stats_ptr(eps, eps_f64, r, n);
+            const unsigned long long b = (unsigned long long)__double_as_longlong(epsS);
+            st[0] = (uint32_t)b;
+            st[1] = (uint32_t)(b >> 32);
+            st[2] = __float_as_uint(m);
+        }
+    }
+}
+
+// lane per row: S = (((e0 + e1) + e2) + ...), the sequential profile's left fold
+template <bool VEC>
+__global__ void __launch_bounds__(128) k_smc_fold(const float* __restrict__ e, void* __restrict__ eps,
+                                                  int eps_f64, int64_t rows, int64_t n) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const float* er = e + r * n;
+    float acc;
+    if (VEC) {
+        const float4* e4 = reinterpret_cast<const float4*>(er);
+        const int64_t n4 = n >> 2;
+        float4 v = e4[0];
+        acc = __fadd_rn(__fadd_rn(__fadd_rn(v.x, v.y), v.z), v.w);
+        // batches of 8 float4: the next batch is in flight while this one folds
+        constexpr int NB = 8;
+        float4 cur[NB], nxt[NB];
+        int64_t c = 1;
+        const int64_t nb = (n4 - 1) / NB;  // full batches after element group 0
+#pragma unroll
+        for (int k = 0; k < NB; k++) cur[k] = nb > 0 ? e4[c + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t b = 0; b < nb; b++) {
+            const int64_t cn = c + NB;
+            if (b + 1 < nb) {
+#pragma unroll
+                for (int k = 0; k < NB; k++) nxt[k] = e4[cn + k];
+            }
+#pragma unroll
+            for (int k = 0; k < NB; k++)
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, cur[k].x), cur[k].y), cur[k].z),
+                                cur[k].w);
+#pragma unroll
+            for (int k = 0; k < NB; k++) cur[k] = nxt[k];
+            c = cn;
+        }
+        for (; c < n4; c++) {
+            const float4 a = e4[c];
+            acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, a.x), a.y), a.z), a.w);
+        }
+    } else {
+        acc = er[0];
+        for (int64_t c = 1; c < n; c++) acc = __fadd_rn(acc, er[c]);
+    }
+    stats_ptr(eps, eps_f64, r, n)[3] = __float_as_uint(acc);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_smc_epi(const float* __restrict__ x, float* __restrict__ y,
+                                                 void* __restrict__ eps, int eps_f64, int64_t rows,
+                                                 int64_t n, double u, double slack) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+         r += nwarps) {
+        const uint32_t* st = stats_ptr(eps, eps_f64, r, n);
+        const double epsS =
+            __longlong_as_double((long long)(((unsigned long long)st[1] << 32) | st[0]));
+        const float m = __uint_as_float(st[2]), S = __uint_as_float(st[3]);
+        __syncwarp();  // every lane holds the stats before the slot is overwritten
+        const double S64 = (double)S, S2 = __dmul_rn(S64, S64);
+        // divisions by per-row constants as reciprocal multiplies: <= 2 ulp FP64,
+        // covered by `slack` (>= 2^-50)
+        const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(epsS, S2);
+        const double m64a = fabs((double)m), two_u = __dmul_rn(2.0, u);
+        const float* xr = x + r * n;
+        float* yr = y + r * n;
+        const int64_t ob = r * n;
+        if (VEC) {
+            const float4* x4 = reinterpret_cast<const float4*>(xr);
+            float4* y4 = reinterpret_cast<float4*>(yr);
+            for (int64_t c = lane; c < (n >> 2); c += 32) {
+                const float4 xv = __ldg(x4 + c);
+                const float4 ev = y4[c];
+                const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, es[4] = {ev.x, ev.y, ev.z, ev.w};
+                float ys[4];
+                double vs[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    ys[k] = __fdiv_rn(es[k], S);
+                    const double e64 = (double)es[k];
+                    const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xs[k]), m64a));
+                    const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+                    vs[k] = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
+                                      __dmul_rn(u, fabs((double)ys[k])));
+                }
+                y4[c] = make_float4(ys[0], ys[1], ys[2], ys[3]);
+                const double sl = __dadd_rn(1.0, slack);
+                if (eps_f64) {
+                    double2* e2 = reinterpret_cast<double2*>(static_cast<double*>(eps) + ob) + 2 * c;
+                    e2[0] = make_double2(__dmul_rn(vs[0], sl), __dmul_rn(vs[1], sl));
+                    e2[1] = make_double2(__dmul_rn(vs[2], sl), __dmul_rn(vs[3], sl));
+                } else {
+                    reinterpret_cast<float4*>(static_cast<float*>(eps) + ob)[c] = make_float4(
+                        __double2float_ru(__dmul_rn(vs[0], sl)), __double2float_ru(__dmul_rn(vs[1], sl)),
+                        __double2float_ru(__dmul_rn(vs[2], sl)), __double2float_ru(__dmul_rn(vs[3], sl)));
+                }
+            }
+        } else {
+            for (int64_t c = lane; c < n; c += 32) {
+                const float xv = __ldg(xr + c), ev = yr[c];
+                const float yv = __fdiv_rn(ev, S);
+                yr[c] = yv;
+                const double e64 = (double)ev;
+                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
+                const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+                const double v = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
+                                           __dmul_rn(u, fabs((double)yv)));
+                store_eps(eps, eps_f64, ob + c, v, slack);
+            }
+        }
+    }
+}
+
+// design C for many long rows (returns -1 when it does not apply)
+static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
+                     double u, double rc, double slack, cudaStream_t st) {
+    if (n < 128 || rows < 1024) return -1;
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                       reinterpret_cast<uintptr_t>(eps)) & 15) == 0 && (n & 3) == 0;
+    const int64_t wblocks = std::min<int64_t>(ceil_div(rows, 8), (int64_t)kNumSMs * 8);
+    if (vec) {
+        k_smc_rows<true><<<(unsigned)wblocks, 256, 0, st>>>(x, y, eps, eps_f64, rows, n, u, rc);
+        k_smc_fold<true><<<(unsigned)ceil_div(rows, 128), 128, 0, st>>>(y, eps, eps_f64, rows, n);
+        k_smc_epi<true><<<(unsigned)wblocks, 256, 0, st>>>(x, y, eps, eps_f64, rows, n, u, slack);
+    } else {
+        k_smc_rows<false><<<(unsigned)wblocks, 256, 0, st>>>(x, y, eps, eps_f64, rows, n, u, rc);
+        k_smc_fold<false><<<(unsigned)ceil_div(rows, 128), 128, 0, st>>>(y, eps, eps_f64, rows, n);
+        k_smc_epi<false><<<(unsigned)wblocks, 256, 0, st>>>(x, y, eps, eps_f64, rows, n, u, slack);
+    }
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
 }
 
 // rows per CTA for design B (0 = use the transposed-tile kernels)

@@ -226,3 +226,26 @@ def test_mlp_co_execute_matches_reference(B, ref_mlp):
                 assert_bound(flat[ent["idx"]], ref_s, f"{run}/{mode}/{node}")
                 assert ent["eps_sum"] <= flat.sum() * (1 + 1e-12)
                 assert flat.sum() <= ent["eps_sum"] * (1 + RTOL)
+
+
+@pytest.mark.parametrize("shape,f64", [((4096, 384), True), ((4096, 384), False),
+                                       ((1536, 131), True), ((1030, 2048), False)])
+def test_softmax_many_long_rows(B, shape, f64):
+    """Design C (max/exp warp per row, lane-per-row sequential fold, epilogue):
+    values bit-exact, bound within [ref, ref(1+1e-5)] (FP32 eps rounded up)."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    x = (rng.standard_normal(shape) * 4).astype(np.float32)
+    x[3, :7] = -np.inf  # exp(-inf - m) = 0 participates in the fold
+    x[5, 11] = 80.0
+    y_ref, e_ref = OB.softmax_bound_parts(x, -1, OB.FpModel())
+    y, e = B.softmax_device(torch.from_numpy(x).cuda(), -1, B.FpModel(), eps_f64=f64)
+    y, e = y.cpu().numpy(), e.cpu().numpy().astype(np.float64)
+    assert np.array_equal(y.view(np.uint32), y_ref.view(np.uint32))
+    nan = np.isnan(e_ref)  # x = -inf: eps_z = inf, 0 * inf in the reference formula
+    assert np.array_equal(np.isnan(e), nan)
+    e, e_ref = e[~nan], e_ref[~nan]
+    if f64:
+        assert_bound(e, e_ref, "softmax C f64")
+    else:
+        assert np.all(e >= e_ref)
+        assert np.all(e <= e_ref * (1 + RTOL) + np.spacing(e_ref.astype(np.float32)) * 2)
