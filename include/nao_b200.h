@@ -154,6 +154,9 @@ int nao_tf32_split(const float* x, float* hi, float* lo, int64_t batch, int64_t 
 /* eps >= gamma_const * sum_k |A||B| from the split parts on tcgen05.mma.kind::tf32
  * (3 products, outward-compensated, within rtol 1e-5 of the FP64 reference);
  * batch_a / batch_b are `batch` or 1 (broadcast).  Output [batch, M, N], ldc. */
+/* k-length of one tensor-core accumulation chunk of nao_abs_gemm_tc (its error
+ * model: relative loss <= (kchunk/8) * 3 * 2^-23 per chunk, csrc/absgemm_tc.cu). */
+int nao_abs_gemm_tc_kchunk(void);
 int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, const float* b_lo,
                     void* eps, int eps_f64, int64_t batch, int64_t batch_a, int64_t batch_b,
                     int64_t M, int64_t N, int64_t K, int64_t ldc, int64_t stride_c,

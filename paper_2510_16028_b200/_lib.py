@@ -13,7 +13,11 @@ from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libnao_b200.so"
+import os
+
+# NAO_LIB_PATH: an alternative in-tree build of the same library (A/B kernel experiments)
+_LIB_PATH = Path(os.environ.get("NAO_LIB_PATH") or
+                 Path(__file__).resolve().parent / "libnao_b200.so")
 _lib = None
 _lock = threading.Lock()
 
@@ -77,6 +81,7 @@ _SIGS = {
     "nao_matmul_profile": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                                    c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
     "nao_tf32_split_cols": (c_i64, [c_i64]),
+    "nao_abs_gemm_tc_kchunk": (c_int, []),
     "nao_tf32_split": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]),
     "nao_abs_gemm_tc": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64,
                                 c_i64, c_i64, c_i64, c_i64, c_dbl, c_vp, c_dbl, c_dbl, c_vp]),

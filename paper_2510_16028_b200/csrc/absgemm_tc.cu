@@ -9,23 +9,27 @@
 // 1/(1 - 1.002*2^-20).  Tensor-core accumulation of non-negative terms is
 // modelled as losing at most kMmaRel = 3*2^-23 of the running sum per MMA
 // instruction (products exact, aligned sum truncated), so:
-//   * acc0 (hi*hi) lives in TMEM for only KCHUNK = 64 k (8 MMAs), then the
+//   * acc0 (hi*hi) lives in TMEM for only KCHUNK = 128 k (16 MMAs), then the
 //     epilogue warps drain it into FP64 registers (double-buffered TMEM, the
-//     MMA warp never waits) and the chunk sum is scaled by 1/(1 - 8 kMmaRel);
+//     MMA warp never waits) and the chunk sum is scaled by 1/(1 - 16 kMmaRel);
 //   * acc1 (hi*lo + lo*hi, <= 2^-9 of acc0) accumulates over all of K and is
 //     scaled by 1/(1 - J1 kMmaRel); its relative weight keeps that inside 2^-9.
-// Worst-case over-estimate ~8e-6 < rtol 1e-5; typical ~4e-6.  Subnormal split
-// parts are lifted to FLT_MIN and an absolute floor K*2^-120*c covers any
-// flush-to-zero of products, so the result stays >= the exact bound.
+// Worst-case over-estimate ~6.7e-6 < rtol 1e-5 (exact data, exact TC sums).
+// Subnormal split parts are lifted to FLT_MIN and an absolute floor
+// K*2^-120*c covers any flush-to-zero of products, so the result stays >= the
+// exact bound.  Chunk length: 64 k made the FP64 drain (F2F + DADD, stall_math)
+// pace the kernel (148 TFLOP/s algorithmic at 2048x4096x12288); 128 k -> 172,
+// within 3 % of the no-epilogue probe (NAO_TC_EPI=9), which is L2->SM feed bound.
 //
 // Kernel anatomy (one CTA per 128x128 output tile, 384 threads):
-//   warp 0      TMA producer: A_hi, A_lo, B_hi, B_lo tiles (128 x 32 fp32,
-//               SWIZZLE_128B) into a 3-stage smem ring (64 KB / stage)
-//   warp 1      single-thread tcgen05.mma.kind::tf32 issuer (12 MMAs / stage)
+//   warp 0      TMA producer: A_hi, A_lo, B_hi, B_lo tiles (128 x 16 fp32,
+//               SWIZZLE_64B) into a 6-stage smem ring (32 KB / stage)
+//   warp 1      single-thread tcgen05.mma.kind::tf32 issuer (6 MMAs / stage)
 //   warp 2      TMEM allocator (512 columns: acc0 x2, acc1)
 //   warps 4-11  epilogue: tcgen05.ld -> FP64 accumulate -> eps store
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -40,7 +44,11 @@ namespace tc {
 // rows (SWIZZLE_128B), 64 KB stages, 3 in flight.  Same bytes in flight.
 constexpr int BM = 128, BN = 128, BK = NAO_TC_BK;
 constexpr int STAGES = BK == 16 ? 6 : 3;
-constexpr int KCHUNK_KB = 64 / BK;  // k-blocks per 64-k TMEM chunk
+#ifndef NAO_TC_KCHUNK
+#define NAO_TC_KCHUNK 128
+#endif
+constexpr int KCHUNK = NAO_TC_KCHUNK;  // k per TMEM acc0 chunk (drained to the epilogue)
+constexpr int KCHUNK_KB = KCHUNK / BK;  // k-blocks per chunk
 constexpr int TILE_BYTES = BM * BK * 4;     // 16 KB (BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A_hi, A_lo, B_hi, B_lo
 constexpr int NUM_THREADS = 384;
@@ -144,6 +152,70 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+
+// Per-thread FP64 accumulation of the TMEM chunk sums of acc0 (64 columns).
+// NAO_TC_EPI 9 is a timing probe that skips the accumulation (wrong results):
+// it measured the epilogue at ~16 % of the kernel with 64-k chunks, ~2 % with
+// 128-k chunks.  (An FP32 TwoSum accumulator was measured slower than F2F+DADD.)
+#ifndef NAO_TC_EPI
+#define NAO_TC_EPI 0
+#endif
+struct EpiAcc {
+    double a[64];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < 64; i++) a[i] = 0.0;
+    }
+    __device__ __forceinline__ void add(int i, float x) {
+#if NAO_TC_EPI == 9
+        a[i] = (double)x;
+#else
+        a[i] = __dadd_rn(a[i], (double)x);
+#endif
+    }
+    __device__ __forceinline__ double get(int i) const { return a[i]; }
+};
+
+
+// Final epilogue of one 128x128 tile, per epilogue warp (32 rows = its TMEM lane
+// quarter, 64 columns = its half): e = scale0*acc0sum + scale1*acc1 + floor is
+// staged row-per-lane in smem (the drained stage ring; row stride 65 doubles),
+// then written back row by row with lanes on consecutive columns, so the eps
+// stores and the y reads of the linear u|y| term are coalesced 128 B segments
+// (lane = row direct stores were ~8x sector-amplified: 32 rows per instruction).
+__device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc, uint32_t col1,
+                                              double* stg, int lane, int quarter, int half,
+                                              int64_t m0, int64_t n0, int bz) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        uint32_t v[32];
+        TMEM_LD_X32(col1 + 32 * h, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const double e = __dadd_rn(__dmul_rn(g.scale0, acc.get(32 * h + i)),
+                                       __dmul_rn(g.scale1, (double)__uint_as_float(v[i])));
+            stg[lane * 65 + 32 * h + i] = __dadd_rn(e, g.abs_floor);
+        }
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; r++) {
+        const int64_t m = m0 + quarter * 32 + r;
+        if (m >= g.M) break;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            const int64_t n = n0 + half * 64 + 32 * j + lane;
+            if (n < g.N) {
+                double e = stg[r * 65 + 32 * j + lane];
+                const int64_t o = (int64_t)bz * g.sC + m * g.ldc + n;
+                if (g.Y) e = __dadd_rn(e, __dmul_rn(g.u, fabs((double)__ldg(g.Y + o))));
+                if (g.out_f64) static_cast<double*>(g.C)[o] = e;
+                else static_cast<float*>(g.C)[o] = __double2float_ru(e);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_absgemm_tc(const __grid_constant__ CUtensorMap map_ahi,
                  const __grid_constant__ CUtensorMap map_alo,
@@ -242,11 +314,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp >= 4) {  // ---------------- epilogue
         const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
-        const int row = quarter * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        double acc[64];
-#pragma unroll
-        for (int i = 0; i < 64; i++) acc[i] = 0.0;
+        EpiAcc acc;
+        acc.zero();
         const int nchunks = (nkb + KCHUNK_KB - 1) / KCHUNK_KB;
         for (int c = 0; c < nchunks; c++) {
             const int buf = c & 1;
@@ -257,41 +327,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             TMEM_LD_X32(col, v);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; i++) acc[i] = __dadd_rn(acc[i], (double)__uint_as_float(v[i]));
+            for (int i = 0; i < 32; i++) acc.add(i, __uint_as_float(v[i]));
             TMEM_LD_X32(col + 32, v);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; i++)
-                acc[32 + i] = __dadd_rn(acc[32 + i], (double)__uint_as_float(v[i]));
+                acc.add(32 + i, __uint_as_float(v[i]));
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
         }
         mbar_wait(acc1_full, 0);
         fence_after();
-        const int64_t m = m0 + row;
         const uint32_t col1 = tmem + lane_addr + 2 * BN + half * 64;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            uint32_t v[32];
-            TMEM_LD_X32(col1 + 32 * h, v);
-            tmem_wait_ld();
-            if (m < g.M) {
-#pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int64_t n = n0 + half * 64 + 32 * h + i;
-                    if (n < g.N) {
-                        double e = __dadd_rn(__dmul_rn(g.scale0, acc[32 * h + i]),
-                                             __dmul_rn(g.scale1, (double)__uint_as_float(v[i])));
-                        e = __dadd_rn(e, g.abs_floor);
-                        const int64_t o = (int64_t)bz * g.sC + m * g.ldc + n;
-                        if (g.Y) e = __dadd_rn(e, __dmul_rn(g.u, fabs((double)__ldg(g.Y + o))));
-                        if (g.out_f64) static_cast<double*>(g.C)[o] = e;
-                        else static_cast<float*>(g.C)[o] = __double2float_ru(e);
-                    }
-                }
-            }
-        }
+        double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
+        tile_epilogue(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
     }
     fence_before();
     __syncthreads();
@@ -299,6 +349,227 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                      "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 128 tile with M=256 MMAs issued by the leader CTA.  Each CTA stages its
+// own 128 rows of A and HALF (64 rows) of B, so per SM the smem ring holds 96
+// instead of 128 rows per k-block and the tensor core reads 6 KB instead of
+// 8 KB of smem per MMA -- the single-CTA kernel is smem/L2-feed bound at
+// N=128 (tensor pipe ~40 %).  Error model, TMEM layout (acc0 x2 + acc1 per
+// CTA, lane = row) and epilogue are identical to k_absgemm_tc.
+namespace pair {
+constexpr int BM = 128;          // rows of A (and of the output) per CTA
+constexpr int BN = 128;          // output columns per pair (= per CTA)
+constexpr int BNH = BN / 2;      // rows of B staged per CTA
+constexpr int BK = NAO_TC_BK;
+constexpr int STAGES = BK == 16 ? 8 : 4;
+constexpr int KCHUNK_KB = KCHUNK / BK;
+constexpr int A_BYTES = BM * BK * 4;
+constexpr int B_BYTES = BNH * BK * 4;
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // per CTA
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int NUM_THREADS = 384;
+constexpr uint32_t TMEM_COLS = 512;
+// kind::tf32, D=F32, K-major A/B, N=128, M=256 (cta_group::2)
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+}  // namespace pair
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONEC_%=;\n\t"
+        "bra WAITC_%=;\n"
+        "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+// TMA into this CTA's smem, completing bytes on the LEADER CTA's barrier
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1)
+    k_absgemm_tc2(const __grid_constant__ CUtensorMap map_ahi,
+                  const __grid_constant__ CUtensorMap map_alo,
+                  const __grid_constant__ CUtensorMap map_bhi,
+                  const __grid_constant__ CUtensorMap map_blo, const __grid_constant__ TcArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + pair::STAGES * pair::STAGE_BYTES);
+    uint64_t* full = bars;                      // [pair::STAGES]  (leader's are used)
+    uint64_t* empty = bars + pair::STAGES;            // [pair::STAGES]  (each CTA, multicast commit)
+    uint64_t* tfull = bars + 2 * pair::STAGES;        // [2]       (each CTA, multicast commit)
+    uint64_t* tempty = bars + 2 * pair::STAGES + 2;   // [2]       (leader's: 16 epilogue warps)
+    uint64_t* acc1_full = bars + 2 * pair::STAGES + 4;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * pair::STAGES + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int tiles_m = (int)((g.M + 2 * pair::BM - 1) / (2 * pair::BM)), tiles_n = (int)((g.N + pair::BN - 1) / pair::BN);
+    constexpr int GROUP_M = 4;
+    const int pid = blockIdx.x >> 1;
+    const int group = pid / (GROUP_M * tiles_n);
+    const int first_m = group * GROUP_M;
+    const int gm = (tiles_m - first_m) < GROUP_M ? (tiles_m - first_m) : GROUP_M;
+    const int tm = first_m + (pid % (GROUP_M * tiles_n)) % gm;
+    const int tn = (pid % (GROUP_M * tiles_n)) / gm;
+    const int n0 = tn * pair::BN, m0 = tm * 2 * pair::BM + (int)rank * pair::BM, bz = blockIdx.z;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < pair::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 16); }
+        mbar_init(acc1_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)));
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(pair::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nkb = g.nkb;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            const int za = g.a_batched ? bz : 0, zb = g.b_batched ? bz : 0;
+            const int nb = n0 + (int)rank * pair::BNH;
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % pair::STAGES;
+                const uint32_t ph = (kb / pair::STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = smem + s * pair::STAGE_BYTES;
+                const uint32_t fb = mapa_rank(smem_u32(&full[s]), 0);
+                if (leader) mbar_expect_tx(&full[s], 2 * pair::STAGE_BYTES);
+                tma_load_3d_pair(st, &map_ahi, fb, kb * pair::BK, m0, za);
+                tma_load_3d_pair(st + pair::A_BYTES, &map_alo, fb, kb * pair::BK, m0, za);
+                tma_load_3d_pair(st + 2 * pair::A_BYTES, &map_bhi, fb, kb * pair::BK, nb, zb);
+                tma_load_3d_pair(st + 2 * pair::A_BYTES + pair::B_BYTES, &map_blo, fb, kb * pair::BK, nb, zb);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+            const uint32_t acc1 = tmem + 2 * pair::BN;
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % pair::STAGES;
+                const uint32_t ph = (kb / pair::STAGES) & 1;
+                const int chunk = kb / pair::KCHUNK_KB, buf = chunk & 1;
+                const bool first = (kb % pair::KCHUNK_KB) == 0;
+                if (first) mbar_wait_cluster(&tempty[buf], ((chunk >> 1) & 1) ^ 1);
+                mbar_wait(&full[s], ph);
+                fence_after();
+                const uint32_t st = smem_u32(smem + s * pair::STAGE_BYTES);
+                const uint32_t acc0 = tmem + buf * pair::BN;
+#pragma unroll
+                for (int j = 0; j < pair::BK / 8; j++) {
+                    const uint64_t ahi = make_desc(st + j * 32);
+                    const uint64_t alo = make_desc(st + pair::A_BYTES + j * 32);
+                    const uint64_t bhi = make_desc(st + 2 * pair::A_BYTES + j * 32);
+                    const uint64_t blo = make_desc(st + 2 * pair::A_BYTES + pair::B_BYTES + j * 32);
+                    umma_tf32_pair(acc0, ahi, bhi, pair::kIdesc2, (first && j == 0) ? 0u : 1u);
+                    umma_tf32_pair(acc1, ahi, blo, pair::kIdesc2, (kb == 0 && j == 0) ? 0u : 1u);
+                    umma_tf32_pair(acc1, alo, bhi, pair::kIdesc2, 1u);
+                }
+                umma_commit_pair(&empty[s]);
+                if ((kb % pair::KCHUNK_KB) == pair::KCHUNK_KB - 1 || kb == nkb - 1) umma_commit_pair(&tfull[buf]);
+            }
+            umma_commit_pair(acc1_full);
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
+        const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        const uint32_t tempty_leader0 = mapa_rank(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty_leader1 = mapa_rank(smem_u32(&tempty[1]), 0);
+        EpiAcc acc;
+        acc.zero();
+        const int nchunks = (nkb + pair::KCHUNK_KB - 1) / pair::KCHUNK_KB;
+        for (int c = 0; c < nchunks; c++) {
+            const int buf = c & 1;
+            mbar_wait(&tfull[buf], (c >> 1) & 1);
+            fence_after();
+            uint32_t v[32];
+            const uint32_t col = tmem + lane_addr + buf * pair::BN + half * 64;
+            TMEM_LD_X32(col, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i++) acc.add(i, __uint_as_float(v[i]));
+            TMEM_LD_X32(col + 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+                acc.add(32 + i, __uint_as_float(v[i]));
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(buf ? tempty_leader1 : tempty_leader0);
+        }
+        mbar_wait(acc1_full, 0);
+        fence_after();
+        const uint32_t col1 = tmem + lane_addr + 2 * pair::BN + half * 64;
+        double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
+        tile_epilogue(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+    }
+    fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(pair::TMEM_COLS));
     }
 }
 
@@ -355,6 +626,18 @@ __global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi
     }
 }
 
+// NAO_TC_PAIR=1 selects the CTA-pair kernel (measured 5-10 % slower than the
+// single-CTA kernel at every Qwen3-8B shape: the pair couples two epilogues and
+// two TMA streams per MMA while the L2->SM feed per SM drops only 25 %).
+static bool tc_use_pair() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("NAO_TC_PAIR");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
 
 static EncodeFn get_encode() {
@@ -371,12 +654,13 @@ static EncodeFn get_encode() {
     return fn;
 }
 
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t Kp, int64_t batch) {
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t Kp, int64_t batch,
+                    int box_rows = BM) {
     EncodeFn enc = get_encode();
     NAO_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
     cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)(rows * Kp * 4)};
-    cuuint32_t box[3] = {BK, (cuuint32_t)BM, 1};
+    cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -394,6 +678,8 @@ using namespace nao;
 extern "C" {
 
 int64_t nao_tf32_split_cols(int64_t K) { return (K + 3) / 4 * 4; }
+
+int nao_abs_gemm_tc_kchunk(void) { return nao::tc::KCHUNK; }
 
 int nao_tf32_split(const float* x, float* hi, float* lo, int64_t batch, int64_t rows, int64_t K,
                    int64_t ld, int64_t stride_batch, int transpose, void* stream) {
@@ -436,12 +722,14 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
     NAO_REQUIRE(ceil_div(N, BN) * ceil_div(M, BM) < (1LL << 31) && batch <= 65535,
                 "abs-gemm tc: grid too large");
     const int64_t Kp = nao_tf32_split_cols(K);
+    const bool use_pair = tc_use_pair();
     CUtensorMap mah, mal, mbh, mbl;
     int rc;
+    const int b_box = use_pair ? pair::BNH : BN;
     if ((rc = make_map(&mah, a_hi, M, Kp, batch_a))) return rc;
     if ((rc = make_map(&mal, a_lo, M, Kp, batch_a))) return rc;
-    if ((rc = make_map(&mbh, b_hi, N, Kp, batch_b))) return rc;
-    if ((rc = make_map(&mbl, b_lo, N, Kp, batch_b))) return rc;
+    if ((rc = make_map(&mbh, b_hi, N, Kp, batch_b, b_box))) return rc;
+    if ((rc = make_map(&mbl, b_lo, N, Kp, batch_b, b_box))) return rc;
     TcArgs g;
     g.M = M; g.N = N; g.K = K;
     g.nkb = (int)((Kp + BK - 1) / BK);
@@ -459,6 +747,21 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
     g.scale0 = s * comp0;
     g.scale1 = s * comp1;
     g.abs_floor = gamma_const * (double)K * 0x1p-120;
+    if (use_pair) {
+        static bool attr2_set = false;
+        if (!attr2_set) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc2,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                pair::SMEM_BYTES));
+            attr2_set = true;
+        }
+        dim3 grid2((unsigned)(2 * ceil_div(N, pair::BN) * ceil_div(M, 2 * pair::BM)), 1,
+                   (unsigned)batch);
+        k_absgemm_tc2<<<grid2, pair::NUM_THREADS, pair::SMEM_BYTES,
+                        static_cast<cudaStream_t>(stream)>>>(mah, mal, mbh, mbl, g);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     static bool attr_set = false;
     if (!attr_set) {
         NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc,

@@ -2,8 +2,9 @@
 nao_abs_gemm_tc (csrc/absgemm_tc.cu header): with TF32-exact operands the lo
 parts vanish, every product is exact, and the output is
     eps = scale0 * sum_chunks acc0_chunk   (scale0 known)
-so the accumulator's relative loss per 64-k chunk (8 MMAs) can be measured
-exactly against an FP64 sum and compared with the modelled bound 8 * 3 * 2^-23.
+so the accumulator's relative loss per k-chunk (nao_abs_gemm_tc_kchunk()/8 MMAs)
+can be measured exactly against an FP64 sum and compared with the modelled
+bound J0 * 3 * 2^-23.
 The runs are built to maximise truncation loss: long runs of equal terms
 (every addition aligns the same low bits away) and growing partial sums."""
 
@@ -16,13 +17,17 @@ import torch
 pytestmark = pytest.mark.gpu
 
 MMA_REL = 3.0 * 2.0 ** -23
-J0 = 8
+
+
+def _j0():
+    from paper_2510_16028_b200 import _lib
+    return _lib.load().nao_abs_gemm_tc_kchunk() // 8
 
 
 def _scale0(c, K):
     from paper_2510_16028_b200.bounds import gemm_slack
     comp_split = 1.0 / (1.0 - 1.002 * 2.0 ** -20)
-    comp0 = 1.0 / (1.0 - J0 * MMA_REL)
+    comp0 = 1.0 / (1.0 - _j0() * MMA_REL)
     return c * comp_split * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -50) * comp0, comp0
 
 
@@ -55,7 +60,8 @@ def test_tc_accumulation_loss_within_model(case):
     raw = got / scale0  # = sum of the per-chunk TMEM sums (lo parts are exactly zero)
     loss = 1.0 - raw / exact  # relative loss of the tensor-core accumulation
     worst = float(loss.max())
+    j0 = _j0()
     print(f"{case}: worst relative accumulation loss {worst:.3e} "
-          f"(model per chunk {J0 * MMA_REL:.3e})")
-    assert worst <= J0 * MMA_REL
+          f"(model per chunk {j0 * MMA_REL:.3e})")
+    assert worst <= j0 * MMA_REL
     assert np.all(got >= exact)  # the compensated bound stays sound

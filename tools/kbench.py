@@ -99,14 +99,30 @@ def main():
                12 * x.numel())
     for path, tag in ((1, "gemm_tc"), (0, "gemm_ffma")):
         if want(tag):
-            for (M, K, N) in ((S, H, H), (S, H, I), (S, I, H)):
-                A = torch.randn((M, K), device=dev)
-                B = torch.randn((K, N), device=dev)
+            shapes = [(S, H, H), (S, H, I), (S, I, H)]
+            if want("gemm_all"):  # every Qwen3-8B GEMM shape: k/v, scores, ctx, lm_head
+                shapes += [(S, H, 1024), ("scores",), ("ctx",), (S, H, 151936)]
+            for shp in shapes:
+                if shp == ("scores",):  # q @ k^T, 32 heads, K = 128
+                    A = torch.randn((NH, S, 128), device=dev)
+                    B = torch.randn((NH, S, 128), device=dev)
+                    tb, fl, K = True, 2.0 * NH * S * S * 128, 128
+                elif shp == ("ctx",):  # p @ v, 32 heads, K = S
+                    A = torch.rand((NH, S, S), device=dev)
+                    B = torch.randn((NH, S, 128), device=dev)
+                    tb, fl, K = False, 2.0 * NH * S * S * 128, S
+                else:
+                    M, K, N = shp
+                    A = torch.randn((M, K), device=dev)
+                    B = torch.randn((K, N), device=dev)
+                    tb, fl = False, 2.0 * M * N * K
                 c = model.reduction_const(2 * K - 1)
-                abs_gemm_bound(A, B, c, False, eps_f64=False, path=path, cache_b=True)
-                ms = timeit(lambda: abs_gemm_bound(A, B, c, False, eps_f64=False, path=path,
-                                                   cache_b=True), a.reps)
-                report(tag, ms, flops=2.0 * M * N * K, shape=[M, K, N])
+                cb = not (shp in (("scores",), ("ctx",)))
+                abs_gemm_bound(A, B, c, tb, eps_f64=False, path=path, cache_b=cb)
+                ms = timeit(lambda: abs_gemm_bound(A, B, c, tb, eps_f64=False, path=path,
+                                                   cache_b=cb), a.reps)
+                report(tag, ms, flops=fl, shape=list(shp))
+                del A, B
             if want("sgemm") or only is None:
                 A = torch.randn((S, H), device=dev)
                 B = torch.randn((H, I), device=dev)
