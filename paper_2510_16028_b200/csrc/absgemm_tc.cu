@@ -29,6 +29,7 @@
 //   warps 4-11  epilogue: tcgen05.ld -> FP64 accumulate -> eps store
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -64,6 +65,8 @@ struct TcArgs {
     int64_t ldc, sC;
     int out_f64;
     double scale0, scale1, abs_floor, u;
+    // FP32 images rounded up (short-K epilogue, all-FP32 with round-up arithmetic)
+    float scale0f, scale1f, abs_floorf, uf;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -342,6 +345,184 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t col1 = tmem + lane_addr + 2 * BN + half * 64;
         double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
         tile_epilogue(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent variant for short K (K <= KCHUNK: one TMEM chunk per tile), e.g.
+// attention scores q k^T with K = head_dim.  There the per-tile fixed costs
+// (TMEM alloc, barrier init, pipeline fill, epilogue) of the one-CTA-per-tile
+// kernel dominate (8192 tiles of 24 MMAs for Qwen3-8B scores).  One CTA per SM
+// walks tiles t = blockIdx.x + i*gridDim.x; TMEM holds two tile slots
+// (acc0 | acc1, 256 columns each), so the MMAs of tile i+1 overlap the
+// epilogue of tile i; the stage ring streams k-blocks across tile boundaries;
+// the epilogue stages FP32 (rounded up) rows in a dedicated smem area and
+// stores coalesced.  FP32 eps output only (the streaming verifier's format).
+namespace shortk {
+constexpr int STAGES = 4;
+constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+constexpr int STG_BYTES = 8 * 32 * 65 * 4;
+constexpr int SMEM_BYTES = RING_BYTES + STG_BYTES + 1024 + 256;
+}  // namespace shortk
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_absgemm_tc_short(const __grid_constant__ CUtensorMap map_ahi,
+                       const __grid_constant__ CUtensorMap map_alo,
+                       const __grid_constant__ CUtensorMap map_bhi,
+                       const __grid_constant__ CUtensorMap map_blo, const __grid_constant__ TcArgs g,
+                       int batch) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* stg_all = reinterpret_cast<float*>(smem + shortk::RING_BYTES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + shortk::RING_BYTES + shortk::STG_BYTES);
+    uint64_t* full = bars;                              // [STAGES]
+    uint64_t* empty = bars + shortk::STAGES;            // [STAGES]
+    uint64_t* tfull = bars + 2 * shortk::STAGES;        // [2] tile slots
+    uint64_t* tempty = bars + 2 * shortk::STAGES + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * shortk::STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+    const int64_t tiles_per_b = (int64_t)tiles_m * tiles_n;
+    const int64_t n_tiles = tiles_per_b * batch;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < shortk::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)));
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)));
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nkb = g.nkb;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int kg = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                const int bz = (int)(t / tiles_per_b);
+                const int64_t r = t % tiles_per_b;
+                const int m0 = (int)(r / tiles_n) * BM, n0 = (int)(r % tiles_n) * BN;
+                const int za = g.a_batched ? bz : 0, zb = g.b_batched ? bz : 0;
+                for (int kb = 0; kb < nkb; kb++, kg++) {
+                    const int s = kg % shortk::STAGES;
+                    const uint32_t ph = (kg / shortk::STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], STAGE_BYTES);
+                    tma_load_3d(st, &map_ahi, &full[s], kb * BK, m0, za);
+                    tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * BK, m0, za);
+                    tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * BK, n0, zb);
+                    tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * BK, n0, zb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int kg = 0, i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, i++) {
+                const int slot = i & 1;
+                mbar_wait(&tempty[slot], ((i >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t acc0 = tmem + slot * 256, acc1 = acc0 + BN;
+                for (int kb = 0; kb < nkb; kb++, kg++) {
+                    const int s = kg % shortk::STAGES;
+                    const uint32_t ph = (kg / shortk::STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    fence_after();
+                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+                    for (int j = 0; j < BK / 8; j++) {
+                        const uint64_t ahi = make_desc(st + j * 32);
+                        const uint64_t alo = make_desc(st + TILE_BYTES + j * 32);
+                        const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
+                        const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
+                        const uint32_t first = (kb == 0 && j == 0) ? 0u : 1u;
+                        umma_tf32(acc0, ahi, bhi, kIdesc, first);
+                        umma_tf32(acc1, ahi, blo, kIdesc, first);
+                        umma_tf32(acc1, alo, bhi, kIdesc, 1u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[slot]);
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue
+        const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        float* stg = stg_all + ew * (32 * 65);
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, i++) {
+            const int slot = i & 1;
+            const int bz = (int)(t / tiles_per_b);
+            const int64_t r = t % tiles_per_b;
+            const int64_t m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+            mbar_wait(&tfull[slot], (i >> 1) & 1);
+            fence_after();
+            const uint32_t c0 = tmem + lane_addr + slot * 256 + half * 64;
+            // e = RU(RU(s0 acc0) + s1 acc1) + floor in FP32 round-up arithmetic: each
+            // step rounds toward +inf, so e >= the FP64 expression of the long
+            // kernel; the extra over-estimate is < 4 * 2^-23 relative.
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t v0[32], v1[32];
+                TMEM_LD_X32(c0 + 32 * h, v0);
+                TMEM_LD_X32(c0 + BN + 32 * h, v1);
+                tmem_wait_ld();
+                if (h == 1) {  // both halves read: hand the slot back to the MMA warp
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[slot]);
+                }
+#pragma unroll
+                for (int k = 0; k < 32; k++) {
+                    const float e = __fmaf_ru(g.scale1f, __uint_as_float(v1[k]),
+                                              __fmul_ru(g.scale0f, __uint_as_float(v0[k])));
+                    stg[lane * 65 + 32 * h + k] = __fadd_ru(e, g.abs_floorf);
+                }
+            }
+            __syncwarp();
+            const int64_t mq = m0 + quarter * 32;
+            const int rows = (int)((g.M - mq) < 32 ? (g.M - mq) : 32);
+            const int64_t nb = n0 + half * 64 + lane;
+            float* crow = static_cast<float*>(g.C) + (int64_t)bz * g.sC + mq * g.ldc + nb;
+            const float* yrow = g.Y ? g.Y + (int64_t)bz * g.sC + mq * g.ldc + nb : nullptr;
+            const bool ok0 = nb < g.N, ok1 = nb + 32 < g.N;
+            for (int rr = 0; rr < rows; rr++) {
+                float e0 = stg[rr * 65 + lane], e1 = stg[rr * 65 + 32 + lane];
+                if (yrow) {
+                    if (ok0) e0 = __fmaf_ru(g.uf, fabsf(__ldg(yrow)), e0);
+                    if (ok1) e1 = __fmaf_ru(g.uf, fabsf(__ldg(yrow + 32)), e1);
+                    yrow += g.ldc;
+                }
+                if (ok0) crow[0] = e0;
+                if (ok1) crow[32] = e1;
+                crow += g.ldc;
+            }
+            __syncwarp();
+        }
     }
     fence_before();
     __syncthreads();
@@ -638,6 +819,23 @@ static bool tc_use_pair() {
     return v == 1;
 }
 
+// NAO_TC_SHORT=0 disables the persistent short-K kernel (A/B measurements)
+static bool tc_no_short() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("NAO_TC_SHORT");
+        v = (e && e[0] == '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// host double -> float rounded toward +inf
+static float f32_ru(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = nextafterf(f, INFINITY);
+    return f;
+}
+
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
 
 static EncodeFn get_encode() {
@@ -745,8 +943,27 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
     const double comp1 = 1.0 / (1.0 - j1 * mma_rel);
     const double s = gamma_const * comp_split * (1.0 + slack) * (1.0 + 0x1p-50);
     g.scale0 = s * comp0;
+    g.scale0f = f32_ru(g.scale0);
     g.scale1 = s * comp1;
     g.abs_floor = gamma_const * (double)K * 0x1p-120;
+    g.scale1f = f32_ru(g.scale1);
+    g.abs_floorf = f32_ru(g.abs_floor);
+    g.uf = f32_ru(u);
+    if (!eps_f64 && g.nkb <= KCHUNK_KB && !tc_no_short()) {
+        static bool attr3_set = false;
+        if (!attr3_set) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc_short,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                shortk::SMEM_BYTES));
+            attr3_set = true;
+        }
+        const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * batch;
+        const unsigned ctas = (unsigned)(tiles < kNumSMs ? tiles : kNumSMs);
+        k_absgemm_tc_short<<<ctas, NUM_THREADS, shortk::SMEM_BYTES,
+                             static_cast<cudaStream_t>(stream)>>>(mah, mal, mbh, mbl, g, (int)batch);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     if (use_pair) {
         static bool attr2_set = false;
         if (!attr2_set) {

@@ -249,3 +249,26 @@ def test_softmax_many_long_rows(B, shape, f64):
     else:
         assert np.all(e >= e_ref)
         assert np.all(e <= e_ref * (1 + RTOL) + np.spacing(e_ref.astype(np.float32)) * 2)
+
+
+@pytest.mark.parametrize("K", [1, 64, 128])
+def test_abs_gemm_tc_short_k_persistent(B, K):
+    """K <= one TMEM chunk -> the persistent k_absgemm_tc_short (FP32 eps): many
+    more tiles than SMs (slot reuse), ragged M/N, batched q k^T, linear u|y|."""
+    rng = np.random.default_rng(K)
+    q = rng.standard_normal((40, 300, K)).astype(np.float32)
+    k = rng.standard_normal((40, 333, K)).astype(np.float32)
+    c = OB.FpModel().reduction_const(2 * K - 1)
+    ref = OB.matmul_bound(q, k, OB.FpModel(), transpose_b=True)
+    got = B.abs_gemm_bound(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), c, True,
+                           eps_f64=False, path=1).cpu().numpy()
+    assert_bound(got, ref, "scores")
+    x = rng.standard_normal((1000, K)).astype(np.float32)
+    w = rng.standard_normal((K, 700)).astype(np.float32)
+    y = (x @ w).astype(np.float32)
+    u = 2.0 ** -24
+    ref = OB.matmul_bound(x, w, OB.FpModel()) + u * np.abs(y.astype(np.float64))
+    got = B.abs_gemm_bound(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), c, False,
+                           y=torch.from_numpy(y).cuda(), u=u, eps_f64=False, path=1,
+                           cache_b=True).cpu().numpy()
+    assert_bound(got, ref, "linear")
