@@ -339,7 +339,10 @@ def apply_value(node, xs, profile) -> torch.Tensor:
     if kind == "embedding":
         ids, table = xs
         idx = ids.to(torch.int64)
-        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= table.shape[0]):
+        # the range check reads back to the host; a CUDA-graph capture validates
+        # its ids before recording (executor.GraphedRun) and skips it here
+        if idx.numel() and not torch.cuda.is_current_stream_capturing() and (
+                int(idx.min()) < 0 or int(idx.max()) >= table.shape[0]):
             raise ValueError("embedding index out of range")
         return table[idx]
     raise ExecutionError(f"unsupported op kind {kind!r}")

@@ -80,6 +80,73 @@ def inject_drift(y: torch.Tensor, seed: int, period: int = 16, fault_scale: floa
     return out
 
 
+class _RunState:
+    """Carry-over between the stream segments of one run."""
+
+    def __init__(self):
+        self.pending, self.pend_idx, self.pend_bytes = [], [], 0
+
+
+def _segments(lo: int, hi: int, size: int):
+    return [(a, min(a + size, hi)) for a in range(lo, hi, size)]
+
+
+class GraphedRun:
+    """A verification (or plain forward) recorded as CUDA graphs: replay() is
+    one cudaGraphLaunch per segment; outputs land in the same buffers."""
+
+    def __init__(self):
+        self.graphs, self.pool, self.stream = [], None, None
+        self.roots = self.records = None
+        self.outputs = {}
+
+    @classmethod
+    def record(cls, sv, inputs, claimed_fn, start, end, frontier, seg_nodes):
+        self = cls()
+        self.pool = torch.cuda.graph_pool_handle()
+        self.stream = torch.cuda.Stream(sv.dev)
+        torch.cuda.synchronize(sv.dev)
+        st = sv._begin(inputs, start, end, frontier)
+        for lo, hi in _segments(start, st.end, seg_nodes):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, pool=self.pool, stream=self.stream):
+                sv._nodes(st, lo, hi, claimed_fn)
+            self.graphs.append(gph)
+        self.roots, self.records = sv._finish(st)
+        self.outputs = sv.outputs
+        torch.cuda.synchronize(sv.dev)
+        return self
+
+    @classmethod
+    def record_plain(cls, graph, inputs, device, start, end, frontier, seg_nodes=96):
+        self = cls()
+        dev = torch.device(device)
+        self.pool = torch.cuda.graph_pool_handle()
+        self.stream = torch.cuda.Stream(dev)
+        torch.cuda.synchronize(dev)
+        end = graph.n_nodes if end is None else end
+        values = dict(frontier or {})
+        last = last_uses(graph, start, end)
+        for lo, hi in _segments(start, end, seg_nodes):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph, pool=self.pool, stream=self.stream):
+                _plain_nodes(graph, inputs, dev, values, last, lo, hi)
+            self.graphs.append(gph)
+        self.outputs = values
+        torch.cuda.synchronize(dev)
+        return self
+
+    def replay(self):
+        """Enqueue every segment on the caller's current stream."""
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            for gph in self.graphs:
+                gph.replay()
+        cur.wait_stream(self.stream)
+        return self.roots, self.records
+
+
 @dataclass
 class NodeStats:
     bytes_committed: int = 0
@@ -129,60 +196,89 @@ class StreamingVerifier:
     # ----------------------------------------------------------------- run
     def run(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
             frontier: dict | None = None, stats: NodeStats | None = None):
-        return self._run(inputs, claimed_fn, start, end, frontier, stats)
-
-    def _run(self, inputs, claimed_fn, start, end, frontier, stats):
         """Verify nodes [start, end).  claimed_fn(node, y) -> the claimed CUDA tensor
         of node (the proposer's trace; given the locally recomputed y for harnesses).
         frontier maps external producer node index -> tensor (slice execution,
         graph.py:244-272).  Returns (roots [n,32] uint8, records [n, R] uint8)."""
+        st = self._begin(inputs, start, end, frontier)
+        self._nodes(st, start, st.end, claimed_fn, stats)
+        return self._finish(st)
+
+    def _begin(self, inputs, start, end, frontier, roots=None, records=None):
         g = self.g
         end = g.n_nodes if end is None else end
         n = end - start
-        roots = torch.empty((n, 32), dtype=torch.uint8, device=self.dev)
-        records = new_result_buffer(self.dev, n)
-        last = last_uses(g, start, end)
-        values = dict(frontier or {})
-        pending, pend_idx, pend_bytes = [], [], 0
         _lib.load()
+        st = _RunState()
+        st.inputs, st.start, st.end = inputs, start, end
+        st.roots = roots if roots is not None else torch.empty((n, 32), dtype=torch.uint8,
+                                                                device=self.dev)
+        st.records = records if records is not None else new_result_buffer(self.dev, n)
+        st.last = last_uses(g, start, end)
+        st.values = dict(frontier or {})
+        st.all_idx = torch.arange(n, device=self.dev)
+        st.grid_arr = _lib.dbl_array(self.grid)
+        return st
+
+    def _finish(self, st):
+        self.outputs = {k: v for k, v in st.values.items()}
+        return st.roots, st.records
+
+    def _nodes(self, st, lo, hi, claimed_fn, stats=None):
+        """Process nodes [lo, hi) of the run, then flush pending commits and
+        join the side streams (a self-contained stream segment: it can be
+        captured as one CUDA graph)."""
+        g = self.g
         main = torch.cuda.current_stream(self.dev)
         s_chk = self._s_chk or main
         s_com = self._s_com or main
+        capturing = torch.cuda.is_current_stream_capturing()
         if self.overlap:  # side streams start after everything already queued on main
             s_chk.wait_stream(main)
             s_com.wait_stream(main)
         with torch.cuda.stream(s_chk):
             ws_chk = _lib.check_accumulator(self.dev)
         chk_ptr = s_chk.cuda_stream
-        grid_arr = _lib.dbl_array(self.grid)
-        all_idx = torch.arange(n, device=self.dev)
+        start = st.start
+        # tensors read on a side stream: record_stream when eager; held until
+        # the segment's join when capturing (a capture cannot record events)
+        keep = []
+
+        def side_use(t, s):
+            if not self.overlap:
+                return
+            if capturing:
+                keep.append(t)
+            else:
+                t.record_stream(s)
 
         def flush():
-            nonlocal pending, pend_idx, pend_bytes
-            if not pending:
+            if not st.pending:
                 return
             if self.overlap:
                 s_com.wait_stream(main)
             with torch.cuda.stream(s_com):
-                r = commit_tensors(pending, self.chunk, self.alg)
-                lo, hi = pend_idx[0], pend_idx[-1] + 1
-                if hi - lo == len(pend_idx):
-                    roots[lo:hi].copy_(r)
+                r = commit_tensors(st.pending, self.chunk, self.alg)
+                lo_i, hi_i = st.pend_idx[0], st.pend_idx[-1] + 1
+                if hi_i - lo_i == len(st.pend_idx):
+                    st.roots[lo_i:hi_i].copy_(r)
                 else:
-                    roots.index_copy_(0, all_idx[torch.as_tensor(pend_idx)], r)
-            if self.overlap:
-                for t in pending:
-                    t.record_stream(s_com)
-            pending, pend_idx, pend_bytes = [], [], 0
+                    st.roots.index_copy_(0, st.all_idx[torch.as_tensor(st.pend_idx)], r)
+            for t in st.pending:
+                side_use(t, s_com)
+            if self.overlap and capturing:
+                keep.append(r)
+            st.pending, st.pend_idx, st.pend_bytes = [], [], 0
 
-        for node in g.nodes[start:end]:
+        values, last = st.values, st.last
+        for node in g.nodes[lo:hi]:
             xs = []
             for ref in node.inputs:
                 cat, key = parse_ref(ref)
                 if cat == "node":
                     xs.append(values[key])
                 elif cat == "input":
-                    xs.append(to_device(inputs[key], self.dev))
+                    xs.append(to_device(st.inputs[key], self.dev))
                 else:
                     xs.append(to_device(g.weights[key], self.dev))
             try:
@@ -195,27 +291,28 @@ class StreamingVerifier:
             y = y.contiguous()
             yc = claimed_fn(node, y)
             tau_a, tau_r = self._taus(node.name)
-            kind, eps_ptr, scale, lo = _lib.EPS_ZERO, None, 0.0, 1.0
+            kind, eps_ptr, scale, lo_f = _lib.EPS_ZERO, None, 0.0, 1.0
             if isinstance(eps, tuple):
                 if eps[0] == "scaled":
                     kind, scale = _lib.EPS_SCALED_LOCAL, float(eps[1])
             else:
                 kind = _lib.EPS_TENSOR_F64 if eps.dtype == torch.float64 else _lib.EPS_TENSOR_F32
-                lo = 1.0 if eps.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
+                lo_f = 1.0 if eps.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
                 eps_ptr = eps.data_ptr()
             i = node.index - start
             if y.numel():
                 if self.overlap:
                     s_chk.wait_stream(main)
-                    y.record_stream(s_chk)
-                    yc.record_stream(s_chk)
+                    side_use(y, s_chk)
+                    side_use(yc, s_chk)
                     if not isinstance(eps, tuple):
-                        eps.record_stream(s_chk)
+                        side_use(eps, s_chk)
                 with torch.cuda.stream(s_chk):
                     _lib.call("nao_check", y.data_ptr(), yc.data_ptr(), y.numel(), kind, eps_ptr,
-                              scale, lo, grid_arr, _lib.dbl_array(tau_a), _lib.dbl_array(tau_r),
-                              len(self.grid), self.epsilon, records[i].data_ptr(),
-                              ws_chk.data_ptr(), ws_chk.numel(), chk_ptr)
+                              scale, lo_f, st.grid_arr, _lib.dbl_array(tau_a),
+                              _lib.dbl_array(tau_r), len(self.grid), self.epsilon,
+                              st.records[i].data_ptr(), ws_chk.data_ptr(), ws_chk.numel(),
+                              chk_ptr)
             if stats is not None:
                 stats.elements_checked += y.numel()
                 stats.bytes_committed += y.numel() * 4
@@ -224,10 +321,10 @@ class StreamingVerifier:
             del eps, y
             yc = yc.contiguous()
             values[node.index] = yc
-            pending.append(yc)
-            pend_idx.append(i)
-            pend_bytes += yc.numel() * 4
-            if pend_bytes >= self.flush_bytes or len(pending) >= 120:
+            st.pending.append(yc)
+            st.pend_idx.append(i)
+            st.pend_bytes += yc.numel() * 4
+            if st.pend_bytes >= self.flush_bytes or len(st.pending) >= 120:
                 flush()
             for ref in node.inputs:
                 cat, key = parse_ref(ref)
@@ -239,8 +336,18 @@ class StreamingVerifier:
         if self.overlap:
             main.wait_stream(s_chk)
             main.wait_stream(s_com)
-        self.outputs = {k: v for k, v in values.items()}
-        return roots, records
+        keep.clear()
+
+    # ------------------------------------------------------------ graphs
+    def capture(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
+                frontier: dict | None = None, seg_nodes: int = 96):
+        """Record the verification of nodes [start, end) as a chain of CUDA
+        graphs (segments of ~seg_nodes nodes, one shared memory pool) and
+        return a GraphedRun whose replay() re-runs it with no host work per
+        node.  `inputs` / `frontier` / weights must stay at the same device
+        addresses (refill them in place between replays).  Call run() once
+        first (warm-up: weight split caches, workspaces)."""
+        return GraphedRun.record(self, inputs, claimed_fn, start, end, frontier, seg_nodes)
 
     def trace_root(self, roots: torch.Tensor) -> torch.Tensor:
         """Merkle root over per-node roots (leaf = H(0x00||root)), on device."""
@@ -277,14 +384,8 @@ def plain_value(node, xs, profile=NATIVE) -> torch.Tensor:
     return apply_value(node, xs, profile)
 
 
-def plain_forward(graph, inputs: dict, device="cuda", start: int = 0, end: int | None = None,
-                  frontier: dict | None = None):
-    g = graph
-    end = g.n_nodes if end is None else end
-    last = last_uses(g, start, end)
-    values = dict(frontier or {})
-    dev = torch.device(device)
-    for node in g.nodes[start:end]:
+def _plain_nodes(g, inputs, dev, values, last, lo, hi):
+    for node in g.nodes[lo:hi]:
         xs = []
         for ref in node.inputs:
             cat, key = parse_ref(ref)
@@ -299,4 +400,13 @@ def plain_forward(graph, inputs: dict, device="cuda", start: int = 0, end: int |
             cat, key = parse_ref(ref)
             if cat == "node" and last.get(key, -1) == node.index and key in values:
                 del values[key]
+
+
+def plain_forward(graph, inputs: dict, device="cuda", start: int = 0, end: int | None = None,
+                  frontier: dict | None = None):
+    g = graph
+    end = g.n_nodes if end is None else end
+    last = last_uses(g, start, end)
+    values = dict(frontier or {})
+    _plain_nodes(g, inputs, torch.device(device), values, last, start, end)
     return values

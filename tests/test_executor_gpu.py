@@ -114,3 +114,55 @@ def test_streaming_decoder_bounds_vs_oracle():
     assert viol["l1_down"] > 0
     outs = plain_forward(g, ids)
     assert set(outs) >= {g.n_nodes - 1}
+
+
+@pytest.mark.parametrize("seg", [7, 1000])
+def test_graphed_replay_matches_eager(seg):
+    """StreamingVerifier.capture: CUDA-graph replay (segments of `seg` nodes,
+    side streams forked/joined inside each graph) gives the eager run's roots,
+    check records and outputs bit for bit, replay after replay, and follows
+    in-place refills of the input buffer."""
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.engine import to_device
+    from paper_2510_16028_b200.executor import (GraphedRun, StreamingVerifier, drift_claim,
+                                                plain_forward)
+    from paper_2510_16028_b200.lowerings import DecoderShape, build_decoder
+    from paper_2510_16028_b200.tensor import Rng
+    shape = DecoderShape("tiny-qwen", layers=2, hidden=128, heads=4, kv_heads=2, head_dim=32,
+                         inter=256, vocab=500, seq=64)
+    spec = build_decoder(shape, seed=5)
+    g = spec.graph
+    ids = spec.make_inputs(Rng(11))
+    sv = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256)
+
+    def claimed_fn(node, y):
+        return drift_claim(node, y, seed=2, period=4, fault_node="l1_down")
+
+    r0, c0 = sv.run(ids, claimed_fn)
+    out0 = {k: v.clone() for k, v in sv.outputs.items()}
+    r0, c0 = r0.clone(), c0.clone()
+    gr = sv.capture(ids, claimed_fn, seg_nodes=seg)
+    for _ in range(2):
+        r1, c1 = gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(r1, r0)
+        assert torch.equal(c1, c0)
+        for k, v in out0.items():
+            assert torch.equal(gr.outputs[k], v)
+    # refill the static input in place: replay follows the new ids
+    ids2 = spec.make_inputs(Rng(12))
+    ids_dev = to_device(ids["ids"])
+    ids_dev.copy_(to_device(ids2["ids"]))
+    r2, c2 = gr.replay()
+    sv2 = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256)
+    r3, c3 = sv2.run(ids2, claimed_fn)
+    torch.cuda.synchronize()
+    assert torch.equal(r2, r3) and torch.equal(c2, c3)
+    assert not torch.equal(r2, r0)
+    # plain forward graphs: same values as eager
+    gp = GraphedRun.record_plain(g, ids, "cuda", 0, None, None, seg_nodes=seg)
+    gp.replay()
+    ref = plain_forward(g, ids, "cuda")
+    torch.cuda.synchronize()
+    for k in ref:
+        assert torch.equal(gp.outputs[k], ref[k])
