@@ -180,7 +180,7 @@ def run_ours(args):
 
     fault = args.fault_node
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
-                           chunk_bytes=args.chunk)
+                           chunk_bytes=args.chunk, fuse_check=not args.separate_check)
 
     def claimed_fn(node, y):
         return drift_claim(node, y, 1, args.drift_period, fault)
@@ -271,7 +271,7 @@ def run_ours(args):
             return 4.0 * a[4] * a[5] + (4.0 + (8.0 if a[3] else 4.0)) * a[4]
         if name == "nao_unary_fp64":
             return 8.0 * a[2]
-        if name == "nao_merkle_commit_tensors":
+        if name in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
             return float(sum(a[2][i] for i in range(a[0])))
         if name == "nao_check":
             return 8.0 * a[2] + (4.0 if a[3] == 0 else 8.0 if a[3] == 1 else 0.0) * a[2]
@@ -380,7 +380,8 @@ def run_ours(args):
                     "peak_source": "derived FP32 FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz "
                                    "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
                     "traffic": None}
-        elif dom == "nao_merkle_commit_tensors" and args.hash == "keccak256":
+        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors") and \
+                args.hash == "keccak256":
             # Keccak-f[1600] is integer-ALU bound, not HBM bound: 24 rounds x 180
             # ALU ops (122 LOP3 + 58 SHF.L.W, cuobjdump) per 136-byte block on a
             # 64-lane/clk/SM ALU pipe (profiles/r1_keccak_pipe_balance.md)
@@ -415,7 +416,8 @@ def run_ours(args):
                             else f"{sum(v['units']) / t / 1e9:.0f} GB/s")
         roof["kernel_rates"] = rates
 
-    commit_ms = shares.get("nao_merkle_commit_tensors", 0.0)
+    commit_ms = (shares.get("nao_merkle_commit_tensors", 0.0) +
+                 shares.get("nao_commit_check_tensors", 0.0))
     merkle_gbs = (stats.bytes_committed / (commit_ms * 1e-3) / 1e9) if commit_ms else None
 
     if rank != 0:
@@ -594,6 +596,8 @@ def main(argv=None):
     ap.add_argument("--calib-samples", type=int, default=4)
     ap.add_argument("--debug-exceed", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--separate-check", action="store_true",
+                    help="standalone nao_check per node instead of the check fused into commit")
     ap.add_argument("--graphs", type=int, default=0, metavar="SEG",
                     help="replay both arms as CUDA graphs of SEG-node segments (0 = eager "
                          "dispatch; the host enqueues faster than the GPU drains either way)")

@@ -108,6 +108,39 @@ int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind,
               double eps_scale, double lo_factor, const double* grid, const double* tau_abs,
               const double* tau_rel, int n_grid, double epsilon, nao_check_result* result,
               void* workspace, size_t workspace_bytes, void* stream);
+/* Per-node verdict spec: grid + thresholds prepared once on the host
+ * (ThresholdSet.lookup(name), calibration.py:117-191) and kept in device
+ * memory; nao_verdict_spec_bytes() bytes, filled by nao_verdict_spec_fill
+ * into a HOST buffer the caller then copies to the device. */
+size_t nao_verdict_spec_bytes(void);
+int nao_verdict_spec_fill(void* spec_host, const double* grid, const double* tau_abs,
+                          const double* tau_rel, int n_grid, double epsilon);
+/* The check of one claimed tensor, fused into its Merkle commitment
+ * (nao_commit_check_tensors).  local/eps/spec/result are device pointers;
+ * local == NULL disables the check for that tensor. */
+typedef struct nao_check_desc {
+    const float* local;          /* recomputed node output, 16-byte aligned */
+    const void* eps;             /* eps array for NAO_EPS_TENSOR_* (else NULL) */
+    const void* spec;            /* device nao_verdict_spec of the node */
+    nao_check_result* result;    /* device record, written by the last CTA */
+    double eps_scale;            /* NAO_EPS_SCALED_LOCAL */
+    double lo_factor;            /* borderline band (see nao_check) */
+    int32_t eps_kind;
+    int32_t reserved;
+} nao_check_desc;
+/* nao_merkle_commit_tensors + nao_check of every tensor in the SAME pass:
+ * payloads are the claimed tensors; checks[i] (host array, n_tensors entries)
+ * compares payload i with checks[i].local (the reference's leaf route,
+ * dispute.py:639-671, one record per tensor; empty tensors get none).
+ * accum: device scratch of nao_commit_check_accum_bytes(), zero before its
+ * first use and left zeroed by every call (dedicated per stream).
+ * Workspace as nao_merkle_commit_workspace. */
+size_t nao_commit_check_accum_bytes(void);
+int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
+                             const uint64_t* payload_bytes, const uint8_t* const* headers,
+                             const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                             const nao_check_desc* checks, uint8_t* roots_out, void* accum,
+                             void* workspace, size_t workspace_bytes, void* stream);
 /* Exact numpy method="linear" percentile profiles (calibration.py:33-37):
  * of |local-claimed| and |local-claimed|/(|local|+epsilon) (calibration.py:40-49),
  * or of an arbitrary FP64 array.  Outputs are device arrays of n_grid doubles. */

@@ -46,6 +46,13 @@ class CheckResult(ctypes.Structure):
 
 CHECK_RESULT_BYTES = ctypes.sizeof(CheckResult)
 
+
+class CheckDesc(ctypes.Structure):
+    """nao_check_desc: the check fused into nao_commit_check_tensors."""
+    _fields_ = [("local", c_vp), ("eps", c_vp), ("spec", c_vp), ("result", c_vp),
+                ("eps_scale", ctypes.c_double), ("lo_factor", ctypes.c_double),
+                ("eps_kind", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
 # name -> (restype, argtypes)
 _SIGS = {
     "nao_version": (c_int, []),
@@ -59,6 +66,14 @@ _SIGS = {
     "nao_merkle_root_workspace": (c_sz, [c_i64]),
     "nao_merkle_root_of": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "nao_check_workspace": (c_sz, []),
+    "nao_verdict_spec_bytes": (c_sz, []),
+    "nao_verdict_spec_fill": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
+                                      ctypes.POINTER(c_dbl), c_int, c_dbl]),
+    "nao_commit_check_accum_bytes": (c_sz, []),
+    "nao_commit_check_tensors": (c_int, [c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_u64),
+                                         ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_uint32),
+                                         c_u64, c_int, ctypes.POINTER(CheckDesc), c_vp, c_vp,
+                                         c_vp, c_sz, c_vp]),
     "nao_check": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_dbl, c_dbl,
                           ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                           c_int, c_dbl, c_vp, c_vp, c_sz, c_vp]),
@@ -198,6 +213,27 @@ def workspace(nbytes: int, device) -> torch.Tensor:
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
         _ws[key] = buf
     return buf
+
+
+def commit_check_accumulator(device) -> torch.Tensor:
+    """Zero-initialised accumulator of nao_commit_check_tensors per (device, stream)."""
+    dev = torch.device(device)
+    key = ("commit_check", dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws.get(key)
+    if buf is None:
+        buf = torch.zeros(int(load().nao_commit_check_accum_bytes()), dtype=torch.uint8,
+                          device=dev)
+        _ws[key] = buf
+    return buf
+
+
+def verdict_spec(grid, tau_abs, tau_rel, epsilon) -> bytes:
+    """Host bytes of one nao_verdict_spec (upload them to the device)."""
+    L = load(require_cuda=False)
+    buf = ctypes.create_string_buffer(int(L.nao_verdict_spec_bytes()))
+    check(L.nao_verdict_spec_fill(buf, dbl_array(grid), dbl_array(tau_abs), dbl_array(tau_rel),
+                                  len(grid), float(epsilon)), "nao_verdict_spec_fill")
+    return buf.raw
 
 
 def check_accumulator(device) -> torch.Tensor:

@@ -242,9 +242,13 @@ def _as_payload(t: torch.Tensor) -> torch.Tensor:
 
 
 def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
-                   out: torch.Tensor | None = None, leaf_digests: torch.Tensor | None = None):
+                   out: torch.Tensor | None = None, leaf_digests: torch.Tensor | None = None,
+                   checks=None):
     """Chunked tensor roots for CUDA tensors, one batched launch set, no host
-    sync.  Returns an (n, 32) uint8 CUDA tensor (row i = root of tensors[i])."""
+    sync.  Returns an (n, 32) uint8 CUDA tensor (row i = root of tensors[i]).
+    checks: optional list of _lib.CheckDesc (or None entries), one per tensor:
+    the acceptance check of tensor i against checks[i].local runs inside the
+    same hashing pass (nao_commit_check_tensors)."""
     tensors = [_as_payload(t) for t in tensors]
     n = len(tensors)
     if n == 0:
@@ -260,9 +264,21 @@ def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
     L = _lib.load()
     wsb = L.nao_merkle_commit_workspace(n, sizes, chunk_bytes)
     ws = _lib.workspace(wsb, dev)
-    _lib.call("nao_merkle_commit_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes, alg_id(alg),
-              roots.data_ptr(), _lib.ptr(leaf_digests), ws.data_ptr(), ws.numel(),
-              _lib.stream_ptr(dev))
+    if checks is not None:
+        if leaf_digests is not None:
+            raise ValueError("leaf digests are not exported by the fused commit+check")
+        descs = (_lib.CheckDesc * n)()
+        for i, c in enumerate(checks):
+            if c is not None:
+                descs[i] = c
+        acc = _lib.commit_check_accumulator(dev)
+        _lib.call("nao_commit_check_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes,
+                  alg_id(alg), descs, roots.data_ptr(), acc.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream_ptr(dev))
+    else:
+        _lib.call("nao_merkle_commit_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes,
+                  alg_id(alg), roots.data_ptr(), _lib.ptr(leaf_digests), ws.data_ptr(),
+                  ws.numel(), _lib.stream_ptr(dev))
     # keep payload tensors alive until the kernels that read them have run
     if torch.cuda.is_current_stream_capturing() is False:
         for t in tensors:

@@ -23,20 +23,9 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "check_common.cuh"
 
 namespace nao {
-
-constexpr int kMaxGrid = 32;
-
-struct CheckAccum {  // device scratch: zero on first use, left zeroed by every call
-    unsigned long long n_viol, n_border, n_nonfinite;
-    unsigned long long hist_abs[kMaxGrid + 1];
-    unsigned long long hist_rel[kMaxGrid + 1];
-    unsigned long long max_ratio_bits;       // non-negative double
-    unsigned long long amb_lo[2 * kMaxGrid];  // max key <= tau (double bits)
-    unsigned long long amb_hi[2 * kMaxGrid];  // min key >  tau (double bits)
-    unsigned int blocks_done;
-};
 
 struct CheckParams {
     const float* local;
@@ -46,63 +35,8 @@ struct CheckParams {
     int eps_kind;       // NAO_EPS_*
     double eps_scale;   // NAO_EPS_SCALED_LOCAL: eps = scale*|local|
     double lo_factor;   // borderline band
-    double epsilon;     // relative-error guard (calibration.py:19)
-    int G;
-    double t_abs[kMaxGrid];   // thresholds sorted ascending (host)
-    double t_rel[kMaxGrid];
-    // finalize (original grid order)
-    double grid[kMaxGrid];
-    double tau_abs[kMaxGrid];  // effective thresholds
-    double tau_rel[kMaxGrid];
-    int lpos_abs[kMaxGrid];    // #{sorted t < tau_i}
-    int lpos_rel[kMaxGrid];
+    VerdictSpec v;      // grid, thresholds, epsilon
 };
-
-__device__ __forceinline__ int bsearch_pos(const double* t, int G, double key) {
-    int pos = 0;  // number of thresholds strictly below key
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1)
-        if (pos + step <= G && t[pos + step - 1] < key) pos += step;
-    return pos;
-}
-__device__ __forceinline__ int bsearch_pos32(const float* t, int G, float key) {
-    int pos = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1)
-        if (pos + step <= G && t[pos + step - 1] < key) pos += step;
-    return pos;
-}
-
-// Exact FP64 keys of one element (dispute.py:134-138).
-__device__ __forceinline__ double abs_key(float y, float yc) {
-    return fabs(__dsub_rn((double)y, (double)yc));
-}
-__device__ __forceinline__ double rel_key(double diff, float y, double epsilon) {
-    return __ddiv_rn(diff, __dadd_rn(fabs((double)y), epsilon));
-}
-
-// numpy _lerp (_function_base_impl.py:4657-4679), no FMA contraction.
-__device__ __forceinline__ double np_lerp(double a, double b, double t) {
-    double d = __dsub_rn(b, a);
-    double r = __dadd_rn(a, __dmul_rn(d, t));
-    if (t >= 0.5) r = __dsub_rn(b, __dmul_rn(d, __dsub_rn(1.0, t)));
-    return r;
-}
-
-// virtual index (n-1)*q, q = p/100 (_function_base_impl.py:126-129, :4277)
-struct VIdx { int64_t prev, next; double g; bool last; };
-__device__ __forceinline__ VIdx virtual_index(int64_t n, double p) {
-    VIdx v;
-    double q = __ddiv_rn(p, 100.0);
-    double vi = __dmul_rn((double)(n - 1), q);
-    if (vi >= (double)(n - 1)) {
-        v.prev = v.next = n - 1; v.g = __dadd_rn(vi, 1.0); v.last = true;
-    } else {
-        double f = floor(vi);
-        v.prev = (int64_t)f; v.next = v.prev + 1; v.g = __dsub_rn(vi, f); v.last = false;
-    }
-    return v;
-}
 
 constexpr int kCheckThreads = 256, kCheckWarps = kCheckThreads / 32, kQ = 64;
 constexpr float kGuard = 1.0f / 524288.0f;  // 2^-19 relative guard for the FP32 fast path
@@ -115,10 +49,8 @@ struct CheckSmem {
     double qe[kCheckWarps][kQ];                      // non-zero differences
     unsigned long long viol, border, nonfin;
     double maxr;
-    // finalize
-    int amb[2 * kMaxGrid];
-    int n_amb, exceeded, first, is_last;
-    unsigned long long amb_lo[2 * kMaxGrid], amb_hi[2 * kMaxGrid];
+    int is_last;
+    VerdictSmem vs;
 };
 
 template <int EPSK>
@@ -129,47 +61,17 @@ __device__ __forceinline__ double load_eps(const CheckParams& p, int64_t i, floa
     return 0.0;
 }
 
-// Decide every (array, grid point) from the interval histograms; returns the
-// number of ambiguous targets (k+1 keys <= tau) -- those need amb_lo / amb_hi.
-__device__ void finalize_targets(const CheckParams& p, CheckAccum* acc, CheckSmem& sm, bool phase2) {
-    const int G = p.G;
-    const int t = threadIdx.x;
-    if (t == 0) { sm.n_amb = 0; sm.exceeded = 0; sm.first = 0x7fffffff; }
-    __syncthreads();
-    if (t < 2 * G) {
-        const int arr = t / G, i = t % G;
-        const volatile unsigned long long* hist = arr == 0 ? acc->hist_abs : acc->hist_rel;
-        const double tau = arr == 0 ? p.tau_abs[i] : p.tau_rel[i];
-        const int L = arr == 0 ? p.lpos_abs[i] : p.lpos_rel[i];
-        unsigned long long cle = 0;
-        for (int b = 0; b <= L; b++) cle += hist[b];
-        const VIdx v = virtual_index(p.n, p.grid[i]);
-        bool ex;
-        if (v.last) ex = cle < (unsigned long long)p.n;
-        else if (cle <= (unsigned long long)v.prev) ex = true;
-        else if (cle >= (unsigned long long)v.prev + 2) ex = false;
-        else if (!phase2) { sm.amb[arr * kMaxGrid + i] = 1; atomicAdd(&sm.n_amb, 1); ex = false; }
-        else {
-            const double a = __longlong_as_double((long long)sm.amb_lo[arr * kMaxGrid + i]);
-            const double b = __longlong_as_double((long long)sm.amb_hi[arr * kMaxGrid + i]);
-            ex = np_lerp(a, b, v.g) > tau;
-        }
-        if (ex) { atomicOr(&sm.exceeded, 1); atomicMin(&sm.first, arr * G + i); }
-    }
-    __syncthreads();
-}
-
 template <int EPSK>
 __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constant__ CheckParams p,
                                                          CheckAccum* __restrict__ acc,
                                                          nao_check_result* __restrict__ out) {
     __shared__ CheckSmem sm;
-    const int G = p.G;
+    const int G = p.v.G;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x < kMaxGrid) {
         const int i = threadIdx.x;
-        const double ta = i < G ? p.t_abs[i] : INFINITY;
-        const double tr = i < G ? p.t_rel[i] : INFINITY;
+        const double ta = i < G ? p.v.t_abs[i] : INFINITY;
+        const double tr = i < G ? p.v.t_rel[i] : INFINITY;
         sm.t_abs[i] = ta;
         sm.t_rel[i] = tr;
         const float fr = (float)tr;
@@ -177,7 +79,7 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         sm.f_rel_lo[i] = fr * (1.0f - kGuard);
         sm.f_rel_hi[i] = fr * (1.0f + kGuard);
     }
-    if (threadIdx.x < 2 * kMaxGrid) { sm.amb[threadIdx.x] = 0; }
+    if (threadIdx.x < 2 * kMaxGrid) { sm.vs.amb[threadIdx.x] = 0; }
     for (int b = lane; b <= kMaxGrid; b += 32) { sm.wc[w][0][b] = 0; sm.wc[w][1][b] = 0; }
     if (threadIdx.x == 0) { sm.viol = sm.border = sm.nonfin = 0; sm.maxr = 0.0; sm.is_last = 0; }
     __syncthreads();
@@ -206,12 +108,12 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         if (diff != 0.0) {
             pa = bsearch_pos(sm.t_abs, G, diff);
             const float d32 = (float)diff;
-            const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)p.epsilon));
+            const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)p.v.epsilon));
             q = bsearch_pos32(sm.f_rel, G, r32);
             const bool safe = (d32 >= 1e-30f) && (r32 >= 1e-30f) && isfinite(r32) &&
                               (q == G || r32 < sm.f_rel_lo[q]) &&
                               (q == 0 || r32 > sm.f_rel_hi[q - 1]);
-            if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, p.epsilon));
+            if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, p.v.epsilon));
         }
         atomicAdd(&sm.wc[w][0][pa], 1u);
         atomicAdd(&sm.wc[w][1][q], 1u);
@@ -344,29 +246,10 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
 
     // ---- last block: decide all 2G targets, settle ambiguous ones exactly
     __threadfence();
-    finalize_targets(p, acc, sm, false);
-    if (sm.n_amb > 0) {
-        if (threadIdx.x < 2 * kMaxGrid) {
-            sm.amb_lo[threadIdx.x] = 0ull;
-            sm.amb_hi[threadIdx.x] = 0x7ff0000000000000ull;  // +inf
-        }
-        __syncthreads();
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const float y = p.local[i], c = p.claimed[i];
-            const double diff = abs_key(y, c);
-            const double rel = rel_key(diff, y, p.epsilon);
-            for (int t = 0; t < 2 * G; t++) {
-                const int arr = t / G, gi = t % G;
-                if (!sm.amb[arr * kMaxGrid + gi]) continue;
-                const double key = arr == 0 ? diff : rel;
-                const double tau = arr == 0 ? p.tau_abs[gi] : p.tau_rel[gi];
-                const unsigned long long bits = (unsigned long long)__double_as_longlong(key);
-                if (key <= tau) atomicMax(&sm.amb_lo[arr * kMaxGrid + gi], bits);
-                else atomicMin(&sm.amb_hi[arr * kMaxGrid + gi], bits);
-            }
-        }
-        __syncthreads();
-        finalize_targets(p, acc, sm, true);
+    decide_targets(p.v, n, acc->hist_abs, acc->hist_rel, sm.vs, false);
+    if (sm.vs.n_amb > 0) {
+        settle_ambiguous(p.v, p.local, p.claimed, n, sm.vs);
+        decide_targets(p.v, n, acc->hist_abs, acc->hist_rel, sm.vs, true);
     }
     if (threadIdx.x == 0) {
         out->n = (uint64_t)n;
@@ -374,9 +257,9 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         out->n_borderline = acc->n_border;
         out->n_nonfinite = acc->n_nonfinite;
         out->max_ratio = __longlong_as_double((long long)acc->max_ratio_bits);
-        out->threshold_exceeded = sm.exceeded;
-        out->first_exceeded = sm.exceeded ? sm.first : -1;
-        out->n_ambiguous = sm.n_amb;
+        out->threshold_exceeded = sm.vs.exceeded;
+        out->first_exceeded = sm.vs.exceeded ? sm.vs.first : -1;
+        out->n_ambiguous = sm.vs.n_amb;
         out->reserved = 0;
     }
     __syncthreads();
@@ -460,6 +343,33 @@ static int fill_grid(FinalParams& fp, const double* grid, int G) {
     return NAO_OK;
 }
 
+int fill_verdict_spec(VerdictSpec& v, const double* grid, const double* tau_abs,
+                      const double* tau_rel, int n_grid, double epsilon) {
+    NAO_REQUIRE(n_grid > 0 && n_grid <= kMaxGrid, "grid size %d out of range (1..%d)", n_grid,
+                kMaxGrid);
+    NAO_REQUIRE(grid && tau_abs && tau_rel, "null grid/threshold array");
+    memset(&v, 0, sizeof v);
+    v.G = n_grid;
+    v.epsilon = epsilon;
+    double sa[kMaxGrid], sr[kMaxGrid];
+    for (int i = 0; i < n_grid; i++) {
+        NAO_REQUIRE(std::isfinite(grid[i]) && grid[i] >= 0.0 && grid[i] <= 100.0,
+                    "Percentiles must be in the range [0, 100]");
+        v.grid[i] = grid[i];
+        v.tau_abs[i] = sa[i] = tau_abs[i] > 0.0 ? tau_abs[i] : 0.0;
+        v.tau_rel[i] = sr[i] = tau_rel[i] > 0.0 ? tau_rel[i] : 0.0;
+    }
+    std::sort(sa, sa + n_grid);
+    std::sort(sr, sr + n_grid);
+    for (int i = 0; i < n_grid; i++) {
+        v.t_abs[i] = sa[i];
+        v.t_rel[i] = sr[i];
+        v.lpos_abs[i] = (int)(std::lower_bound(sa, sa + n_grid, v.tau_abs[i]) - sa);
+        v.lpos_rel[i] = (int)(std::lower_bound(sr, sr + n_grid, v.tau_rel[i]) - sr);
+    }
+    return NAO_OK;
+}
+
 }  // namespace nao
 
 using namespace nao;
@@ -467,6 +377,15 @@ using namespace nao;
 extern "C" {
 
 size_t nao_check_workspace(void) { return sizeof(CheckAccum) + 256; }
+
+size_t nao_verdict_spec_bytes(void) { return sizeof(VerdictSpec); }
+
+int nao_verdict_spec_fill(void* spec_host, const double* grid, const double* tau_abs,
+                          const double* tau_rel, int n_grid, double epsilon) {
+    NAO_REQUIRE(spec_host != nullptr, "spec buffer is null");
+    return fill_verdict_spec(*static_cast<VerdictSpec*>(spec_host), grid, tau_abs, tau_rel,
+                             n_grid, epsilon);
+}
 
 int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind, const void* eps,
               double eps_scale, double lo_factor, const double* grid, const double* tau_abs,
@@ -491,26 +410,9 @@ int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind,
     static thread_local CheckParams p;
     memset(&p, 0, sizeof p);
     p.local = local; p.claimed = claimed; p.eps = eps; p.n = n; p.eps_kind = eps_kind;
-    p.eps_scale = eps_scale; p.lo_factor = lo_factor; p.epsilon = epsilon; p.G = n_grid;
-    // effective thresholds: ratio obs/tau > 1  <=>  obs > tau (tau > 0) or obs > 0 (tau <= 0)
-    double ea[kMaxGrid], er[kMaxGrid], sa[kMaxGrid], sr[kMaxGrid];
-    for (int i = 0; i < n_grid; i++) {
-        NAO_REQUIRE(std::isfinite(grid[i]) && grid[i] >= 0.0 && grid[i] <= 100.0,
-                    "Percentiles must be in the range [0, 100]");
-        p.grid[i] = grid[i];
-        ea[i] = sa[i] = tau_abs[i] > 0.0 ? tau_abs[i] : 0.0;
-        er[i] = sr[i] = tau_rel[i] > 0.0 ? tau_rel[i] : 0.0;
-        p.tau_abs[i] = ea[i];
-        p.tau_rel[i] = er[i];
-    }
-    std::sort(sa, sa + n_grid);
-    std::sort(sr, sr + n_grid);
-    for (int i = 0; i < n_grid; i++) {
-        p.t_abs[i] = sa[i];
-        p.t_rel[i] = sr[i];
-        p.lpos_abs[i] = (int)(std::lower_bound(sa, sa + n_grid, ea[i]) - sa);
-        p.lpos_rel[i] = (int)(std::lower_bound(sr, sr + n_grid, er[i]) - sr);
-    }
+    p.eps_scale = eps_scale; p.lo_factor = lo_factor;
+    int rc = fill_verdict_spec(p.v, grid, tau_abs, tau_rel, n_grid, epsilon);
+    if (rc) return rc;
     // one resident wave: 3 CTAs per SM (launch bounds), each warp 64 float4 per step
     const int64_t warps_needed = ((n >> 2) + 63) / 64;
     const int blocks = (int)std::max<int64_t>(

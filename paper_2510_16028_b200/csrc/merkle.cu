@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "check_common.cuh"
 #include "hash.cuh"
 
 namespace nao {
@@ -80,6 +81,294 @@ __global__ void __launch_bounds__(128) k_chunk_leaves(const __grid_constant__ Ch
     uint32_t d[8];
     hash_tagged_words<ALG>(ld, nw, 0u, d);
     store_digest(digests + 8 * (tab.out_index[s] + c), d);
+}
+
+// ------------------------------------------ commit with the check fused in
+//
+// k_chunk_leaves_check: the same leaf hashing, plus the acceptance check of
+// the claimed tensor against the locally recomputed one (nao_check's verdict,
+// check.cu) folded into the loads: every claimed word the sponge absorbs is
+// compared with the local word at the same offset.  Equal finite words (the
+// common case) cost a load + two integer ops; the others take a divergent
+// slow path (exact FP64 keys, bound, histogram buckets).  Keccak is
+// integer-ALU bound (~33 ops/byte), so the check's extra HBM read rides under
+// it instead of costing a separate 8 B/element pass.
+// A CTA covers 128 consecutive chunks of ONE tensor; the last CTA of a tensor
+// decides its verdict (histogram verdict + rare exact second pass).
+
+constexpr int kLeafThreads = 128;
+
+struct CheckDesc {  // == nao_check_desc (include/nao_b200.h)
+    const float* local;
+    const void* eps;
+    const VerdictSpec* spec;
+    nao_check_result* result;
+    double eps_scale;
+    double lo_factor;
+    int32_t eps_kind;
+    int32_t reserved;
+};
+static_assert(sizeof(CheckDesc) == sizeof(nao_check_desc), "nao_check_desc layout");
+
+struct CCTable {
+    int n;
+    uint32_t chunk_words;
+    const uint32_t* payload[kMaxSegs];
+    uint64_t nbytes[kMaxSegs];
+    uint64_t out_index[kMaxSegs];
+    uint64_t block_prefix[kMaxSegs + 1];
+    CheckDesc chk[kMaxSegs];
+};
+
+constexpr int kLeafWarps = kLeafThreads / 32;
+constexpr int kMaxFusedChunkWords = 4096;  // 16 KiB chunks: 64 mask words per thread
+constexpr float kGuard32 = 1.0f / 524288.0f;  // 2^-19 guard of the FP32 relative-key search
+
+struct LeafCheckSmem {
+    double t_abs[kMaxGrid], t_rel[kMaxGrid];
+    float f_rel[kMaxGrid], f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];
+    unsigned int wc[kLeafWarps][2][kMaxGrid + 1];  // warp-private interval counters
+    unsigned long long q[kLeafWarps][64];           // warp queue of flagged element indices
+    unsigned long long viol, border, nonfin, nslow;
+    unsigned long long maxr_bits;
+    int is_last;
+    VerdictSmem vs;
+};
+
+__device__ __forceinline__ bool word_needs_check(uint32_t c, uint32_t y) {
+    return (c != y) | ((c & 0x7f800000u) == 0x7f800000u);  // differs, or inf/nan
+}
+
+// Claimed payload words for the sponge; a word that differs from the local
+// word at the same offset (or is inf/nan) sets bit i%64 of this thread's
+// mask word i/64 in shared memory -- the check itself runs after the hash.
+struct CheckedWords {
+    const uint32_t* __restrict__ p;  // claimed (hashed)
+    const uint32_t* __restrict__ q;  // local
+    unsigned long long* mask;        // this thread's mask words (stride kLeafThreads)
+    __device__ __forceinline__ void cmp(uint32_t c, uint32_t y, uint32_t i) const {
+        if (word_needs_check(c, y)) mask[(i >> 6) * kLeafThreads] |= 1ull << (i & 63);
+    }
+    __device__ __forceinline__ uint4 v4(uint32_t i) const {
+        const uint4 c = __ldg(reinterpret_cast<const uint4*>(p) + i);
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(q) + i);
+        cmp(c.x, y.x, 4 * i); cmp(c.y, y.y, 4 * i + 1);
+        cmp(c.z, y.z, 4 * i + 2); cmp(c.w, y.w, 4 * i + 3);
+        return c;
+    }
+    __device__ __forceinline__ uint2 v2(uint32_t i) const {
+        const uint2 c = __ldg(reinterpret_cast<const uint2*>(p) + i);
+        const uint2 y = __ldg(reinterpret_cast<const uint2*>(q) + i);
+        cmp(c.x, y.x, 2 * i); cmp(c.y, y.y, 2 * i + 1);
+        return c;
+    }
+    __device__ __forceinline__ uint32_t w(uint32_t i) const {
+        const uint32_t c = __ldg(p + i), y = __ldg(q + i);
+        cmp(c, y, i);
+        return c;
+    }
+};
+
+// Per-lane check state (the standalone k_check's `process`, check.cu).
+struct LaneCheck {
+    unsigned long long viol = 0, border = 0, nonfin = 0;
+    double best_num = 0.0, best_den = 1.0;  // running max of diff/eps as a fraction
+    bool best_inf = false;
+};
+
+__device__ __forceinline__ void process_flagged(const CheckDesc& d, const float* claimed,
+                                                uint64_t idx, int G, double epsilon,
+                                                LeafCheckSmem& sm, int w, LaneCheck& lc) {
+    const float y = __ldg(d.local + idx), c = __ldg(claimed + idx);
+    if (!isfinite(y) || !isfinite(c)) {
+        lc.nonfin++; lc.viol++;
+        atomicAdd(&sm.wc[w][0][G], 1u); atomicAdd(&sm.wc[w][1][G], 1u);
+        return;
+    }
+    double eps = 0.0;
+    if (d.eps_kind == NAO_EPS_TENSOR_F32) eps = (double)__ldg(static_cast<const float*>(d.eps) + idx);
+    else if (d.eps_kind == NAO_EPS_TENSOR_F64) eps = __ldg(static_cast<const double*>(d.eps) + idx);
+    else if (d.eps_kind == NAO_EPS_SCALED_LOCAL) eps = __dmul_rn(d.eps_scale, fabs((double)y));
+    const double diff = abs_key(y, c);
+    if (diff > eps) lc.viol++;
+    else if (diff > eps * d.lo_factor) lc.border++;
+    if (eps > 0.0) {
+        if (!lc.best_inf && diff * lc.best_den > lc.best_num * eps) { lc.best_num = diff; lc.best_den = eps; }
+    } else if (diff > 0.0) {
+        lc.best_inf = true;
+    }
+    int pa = 0, q = 0;
+    if (diff != 0.0) {
+        pa = bsearch_pos(sm.t_abs, G, diff);
+        const float d32 = (float)diff;
+        const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)epsilon));
+        q = bsearch_pos32(sm.f_rel, G, r32);
+        const bool safe = (d32 >= 1e-30f) && (r32 >= 1e-30f) && isfinite(r32) &&
+                          (q == G || r32 < sm.f_rel_lo[q]) && (q == 0 || r32 > sm.f_rel_hi[q - 1]);
+        if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, epsilon));
+    }
+    atomicAdd(&sm.wc[w][0][pa], 1u);
+    atomicAdd(&sm.wc[w][1][q], 1u);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kLeafThreads) k_chunk_leaves_check(
+    const __grid_constant__ CCTable tab, uint32_t* __restrict__ digests,
+    CheckAccum* __restrict__ accs) {
+    __shared__ LeafCheckSmem sm;
+    extern __shared__ unsigned long long s_mask[];  // [groups][kLeafThreads]
+    const int s = find_seg(tab.block_prefix, tab.n, blockIdx.x);  // block-uniform
+    const CheckDesc& d = tab.chk[s];
+    const bool check = d.local != nullptr;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t total_w = tab.nbytes[s] >> 2;
+    const uint32_t cw = tab.chunk_words;
+    const uint32_t groups = (cw + 63) >> 6;
+    const uint64_t nchunks = (total_w + cw - 1) / cw;
+    const uint64_t c0 = (blockIdx.x - tab.block_prefix[s]) * kLeafThreads;
+    const uint64_t c = c0 + threadIdx.x;
+    int G = 0;
+    double epsilon = 0.0;
+    if (check) {
+        const VerdictSpec* v = d.spec;
+        G = v->G;
+        epsilon = v->epsilon;
+        if (threadIdx.x < kMaxGrid) {
+            const int i = threadIdx.x;
+            const double ta = i < G ? v->t_abs[i] : INFINITY;
+            const double tr = i < G ? v->t_rel[i] : INFINITY;
+            sm.t_abs[i] = ta;
+            sm.t_rel[i] = tr;
+            const float fr = (float)tr;
+            sm.f_rel[i] = fr;
+            sm.f_rel_lo[i] = fr * (1.0f - kGuard32);
+            sm.f_rel_hi[i] = fr * (1.0f + kGuard32);
+        }
+        for (int b = lane; b <= kMaxGrid; b += 32) { sm.wc[w][0][b] = 0u; sm.wc[w][1][b] = 0u; }
+        if (threadIdx.x < 2 * kMaxGrid) sm.vs.amb[threadIdx.x] = 0;
+        if (threadIdx.x == 0) {
+            sm.viol = sm.border = sm.nonfin = sm.nslow = 0ull;
+            sm.maxr_bits = 0ull;
+            sm.is_last = 0;
+        }
+        for (uint32_t g = 0; g < groups; g++) s_mask[g * kLeafThreads + threadIdx.x] = 0ull;
+        __syncthreads();
+    }
+    if (c < nchunks) {
+        const uint64_t off_w = c * cw;
+        const uint32_t nw = (uint32_t)(total_w - off_w < cw ? total_w - off_w : cw);
+        uint32_t dg[8];
+        if (check) {
+            CheckedWords ld{tab.payload[s] + off_w,
+                            reinterpret_cast<const uint32_t*>(d.local) + off_w,
+                            s_mask + threadIdx.x};
+            hash_tagged_words<ALG>(ld, nw, 0u, dg);
+        } else {
+            GlobalWords ld{tab.payload[s] + off_w};
+            hash_tagged_words<ALG>(ld, nw, 0u, dg);
+        }
+        store_digest(digests + 8 * (tab.out_index[s] + c), dg);
+    }
+    if (!check) return;
+    __syncwarp();
+    // ---- warp-cooperative check of the flagged words: lanes push their
+    // flagged element indices into the warp queue (one per lane per round),
+    // 32 queued elements are processed with every lane busy
+    LaneCheck lc;
+    const float* claimed = reinterpret_cast<const float*>(tab.payload[s]);
+    const uint64_t lane_base = c * cw;  // element index of this lane's word 0
+    int qn = 0;                         // warp-uniform
+    unsigned long long nflag = 0;
+    for (uint32_t g = 0; g < groups; g++) {
+        unsigned long long m = s_mask[g * kLeafThreads + threadIdx.x];
+        for (;;) {
+            const bool has = m != 0ull;
+            const unsigned b = __ballot_sync(0xffffffffu, has);
+            if (b == 0u) break;
+            if (has) {
+                const int bit = __ffsll((long long)m) - 1;
+                m &= m - 1ull;
+                sm.q[w][qn + __popc(b & ((1u << lane) - 1u))] = lane_base + 64ull * g + bit;
+            }
+            qn += __popc(b);
+            nflag += has;
+            if (qn >= 32) {
+                __syncwarp();
+                process_flagged(d, claimed, sm.q[w][lane], G, epsilon, sm, w, lc);
+                __syncwarp();
+                if (lane < qn - 32) sm.q[w][lane] = sm.q[w][32 + lane];
+                __syncwarp();
+                qn -= 32;
+            }
+        }
+    }
+    __syncwarp();
+    if (lane < qn) process_flagged(d, claimed, sm.q[w][lane], G, epsilon, sm, w, lc);
+    __syncwarp();
+    // ---- block reduction -> the tensor's accumulator
+    const unsigned long long viol = warp_sum(lc.viol), border = warp_sum(lc.border),
+                             nonfin = warp_sum(lc.nonfin), nf = warp_sum(nflag);
+    double r = lc.best_inf ? INFINITY : (lc.best_num > 0.0 ? lc.best_num / lc.best_den : 0.0);
+    r = warp_max(r);
+    if (lane == 0) {
+        atomicAdd(&sm.viol, viol);
+        atomicAdd(&sm.border, border);
+        atomicAdd(&sm.nonfin, nonfin);
+        atomicAdd(&sm.nslow, nf);
+        if (r > 0.0) atomicMax(&sm.maxr_bits, (unsigned long long)__double_as_longlong(r));
+    }
+    __syncthreads();
+    CheckAccum* acc = accs + s;
+    if (threadIdx.x <= G) {
+        unsigned long long ha = 0, hr = 0;
+        for (int ww = 0; ww < kLeafWarps; ww++) {
+            ha += sm.wc[ww][0][threadIdx.x];
+            hr += sm.wc[ww][1][threadIdx.x];
+        }
+        if (threadIdx.x == 0) {  // equal words: bucket 0 of both arrays
+            const uint64_t c1 = c0 + kLeafThreads < nchunks ? c0 + kLeafThreads : nchunks;
+            const uint64_t w1 = c1 * cw < total_w ? c1 * cw : total_w;
+            const unsigned long long eq = (w1 - c0 * cw) - sm.nslow;
+            ha += eq;
+            hr += eq;
+        }
+        if (ha) atomicAdd(&acc->hist_abs[threadIdx.x], ha);
+        if (hr) atomicAdd(&acc->hist_rel[threadIdx.x], hr);
+    }
+    if (threadIdx.x == 0) {
+        if (sm.viol) atomicAdd(&acc->n_viol, sm.viol);
+        if (sm.border) atomicAdd(&acc->n_border, sm.border);
+        if (sm.nonfin) atomicAdd(&acc->n_nonfinite, sm.nonfin);
+        if (sm.maxr_bits) atomicMax(&acc->max_ratio_bits, sm.maxr_bits);
+        __threadfence();
+        const unsigned int nblk = (unsigned int)(tab.block_prefix[s + 1] - tab.block_prefix[s]);
+        sm.is_last = atomicAdd(&acc->blocks_done, 1u) == nblk - 1;
+    }
+    __syncthreads();
+    if (!sm.is_last) return;
+    __threadfence();
+    const VerdictSpec& v = *d.spec;
+    const int64_t n = (int64_t)total_w;
+    decide_targets(v, n, acc->hist_abs, acc->hist_rel, sm.vs, false);
+    if (sm.vs.n_amb > 0) {
+        settle_ambiguous(v, d.local, claimed, n, sm.vs);
+        decide_targets(v, n, acc->hist_abs, acc->hist_rel, sm.vs, true);
+    }
+    if (threadIdx.x == 0) {
+        nao_check_result* out = d.result;
+        out->n = (uint64_t)n;
+        out->n_violations = acc->n_viol;
+        out->n_borderline = acc->n_border;
+        out->n_nonfinite = acc->n_nonfinite;
+        out->max_ratio = __longlong_as_double((long long)acc->max_ratio_bits);
+        out->threshold_exceeded = sm.vs.exceeded;
+        out->first_exceeded = sm.vs.exceeded ? sm.vs.first : -1;
+        out->n_ambiguous = sm.vs.n_amb;
+        out->reserved = 0;
+    }
+    __syncthreads();
+    unsigned long long* z = reinterpret_cast<unsigned long long*>(acc);
+    for (int i = threadIdx.x; i < (int)(sizeof(CheckAccum) / 8); i += blockDim.x) z[i] = 0ull;
 }
 
 template <int ALG>
@@ -268,12 +557,16 @@ size_t nao_merkle_commit_workspace(int64_t n_tensors, const uint64_t* payload_by
     return (size_t)(32 * (leaves + 2 * lvl) + 3 * 256);
 }
 
-int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
-                              const uint64_t* payload_bytes, const uint8_t* const* headers,
-                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
-                              uint8_t* roots_out, uint8_t* leaf_digests_out, void* workspace,
-                              size_t workspace_bytes, void* stream) {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace nao {
+
+static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
+                               const uint64_t* payload_bytes, const uint8_t* const* headers,
+                               const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                               const nao_check_desc* checks, uint8_t* roots_out,
+                               uint8_t* leaf_digests_out, void* accum, void* workspace,
+                               size_t workspace_bytes, cudaStream_t st) {
     NAO_REQUIRE(n_tensors > 0, "n_tensors must be positive");
     NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg %d",
                 hash_alg);
@@ -291,6 +584,18 @@ int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
                     "payload %lld: not 16-byte aligned", (long long)i);
         NAO_REQUIRE(headers[i] != nullptr && header_lens[i] > 0 && header_lens[i] <= kMaxHeader,
                     "header %lld missing or longer than %d bytes", (long long)i, kMaxHeader);
+        if (checks && checks[i].local) {
+            const nao_check_desc& c = checks[i];
+            NAO_REQUIRE(reinterpret_cast<uintptr_t>(c.local) % 16 == 0,
+                        "check %lld: local must be 16-byte aligned", (long long)i);
+            NAO_REQUIRE(c.eps_kind >= NAO_EPS_TENSOR_F32 && c.eps_kind <= NAO_EPS_ZERO,
+                        "check %lld: bad eps_kind %d", (long long)i, c.eps_kind);
+            NAO_REQUIRE(c.eps_kind == NAO_EPS_SCALED_LOCAL || c.eps_kind == NAO_EPS_ZERO ||
+                            c.eps != nullptr, "check %lld: eps tensor missing", (long long)i);
+            NAO_REQUIRE(c.spec != nullptr && c.result != nullptr,
+                        "check %lld: spec/result missing", (long long)i);
+            NAO_REQUIRE(accum != nullptr, "checks need the accumulator scratch");
+        }
         in_index[i] = leaves;
         n_leaves[i] = 1 + seg_chunks(payload_bytes[i], chunk_bytes);
         leaves += n_leaves[i];
@@ -315,24 +620,89 @@ int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
         int rc = launch_header_leaves(hash_alg, ht, lvl0, st);
         if (rc) return rc;
     }
+    bool any_check = false;
+    for (int64_t i = 0; checks && i < n_tensors; i++) any_check |= checks[i].local != nullptr;
+    NAO_REQUIRE(!any_check || chunk_bytes / 4 <= (uint64_t)kMaxFusedChunkWords,
+                "the fused check supports chunk_bytes <= %d", 4 * kMaxFusedChunkWords);
     for (int64_t b0 = 0; b0 < n_tensors; b0 += kMaxSegs) {
-        ChunkTable ct;
+        if (!any_check) {
+            ChunkTable ct;
+            memset(&ct, 0, sizeof ct);
+            ct.chunk_words = (uint32_t)(chunk_bytes / 4);
+            int cnt = 0;
+            ct.chunk_prefix[0] = 0;
+            for (int64_t i = b0; i < n_tensors && cnt < kMaxSegs; i++, cnt++) {
+                ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
+                ct.nbytes[cnt] = payload_bytes[i];
+                ct.out_index[cnt] = in_index[i] + 1;
+                ct.chunk_prefix[cnt + 1] =
+                    ct.chunk_prefix[cnt] + seg_chunks(payload_bytes[i], chunk_bytes);
+            }
+            ct.n = cnt;
+            int rc = launch_chunk_leaves(hash_alg, ct, lvl0, st);
+            if (rc) return rc;
+            continue;
+        }
+        static thread_local CCTable ct;
         memset(&ct, 0, sizeof ct);
         ct.chunk_words = (uint32_t)(chunk_bytes / 4);
         int cnt = 0;
-        ct.chunk_prefix[0] = 0;
+        ct.block_prefix[0] = 0;
         for (int64_t i = b0; i < n_tensors && cnt < kMaxSegs; i++, cnt++) {
             ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
             ct.nbytes[cnt] = payload_bytes[i];
             ct.out_index[cnt] = in_index[i] + 1;
-            ct.chunk_prefix[cnt + 1] = ct.chunk_prefix[cnt] + seg_chunks(payload_bytes[i], chunk_bytes);
+            ct.block_prefix[cnt + 1] = ct.block_prefix[cnt] +
+                ceil_div((int64_t)seg_chunks(payload_bytes[i], chunk_bytes), kLeafThreads);
+            if (checks && payload_bytes[i] > 0) memcpy(&ct.chk[cnt], &checks[i], sizeof(CheckDesc));
         }
         ct.n = cnt;
-        int rc = launch_chunk_leaves(hash_alg, ct, lvl0, st);
-        if (rc) return rc;
+        const uint64_t blocks = ct.block_prefix[cnt];
+        if (blocks == 0) continue;
+        CheckAccum* accs = static_cast<CheckAccum*>(accum);
+        const size_t dsm = (size_t)((ct.chunk_words + 63) / 64) * kLeafThreads * 8;
+        if (hash_alg == kSHA256) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kSHA256>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            k_chunk_leaves_check<kSHA256><<<(unsigned)blocks, kLeafThreads, dsm, st>>>(ct, lvl0,
+                                                                                     accs);
+        } else {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kKECCAK256>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            k_chunk_leaves_check<kKECCAK256><<<(unsigned)blocks, kLeafThreads, dsm, st>>>(
+                ct, lvl0, accs);
+        }
+        NAO_CHECK_LAUNCH();
     }
     return reduce_trees(hash_alg, (int)n_tensors, in_index.data(), n_leaves.data(), lvl0, sa, sb,
                         reinterpret_cast<uint32_t*>(roots_out), nullptr, st);
+}
+
+}  // namespace nao
+
+extern "C" {
+
+int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
+                              const uint64_t* payload_bytes, const uint8_t* const* headers,
+                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                              uint8_t* roots_out, uint8_t* leaf_digests_out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+    return commit_tensors_impl(n_tensors, payloads, payload_bytes, headers, header_lens,
+                               chunk_bytes, hash_alg, nullptr, roots_out, leaf_digests_out,
+                               nullptr, workspace, workspace_bytes,
+                               static_cast<cudaStream_t>(stream));
+}
+
+size_t nao_commit_check_accum_bytes(void) { return sizeof(CheckAccum) * kMaxSegs; }
+
+int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
+                             const uint64_t* payload_bytes, const uint8_t* const* headers,
+                             const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
+                             const nao_check_desc* checks, uint8_t* roots_out, void* accum,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    return commit_tensors_impl(n_tensors, payloads, payload_bytes, headers, header_lens,
+                               chunk_bytes, hash_alg, checks, roots_out, nullptr, accum,
+                               workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int nao_merkle_hash_leaves(const uint8_t* data, const int64_t* offsets, int64_t n_leaves,

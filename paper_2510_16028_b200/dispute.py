@@ -124,6 +124,56 @@ def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel
     return CheckRecord(res)
 
 
+def commit_check_nodes(claimed, local, eps, taus, chunk_bytes: int = 4096, alg="keccak256",
+                       grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON):
+    """Merkle-commit every claimed tensor and check it against its local
+    recomputation in the same pass (nao_commit_check_tensors).  eps[i] as in
+    check_node; taus[i] = (tau_abs, tau_rel).  Returns (roots [n,32],
+    records [n, R]) on the device (records of empty tensors stay zero)."""
+    from .commitments import commit_tensors
+    n = len(claimed)
+    if not (len(local) == len(eps) == len(taus) == n):
+        raise ValueError("claimed/local/eps/taus lengths differ")
+    dev = to_device(claimed[0]).device
+    recs = new_result_buffer(dev, n)
+    blobs, descs, keep = [], [], []
+    for i in range(n):
+        a = to_device(local[i]).contiguous()
+        b = to_device(claimed[i]).contiguous()
+        if a.numel() != b.numel():
+            raise ValueError("shape mismatch between local and claimed")
+        ta, tr = taus[i]
+        if len(ta) != len(grid) or len(tr) != len(grid):
+            raise ValueError("percentile grid mismatch between observation and thresholds")
+        blobs.append(_lib.verdict_spec(grid, ta, tr, epsilon))
+        kind, eps_ptr, scale, lo = _lib.EPS_ZERO, None, 0.0, 1.0
+        e = eps[i]
+        if isinstance(e, tuple):
+            if e[0] == "scaled":
+                kind, scale = _lib.EPS_SCALED_LOCAL, float(e[1])
+        else:
+            e = e.reshape(-1).contiguous()
+            if e.numel() != a.numel():
+                raise ValueError("bound shape mismatch")
+            kind = _lib.EPS_TENSOR_F64 if e.dtype == torch.float64 else _lib.EPS_TENSOR_F32
+            lo = 1.0 if e.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
+            eps_ptr = e.data_ptr()
+            keep.append(e)
+        keep += [a, b]
+        descs.append((a, b, kind, eps_ptr, scale, lo))
+    size = len(blobs[0])
+    spec = torch.frombuffer(bytearray(b"".join(blobs)), dtype=torch.uint8).to(dev)
+    checks = []
+    for i, (a, b, kind, eps_ptr, scale, lo) in enumerate(descs):
+        checks.append(_lib.CheckDesc(a.data_ptr(), eps_ptr, spec.data_ptr() + i * size,
+                                     recs[i].data_ptr(), scale, lo, kind, 0)
+                      if a.numel() else None)
+    roots = commit_tensors([d[1] for d in descs], chunk_bytes, alg, checks=checks)
+    for t in keep + [spec]:
+        t.record_stream(torch.cuda.current_stream(dev))
+    return roots, recs
+
+
 def leaf_check(claimed, y_ref, eps) -> dict:
     """dispute.py:641-648 on the GPU: any(|claimed - y_ref| > eps) and its count.
     Thresholds are irrelevant here (grid of one point, tau = +inf)."""
@@ -142,5 +192,5 @@ def to_device_eps(eps) -> torch.Tensor:
 
 
 __all__ = ["p_max", "observed_p_max", "screen", "select_offending", "check_node", "leaf_check",
-           "CheckRecord", "new_result_buffer"]
+           "CheckRecord", "new_result_buffer", "commit_check_nodes"]
 _ = ctypes

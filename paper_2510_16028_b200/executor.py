@@ -85,6 +85,7 @@ class _RunState:
 
     def __init__(self):
         self.pending, self.pend_idx, self.pend_bytes = [], [], 0
+        self.pend_checks, self.pend_keep = [], []  # fused check descriptors / their operands
 
 
 def _segments(lo: int, hi: int, size: int):
@@ -158,7 +159,7 @@ class StreamingVerifier:
     def __init__(self, graph, model: FpModel | None = None, profile=NATIVE, thresholds=None,
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
-                 grid=PERCENTILE_GRID, overlap: bool = True):
+                 grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -170,6 +171,11 @@ class StreamingVerifier:
         self.epsilon = float(epsilon)
         self.grid = tuple(grid)
         self._tau_cache = {}
+        # fuse_check: the acceptance check runs inside the Merkle commit pass
+        # (nao_commit_check_tensors: the ALU-bound Keccak hides its HBM read);
+        # False: a separate nao_check launch per node on its own side stream
+        self.fuse_check = bool(fuse_check)
+        self._specs = None  # (device blob, {node index: byte offset}) of verdict specs
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
         # (equal priorities: a low-priority side stream starves and the memory its
@@ -192,6 +198,22 @@ class StreamingVerifier:
                 t = (INF_TAU, INF_TAU)
             self._tau_cache[name] = t
         return t
+
+    def _spec_table(self, start, end):
+        """Device nao_verdict_spec of every node in [start, end) (one upload)."""
+        have = self._specs[1] if self._specs is not None else {}
+        nodes = self.g.nodes[start:end]
+        if self._specs is not None and all(n.index in have for n in nodes):
+            return self._specs
+        blob, offs = [], {}
+        size = int(_lib.load().nao_verdict_spec_bytes())
+        for k, node in enumerate(nodes):
+            tau_a, tau_r = self._taus(node.name)
+            blob.append(_lib.verdict_spec(self.grid, tau_a, tau_r, self.epsilon))
+            offs[node.index] = k * size
+        dev_blob = torch.frombuffer(bytearray(b"".join(blob)), dtype=torch.uint8).to(self.dev)
+        self._specs = (dev_blob, offs)
+        return self._specs
 
     # ----------------------------------------------------------------- run
     def run(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
@@ -218,6 +240,8 @@ class StreamingVerifier:
         st.values = dict(frontier or {})
         st.all_idx = torch.arange(n, device=self.dev)
         st.grid_arr = _lib.dbl_array(self.grid)
+        if self.fuse_check:
+            st.specs = self._spec_table(start, end)
         return st
 
     def _finish(self, st):
@@ -258,17 +282,19 @@ class StreamingVerifier:
             if self.overlap:
                 s_com.wait_stream(main)
             with torch.cuda.stream(s_com):
-                r = commit_tensors(st.pending, self.chunk, self.alg)
+                r = commit_tensors(st.pending, self.chunk, self.alg,
+                                   checks=st.pend_checks if self.fuse_check else None)
                 lo_i, hi_i = st.pend_idx[0], st.pend_idx[-1] + 1
                 if hi_i - lo_i == len(st.pend_idx):
                     st.roots[lo_i:hi_i].copy_(r)
                 else:
                     st.roots.index_copy_(0, st.all_idx[torch.as_tensor(st.pend_idx)], r)
-            for t in st.pending:
+            for t in st.pending + st.pend_keep:
                 side_use(t, s_com)
             if self.overlap and capturing:
                 keep.append(r)
             st.pending, st.pend_idx, st.pend_bytes = [], [], 0
+            st.pend_checks, st.pend_keep = [], []
 
         values, last = st.values, st.last
         for node in g.nodes[lo:hi]:
@@ -300,7 +326,15 @@ class StreamingVerifier:
                 lo_f = 1.0 if eps.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
                 eps_ptr = eps.data_ptr()
             i = node.index - start
-            if y.numel():
+            desc = None
+            if y.numel() and self.fuse_check:
+                blob, offs = st.specs
+                desc = _lib.CheckDesc(y.data_ptr(), eps_ptr, blob.data_ptr() + offs[node.index],
+                                      st.records[i].data_ptr(), scale, lo_f, kind, 0)
+                st.pend_keep.append(y)
+                if not isinstance(eps, tuple):
+                    st.pend_keep.append(eps)
+            elif y.numel():
                 if self.overlap:
                     s_chk.wait_stream(main)
                     side_use(y, s_chk)
@@ -322,6 +356,7 @@ class StreamingVerifier:
             yc = yc.contiguous()
             values[node.index] = yc
             st.pending.append(yc)
+            st.pend_checks.append(desc)
             st.pend_idx.append(i)
             st.pend_bytes += yc.numel() * 4
             if st.pend_bytes >= self.flush_bytes or len(st.pending) >= 120:

@@ -1,0 +1,144 @@
+"""GPU parity: the acceptance check fused into the Merkle commit pass
+(nao_commit_check_tensors) gives, per tensor, the same record as the
+standalone one-pass check (nao_check) and the oracle's verdicts, and the same
+roots as the plain commit -- across eps kinds, drift/fault/non-finite claims,
+thresholds that force the exact second pass, ragged sizes and >128-tensor
+batches (several launches)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import check as OC
+from oracle import commit as OM
+
+pytestmark = pytest.mark.gpu
+GRID = OC.PERCENTILE_GRID
+INF = np.full(len(GRID), np.inf)
+FIELDS = ("n", "n_violations", "n_borderline", "n_nonfinite", "max_ratio",
+          "threshold_exceeded", "first_exceeded", "n_ambiguous")
+
+
+def _drift(y, frac, ulps, rng):
+    yc = y.copy()
+    idx = rng.random(y.size) < frac
+    bits = yc.view(np.int32).reshape(-1)
+    bits[idx] += rng.integers(-ulps, ulps + 1, size=int(idx.sum())).astype(np.int32)
+    return yc
+
+
+def _case(rng, n, mode, eps_kind, tau_mode):
+    y = (rng.standard_normal(n) * 10.0 ** rng.integers(-2, 2, size=n)).astype(np.float32)
+    if mode == "equal":
+        yc = y.copy()
+    elif mode == "drift":
+        yc = _drift(y, 1 / 16, 1, rng)
+    elif mode == "heavy":
+        yc = _drift(y, 1.0, 6, rng)
+        k = rng.integers(0, n, size=max(1, n // 100))
+        yc[k] = yc[k] * np.float32(37.0) + np.float32(1e3)
+        k = rng.integers(0, n, size=max(1, n // 100))
+        yc[k] = -yc[k]
+    else:  # nonfinite
+        yc = _drift(y, 0.1, 2, rng)
+        yc[rng.integers(0, n, size=max(1, n // 500))] = np.inf
+        yc[rng.integers(0, n, size=max(1, n // 700))] = np.nan
+        y[rng.integers(0, n, size=max(1, n // 900))] = np.nan
+    c = 3.3 * 2.0 ** -24
+    eps64 = c * np.abs(y.astype(np.float64))
+    if eps_kind == "scaled":
+        eps, ref_eps = ("scaled", c), eps64
+    elif eps_kind == "f64":
+        eps, ref_eps = torch.from_numpy(eps64).cuda(), eps64
+    elif eps_kind == "f32":
+        e32 = eps64.astype(np.float32)
+        eps, ref_eps = torch.from_numpy(e32).cuda(), e32.astype(np.float64)
+    else:
+        eps, ref_eps = ("zero",), np.zeros(n)
+    if tau_mode == "inf":
+        taus = (INF, INF)
+    else:
+        with np.errstate(invalid="ignore"):
+            a, r = OC.elementwise_errors(y, yc)
+        pa, pr = OC.percentile_profile(a), OC.percentile_profile(r)
+        taus = (pa, pr) if tau_mode == "exact" else (pa * 0.5, pr * 3.0)
+    return y, yc, eps, ref_eps, taus
+
+
+def _records(recs):
+    from paper_2510_16028_b200.dispute import CheckRecord
+    return [CheckRecord(recs[i]).host() for i in range(recs.shape[0])]
+
+
+@pytest.mark.parametrize("alg,chunk", [("keccak256", 4096), ("keccak256", 256),
+                                       ("sha256", 1024)])
+def test_fused_matches_standalone_check(alg, chunk):
+    from paper_2510_16028_b200 import dispute
+    from paper_2510_16028_b200.commitments import commit_tensors
+    rng = np.random.default_rng(hash((alg, chunk)) & 0xFFFF)
+    sizes = [1, 3, 64, 1025, 4097, 70001, 262147]
+    modes = ["equal", "drift", "heavy", "nonfinite"]
+    kinds = ["scaled", "f32", "f64", "zero"]
+    taus_m = ["inf", "exact", "scaled"]
+    cases = []
+    for k in range(24):
+        n = sizes[k % len(sizes)]
+        mode = modes[k % len(modes)]
+        if mode == "nonfinite" and n < 8:
+            mode = "drift"
+        tm = taus_m[(k // 4) % 3] if mode != "nonfinite" else "inf"
+        cases.append(_case(rng, n, mode, kinds[(k // 2) % 4], tm))
+    claimed = [torch.from_numpy(c[1]).cuda() for c in cases]
+    local = [torch.from_numpy(c[0]).cuda() for c in cases]
+    roots, recs = dispute.commit_check_nodes(claimed, local, [c[2] for c in cases],
+                                             [c[4] for c in cases], chunk, alg)
+    plain = commit_tensors(claimed, chunk, alg)
+    torch.cuda.synchronize()
+    assert torch.equal(roots, plain)
+    got = _records(recs)
+    for i, (y, yc, eps, ref_eps, taus) in enumerate(cases):
+        want = dispute.check_node(local[i], claimed[i], eps, taus[0], taus[1]).host()
+        for f in FIELDS:
+            if f == "max_ratio" and np.isnan(want[f]):
+                continue
+            assert got[i][f] == want[f], (i, f, got[i][f], want[f])
+        # and the oracle's verdicts directly
+        with np.errstate(invalid="ignore"):
+            ref = OC.leaf_check(y, yc, ref_eps)
+        if np.all(np.isfinite(y)):
+            assert got[i]["n_violations"] == ref["n_violations"], i
+            pm = OC.observed_p_max(y, yc, taus[0], taus[1])
+            assert bool(got[i]["threshold_exceeded"]) == (pm > 1.0), i
+        assert bytes(roots[i].cpu().numpy()) == OM.tensor_root(
+            yc, chunk, OM.KECCAK256 if alg == "keccak256" else OM.SHA256), i
+
+
+def test_fused_many_tensors_and_empty():
+    """>128 tensors (several launches), an empty tensor in the batch (root
+    only, no record), and the accumulator left clean for the next call."""
+    from paper_2510_16028_b200 import dispute
+    from paper_2510_16028_b200.commitments import commit_tensors
+    rng = np.random.default_rng(3)
+    ys, ycs = [], []
+    for i in range(300):
+        n = int(rng.integers(0, 3000)) if i != 5 else 0
+        y = rng.standard_normal(n).astype(np.float32)
+        ys.append(y)
+        ycs.append(_drift(y, 0.3, 2, rng))
+    claimed = [torch.from_numpy(c).cuda() for c in ycs]
+    local = [torch.from_numpy(c).cuda() for c in ys]
+    eps = [("scaled", 2.0 ** -23)] * len(ys)
+    taus = [(INF, INF)] * len(ys)
+    for rep in range(2):
+        roots, recs = dispute.commit_check_nodes(claimed, local, eps, taus, 256, "keccak256")
+        plain = commit_tensors(claimed, 256, "keccak256")
+        torch.cuda.synchronize()
+        assert torch.equal(roots, plain)
+        got = _records(recs)
+        for i, (y, yc) in enumerate(zip(ys, ycs)):
+            if y.size == 0:
+                assert got[i]["n"] == 0
+                continue
+            ref = OC.leaf_check(y, yc, 2.0 ** -23 * np.abs(y.astype(np.float64)))
+            assert got[i]["n"] == y.size
+            assert got[i]["n_violations"] == ref["n_violations"], (rep, i)
