@@ -412,18 +412,36 @@ int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, doub
 // cross-device drift -- plus an optional relative fault `scale` on every
 // element with (hash % fault_period == 0).
 namespace nao {
+__device__ __forceinline__ float drift_one(float v, int64_t i, uint32_t seed, uint32_t period,
+                                           float fault_scale, uint32_t fault_period) {
+    uint32_t h = (uint32_t)i * 0x9E3779B1u ^ seed;
+    h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
+    if (period && (h % period) == 0 && v != 0.0f && isfinite(v))
+        v = __int_as_float(__float_as_int(v) + ((h >> 20) & 1 ? 1 : -1));
+    if (fault_period && ((h >> 8) % fault_period) == 0) v = v * (1.0f + fault_scale);
+    return v;
+}
+
+// float4 per thread per step (16-byte aligned y/out); scalar tail
 __global__ void k_inject_drift(const float* __restrict__ y, float* __restrict__ out, int64_t n,
                                uint32_t seed, uint32_t period, float fault_scale,
                                uint32_t fault_period) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t h = (uint32_t)i * 0x9E3779B1u ^ seed;
-        h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-        float v = __ldg(y + i);
-        if (period && (h % period) == 0 && v != 0.0f && isfinite(v))
-            v = __int_as_float(__float_as_int(v) + ((h >> 20) & 1 ? 1 : -1));
-        if (fault_period && ((h >> 8) % fault_period) == 0) v = v * (1.0f + fault_scale);
-        out[i] = v;
+    const int64_t nv = n >> 2;
+    const float4* y4 = reinterpret_cast<const float4*>(y);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+        float4 a = __ldg(y4 + v);
+        const int64_t i = 4 * v;
+        a.x = drift_one(a.x, i, seed, period, fault_scale, fault_period);
+        a.y = drift_one(a.y, i + 1, seed, period, fault_scale, fault_period);
+        a.z = drift_one(a.z, i + 2, seed, period, fault_scale, fault_period);
+        a.w = drift_one(a.w, i + 3, seed, period, fault_scale, fault_period);
+        __stcs(o4 + v, a);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+        const int64_t i = (nv << 2) + threadIdx.x;
+        out[i] = drift_one(__ldg(y + i), i, seed, period, fault_scale, fault_period);
     }
 }
 }  // namespace nao
@@ -432,7 +450,9 @@ extern "C" int nao_inject_drift(const float* y, float* out, int64_t n, uint32_t 
                                 uint32_t period, float fault_scale, uint32_t fault_period,
                                 void* stream) {
     if (n == 0) return NAO_OK;
-    nao::k_inject_drift<<<nao::ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    NAO_REQUIRE((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(out)) % 16 == 0,
+                "y/out must be 16-byte aligned");
+    nao::k_inject_drift<<<nao::ew_grid((n + 3) / 4), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         y, out, n, seed, period, fault_scale, fault_period);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
@@ -527,7 +547,7 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
             for (int64_t c = threadIdx.x; c < n; c += kThreads) sa = __dadd_rn(sa, fabs((double)row[c]));
             sa = block_sum(sa, red);
             if (threadIdx.x == 0) s_d0[r] = sa;
-        } else if (kind <= 3) {
+        } else if (kind <= 3) {  // sum / mean: order-free FP64 sum |x| by the whole CTA
             double sa = 0.0;
             for (int64_t c = threadIdx.x; c < n; c += kThreads) sa = __dadd_rn(sa, fabs((double)row[c]));
             sa = block_sum(sa, red);
@@ -542,7 +562,27 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
         float acc = row[0];
         if (kind == 4) { for (int64_t c = 1; c < n; c++) acc = fmaxf(acc, row[c]); }
         else if (kind == 5) { for (int64_t c = 1; c < n; c++) acc = fminf(acc, row[c]); }
-        else {
+        else if (kind >= 2 && (n & 3) == 0 && n >= 8) {
+            // sum / mean left fold from 16-byte smem loads, the next 8 in flight
+            const float4* r4 = reinterpret_cast<const float4*>(row);
+            const int64_t n4 = n >> 2;
+            float4 v = r4[0];
+            acc = __fadd_rn(__fadd_rn(__fadd_rn(v.x, v.y), v.z), v.w);
+            int64_t c = 1;
+            for (; c + 8 <= n4; c += 8) {
+                float4 b[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) b[k] = r4[c + k];
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, b[k].x), b[k].y), b[k].z),
+                                    b[k].w);
+            }
+            for (; c < n4; c++) {
+                v = r4[c];
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v.x), v.y), v.z), v.w);
+            }
+        } else {
 #pragma unroll 8
             for (int64_t c = 1; c < n; c++) acc = __fadd_rn(acc, row[c]);
         }
@@ -852,6 +892,10 @@ static int rows_per_cta(int64_t rows, int64_t n, int kind) {
     const int64_t per_row = bufs * n * 4;
     const int64_t budget = 96 * 1024;
     if (per_row > budget) return 0;
+    // reductions: short rows -> lane-per-row transposed tiles (k_reduce_rows);
+    // long rows -> one row per CTA (the serial fold is the critical path, so
+    // spread rows over as many SMs / CTAs as possible)
+    if (kind >= 2) return n <= 1024 ? 0 : 1;
     int64_t R = budget / per_row;
     if (R > 32) R = 32;
     // transposed-tile kernels win when there are enough rows to fill the GPU with warps

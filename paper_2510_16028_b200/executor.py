@@ -74,6 +74,8 @@ def inject_drift(y: torch.Tensor, seed: int, period: int = 16, fault_scale: floa
                  fault_period: int = 0) -> torch.Tensor:
     """Claimed tensor = y with honest +-1-ulp drift (+ optional fault); see nao_inject_drift."""
     y = y.contiguous()
+    if y.data_ptr() % 16:
+        y = y.clone()
     out = torch.empty_like(y)
     _lib.call("nao_inject_drift", y.data_ptr(), out.data_ptr(), y.numel(), seed & 0xFFFFFFFF,
               period, float(fault_scale), fault_period, _lib.stream_ptr(y.device))

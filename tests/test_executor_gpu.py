@@ -166,3 +166,29 @@ def test_graphed_replay_matches_eager(seg):
     torch.cuda.synchronize()
     for k in ref:
         assert torch.equal(gp.outputs[k], ref[k])
+
+
+@pytest.mark.parametrize("n", [1, 5, 1027, 65536 + 3])
+def test_inject_drift_matches_numpy(n):
+    """nao_inject_drift (float4 body + scalar tail) against a numpy restatement
+    of its per-element hash."""
+    from paper_2510_16028_b200.executor import inject_drift
+    rng = np.random.default_rng(n)
+    y = rng.standard_normal(n).astype(np.float32)
+    y[::97] = 0.0
+    seed, period, fs, fp = 1234, 5, 1e-3, 7
+    out = inject_drift(torch.from_numpy(y).cuda(), seed, period, fs, fp).cpu().numpy()
+    i = np.arange(n, dtype=np.uint64)
+    m32 = np.uint64(0xFFFFFFFF)
+    h = ((i * np.uint64(0x9E3779B1)) & m32) ^ np.uint64(seed)
+    h ^= h >> np.uint64(16); h = (h * np.uint64(0x85EBCA6B)) & m32
+    h ^= h >> np.uint64(13); h = (h * np.uint64(0xC2B2AE35)) & m32
+    h ^= h >> np.uint64(16)
+    ref = y.copy()
+    flip = ((h % np.uint64(period)) == 0) & (y != 0) & np.isfinite(y)
+    bits = ref.view(np.int32)
+    step = np.where(((h >> np.uint64(20)) & np.uint64(1)) == 1, 1, -1).astype(np.int32)
+    bits[flip] += step[flip]
+    fault = ((h >> np.uint64(8)) % np.uint64(fp)) == 0
+    ref[fault] = ref[fault] * (np.float32(1.0) + np.float32(fs))
+    np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))

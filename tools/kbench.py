@@ -89,6 +89,16 @@ def main():
         n = x.numel()
         report("softmax_bound_f32eps", timeit(lambda: softmax_device(x, -1, model, False), a.reps),
                12 * n)
+    if want("reduce"):
+        from paper_2510_16028_b200.bounds import reduce_device
+        for shape in ((S, H), (S * NH, 128), (S * 8, 128)):
+            x = torch.randn(shape, device=dev)
+            report("mean_bound_f32eps", timeit(lambda: reduce_device("mean", x, -1, model, False),
+                                               a.reps), 4 * x.numel() + 8 * shape[0],
+                   shape=list(shape))
+    if want("drift"):
+        x = torch.randn((NH, S, S), device=dev)
+        report("inject_drift", timeit(lambda: inject_drift(x, 1, 16), a.reps), 8 * x.numel())
     if want("layernorm"):
         x = torch.randn((S, H), device=dev)
         report("layernorm_bound_f32eps", timeit(lambda: layernorm_device(x, -1, 1e-6, model, False),
