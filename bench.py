@@ -263,6 +263,10 @@ def run_ours(args):
             return 2.0 * a[6] * a[9] * a[10] * a[11]
         if name == "nao_tf32_split":
             return 12.0 * a[3] * a[4] * a[5]
+        if name == "nao_abs_gemm_tc16":
+            return 2.0 * a[11] * a[14] * a[15] * a[16]
+        if name == "nao_f16_split":  # read 4 B, write 2 x 2 B per element
+            return 8.0 * a[4] * a[5] * a[6]
         if name in ("nao_softmax_bound", "nao_layernorm_bound"):
             return 12.0 * a[4] * a[5]
         if name == "nao_inject_drift":
@@ -372,6 +376,16 @@ def run_ours(args):
                                    "MMAs per product (3xTF32 split): algorithmic ceiling",
                     "mma_tflops": round(3 * achieved, 1), "tf32_peak": round(tf32, 1),
                     "traffic": None}
+        elif dom == "nao_abs_gemm_tc16":
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
+            f16 = peaks.get("bf16_tflops", 1590.0)
+            peak = f16 / 3.0
+            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
+                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) = FP16 dense, / 3 "
+                                   "MMAs per product (FP16 3-split): algorithmic ceiling",
+                    "mma_tflops": round(3 * achieved, 1), "f16_peak": round(f16, 1),
+                    "traffic": None}
         elif dom == "nao_abs_gemm_bound":
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
             peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 SIMT peak (derived, not measured)
@@ -411,7 +425,7 @@ def run_ours(args):
         for k, v in timers.items():
             t = sum(v["ms"]) * 1e-3
             if t > 0 and sum(v["units"]) > 0:
-                flops = k in ("nao_abs_gemm_tc", "nao_abs_gemm_bound")
+                flops = k in ("nao_abs_gemm_tc", "nao_abs_gemm_tc16", "nao_abs_gemm_bound")
                 rates[k] = (f"{sum(v['units']) / t / 1e12:.1f} TFLOP/s" if flops
                             else f"{sum(v['units']) / t / 1e9:.0f} GB/s")
         roof["kernel_rates"] = rates

@@ -47,7 +47,7 @@ enum nao_unary_kind {
     NAO_UN_EXP = 0, NAO_UN_LOG = 1, NAO_UN_SQRT = 2, NAO_UN_RSQRT = 3,
     NAO_UN_TANH = 4, NAO_UN_GELU = 5, NAO_UN_SILU = 6
 };
-enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1 };
+enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1, NAO_GEMM_TC_F16X3 = 2 };
 
 /* ------------------------------------------------------------ library */
 int nao_version(void);
@@ -195,6 +195,29 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
                     int64_t M, int64_t N, int64_t K, int64_t ldc, int64_t stride_c,
                     double gamma_const, const float* y_or_null, double u, double slack,
                     void* stream);
+/* FP16 3-split of matmul_bound on tcgen05.mma.kind::f16 (2x the TF32 rate,
+ * half the operand bytes).  nao_f16_split: |x| -> K-major FP16 parts
+ * [batch, rows, Kp] (Kp = nao_f16_split_cols(K)) and row_info int32[2*batch*rows]:
+ * row exponents e then counts of "tiny" elements, with |x| <= 2^e (hi + 2^-10 lo),
+ * relative excess <= 2^-20 for |x| >= 2^(e-14) and absolute excess < 2^(e-24)
+ * below (tiny; exact power-of-two scaling puts the row max in [2^14, 2^15)).
+ * nao_abs_gemm_tc16 = nao_abs_gemm_tc on those parts; outputs whose tiny-part
+ * excess could exceed 2^-20 of their value are recomputed exactly in FP64 from
+ * the original operands A [batch_a, M, K] / B ([batch_b, K, N], or [batch_b, N, K]
+ * with transpose_b), so the result stays within rtol 1e-5 of the FP64 bound.
+ * fix_ws: zeroed device scratch of nao_abs_gemm_tc16_fix_workspace() bytes per
+ * stream, left zeroed by every call. */
+int64_t nao_f16_split_cols(int64_t K);
+int nao_f16_split(const float* x, void* hi, void* lo, int32_t* row_info, int64_t batch,
+                  int64_t rows, int64_t K, int64_t ld, int64_t stride_batch, int transpose,
+                  void* stream);
+size_t nao_abs_gemm_tc16_fix_workspace(void);
+int nao_abs_gemm_tc16(const void* a_hi, const void* a_lo, const int32_t* a_info, const void* b_hi,
+                      const void* b_lo, const int32_t* b_info, const float* A, const float* B,
+                      int transpose_b, void* eps, int eps_f64, int64_t batch, int64_t batch_a,
+                      int64_t batch_b, int64_t M, int64_t N, int64_t K, int64_t ldc,
+                      int64_t stride_c, double gamma_const, const float* y_or_null, double u,
+                      double slack, void* fix_ws, size_t fix_ws_bytes, void* stream);
 /* matmul_op values under the sequential profile (engine.py:157-182),
  * C contiguous [batch, M, N]; fma selects the "+fma" FP64-step emulation. */
 int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, int64_t M,

@@ -33,7 +33,7 @@ HASH_SHA256, HASH_KECCAK256 = 0, 1
 EPS_TENSOR_F32, EPS_TENSOR_F64, EPS_SCALED_LOCAL, EPS_ZERO = 0, 1, 2, 3
 RED_SUM, RED_MEAN, RED_MAX, RED_MIN = 0, 1, 2, 3
 UNARY = {"exp": 0, "log": 1, "sqrt": 2, "rsqrt": 3, "tanh": 4, "gelu": 5, "silu": 6}
-GEMM_FFMA_RU, GEMM_TC_TF32X3 = 0, 1
+GEMM_FFMA_RU, GEMM_TC_TF32X3, GEMM_TC_F16X3 = 0, 1, 2
 
 
 class CheckResult(ctypes.Structure):
@@ -100,6 +100,13 @@ _SIGS = {
     "nao_tf32_split": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]),
     "nao_abs_gemm_tc": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64,
                                 c_i64, c_i64, c_i64, c_i64, c_dbl, c_vp, c_dbl, c_dbl, c_vp]),
+    "nao_f16_split_cols": (c_i64, [c_i64]),
+    "nao_f16_split": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int,
+                              c_vp]),
+    "nao_abs_gemm_tc16_fix_workspace": (c_sz, []),
+    "nao_abs_gemm_tc16": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                                  c_int, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+                                  c_dbl, c_vp, c_dbl, c_dbl, c_vp, c_sz, c_vp]),
     "nao_inject_drift": (c_int, [c_vp, c_vp, c_i64, ctypes.c_uint32, ctypes.c_uint32,
                                  ctypes.c_float, ctypes.c_uint32, c_vp]),
 }
@@ -234,6 +241,18 @@ def verdict_spec(grid, tau_abs, tau_rel, epsilon) -> bytes:
     check(L.nao_verdict_spec_fill(buf, dbl_array(grid), dbl_array(tau_abs), dbl_array(tau_rel),
                                   len(grid), float(epsilon)), "nao_verdict_spec_fill")
     return buf.raw
+
+
+def gemm_fix_workspace(device) -> torch.Tensor:
+    """Zeroed fix-up list of nao_abs_gemm_tc16 per (device, stream)."""
+    dev = torch.device(device)
+    key = ("tc16fix", dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws.get(key)
+    if buf is None:
+        buf = torch.zeros(int(load().nao_abs_gemm_tc16_fix_workspace()), dtype=torch.uint8,
+                          device=dev)
+        _ws[key] = buf
+    return buf
 
 
 def check_accumulator(device) -> torch.Tensor:

@@ -140,10 +140,20 @@ def _eps_buffer(shape, device, f64: bool) -> torch.Tensor:
 
 # ---------------------------------------------------------------- kernels
 
-def default_gemm_path() -> int:
-    """tcgen05 3xTF32 unless NAO_GEMM_PATH=ffma (both are sound)."""
-    env = os.environ.get("NAO_GEMM_PATH", "tc").lower()
-    return _lib.GEMM_FFMA_RU if env in ("ffma", "simt", "0") else _lib.GEMM_TC_TF32X3
+F16_MIN_K = 256  # short K is epilogue bound: the TF32 split wins there (kbench)
+
+
+def default_gemm_path(K: int | None = None) -> int:
+    """NAO_GEMM_PATH = auto (default: tcgen05 FP16 3-split for K > 256, 3xTF32
+    below), tc / tf32, f16, or ffma.  All are sound."""
+    env = os.environ.get("NAO_GEMM_PATH", "auto").lower()
+    if env in ("ffma", "simt", "0"):
+        return _lib.GEMM_FFMA_RU
+    if env in ("f16", "tc16", "2"):
+        return _lib.GEMM_TC_F16X3
+    if env in ("tc", "tf32", "1"):
+        return _lib.GEMM_TC_TF32X3
+    return _lib.GEMM_TC_F16X3 if (K is not None and K > F16_MIN_K) else _lib.GEMM_TC_TF32X3
 
 
 # hi/lo TF32 splits of operands that outlive a call (weights), keyed by the
@@ -171,18 +181,58 @@ def tf32_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool
     return hi, lo
 
 
+def f16_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool):
+    """|x| -> (hi, lo, row_exp): K-major [batch, rows, Kp] FP16 parts with
+    |x| <= 2^e (hi + 2^-10 lo) per row (nao_f16_split)."""
+    key = ("f16", id(x3))
+    if cache:
+        hit = _SPLITS.get(key)
+        if hit is not None and hit[0]() is x3 and hit[1] == x3._version:
+            return hit[2], hit[3], hit[4]
+    batch = x3.numel() // (rows * K) if rows * K else 1
+    if transpose and not cache:
+        # per-call operand stored [K, rows] (e.g. V of p @ v): one transposing
+        # copy, then the row kernel (the column kernel is meant for one-time
+        # weight splits)
+        x3 = x3.reshape(batch, K, rows).transpose(1, 2).contiguous()
+        transpose = False
+    Kp = (K + 7) // 8 * 8
+    hi = torch.empty((batch, rows, Kp), dtype=torch.float16, device=x3.device)
+    lo = torch.empty_like(hi)
+    ex = torch.empty((2, batch, rows), dtype=torch.int32, device=x3.device)  # exps, tiny counts
+    ld = rows if transpose else K
+    _lib.call("nao_f16_split", x3.data_ptr(), hi.data_ptr(), lo.data_ptr(), ex.data_ptr(), batch,
+              rows, K, ld, rows * K, int(transpose), _lib.stream_ptr(x3.device))
+    if cache:
+        _SPLITS[key] = (weakref.ref(x3, lambda _r, k=key: _SPLITS.pop(k, None)), x3._version,
+                        hi, lo, ex)
+    return hi, lo, ex
+
+
 def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
                    y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
                    path: int | None = None, cache_b: bool = False) -> torch.Tensor:
     """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors)."""
-    path = default_gemm_path() if path is None else path
     a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
+    path = default_gemm_path(K) if path is None else path
     eps = _eps_buffer(out_shape, a.device, eps_f64)
     yc = None
     if y is not None:
         yc = y.contiguous()
         if tuple(yc.shape) != tuple(out_shape):
             raise ValueError("linear bound: output shape mismatch")
+    if path == _lib.GEMM_TC_F16X3:
+        cb = cache_b and b3.data_ptr() == b.data_ptr()
+        ahi, alo, aex = f16_split(a3, M, K, False, False)
+        bhi, blo, bex = f16_split(b if cb else b3, N, K, not transpose_b, cb)
+        fix = _lib.gemm_fix_workspace(a.device)
+        bsrc = b if cb else b3
+        _lib.call("nao_abs_gemm_tc16", ahi.data_ptr(), alo.data_ptr(), aex.data_ptr(),
+                  bhi.data_ptr(), blo.data_ptr(), bex.data_ptr(), a3.data_ptr(), bsrc.data_ptr(),
+                  int(transpose_b), eps.data_ptr(), int(eps_f64), nb, nb if sa else 1,
+                  nb if sb else 1, M, N, K, N, M * N, float(const), _lib.ptr(yc), float(u),
+                  gemm_slack(K), fix.data_ptr(), fix.numel(), _lib.stream_ptr(a.device))
+        return eps
     if path == _lib.GEMM_TC_TF32X3:
         ahi, alo = tf32_split(a3, M, K, False, False)
         bhi, blo = tf32_split(b if (cache_b and b3.data_ptr() == b.data_ptr()) else b3,

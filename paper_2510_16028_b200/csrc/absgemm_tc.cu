@@ -28,6 +28,7 @@
 //   warp 2      TMEM allocator (512 columns: acc0 x2, acc1)
 //   warps 4-11  epilogue: tcgen05.ld -> FP64 accumulate -> eps store
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 #include <cmath>
 #include <cstdlib>
@@ -67,7 +68,27 @@ struct TcArgs {
     double scale0, scale1, abs_floor, u;
     // FP32 images rounded up (short-K epilogue, all-FP32 with round-up arithmetic)
     float scale0f, scale1f, abs_floorf, uf;
+    // FP16 format only: power-of-two operand scales, x = 2^e * (hi + 2^-10 lo)
+    const int32_t* a_exp;   // [batch_a, M]
+    const int32_t* b_exp;   // [batch_b, N]
+    const int32_t* a_tiny;  // [batch_a, M] parts below the normal half range
+    const int32_t* b_tiny;
+    double fix_thr;         // flag when e_scaled <= fix_thr * (tiny_a + tiny_b)
+    float fix_thrf;
+    unsigned long long* fix_count;  // flagged outputs (exact FP64 recompute)
+    unsigned long long* fix_list;
+    unsigned long long fix_cap;
 };
+
+// Record an output element for the exact FP64 fix-up pass.
+__device__ __forceinline__ void flag_fix(const TcArgs& g, int bz, int64_t m, int64_t n) {
+    const unsigned long long i = atomicAdd(g.fix_count, 1ull);
+    if (i < g.fix_cap)
+        g.fix_list[i] = ((unsigned long long)bz * (unsigned long long)g.M + (unsigned long long)m) *
+                            (unsigned long long)g.N + (unsigned long long)n;
+}
+
+enum : int { kFmtTF32 = 0, kFmtF16 = 1 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -124,6 +145,15 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // K-major swizzled smem operand descriptor: rows of BK*4 bytes, 8-row groups
 // 8*BK*4 bytes apart (SWIZZLE_128B for 128 B rows, SWIZZLE_64B for 64 B rows)
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
@@ -138,6 +168,35 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
 // kind::tf32, D=F32, A=B=TF32, both K-major, N=BN, M=BM
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(BM >> 4) << 24);
+
+// kind::f16, D=F32, A=B=F16, both K-major, N=BN, M=BM (64-byte rows = 32 halves:
+// the same smem tile geometry and 32-byte K-steps as the TF32 tiles)
+constexpr uint32_t kIdescF16 = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                               ((uint32_t)(BM >> 4) << 24);
+
+// elements per 64-byte k-block of a format
+template <int FMT>
+struct FmtK { static constexpr int kb = FMT == 1 ? 32 : BK; };
+
+template <int FMT>
+__device__ __forceinline__ void umma_fmt(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+    if constexpr (FMT == kFmtF16) umma_f16(d, a, b, kIdescF16, acc);
+    else umma_tf32(d, a, b, kIdesc, acc);
+}
+
+// 2^(ea + eb) as an exact FP64 power of two (|ea + eb| < 1000): a b = a_s b_s 2^(ea+eb)
+__device__ __forceinline__ double pow2_sum(int ea, int eb) {
+    return __hiloint2double((1023 + ea + eb) << 20, 0);
+}
+__device__ __forceinline__ float pow2f(int t) { return __int_as_float((127 + t) << 23); }  // |t|<=126
+// e * 2^-t in FP32, rounded toward +inf (two steps keep 2^-t1 / 2^-t2 normal)
+__device__ __forceinline__ float mul_pow2_ru(float e, int t) {
+    const int t1 = t > 126 ? 126 : (t < -127 ? -127 : t);
+    int t2 = t - t1;
+    t2 = t2 > 126 ? 126 : (t2 < -127 ? -127 : t2);
+    e = __fmul_ru(e, __int_as_float((127 - t1) << 23));
+    return t2 ? __fmul_ru(e, __int_as_float((127 - t2) << 23)) : e;
+}
 
 #define TMEM_LD_X32(taddr, v)                                                                     \
     asm volatile(                                                                                 \
@@ -186,9 +245,35 @@ struct EpiAcc {
 // then written back row by row with lanes on consecutive columns, so the eps
 // stores and the y reads of the linear u|y| term are coalesced 128 B segments
 // (lane = row direct stores were ~8x sector-amplified: 32 rows per instruction).
+__device__ __noinline__ void long_flag(const TcArgs& g, double e, int i, int tbh, int ta, int bz,
+                                       int64_t mrow, int64_t n) {
+    const int nt = ta + __shfl_sync(0xffffffffu, tbh, i);
+    if (nt > 0 && n < g.N && mrow < g.M && e <= g.fix_thr * (double)nt) flag_fix(g, bz, mrow, n);
+}
+
+template <int FMT>
 __device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc, uint32_t col1,
                                               double* stg, int lane, int quarter, int half,
                                               int64_t m0, int64_t n0, int bz) {
+    const int64_t mrow = m0 + quarter * 32 + lane;
+    int ea = 0, ta = 0, eb[2] = {0, 0}, tb[2] = {0, 0};
+    bool tiny_tile = false;
+    double flag_lim = -1.0;
+    if constexpr (FMT == kFmtF16) {
+        const int64_t ao = (g.a_batched ? (int64_t)bz * g.M : 0) + mrow;
+        if (mrow < g.M) { ea = __ldg(g.a_exp + ao); ta = __ldg(g.a_tiny + ao); }
+        const int64_t bo = g.b_batched ? (int64_t)bz * g.N : 0;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int64_t n = n0 + half * 64 + 32 * h + lane;
+            if (n < g.N) { eb[h] = __ldg(g.b_exp + bo + n); tb[h] = __ldg(g.b_tiny + bo + n); }
+        }
+        tiny_tile = __any_sync(0xffffffffu, (ta | tb[0] | tb[1]) != 0);
+        int tmax = tb[0] > tb[1] ? tb[0] : tb[1];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        flag_lim = g.fix_thr * (double)(ta + tmax);
+    }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         uint32_t v[32];
@@ -196,8 +281,13 @@ __device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; i++) {
-            const double e = __dadd_rn(__dmul_rn(g.scale0, acc.get(32 * h + i)),
-                                       __dmul_rn(g.scale1, (double)__uint_as_float(v[i])));
+            double e = __dadd_rn(__dmul_rn(g.scale0, acc.get(32 * h + i)),
+                                 __dmul_rn(g.scale1, (double)__uint_as_float(v[i])));
+            if constexpr (FMT == kFmtF16) {
+                if (tiny_tile && __any_sync(0xffffffffu, e <= flag_lim))
+                    long_flag(g, e, i, tb[h], ta, bz, mrow, n0 + half * 64 + 32 * h + i);
+                e = __dmul_rn(e, pow2_sum(ea, __shfl_sync(0xffffffffu, eb[h], i)));
+            }
             stg[lane * 65 + 32 * h + i] = __dadd_rn(e, g.abs_floor);
         }
     }
@@ -219,6 +309,7 @@ __device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc
     }
 }
 
+template <int FMT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_absgemm_tc(const __grid_constant__ CUtensorMap map_ahi,
                  const __grid_constant__ CUtensorMap map_alo,
@@ -271,6 +362,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_after();
     const uint32_t tmem = *tmem_slot;
     const int nkb = g.nkb;
+    constexpr int KBE = FmtK<FMT>::kb;  // k elements per stage
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -281,10 +373,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
                 mbar_expect_tx(&full[s], STAGE_BYTES);
-                tma_load_3d(st, &map_ahi, &full[s], kb * BK, m0, za);
-                tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * BK, m0, za);
-                tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * BK, n0, zb);
-                tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * BK, n0, zb);
+                tma_load_3d(st, &map_ahi, &full[s], kb * KBE, m0, za);
+                tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * KBE, m0, za);
+                tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * KBE, n0, zb);
+                tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * KBE, n0, zb);
             }
         }
     } else if (warp == 1) {
@@ -306,9 +398,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint64_t alo = make_desc(st + TILE_BYTES + j * 32);
                     const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
                     const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
-                    umma_tf32(acc0, ahi, bhi, kIdesc, (first && j == 0) ? 0u : 1u);
-                    umma_tf32(acc1, ahi, blo, kIdesc, (kb == 0 && j == 0) ? 0u : 1u);
-                    umma_tf32(acc1, alo, bhi, kIdesc, 1u);
+                    umma_fmt<FMT>(acc0, ahi, bhi, (first && j == 0) ? 0u : 1u);
+                    umma_fmt<FMT>(acc1, ahi, blo, (kb == 0 && j == 0) ? 0u : 1u);
+                    umma_fmt<FMT>(acc1, alo, bhi, 1u);
                 }
                 umma_commit(&empty[s]);
                 if ((kb % KCHUNK_KB) == KCHUNK_KB - 1 || kb == nkb - 1) umma_commit(&tfull[buf]);
@@ -344,7 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_after();
         const uint32_t col1 = tmem + lane_addr + 2 * BN + half * 64;
         double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
-        tile_epilogue(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+        tile_epilogue<FMT>(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
     }
     fence_before();
     __syncthreads();
@@ -373,6 +465,18 @@ constexpr int STG_BYTES = 8 * 32 * 65 * 4;
 constexpr int SMEM_BYTES = RING_BYTES + STG_BYTES + 1024 + 256;
 }  // namespace shortk
 
+// FP16 short-K epilogue, rare element path (tiles with tiny parts or extreme
+// exponents): tiny-part flag for the exact fix-up, and the two-step scaling.
+__device__ __noinline__ float short_rare(const TcArgs& g, float e, int k, int tbh, int ebh, int ta,
+                                         int ea, int bz, int64_t mrow, int64_t n, bool tiny) {
+    const int nt = ta + __shfl_sync(0xffffffffu, tbh, k);
+    const int ebk = __shfl_sync(0xffffffffu, ebh, k);
+    if (tiny && nt > 0 && n < g.N && mrow < g.M && e <= g.fix_thrf * (float)nt)
+        flag_fix(g, bz, mrow, n);
+    return mul_pow2_ru(e, -(ea + ebk));
+}
+
+template <int FMT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_absgemm_tc_short(const __grid_constant__ CUtensorMap map_ahi,
                        const __grid_constant__ CUtensorMap map_alo,
@@ -417,6 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     fence_after();
     const uint32_t tmem = *tmem_slot;
     const int nkb = g.nkb;
+    constexpr int KBE = FmtK<FMT>::kb;  // k elements per stage
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -432,10 +537,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * STAGE_BYTES;
                     mbar_expect_tx(&full[s], STAGE_BYTES);
-                    tma_load_3d(st, &map_ahi, &full[s], kb * BK, m0, za);
-                    tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * BK, m0, za);
-                    tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * BK, n0, zb);
-                    tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * BK, n0, zb);
+                    tma_load_3d(st, &map_ahi, &full[s], kb * KBE, m0, za);
+                    tma_load_3d(st + TILE_BYTES, &map_alo, &full[s], kb * KBE, m0, za);
+                    tma_load_3d(st + 2 * TILE_BYTES, &map_bhi, &full[s], kb * KBE, n0, zb);
+                    tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * KBE, n0, zb);
                 }
             }
         }
@@ -460,9 +565,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
                         const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
                         const uint32_t first = (kb == 0 && j == 0) ? 0u : 1u;
-                        umma_tf32(acc0, ahi, bhi, kIdesc, first);
-                        umma_tf32(acc1, ahi, blo, kIdesc, first);
-                        umma_tf32(acc1, alo, bhi, kIdesc, 1u);
+                        umma_fmt<FMT>(acc0, ahi, bhi, first);
+                        umma_fmt<FMT>(acc1, ahi, blo, first);
+                        umma_fmt<FMT>(acc1, alo, bhi, 1u);
                     }
                     umma_commit(&empty[s]);
                 }
@@ -479,6 +584,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int bz = (int)(t / tiles_per_b);
             const int64_t r = t % tiles_per_b;
             const int64_t m0 = (r / tiles_n) * BM, n0 = (r % tiles_n) * BN;
+            // FP16: per-thread row scale, per-lane column scales broadcast by shuffles;
+            // 2^(ea+eb) = rowf * colf when both exponents are in FP32 range
+            const int64_t mrow = m0 + quarter * 32 + lane;
+            int ea = 0, ta = 0, eb[2] = {0, 0}, tb[2] = {0, 0};
+            bool tiny_tile = false, in_range = true;
+            float rowf = 1.f, colf[2] = {1.f, 1.f}, flag_lim = -1.f;
+            if constexpr (FMT == kFmtF16) {
+                const int64_t ao = (g.a_batched ? (int64_t)bz * g.M : 0) + mrow;
+                if (mrow < g.M) { ea = __ldg(g.a_exp + ao); ta = __ldg(g.a_tiny + ao); }
+                const int64_t bo = g.b_batched ? (int64_t)bz * g.N : 0;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int64_t n = n0 + half * 64 + 32 * h + lane;
+                    if (n < g.N) { eb[h] = __ldg(g.b_exp + bo + n); tb[h] = __ldg(g.b_tiny + bo + n); }
+                    colf[h] = pow2f(eb[h] < -126 ? -126 : (eb[h] > 126 ? 126 : eb[h]));
+                }
+                rowf = pow2f(ea < -126 ? -126 : (ea > 126 ? 126 : ea));
+                tiny_tile = __any_sync(0xffffffffu, (ta | tb[0] | tb[1]) != 0);
+                // no element of this row can need the exact fix-up unless its value is
+                // <= fix_thr * (ta + max tb over the tile's columns)
+                int tmax = tb[0] > tb[1] ? tb[0] : tb[1];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+                flag_lim = g.fix_thrf * (float)(ta + tmax);
+                in_range = __all_sync(0xffffffffu, ea >= -126 && ea <= 126 && eb[0] >= -126 &&
+                                                       eb[0] <= 126 && eb[1] >= -126 && eb[1] <= 126);
+            }
             mbar_wait(&tfull[slot], (i >> 1) & 1);
             fence_after();
             const uint32_t c0 = tmem + lane_addr + slot * 256 + half * 64;
@@ -498,8 +630,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
 #pragma unroll
                 for (int k = 0; k < 32; k++) {
-                    const float e = __fmaf_ru(g.scale1f, __uint_as_float(v1[k]),
-                                              __fmul_ru(g.scale0f, __uint_as_float(v0[k])));
+                    float e = __fmaf_ru(g.scale1f, __uint_as_float(v1[k]),
+                                        __fmul_ru(g.scale0f, __uint_as_float(v0[k])));
+                    if constexpr (FMT == kFmtF16) {
+                        const bool rare = __any_sync(0xffffffffu, e <= flag_lim) || !in_range;
+                        if (rare)  // warp-uniform, rare: out of line
+                            e = short_rare(g, e, k, tb[h], eb[h], ta, ea, bz, mrow,
+                                           n0 + half * 64 + 32 * h + k, tiny_tile);
+                        else
+                            e = __fmul_ru(__fmul_ru(e, rowf), __shfl_sync(0xffffffffu, colf[h], k));
+                    }
                     stg[lane * 65 + 32 * h + k] = __fadd_ru(e, g.abs_floorf);
                 }
             }
@@ -743,7 +883,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1
         fence_after();
         const uint32_t col1 = tmem + lane_addr + 2 * pair::BN + half * 64;
         double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
-        tile_epilogue(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+        tile_epilogue<kFmtTF32>(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
     }
     fence_before();
     cluster_sync_all();
@@ -852,19 +992,373 @@ static EncodeFn get_encode() {
     return fn;
 }
 
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t Kp, int64_t batch,
-                    int box_rows = BM) {
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t Kp, int64_t batch,
+                    int box_rows = BM, int fmt = kFmtTF32) {
     EncodeFn enc = get_encode();
     NAO_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+    const int es = fmt == kFmtF16 ? 2 : 4;
+    const int bk = 64 / es;  // 64-byte K rows (SWIZZLE_64B)
     cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)rows, (cuuint64_t)batch};
-    cuuint64_t strides[2] = {(cuuint64_t)Kp * 4, (cuuint64_t)(rows * Kp * 4)};
-    cuuint32_t box[3] = {BK, (cuuint32_t)box_rows, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     BK == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+    cuuint64_t strides[2] = {(cuuint64_t)Kp * es, (cuuint64_t)(rows * Kp * es)};
+    cuuint32_t box[3] = {(cuuint32_t)(fmt == kFmtF16 ? bk : BK), (cuuint32_t)box_rows, 1};
+    cuuint32_t est[3] = {1, 1, 1};
+    CUresult r = enc(map, fmt == kFmtF16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(base), dims, strides, box, est,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     (fmt != kFmtF16 && BK == 32) ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                  : CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     NAO_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return NAO_OK;
+}
+
+// ------------------------------------------------------------ FP16 split
+// |x| -> x_s = |x| * 2^-e (e per row: the row max lands in [2^14, 2^15)), then
+//   x_s >= 2^-14 : hi = RZ_f16(x_s),  lo = RU_f16((x_s - hi) * 2^10)
+//   x_s <  2^-14 : hi = RU_f16(x_s) (subnormal half),  lo = 0
+// so x_s <= hi + 2^-10 lo, with relative excess <= 2^-20 (1.001) for normal
+// hi and absolute excess < 2^-24 for the tiny ones; lo <= 2^-10 hi (1.001).
+// FP32 arithmetic: the power-of-two scaling is exact (rounded UP when it
+// would leave the FP32 range), remainders are exact, the FP16 roundings are
+// bit operations, so every part is an exact half.
+__device__ __forceinline__ float scale_ru(float a, int t) {  // a * 2^t, rounded up
+    const int t1 = t > 126 ? 126 : (t < -126 ? -126 : t);
+    int t2 = t - t1;
+    t2 = t2 > 126 ? 126 : (t2 < -126 ? -126 : t2);
+    a = __fmul_ru(a, pow2f(t1));
+    return t2 ? __fmul_ru(a, pow2f(t2)) : a;
+}
+__device__ __forceinline__ float ru_f16f(float v) {  // v >= 0, finite, < 65504
+    if (v >= 0x1p-14f) {
+        const uint32_t b = __float_as_uint(v);
+        return __uint_as_float((b & 0x1FFFu) ? (b & ~0x1FFFu) + 0x2000u : b);
+    }
+    return ceilf(v * 0x1p24f) * 0x1p-24f;  // subnormal half grid (exact scalings)
+}
+// returns 1 when the element is "tiny" (non-zero, below the normal half range)
+__device__ __forceinline__ int split16_one(float x, int e, __half& h, __half& l) {
+    const float a = scale_ru(fabsf(x), -e);
+    float hf, lf = 0.f;
+    if (!(a < INFINITY)) { hf = a; }  // inf / nan propagate
+    else if (a >= 0x1p-14f) {
+        hf = __uint_as_float(__float_as_uint(a) & ~0x1FFFu);  // RZ to 11 significant bits
+        lf = ru_f16f(__fmul_rn(__fsub_rn(a, hf), 0x1p10f));    // exact remainder * 2^10
+    } else {
+        hf = ru_f16f(a);
+    }
+    h = __float2half_rn(hf);  // exact (representable)
+    l = __float2half_rn(lf);
+    return (a > 0.f && a < 0x1p-14f) ? 1 : 0;
+}
+__device__ __forceinline__ int row_scale_exp(float amax) {
+    if (!(amax > 0.f) || !(amax < INFINITY)) return 0;
+    int e;
+    frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
+    return e - 15;
+}
+__device__ __forceinline__ float nan_max(float m, float v) {  // max that keeps NaN
+    return (v == v) ? fmaxf(m, v) : v;
+}
+
+// x row-major [rows, K] (ld), a warp per row: max pass, then the split pass
+// (the row is re-read from L1/L2).  VEC: K % 8 == 0, ld % 4 == 0, 16-byte base.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_split_f16_rows(const float* __restrict__ x,
+                                                       __half* __restrict__ hi,
+                                                       __half* __restrict__ lo,
+                                                       int32_t* __restrict__ sexp, int64_t batch,
+                                                       int64_t rows, int64_t K, int64_t Kp,
+                                                       int64_t ld, int64_t sbatch) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         t < batch * rows; t += nw) {
+        const int64_t b = t / rows, r = t % rows;
+        const float* xr = x + b * sbatch + r * ld;
+        float m = 0.f;
+        if (VEC) {
+            const float4* x4 = reinterpret_cast<const float4*>(xr);
+            for (int64_t k = lane; k < (K >> 2); k += 32) {
+                const float4 v = __ldg(x4 + k);
+                m = nan_max(nan_max(nan_max(nan_max(m, fabsf(v.x)), fabsf(v.y)), fabsf(v.z)),
+                            fabsf(v.w));
+            }
+        } else {
+            for (int64_t k = lane; k < K; k += 32) m = nan_max(m, fabsf(__ldg(xr + k)));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const int e = row_scale_exp(m);
+        int tiny = 0;
+        __half* hr = hi + t * Kp;
+        __half* lr = lo + t * Kp;
+        if (VEC) {
+            const float4* x4 = reinterpret_cast<const float4*>(xr);
+            for (int64_t k = lane; k < (K >> 2); k += 32) {
+                const float4 v = __ldg(x4 + k);
+                __half h[4], l[4];
+                tiny += split16_one(v.x, e, h[0], l[0]) + split16_one(v.y, e, h[1], l[1]) +
+                        split16_one(v.z, e, h[2], l[2]) + split16_one(v.w, e, h[3], l[3]);
+                reinterpret_cast<uint2*>(hr)[k] = *reinterpret_cast<const uint2*>(h);
+                reinterpret_cast<uint2*>(lr)[k] = *reinterpret_cast<const uint2*>(l);
+            }
+        } else {
+            for (int64_t k = lane; k < Kp; k += 32) {
+                __half h = __float2half(0.f), l = __float2half(0.f);
+                if (k < K) tiny += split16_one(__ldg(xr + k), e, h, l);
+                hr[k] = h;
+                lr[k] = l;
+            }
+        }
+        tiny = warp_sum(tiny);
+        if (lane == 0) {
+            sexp[t] = e;
+            sexp[batch * rows + t] = tiny;  // second block: tiny-part counts
+        }
+    }
+}
+
+// x is [K, rows] row-major per batch (ld): output row r = input column r.
+// A CTA owns 32 output rows: column maxima over K, then 32x32 transposed tiles.
+__global__ void __launch_bounds__(256) k_split_f16_cols(const float* __restrict__ x,
+                                                       __half* __restrict__ hi,
+                                                       __half* __restrict__ lo,
+                                                       int32_t* __restrict__ sexp, int64_t batch,
+                                                       int64_t rows, int64_t K, int64_t Kp,
+                                                       int64_t ld, int64_t sbatch) {
+    __shared__ float tile[32][33];
+    __shared__ float cmax[8][32];
+    __shared__ int cexp[32];
+    __shared__ int ctiny[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t ctiles = (rows + 31) / 32;
+    for (int64_t bt = blockIdx.x; bt < batch * ctiles; bt += gridDim.x) {
+        const int64_t b = bt / ctiles, c0 = (bt % ctiles) * 32;
+        const float* xb = x + b * sbatch;
+        const int64_t c = c0 + lane;
+        float m = 0.f;
+        if (c < rows)
+            for (int64_t k = w; k < K; k += 8) m = nan_max(m, fabsf(__ldg(xb + k * ld + c)));
+        cmax[w][lane] = m;
+        __syncthreads();
+        if (w == 0) {
+            float mm = cmax[0][lane];
+            for (int i = 1; i < 8; i++) mm = nan_max(mm, cmax[i][lane]);
+            const int e = row_scale_exp(mm);
+            if (c < rows) sexp[b * rows + c] = e;
+            cexp[lane] = e;
+            ctiny[lane] = 0;
+        }
+        __syncthreads();
+        for (int64_t k0 = 0; k0 < Kp; k0 += 32) {
+            for (int i = w; i < 32; i += 8) {
+                const int64_t k = k0 + i;
+                tile[i][lane] = (k < K && c < rows) ? __ldg(xb + k * ld + c) : 0.f;
+            }
+            __syncthreads();
+            for (int j = w; j < 32; j += 8) {  // output row c0 + j, k = k0 + lane
+                const int64_t r = c0 + j, k = k0 + lane;
+                if (r < rows && k < Kp) {
+                    __half h = __float2half(0.f), l = __float2half(0.f);
+                    if (k < K && split16_one(tile[lane][j], cexp[j], h, l)) atomicAdd(&ctiny[j], 1);
+                    hi[(b * rows + r) * Kp + k] = h;
+                    lo[(b * rows + r) * Kp + k] = l;
+                }
+            }
+            __syncthreads();
+        }
+        if (w == 0 && c < rows) sexp[batch * rows + b * rows + c] = ctiny[lane];
+        __syncthreads();
+    }
+}
+
+// Exact FP64 recompute of flagged outputs (FP16 path): eps = s * sum |a||b|
+// (+ u|y|), a warp per element.  count > capacity: every element of a row /
+// column with tiny parts is recomputed instead.  Leaves the count at zero.
+struct FixArgs {
+    const float* A;       // [batch_a, M, K]
+    const float* B;       // [batch_b, K, N] or [batch_b, N, K] (trans_b)
+    int64_t sA, sB;       // batch strides (0 = broadcast)
+    int trans_b;
+    int64_t M, N, K, batch;
+    void* C;
+    const float* Y;
+    int64_t ldc, sC;
+    int out_f64;
+    double s, u;
+    const int32_t* a_tiny;
+    const int32_t* b_tiny;
+    int a_batched, b_batched;
+    unsigned long long* count;
+    const unsigned long long* list;
+    unsigned long long cap;
+};
+
+__device__ __forceinline__ void fix_one(const FixArgs& f, int64_t bz, int64_t m, int64_t n,
+                                        int lane) {
+    const float* a = f.A + bz * f.sA + m * f.K;
+    const float* b = f.B + bz * f.sB;
+    double acc = 0.0;
+    for (int64_t k = lane; k < f.K; k += 32) {
+        const double bv = f.trans_b ? (double)__ldg(b + n * f.K + k) : (double)__ldg(b + k * f.N + n);
+        acc = __dadd_rn(acc, __dmul_rn(fabs((double)__ldg(a + k)), fabs(bv)));
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        const int64_t o = bz * f.sC + m * f.ldc + n;
+        double e = __dmul_rn(f.s, acc);
+        if (f.Y) e = __dadd_rn(e, __dmul_rn(f.u, fabs((double)__ldg(f.Y + o))));
+        if (f.out_f64) static_cast<double*>(f.C)[o] = e;
+        else static_cast<float*>(f.C)[o] = __double2float_ru(e);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_absgemm_fix(const __grid_constant__ FixArgs f) {
+    const unsigned long long cnt = *(volatile unsigned long long*)f.count;
+    if (cnt == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (cnt <= f.cap) {
+        for (int64_t i = w0; i < (int64_t)cnt; i += nw) {
+            const unsigned long long idx = f.list[i];
+            const int64_t n = (int64_t)(idx % (unsigned long long)f.N);
+            const int64_t m = (int64_t)((idx / (unsigned long long)f.N) % (unsigned long long)f.M);
+            const int64_t bz = (int64_t)(idx / ((unsigned long long)f.N * (unsigned long long)f.M));
+            fix_one(f, bz, m, n, lane);
+        }
+    } else {
+        const int64_t total = f.batch * f.M * f.N;
+        for (int64_t t = w0; t < total; t += nw) {
+            const int64_t n = t % f.N, m = (t / f.N) % f.M, bz = t / (f.N * f.M);
+            const int ta = __ldg(f.a_tiny + (f.a_batched ? bz * f.M : 0) + m);
+            const int tb = __ldg(f.b_tiny + (f.b_batched ? bz * f.N : 0) + n);
+            if (ta + tb > 0) fix_one(f, bz, m, n, lane);
+        }
+    }
+}
+
+template <int FMT>
+static int launch_tc(const void* a_hi, const void* a_lo, const int32_t* a_exp, const void* b_hi,
+                     const void* b_lo, const int32_t* b_exp, void* eps, int eps_f64,
+                     int64_t batch, int64_t batch_a, int64_t batch_b, int64_t M, int64_t N,
+                     int64_t K, int64_t ldc, int64_t stride_c, double gamma_const,
+                     const float* y_or_null, double u, double slack, cudaStream_t stream,
+                     const float* A = nullptr, const float* B = nullptr, int trans_b = 0,
+                     void* fix_ws = nullptr, size_t fix_ws_bytes = 0) {
+    NAO_REQUIRE(a_hi && a_lo && b_hi && b_lo && eps, "abs-gemm tc: null pointer");
+    NAO_REQUIRE(FMT == kFmtTF32 || (a_exp && b_exp), "abs-gemm tc f16: exponent arrays missing");
+    NAO_REQUIRE(FMT == kFmtTF32 || (A && B && fix_ws && fix_ws_bytes >= 128),
+                "abs-gemm tc f16: operands / fix-up workspace missing");
+    NAO_REQUIRE(M >= 1 && N >= 1 && K >= 1 && batch >= 1, "abs-gemm tc: bad shape");
+    NAO_REQUIRE((batch_a == batch || batch_a == 1) && (batch_b == batch || batch_b == 1),
+                "abs-gemm tc: bad batch broadcast");
+    NAO_REQUIRE(ceil_div(N, BN) * ceil_div(M, BM) < (1LL << 31) && batch <= 65535,
+                "abs-gemm tc: grid too large");
+    const int64_t Kp = FMT == kFmtF16 ? (K + 7) / 8 * 8 : (K + 3) / 4 * 4;
+    const int bk = FMT == kFmtF16 ? 32 : BK;  // elements per 64-byte k-block
+    const bool use_pair = FMT == kFmtTF32 && tc_use_pair();
+    CUtensorMap mah, mal, mbh, mbl;
+    int rc;
+    const int b_box = use_pair ? pair::BNH : BN;
+    if ((rc = make_map(&mah, a_hi, M, Kp, batch_a, BM, FMT))) return rc;
+    if ((rc = make_map(&mal, a_lo, M, Kp, batch_a, BM, FMT))) return rc;
+    if ((rc = make_map(&mbh, b_hi, N, Kp, batch_b, b_box, FMT))) return rc;
+    if ((rc = make_map(&mbl, b_lo, N, Kp, batch_b, b_box, FMT))) return rc;
+    TcArgs g;
+    memset(&g, 0, sizeof g);
+    g.M = M; g.N = N; g.K = K;
+    g.nkb = (int)((Kp + bk - 1) / bk);
+    g.a_batched = batch_a > 1; g.b_batched = batch_b > 1;
+    g.C = eps; g.Y = y_or_null; g.ldc = ldc; g.sC = stride_c; g.out_f64 = eps_f64; g.u = u;
+    g.a_exp = a_exp; g.b_exp = b_exp;
+    if (FMT == kFmtF16) {
+        g.a_tiny = a_exp + batch_a * M;  // second block of the split's row info
+        g.b_tiny = b_exp + batch_b * N;
+        g.fix_count = static_cast<unsigned long long*>(fix_ws);
+        g.fix_list = g.fix_count + 8;
+        g.fix_cap = (unsigned long long)(fix_ws_bytes / 8 - 8);
+    }
+    // compensation factors (see header); 2 MMA instructions per 64-byte k-block
+    const double mma_rel = 3.0 * 0x1p-23;
+    const double j0 = (double)(KCHUNK_KB * 2);
+    const double j1 = 2.0 * (double)g.nkb * 2;
+    const double comp_split = 1.0 / (1.0 - 1.002 * 0x1p-20);
+    const double comp0 = 1.0 / (1.0 - j0 * mma_rel);
+    NAO_REQUIRE(j1 * mma_rel < 0.5, "abs-gemm tc: K too large for the acc1 error model");
+    const double comp1 = 1.0 / (1.0 - j1 * mma_rel);
+    const double s = gamma_const * comp_split * (1.0 + slack) * (1.0 + 0x1p-50);
+    g.scale0 = s * comp0;
+    g.scale0f = f32_ru(g.scale0);
+    // FP16 lo parts carry a 2^10 scale
+    g.scale1 = s * comp1 * (FMT == kFmtF16 ? 0x1p-10 : 1.0);
+    g.abs_floor = gamma_const * (double)K * 0x1p-120;
+    g.scale1f = f32_ru(g.scale1);
+    g.abs_floorf = f32_ru(g.abs_floor);
+    g.uf = f32_ru(u);
+    // excess of the tiny parts <= 2^-24 * 2^15 * 1.001 per tiny element (scaled
+    // units); unflagged outputs have it <= 2^-20 of their value
+    g.fix_thr = g.scale0 * 0x1p11 * 1.002;
+    g.fix_thrf = (float)(g.fix_thr * (1.0 + 0x1p-20));
+    int rc_k = NAO_OK;
+    if (!eps_f64 && g.nkb <= KCHUNK_KB && !tc_no_short()) {
+        static bool attr3_set = false;
+        if (!attr3_set) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc_short<FMT>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                shortk::SMEM_BYTES));
+            attr3_set = true;
+        }
+        const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * batch;
+        const unsigned ctas = (unsigned)(tiles < kNumSMs ? tiles : kNumSMs);
+        k_absgemm_tc_short<FMT><<<ctas, NUM_THREADS, shortk::SMEM_BYTES, stream>>>(
+            mah, mal, mbh, mbl, g, (int)batch);
+        NAO_CHECK_LAUNCH();
+    } else if (use_pair) {
+        static bool attr2_set = false;
+        if (!attr2_set) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc2,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                pair::SMEM_BYTES));
+            attr2_set = true;
+        }
+        dim3 grid2((unsigned)(2 * ceil_div(N, pair::BN) * ceil_div(M, 2 * pair::BM)), 1,
+                   (unsigned)batch);
+        k_absgemm_tc2<<<grid2, pair::NUM_THREADS, pair::SMEM_BYTES, stream>>>(mah, mal, mbh, mbl,
+                                                                             g);
+        NAO_CHECK_LAUNCH();
+    } else {
+    static bool attr_set = false;
+    if (!attr_set) {
+        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc<FMT>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            SMEM_BYTES));
+        attr_set = true;
+    }
+    dim3 grid((unsigned)(ceil_div(N, BN) * ceil_div(M, BM)), 1, (unsigned)batch);
+    k_absgemm_tc<FMT><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, g);
+    NAO_CHECK_LAUNCH();
+    }
+    (void)rc_k;
+    if (FMT == kFmtF16) {  // exact recompute of flagged outputs, then reset the count
+        FixArgs f;
+        memset(&f, 0, sizeof f);
+        f.A = A; f.B = B;
+        f.sA = batch_a > 1 ? M * K : 0;
+        f.sB = batch_b > 1 ? N * K : 0;
+        f.trans_b = trans_b;
+        f.M = M; f.N = N; f.K = K; f.batch = batch;
+        f.C = eps; f.Y = y_or_null; f.ldc = ldc; f.sC = stride_c; f.out_f64 = eps_f64;
+        f.s = gamma_const * (1.0 + slack) * (1.0 + 0x1p-50);
+        f.u = u;
+        f.a_tiny = g.a_tiny; f.b_tiny = g.b_tiny;
+        f.a_batched = g.a_batched; f.b_batched = g.b_batched;
+        f.count = g.fix_count; f.list = g.fix_list; f.cap = g.fix_cap;
+        k_absgemm_fix<<<kNumSMs * 4, 256, 0, stream>>>(f);
+        NAO_CHECK_LAUNCH();
+        NAO_CHECK_CUDA(cudaMemsetAsync(g.fix_count, 0, 8, stream));
+    }
     return NAO_OK;
 }
 
@@ -912,85 +1406,59 @@ int nao_abs_gemm_tc(const float* a_hi, const float* a_lo, const float* b_hi, con
                     int64_t M, int64_t N, int64_t K, int64_t ldc, int64_t stride_c,
                     double gamma_const, const float* y_or_null, double u, double slack,
                     void* stream) {
-    using namespace nao::tc;
-    NAO_REQUIRE(a_hi && a_lo && b_hi && b_lo && eps, "abs-gemm tc: null pointer");
-    NAO_REQUIRE(M >= 1 && N >= 1 && K >= 1 && batch >= 1, "abs-gemm tc: bad shape");
-    NAO_REQUIRE((batch_a == batch || batch_a == 1) && (batch_b == batch || batch_b == 1),
-                "abs-gemm tc: bad batch broadcast");
-    NAO_REQUIRE(ceil_div(N, BN) * ceil_div(M, BM) < (1LL << 31) && batch <= 65535,
-                "abs-gemm tc: grid too large");
-    const int64_t Kp = nao_tf32_split_cols(K);
-    const bool use_pair = tc_use_pair();
-    CUtensorMap mah, mal, mbh, mbl;
-    int rc;
-    const int b_box = use_pair ? pair::BNH : BN;
-    if ((rc = make_map(&mah, a_hi, M, Kp, batch_a))) return rc;
-    if ((rc = make_map(&mal, a_lo, M, Kp, batch_a))) return rc;
-    if ((rc = make_map(&mbh, b_hi, N, Kp, batch_b, b_box))) return rc;
-    if ((rc = make_map(&mbl, b_lo, N, Kp, batch_b, b_box))) return rc;
-    TcArgs g;
-    g.M = M; g.N = N; g.K = K;
-    g.nkb = (int)((Kp + BK - 1) / BK);
-    g.a_batched = batch_a > 1; g.b_batched = batch_b > 1;
-    g.C = eps; g.Y = y_or_null; g.ldc = ldc; g.sC = stride_c; g.out_f64 = eps_f64; g.u = u;
-    // compensation factors (see header)
-    const double mma_rel = 3.0 * 0x1p-23;
-    const double j0 = (double)(KCHUNK_KB * BK / 8);
-    const double j1 = 2.0 * (double)g.nkb * (BK / 8);
-    const double comp_split = 1.0 / (1.0 - 1.002 * 0x1p-20);
-    const double comp0 = 1.0 / (1.0 - j0 * mma_rel);
-    NAO_REQUIRE(j1 * mma_rel < 0.5, "abs-gemm tc: K too large for the acc1 error model");
-    const double comp1 = 1.0 / (1.0 - j1 * mma_rel);
-    const double s = gamma_const * comp_split * (1.0 + slack) * (1.0 + 0x1p-50);
-    g.scale0 = s * comp0;
-    g.scale0f = f32_ru(g.scale0);
-    g.scale1 = s * comp1;
-    g.abs_floor = gamma_const * (double)K * 0x1p-120;
-    g.scale1f = f32_ru(g.scale1);
-    g.abs_floorf = f32_ru(g.abs_floor);
-    g.uf = f32_ru(u);
-    if (!eps_f64 && g.nkb <= KCHUNK_KB && !tc_no_short()) {
-        static bool attr3_set = false;
-        if (!attr3_set) {
-            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc_short,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                shortk::SMEM_BYTES));
-            attr3_set = true;
-        }
-        const int64_t tiles = ceil_div(N, BN) * ceil_div(M, BM) * batch;
-        const unsigned ctas = (unsigned)(tiles < kNumSMs ? tiles : kNumSMs);
-        k_absgemm_tc_short<<<ctas, NUM_THREADS, shortk::SMEM_BYTES,
-                             static_cast<cudaStream_t>(stream)>>>(mah, mal, mbh, mbl, g, (int)batch);
-        NAO_CHECK_LAUNCH();
-        return NAO_OK;
+    return nao::tc::launch_tc<nao::tc::kFmtTF32>(
+        a_hi, a_lo, nullptr, b_hi, b_lo, nullptr, eps, eps_f64, batch, batch_a, batch_b, M, N, K,
+        ldc, stride_c, gamma_const, y_or_null, u, slack, static_cast<cudaStream_t>(stream));
+}
+
+int64_t nao_f16_split_cols(int64_t K) { return (K + 7) / 8 * 8; }
+
+int nao_f16_split(const float* x, void* hi, void* lo, int32_t* row_info, int64_t batch,
+                  int64_t rows, int64_t K, int64_t ld, int64_t stride_batch, int transpose,
+                  void* stream) {
+    NAO_REQUIRE(x && hi && lo && row_info, "f16 split: null pointer");
+    int32_t* row_exp = row_info;
+    NAO_REQUIRE(batch >= 1 && rows >= 0 && K >= 1, "f16 split: bad shape");
+    const int64_t Kp = nao_f16_split_cols(K);
+    if (rows == 0) return NAO_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!transpose) {
+        int64_t blocks = ceil_div(batch * rows, 8);
+        if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+        const bool vec = (K % 8) == 0 && (ld % 4) == 0 && (stride_batch % 4) == 0 &&
+                         (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+        if (vec)
+            tc::k_split_f16_rows<true><<<(unsigned)blocks, 256, 0, st>>>(
+                x, static_cast<__half*>(hi), static_cast<__half*>(lo), row_exp, batch, rows, K,
+                Kp, ld, stride_batch);
+        else
+            tc::k_split_f16_rows<false><<<(unsigned)blocks, 256, 0, st>>>(
+                x, static_cast<__half*>(hi), static_cast<__half*>(lo), row_exp, batch, rows, K,
+                Kp, ld, stride_batch);
+    } else {
+        int64_t blocks = batch * ceil_div(rows, 32);
+        if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+        tc::k_split_f16_cols<<<(unsigned)blocks, 256, 0, st>>>(
+            x, static_cast<__half*>(hi), static_cast<__half*>(lo), row_exp, batch, rows, K, Kp,
+            ld, stride_batch);
     }
-    if (use_pair) {
-        static bool attr2_set = false;
-        if (!attr2_set) {
-            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc2,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                pair::SMEM_BYTES));
-            attr2_set = true;
-        }
-        dim3 grid2((unsigned)(2 * ceil_div(N, pair::BN) * ceil_div(M, 2 * pair::BM)), 1,
-                   (unsigned)batch);
-        k_absgemm_tc2<<<grid2, pair::NUM_THREADS, pair::SMEM_BYTES,
-                        static_cast<cudaStream_t>(stream)>>>(mah, mal, mbh, mbl, g);
-        NAO_CHECK_LAUNCH();
-        return NAO_OK;
-    }
-    static bool attr_set = false;
-    if (!attr_set) {
-        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            SMEM_BYTES));
-        attr_set = true;
-    }
-    dim3 grid((unsigned)(ceil_div(N, BN) * ceil_div(M, BM)), 1, (unsigned)batch);
-    k_absgemm_tc<<<grid, NUM_THREADS, SMEM_BYTES, static_cast<cudaStream_t>(stream)>>>(
-        mah, mal, mbh, mbl, g);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
+}
+
+// FP16 parts from nao_f16_split (hi/lo [batch_x, rows, Kp] halves + row exponents)
+size_t nao_abs_gemm_tc16_fix_workspace(void) { return (size_t)8 << 20; }
+
+int nao_abs_gemm_tc16(const void* a_hi, const void* a_lo, const int32_t* a_info, const void* b_hi,
+                      const void* b_lo, const int32_t* b_info, const float* A, const float* B,
+                      int transpose_b, void* eps, int eps_f64, int64_t batch, int64_t batch_a,
+                      int64_t batch_b, int64_t M, int64_t N, int64_t K, int64_t ldc,
+                      int64_t stride_c, double gamma_const, const float* y_or_null, double u,
+                      double slack, void* fix_ws, size_t fix_ws_bytes, void* stream) {
+    return nao::tc::launch_tc<nao::tc::kFmtF16>(
+        a_hi, a_lo, a_info, b_hi, b_lo, b_info, eps, eps_f64, batch, batch_a, batch_b, M, N, K,
+        ldc, stride_c, gamma_const, y_or_null, u, slack, static_cast<cudaStream_t>(stream), A, B,
+        transpose_b, fix_ws, fix_ws_bytes);
 }
 
 }  // extern "C"

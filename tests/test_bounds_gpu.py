@@ -89,7 +89,8 @@ def test_matmul_bound_api(B):
         B.matmul_bound(np.ones((2, 3), np.float32), np.ones((4, 2), np.float32), B.FpModel())
 
 
-PATHS = [0, 1]  # NAO_GEMM_FFMA_RU, NAO_GEMM_TC_TF32X3
+PATHS = [0, 1, 2]  # NAO_GEMM_FFMA_RU, NAO_GEMM_TC_TF32X3, NAO_GEMM_TC_F16X3
+TC_PATHS = [1, 2]
 
 
 @pytest.mark.parametrize("path", PATHS)
@@ -128,8 +129,10 @@ def test_abs_gemm_heterogeneous_rows(B, path):
     assert_bound(got, ref, "hetero")
 
 
-@pytest.mark.parametrize("case", ["equal", "ramp", "sparse", "tf32_edge", "subnormal"])
-def test_abs_gemm_tc_adversarial(B, case):
+@pytest.mark.parametrize("path", TC_PATHS)
+@pytest.mark.parametrize("case", ["equal", "ramp", "sparse", "tf32_edge", "subnormal",
+                                  "wide_range", "one_hot_rows"])
+def test_abs_gemm_tc_adversarial(B, case, path):
     """Data that stresses the tensor-core accumulation / split error model:
     long runs of equal terms (truncation bias), values on TF32 boundaries,
     sparse rows and subnormals.  Must stay inside [ref, ref (1 + 1e-5)]."""
@@ -148,34 +151,43 @@ def test_abs_gemm_tc_adversarial(B, case):
         base = (rng.random((M, K)) + 1).astype(np.float32)
         a = (base.view(np.uint32) | 0x1FFF).view(np.float32)  # all 13 dropped bits set
         b = ((rng.random((K, N)) + 1).astype(np.float32).view(np.uint32) | 0x1000).view(np.float32)
-    else:
+    elif case == "subnormal":
         a = (rng.random((M, K)) * 1e-39).astype(np.float32)
         b = (rng.random((K, N)) * 1e-3).astype(np.float32)
+    elif case == "wide_range":  # 2^-40 .. 2^40 inside every row and column
+        a = (2.0 ** rng.integers(-40, 40, size=(M, K)) * (rng.random((M, K)) + 1)).astype(np.float32)
+        b = (2.0 ** rng.integers(-40, 40, size=(K, N)) * (rng.random((K, N)) + 1)).astype(np.float32)
+    else:  # one huge entry per row paired with a zero of B; the rest tiny (FP16 tiny parts)
+        a = np.full((M, K), 1e-12, np.float32)
+        a[:, 0] = 1e3
+        b = (rng.random((K, N)) + 0.5).astype(np.float32)
+        b[0, :] = 0.0
     ref = OB.matmul_bound(a, b, OB.FpModel())
     got = B.abs_gemm_bound(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                           OB.FpModel().reduction_const(2 * K - 1), path=1).cpu().numpy()
+                           OB.FpModel().reduction_const(2 * K - 1), path=path).cpu().numpy()
     if case == "subnormal":  # absolute floor K*2^-120 dominates tiny products: sound, not tight
         assert np.all(got >= ref)
     else:
         assert_bound(got, ref, case)
 
 
-def test_abs_gemm_tc_batched_and_cached_weight(B):
+@pytest.mark.parametrize("path", TC_PATHS)
+def test_abs_gemm_tc_batched_and_cached_weight(B, path):
     rng = np.random.default_rng(2)
     q = torch.from_numpy(rng.standard_normal((8, 200, 64)).astype(np.float32)).cuda()
     k = torch.from_numpy(rng.standard_normal((8, 300, 64)).astype(np.float32)).cuda()
     ref = OB.matmul_bound(q.cpu().numpy(), k.cpu().numpy(), OB.FpModel(), transpose_b=True)
     c = OB.FpModel().reduction_const(127)
-    got = B.abs_gemm_bound(q, k, c, True, path=1).cpu().numpy()
+    got = B.abs_gemm_bound(q, k, c, True, path=path).cpu().numpy()
     assert_bound(got, ref, "batched tb")
     w = torch.from_numpy(rng.standard_normal((64, 96)).astype(np.float32)).cuda()
     ref = OB.matmul_bound(q.cpu().numpy(), w.cpu().numpy(), OB.FpModel())
     for _ in range(2):  # second call hits the cached weight split
-        got = B.abs_gemm_bound(q, w, c, False, path=1, cache_b=True).cpu().numpy()
+        got = B.abs_gemm_bound(q, w, c, False, path=path, cache_b=True).cpu().numpy()
         assert_bound(got, ref, "bcast weight")
     w.mul_(2.0)  # in-place change bumps _version -> cache must not be used
     ref = OB.matmul_bound(q.cpu().numpy(), w.cpu().numpy(), OB.FpModel())
-    got = B.abs_gemm_bound(q, w, c, False, path=1, cache_b=True).cpu().numpy()
+    got = B.abs_gemm_bound(q, w, c, False, path=path, cache_b=True).cpu().numpy()
     assert_bound(got, ref, "weight changed")
 
 
@@ -251,8 +263,9 @@ def test_softmax_many_long_rows(B, shape, f64):
         assert np.all(e <= e_ref * (1 + RTOL) + np.spacing(e_ref.astype(np.float32)) * 2)
 
 
-@pytest.mark.parametrize("K", [1, 64, 128])
-def test_abs_gemm_tc_short_k_persistent(B, K):
+@pytest.mark.parametrize("path", TC_PATHS)
+@pytest.mark.parametrize("K", [1, 64, 128, 256])
+def test_abs_gemm_tc_short_k_persistent(B, K, path):
     """K <= one TMEM chunk -> the persistent k_absgemm_tc_short (FP32 eps): many
     more tiles than SMs (slot reuse), ragged M/N, batched q k^T, linear u|y|."""
     rng = np.random.default_rng(K)
@@ -261,7 +274,7 @@ def test_abs_gemm_tc_short_k_persistent(B, K):
     c = OB.FpModel().reduction_const(2 * K - 1)
     ref = OB.matmul_bound(q, k, OB.FpModel(), transpose_b=True)
     got = B.abs_gemm_bound(torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), c, True,
-                           eps_f64=False, path=1).cpu().numpy()
+                           eps_f64=False, path=path).cpu().numpy()
     assert_bound(got, ref, "scores")
     x = rng.standard_normal((1000, K)).astype(np.float32)
     w = rng.standard_normal((K, 700)).astype(np.float32)
@@ -269,6 +282,6 @@ def test_abs_gemm_tc_short_k_persistent(B, K):
     u = 2.0 ** -24
     ref = OB.matmul_bound(x, w, OB.FpModel()) + u * np.abs(y.astype(np.float64))
     got = B.abs_gemm_bound(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), c, False,
-                           y=torch.from_numpy(y).cuda(), u=u, eps_f64=False, path=1,
+                           y=torch.from_numpy(y).cuda(), u=u, eps_f64=False, path=path,
                            cache_b=True).cpu().numpy()
     assert_bound(got, ref, "linear")

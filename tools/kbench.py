@@ -107,7 +107,7 @@ def main():
         x = torch.randn((S, I), device=dev)
         report("tf32_split", timeit(lambda: tf32_split(x, S, I, False, False), a.reps),
                12 * x.numel())
-    for path, tag in ((1, "gemm_tc"), (0, "gemm_ffma")):
+    for path, tag in ((1, "gemm_tc"), (2, "gemm_tc16"), (0, "gemm_ffma")):
         if want(tag):
             shapes = [(S, H, H), (S, H, I), (S, I, H)]
             if want("gemm_all"):  # every Qwen3-8B GEMM shape: k/v, scores, ctx, lm_head
@@ -131,7 +131,13 @@ def main():
                 abs_gemm_bound(A, B, c, tb, eps_f64=False, path=path, cache_b=cb)
                 ms = timeit(lambda: abs_gemm_bound(A, B, c, tb, eps_f64=False, path=path,
                                                    cache_b=cb), a.reps)
-                report(tag, ms, flops=fl, shape=list(shp))
+                if path == 2:  # the f16 split of the activation operand alone
+                    from paper_2510_16028_b200.bounds import f16_split
+                    rows, KK = A.shape[-2], A.shape[-1]
+                    ms_s = timeit(lambda: f16_split(A, rows, KK, False, False), a.reps)
+                    report(tag, ms, flops=fl, shape=list(shp), split_ms=round(ms_s, 4))
+                else:
+                    report(tag, ms, flops=fl, shape=list(shp))
                 del A, B
             if want("sgemm") or only is None:
                 A = torch.randn((S, H), device=dev)
