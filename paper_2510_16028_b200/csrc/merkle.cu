@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "check_common.cuh"
@@ -128,7 +129,7 @@ struct LeafCheckSmem {
     double t_abs[kMaxGrid], t_rel[kMaxGrid];
     float f_rel[kMaxGrid], f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];
     unsigned int wc[kLeafWarps][2][kMaxGrid + 1];  // warp-private interval counters
-    unsigned long long q[kLeafWarps][64];           // warp queue of flagged element indices
+    unsigned long long q[kLeafWarps][96];           // warp queue of flagged element indices
     unsigned long long viol, border, nonfin, nslow;
     unsigned long long maxr_bits;
     int is_last;
@@ -176,19 +177,30 @@ struct LaneCheck {
     bool best_inf = false;
 };
 
-__device__ __forceinline__ void process_flagged(const CheckDesc& d, const float* claimed,
-                                                uint64_t idx, int G, double epsilon,
-                                                LeafCheckSmem& sm, int w, LaneCheck& lc) {
-    const float y = __ldg(d.local + idx), c = __ldg(claimed + idx);
+struct Flagged { float y, c; double eps; };
+
+__device__ __forceinline__ Flagged load_flagged(const CheckDesc& d, const float* claimed,
+                                                uint64_t idx) {
+    Flagged f;
+    f.y = __ldg(d.local + idx);
+    f.c = __ldg(claimed + idx);
+    f.eps = 0.0;
+    if (d.eps_kind == NAO_EPS_TENSOR_F32) f.eps = (double)__ldg(static_cast<const float*>(d.eps) + idx);
+    else if (d.eps_kind == NAO_EPS_TENSOR_F64) f.eps = __ldg(static_cast<const double*>(d.eps) + idx);
+    return f;
+}
+
+__device__ __forceinline__ void process_flagged(const CheckDesc& d, const Flagged& f, int G,
+                                                double epsilon, LeafCheckSmem& sm, int w,
+                                                LaneCheck& lc) {
+    const float y = f.y, c = f.c;
     if (!isfinite(y) || !isfinite(c)) {
         lc.nonfin++; lc.viol++;
         atomicAdd(&sm.wc[w][0][G], 1u); atomicAdd(&sm.wc[w][1][G], 1u);
         return;
     }
-    double eps = 0.0;
-    if (d.eps_kind == NAO_EPS_TENSOR_F32) eps = (double)__ldg(static_cast<const float*>(d.eps) + idx);
-    else if (d.eps_kind == NAO_EPS_TENSOR_F64) eps = __ldg(static_cast<const double*>(d.eps) + idx);
-    else if (d.eps_kind == NAO_EPS_SCALED_LOCAL) eps = __dmul_rn(d.eps_scale, fabs((double)y));
+    double eps = f.eps;
+    if (d.eps_kind == NAO_EPS_SCALED_LOCAL) eps = __dmul_rn(d.eps_scale, fabs((double)y));
     const double diff = abs_key(y, c);
     if (diff > eps) lc.viol++;
     else if (diff > eps * d.lo_factor) lc.border++;
@@ -212,12 +224,10 @@ __device__ __forceinline__ void process_flagged(const CheckDesc& d, const float*
 }
 
 template <int ALG>
-__global__ void __launch_bounds__(kLeafThreads) k_chunk_leaves_check(
-    const __grid_constant__ CCTable tab, uint32_t* __restrict__ digests,
-    CheckAccum* __restrict__ accs) {
-    __shared__ LeafCheckSmem sm;
-    extern __shared__ unsigned long long s_mask[];  // [groups][kLeafThreads]
-    const int s = find_seg(tab.block_prefix, tab.n, blockIdx.x);  // block-uniform
+__device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* __restrict__ digests,
+                                                 CheckAccum* __restrict__ accs, LeafCheckSmem& sm,
+                                                 unsigned long long* s_mask, uint64_t vb) {
+    const int s = find_seg(tab.block_prefix, tab.n, vb);  // block-uniform
     const CheckDesc& d = tab.chk[s];
     const bool check = d.local != nullptr;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_chunk_leaves_check(
     const uint32_t cw = tab.chunk_words;
     const uint32_t groups = (cw + 63) >> 6;
     const uint64_t nchunks = (total_w + cw - 1) / cw;
-    const uint64_t c0 = (blockIdx.x - tab.block_prefix[s]) * kLeafThreads;
+    const uint64_t c0 = (vb - tab.block_prefix[s]) * kLeafThreads;
     const uint64_t c = c0 + threadIdx.x;
     int G = 0;
     double epsilon = 0.0;
@@ -292,18 +302,26 @@ __global__ void __launch_bounds__(kLeafThreads) k_chunk_leaves_check(
             }
             qn += __popc(b);
             nflag += has;
-            if (qn >= 32) {
+            if (qn >= 64) {  // two entries per lane: four loads in flight before the math
                 __syncwarp();
-                process_flagged(d, claimed, sm.q[w][lane], G, epsilon, sm, w, lc);
+                const Flagged f0 = load_flagged(d, claimed, sm.q[w][lane]);
+                const Flagged f1 = load_flagged(d, claimed, sm.q[w][32 + lane]);
+                process_flagged(d, f0, G, epsilon, sm, w, lc);
+                process_flagged(d, f1, G, epsilon, sm, w, lc);
                 __syncwarp();
-                if (lane < qn - 32) sm.q[w][lane] = sm.q[w][32 + lane];
+                if (lane < qn - 64) sm.q[w][lane] = sm.q[w][64 + lane];
                 __syncwarp();
-                qn -= 32;
+                qn -= 64;
             }
         }
     }
     __syncwarp();
-    if (lane < qn) process_flagged(d, claimed, sm.q[w][lane], G, epsilon, sm, w, lc);
+    for (int base = 0; base < qn; base += 32) {
+        if (base + lane < qn) {
+            const Flagged f = load_flagged(d, claimed, sm.q[w][base + lane]);
+            process_flagged(d, f, G, epsilon, sm, w, lc);
+        }
+    }
     __syncwarp();
     // ---- block reduction -> the tensor's accumulator
     const unsigned long long viol = warp_sum(lc.viol), border = warp_sum(lc.border),
@@ -369,6 +387,24 @@ __global__ void __launch_bounds__(kLeafThreads) k_chunk_leaves_check(
     __syncthreads();
     unsigned long long* z = reinterpret_cast<unsigned long long*>(acc);
     for (int i = threadIdx.x; i < (int)(sizeof(CheckAccum) / 8); i += blockDim.x) z[i] = 0ull;
+}
+
+// Persistent over virtual blocks (grid may be smaller than the block count, so
+// the commit can share SMs with concurrently running forward kernels).
+#ifndef NAO_LEAF_MINB
+#define NAO_LEAF_MINB 4  // <= 128 registers: 4 CTAs (16 warps) per SM for the sponge
+#endif
+template <int ALG>
+__global__ void __launch_bounds__(kLeafThreads, NAO_LEAF_MINB) k_chunk_leaves_check(
+    const __grid_constant__ CCTable tab, uint32_t* __restrict__ digests,
+    CheckAccum* __restrict__ accs) {
+    __shared__ LeafCheckSmem sm;
+    extern __shared__ unsigned long long s_mask[];  // [groups][kLeafThreads]
+    const uint64_t nvb = tab.block_prefix[tab.n];
+    for (uint64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+        leaf_check_block<ALG>(tab, digests, accs, sm, s_mask, vb);
+        __syncthreads();
+    }
 }
 
 template <int ALG>
@@ -657,8 +693,13 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
             if (checks && payload_bytes[i] > 0) memcpy(&ct.chk[cnt], &checks[i], sizeof(CheckDesc));
         }
         ct.n = cnt;
-        const uint64_t blocks = ct.block_prefix[cnt];
+        uint64_t blocks = ct.block_prefix[cnt];
         if (blocks == 0) continue;
+        static const uint64_t max_ctas = [] {
+            const char* e = getenv("NAO_COMMIT_CTAS");
+            return (uint64_t)(e ? atoll(e) : 0);
+        }();
+        if (max_ctas && blocks > max_ctas) blocks = max_ctas;
         CheckAccum* accs = static_cast<CheckAccum*>(accum);
         const size_t dsm = (size_t)((ct.chunk_words + 63) / 64) * kLeafThreads * 8;
         if (hash_alg == kSHA256) {

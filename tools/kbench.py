@@ -84,6 +84,19 @@ def main():
             nb = sum(t.numel() * 4 for t in ts)
             report(f"commit_{alg}_batch20x33MB", timeit(lambda: commit_tensors(ts, 4096, alg),
                                                         a.reps), nb)
+    if want("commitcheck"):
+        from paper_2510_16028_b200.dispute import commit_check_nodes
+        ys = [torch.randn((NH, S, S), device=dev)] + [torch.randn((S, H), device=dev)
+                                                      for _ in range(8)]
+        ycs = [inject_drift(y, 1, 16) if i % 2 == 0 else y.clone() for i, y in enumerate(ys)]
+        nb = sum(t.numel() * 4 for t in ys)
+        tau = np.linspace(1e-9, 1e-3, 23)
+        eps = [("scaled", 2 ** -23)] * len(ys)
+        taus = [(tau, tau)] * len(ys)
+        report("commit_check_keccak", timeit(lambda: commit_check_nodes(ycs, ys, eps, taus, 4096,
+                                                                         "keccak256"), a.reps), nb)
+        report("commit_only_keccak", timeit(lambda: commit_tensors(ycs, 4096, "keccak256"),
+                                            a.reps), nb)
     if want("softmax"):
         x = torch.randn((NH, S, S), device=dev) * 3
         n = x.numel()
