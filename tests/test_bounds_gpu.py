@@ -241,10 +241,13 @@ def test_mlp_co_execute_matches_reference(B, ref_mlp):
 
 
 @pytest.mark.parametrize("shape,f64", [((4096, 384), True), ((4096, 384), False),
-                                       ((1536, 131), True), ((1030, 2048), False)])
+                                       ((1536, 131), True), ((1030, 2048), False),
+                                       ((1030, 2048), True), ((777, 1024), False),
+                                       ((6, 2048), True), ((3000, 1024), True)])
 def test_softmax_many_long_rows(B, shape, f64):
-    """Design C (max/exp warp per row, lane-per-row sequential fold, epilogue):
-    values bit-exact, bound within [ref, ref(1+1e-5)] (FP32 eps rounded up)."""
+    """Design C (max/exp warp per row, lane-per-row sequential fold, epilogue)
+    at GPT-2 (n=1024) and Qwen (n=2048) row lengths: values bit-exact, bound
+    within [ref, ref(1+1e-5)] (FP32 eps rounded up)."""
     rng = np.random.default_rng(shape[0] + shape[1])
     x = (rng.standard_normal(shape) * 4).astype(np.float32)
     x[3, :7] = -np.inf  # exp(-inf - m) = 0 participates in the fold
