@@ -1119,6 +1119,60 @@ __global__ void __launch_bounds__(256) k_split_f16_rows(const float* __restrict_
     }
 }
 
+// Single DRAM pass: a CTA per row stages the row in shared memory (float4,
+// coalesced), block-reduces the max, then splits from shared memory.
+// Needs K % 8 == 0, ld % 4 == 0, 16-byte aligned x, K * 4 <= 96 KB.
+constexpr int kSplitThreads = 256;
+__global__ void __launch_bounds__(kSplitThreads) k_split_f16_rows_smem(
+    const float* __restrict__ x, __half* __restrict__ hi, __half* __restrict__ lo,
+    int32_t* __restrict__ sexp, int64_t batch, int64_t rows, int64_t K, int64_t ld,
+    int64_t sbatch) {
+    extern __shared__ float4 srow[];
+    __shared__ float wmax[kSplitThreads / 32];
+    __shared__ int wtiny[kSplitThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t K4 = K >> 2;
+    for (int64_t t = blockIdx.x; t < batch * rows; t += gridDim.x) {
+        const int64_t b = t / rows, r = t % rows;
+        const float4* xr = reinterpret_cast<const float4*>(x + b * sbatch + r * ld);
+        float m = 0.f;
+        for (int64_t k = threadIdx.x; k < K4; k += kSplitThreads) {
+            const float4 v = __ldg(xr + k);
+            srow[k] = v;
+            m = nan_max(nan_max(nan_max(nan_max(m, fabsf(v.x)), fabsf(v.y)), fabsf(v.z)),
+                        fabsf(v.w));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = nan_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) wmax[w] = m;
+        __syncthreads();
+        m = wmax[0];
+#pragma unroll
+        for (int i = 1; i < kSplitThreads / 32; i++) m = nan_max(m, wmax[i]);
+        const int e = row_scale_exp(m);
+        uint2* hr = reinterpret_cast<uint2*>(hi + t * K);
+        uint2* lr = reinterpret_cast<uint2*>(lo + t * K);
+        int tiny = 0;
+        for (int64_t k = threadIdx.x; k < K4; k += kSplitThreads) {
+            const float4 v = srow[k];
+            __half h[4], l[4];
+            tiny += split16_one(v.x, e, h[0], l[0]) + split16_one(v.y, e, h[1], l[1]) +
+                    split16_one(v.z, e, h[2], l[2]) + split16_one(v.w, e, h[3], l[3]);
+            __stcs(hr + k, *reinterpret_cast<const uint2*>(h));
+            __stcs(lr + k, *reinterpret_cast<const uint2*>(l));
+        }
+        tiny = warp_sum(tiny);
+        if (lane == 0) wtiny[w] = tiny;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tt = 0;
+            for (int i = 0; i < kSplitThreads / 32; i++) tt += wtiny[i];
+            sexp[t] = e;
+            sexp[batch * rows + t] = tt;
+        }
+    }
+}
+
 // x is [K, rows] row-major per batch (ld): output row r = input column r.
 // A CTA owns 32 output rows: column maxima over K, then 32x32 transposed tiles.
 __global__ void __launch_bounds__(256) k_split_f16_cols(const float* __restrict__ x,
@@ -1427,7 +1481,20 @@ int nao_f16_split(const float* x, void* hi, void* lo, int32_t* row_info, int64_t
         if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
         const bool vec = (K % 8) == 0 && (ld % 4) == 0 && (stride_batch % 4) == 0 &&
                          (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-        if (vec)
+        if (vec && K * 4 <= 96 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                NAO_CHECK_CUDA(cudaFuncSetAttribute(tc::k_split_f16_rows_smem,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    96 * 1024));
+                attr = true;
+            }
+            int64_t nb = batch * rows;
+            if (nb > kNumSMs * 32) nb = kNumSMs * 32;
+            tc::k_split_f16_rows_smem<<<(unsigned)nb, tc::kSplitThreads, (size_t)K * 4, st>>>(
+                x, static_cast<__half*>(hi), static_cast<__half*>(lo), row_exp, batch, rows, K,
+                ld, stride_batch);
+        } else if (vec)
             tc::k_split_f16_rows<true><<<(unsigned)blocks, 256, 0, st>>>(
                 x, static_cast<__half*>(hi), static_cast<__half*>(lo), row_exp, batch, rows, K,
                 Kp, ld, stride_batch);
