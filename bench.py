@@ -415,6 +415,17 @@ def run_ours(args):
                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks
                     else "fallback", "traffic": None}
+        # DRAM traffic of the dominant kernel: ratio of measured dram bytes to the
+        # algorithmic unit in one `ncu --set full` capture of this bench command
+        # (profiles/r1_traffic.json), applied to this run's per-launch units
+        try:
+            tr = json.load(open(ROOT / "profiles" / "r1_traffic.json")).get(dom)
+            if tr and "ratio_dram_to_hashed" in tr:
+                roof["traffic"] = round(tr["ratio_dram_to_hashed"] * per_launch_units)
+                roof["traffic_unit"] = "bytes per launch (ncu dram read+write, ratio "
+                roof["traffic_unit"] += f"{tr['ratio_dram_to_hashed']} x hashed bytes)"
+        except Exception:
+            pass
         roof["share_of_serial_step"] = round(shares[dom] / t_serial, 4)
         roof["serial_step_ms"] = round(t_serial, 2)
         roof["kernel_ms_per_step"] = {k: round(v, 2) for k, v in sorted(
