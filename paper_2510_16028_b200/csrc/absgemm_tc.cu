@@ -45,7 +45,10 @@ namespace tc {
 // BK = 16: 64 B rows (SWIZZLE_64B), 32 KB stages, 6 in flight;  BK = 32: 128 B
 // rows (SWIZZLE_128B), 64 KB stages, 3 in flight.  Same bytes in flight.
 constexpr int BM = 128, BN = 128, BK = NAO_TC_BK;
-constexpr int STAGES = BK == 16 ? 6 : 3;
+#ifndef NAO_TC_STAGES
+#define NAO_TC_STAGES (NAO_TC_BK == 16 ? 6 : 3)
+#endif
+constexpr int STAGES = NAO_TC_STAGES;
 #ifndef NAO_TC_KCHUNK
 #define NAO_TC_KCHUNK 128
 #endif
@@ -330,7 +333,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // grouped rasterization: consecutive CTAs sweep GROUP_M row tiles per column
     // tile, so the B tiles in flight are shared by GROUP_M CTAs through L2
     const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
-    constexpr int GROUP_M = 8;
+#ifndef NAO_TC_GROUP_M
+#define NAO_TC_GROUP_M 8
+#endif
+    constexpr int GROUP_M = NAO_TC_GROUP_M;
     const int pid = blockIdx.x;
     const int group = pid / (GROUP_M * tiles_n);
     const int first_m = group * GROUP_M;
@@ -370,6 +376,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int kb = 0; kb < nkb; kb++) {
                 const int s = kb % STAGES;
                 const uint32_t ph = (kb / STAGES) & 1;
+#ifdef NAO_TC_NOWAIT
+                if (kb >= STAGES) break;
+#endif
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = smem + s * STAGE_BYTES;
                 mbar_expect_tx(&full[s], STAGE_BYTES);
@@ -388,7 +397,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int chunk = kb / KCHUNK_KB, buf = chunk & 1;
                 const bool first = (kb % KCHUNK_KB) == 0;
                 if (first) mbar_wait(&tempty[buf], ((chunk >> 1) & 1) ^ 1);
+#ifdef NAO_TC_NOWAIT  // timing probe only (wrong results): MMA rate without the TMA feed
+                if (kb < STAGES) mbar_wait(&full[s], ph);
+#else
                 mbar_wait(&full[s], ph);
+#endif
                 fence_after();
                 const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
                 const uint32_t acc0 = tmem + buf * BN;
