@@ -47,6 +47,23 @@ enum nao_unary_kind {
     NAO_UN_EXP = 0, NAO_UN_LOG = 1, NAO_UN_SQRT = 2, NAO_UN_RSQRT = 3,
     NAO_UN_TANH = 4, NAO_UN_GELU = 5, NAO_UN_SILU = 6
 };
+/* device-profile reduction orders (engine.py:75-113) */
+enum nao_order {
+    NAO_ORDER_SEQUENTIAL = 0, NAO_ORDER_PAIRWISE = 1, NAO_ORDER_BLOCKED = 2, NAO_ORDER_PERMUTED = 3
+};
+/* A DeviceProfile (engine.py:29-55) for the FP32 value path: the order of
+ * every reduction (matmul inner products, softmax / layernorm / sum / mean
+ * folds) and the fma policy of matmul.  perm: device int64[perm_n], the
+ * numpy Philox permutation of the reduced length (engine.py:75-77), for
+ * NAO_ORDER_PERMUTED.  A NULL profile means sequential, no fma. */
+typedef struct nao_profile {
+    int32_t order;
+    int32_t block_size;
+    const int64_t* perm;
+    int64_t perm_n;
+    int32_t fma;
+    int32_t reserved;
+} nao_profile;
 enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1, NAO_GEMM_TC_F16X3 = 2 };
 
 /* ------------------------------------------------------------ library */
@@ -158,13 +175,16 @@ int nao_percentile_profile(const double* values, int64_t n, const double* grid, 
  * roundoff, rc = FpModel.reduction_const(n-1) (bounds.py:42-45). */
 /* softmax_bound_parts, bounds.py:114-135 (values: engine.py:185-194, sequential) */
 int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                      double u, double rc, double slack, void* stream);
+                      double u, double rc, double slack, const nao_profile* profile,
+                      void* stream);
 /* layernorm_bound_parts, bounds.py:143-169 (values: engine.py:197-213) */
 int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                        float ln_eps, double u, double rc, double slack, void* stream);
+                        float ln_eps, double u, double rc, double slack,
+                        const nao_profile* profile, void* stream);
 /* op_bound sum/mean/max/min, bounds.py:194-208 (values: engine.py:240-251) */
 int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                     int kind, double u, double rc, double slack, void* stream);
+                     int kind, double u, double rc, double slack, const nao_profile* profile,
+                     void* stream);
 /* _unary_intrinsic values, engine.py:133-154 (FP64 evaluation, one rounding) */
 int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* stream);
 /* eps = scale*|y|: single-rounding (u) / intrinsic (2u) templates, bounds.py:196-199 */
@@ -218,12 +238,13 @@ int nao_abs_gemm_tc16(const void* a_hi, const void* a_lo, const int32_t* a_info,
                       int64_t batch_b, int64_t M, int64_t N, int64_t K, int64_t ldc,
                       int64_t stride_c, double gamma_const, const float* y_or_null, double u,
                       double slack, void* fix_ws, size_t fix_ws_bytes, void* stream);
-/* matmul_op values under the sequential profile (engine.py:157-182),
- * C contiguous [batch, M, N]; fma selects the "+fma" FP64-step emulation. */
+/* matmul_op values (engine.py:157-182) under `profile` (NULL: sequential):
+ * FP32 products reduced over K in the profile's order, or with profile->fma
+ * the sequential FP64-step loop.  C contiguous [batch, M, N]. */
 int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, int64_t M,
                        int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t stride_a,
-                       int64_t stride_b, int64_t stride_c, int transpose_b, int fma,
-                       void* stream);
+                       int64_t stride_b, int64_t stride_c, int transpose_b,
+                       const nao_profile* profile, void* stream);
 
 /* Additive fault / drift hook on a node output (engine.py:325-351 `inject`):
  * out = y with +-1-ulp flips on ~n/period elements and a relative fault

@@ -2,8 +2,10 @@
 bound templates and the FP32 value path they are co-computed with:
   /root/reference/pkg/src/fpverify/bounds.py   (FpModel, gamma, templates)
   /root/reference/pkg/src/fpverify/engine.py   (reduction orders, parts, apply_op)
-Only the reduction orders the B200 path emulates are restated here:
-"sequential" (default proposer profile, config.py:14) with and without fma.
+Reduction orders (engine.py:75-113): "sequential" (default proposer profile,
+config.py:14), "pairwise", "blocked" and "permuted" (Philox permutation), each
+with and without fma; `profile` arguments are duck-typed DeviceProfiles
+(.reduction, .block_size, .perm_seed, .fma), None = sequential.
 Extension kinds (not in the reference, SURVEY.md 2.3) are marked as such;
 their parity is unpinned by reference tests.
 """
@@ -64,6 +66,47 @@ def fold_last(arr: np.ndarray) -> np.ndarray:
     return acc
 
 
+def permutation(seed: int, n: int) -> np.ndarray:
+    """engine.py:75-77 (numpy Philox: the permuted profile's fixed order)."""
+    gen = np.random.Generator(np.random.Philox(key=seed, counter=n << 128))
+    return gen.permutation(n)
+
+
+def pairwise_last(arr: np.ndarray) -> np.ndarray:
+    """engine.py:87-92: recursive halving, left half = ceil(n/2)."""
+    n = arr.shape[-1]
+    if n == 1:
+        return arr[..., 0]
+    mid = (n + 1) // 2
+    return pairwise_last(arr[..., :mid]) + pairwise_last(arr[..., mid:])
+
+
+def reduce_last_axis(arr: np.ndarray, profile=None) -> np.ndarray:
+    """engine.py:95-113: the trailing-axis reduction in the profile's order."""
+    n = arr.shape[-1]
+    if n == 0:
+        raise ValueError("cannot reduce an empty axis")
+    red = "sequential" if profile is None else profile.reduction
+    if red == "sequential":
+        return fold_last(arr)
+    if red == "pairwise":
+        return pairwise_last(arr)
+    if red == "blocked":
+        b = max(1, int(profile.block_size))
+        parts = [fold_last(arr[..., i:min(i + b, n)]) for i in range(0, n, b)]
+        acc = parts[0]
+        for q in parts[1:]:
+            acc = acc + q
+        return acc
+    if red == "permuted":
+        return fold_last(arr[..., permutation(int(profile.perm_seed), n)])
+    raise ValueError(f"unknown reduction strategy {red!r}")
+
+
+def _fma(profile, fma):
+    return bool(fma) or bool(getattr(profile, "fma", False))
+
+
 def unary_intrinsic(kind: str, x: np.ndarray) -> np.ndarray:
     """FP64 evaluation rounded once to FP32 (engine.py:133-154)."""
     with np.errstate(all="ignore"):
@@ -88,9 +131,10 @@ def unary_intrinsic(kind: str, x: np.ndarray) -> np.ndarray:
     return out.astype(np.float32)
 
 
-def matmul_value(a, b, transpose_b=False, fma=False) -> np.ndarray:
-    """Sequential-profile matmul (engine.py:157-182), computed column-block by
-    column-block so it does not materialise the (..., M, K, N) product."""
+def matmul_value(a, b, transpose_b=False, fma=False, profile=None) -> np.ndarray:
+    """matmul_op (engine.py:157-182): FP32 products reduced over K in the
+    profile's order (sequential: column by column, no (..., M, K, N) product);
+    fma: the sequential FP64-step loop whatever the order."""
     a = np.asarray(a, dtype=np.float32)
     b = np.asarray(b, dtype=np.float32)
     if transpose_b:
@@ -98,6 +142,10 @@ def matmul_value(a, b, transpose_b=False, fma=False) -> np.ndarray:
     if a.shape[-1] != b.shape[-2]:
         raise ValueError(f"matmul inner dims disagree: {a.shape} @ {b.shape}")
     k_dim = a.shape[-1]
+    fma = _fma(profile, fma)
+    if not fma and profile is not None and profile.reduction != "sequential":
+        prods = a[..., :, :, None] * b[..., None, :, :]  # (..., M, K, N) fp32
+        return reduce_last_axis(np.moveaxis(prods, -2, -1), profile)
     if fma:
         a64 = a.astype(np.float64)
         b64 = b.astype(np.float64)
@@ -114,26 +162,26 @@ def matmul_value(a, b, transpose_b=False, fma=False) -> np.ndarray:
     return acc
 
 
-def softmax_parts(x, axis):
-    """engine.py:185-194 (sequential profile)."""
+def softmax_parts(x, axis, profile=None):
+    """engine.py:185-194."""
     xm = np.moveaxis(x, axis % x.ndim, -1)
     m = np.max(xm, axis=-1, keepdims=True)
     z = xm - m
     e = unary_intrinsic("exp", z)
-    s = fold_last(e)[..., None]
+    s = reduce_last_axis(e, profile)[..., None]
     y = e / s
     return {"m": m, "z": z, "e": e, "s": s, "y": np.moveaxis(y, -1, axis % x.ndim)}
 
 
-def layernorm_parts(x, axis, eps):
-    """engine.py:197-213 (sequential profile)."""
+def layernorm_parts(x, axis, eps, profile=None):
+    """engine.py:197-213."""
     xm = np.moveaxis(x, axis % x.ndim, -1)
     n = xm.shape[-1]
     inv_n = np.float32(n)
-    mu = (fold_last(xm) / inv_n)[..., None]
+    mu = (reduce_last_axis(xm, profile) / inv_n)[..., None]
     xc = xm - mu
     sq = xc * xc
-    var = (fold_last(sq) / inv_n)[..., None]
+    var = (reduce_last_axis(sq, profile) / inv_n)[..., None]
     sp = var + np.float32(eps)
     sigma = np.sqrt(sp)
     y = xc / sigma
@@ -145,8 +193,8 @@ def _parse_shape(spec) -> tuple:
     return tuple(int(t) for t in str(spec).split(",") if t != "")
 
 
-def apply_op(node, arrays, fma=False) -> np.ndarray:
-    """engine.py:220-285 under the sequential profile (FP32)."""
+def apply_op(node, arrays, fma=False, profile=None) -> np.ndarray:
+    """engine.py:220-285 (FP32) under `profile` (None: sequential)."""
     kind = node.kind
     if kind in ("add", "sub", "mul", "div"):
         a, b = arrays
@@ -161,22 +209,23 @@ def apply_op(node, arrays, fma=False) -> np.ndarray:
     if kind in ("sum", "mean"):
         axis = int(node.attr("axis", -1))
         xm = np.moveaxis(arrays[0], axis % arrays[0].ndim, -1)
-        red = fold_last(xm)
+        red = reduce_last_axis(xm, profile)
         return red if kind == "sum" else red / np.float32(xm.shape[-1])
     if kind in ("max", "min"):
         axis = int(node.attr("axis", -1))
         fn = np.max if kind == "max" else np.min
         return fn(arrays[0], axis=axis % arrays[0].ndim)
     if kind == "matmul":
-        return matmul_value(arrays[0], arrays[1], bool(node.attr("transpose_b", 0)), fma)
+        return matmul_value(arrays[0], arrays[1], bool(node.attr("transpose_b", 0)), fma,
+                            profile)
     if kind == "linear":
         x, w, b = arrays
-        return matmul_value(x, w, False, fma) + b
+        return matmul_value(x, w, False, fma, profile) + b
     if kind == "softmax":
-        return softmax_parts(arrays[0], int(node.attr("axis", -1)))["y"]
+        return softmax_parts(arrays[0], int(node.attr("axis", -1)), profile)["y"]
     if kind == "layernorm":
         return layernorm_parts(arrays[0], int(node.attr("axis", -1)),
-                               float(node.attr("eps", 1e-5)))["y"]
+                               float(node.attr("eps", 1e-5)), profile)["y"]
     if kind == "concat":
         return np.concatenate(arrays, axis=int(node.attr("axis", 0)))
     if kind == "slice":
@@ -250,10 +299,10 @@ def matmul_bound(a, b, model: FpModel, fma=False, transpose_b=False) -> np.ndarr
     return model.reduction_const(count) * (a64 @ b64)
 
 
-def softmax_bound_parts(x, axis, model: FpModel):
+def softmax_bound_parts(x, axis, model: FpModel, profile=None):
     """bounds.py:114-135."""
     x = np.asarray(x)
-    parts = softmax_parts(x, axis)
+    parts = softmax_parts(x, axis, profile)
     u = model.u
     n = parts["e"].shape[-1]
     rc = model.reduction_const(n - 1)
@@ -270,10 +319,10 @@ def softmax_bound_parts(x, axis, model: FpModel):
     return parts["y"], np.moveaxis(eps_y, -1, axis % x.ndim)
 
 
-def layernorm_bound_parts(x, axis, eps_attr, model: FpModel):
+def layernorm_bound_parts(x, axis, eps_attr, model: FpModel, profile=None):
     """bounds.py:143-169."""
     x = np.asarray(x)
-    parts = layernorm_parts(x, axis, eps_attr)
+    parts = layernorm_parts(x, axis, eps_attr, profile)
     u = model.u
     n = parts["xc"].shape[-1]
     rc = model.reduction_const(n - 1)
@@ -297,15 +346,16 @@ def layernorm_bound_parts(x, axis, eps_attr, model: FpModel):
     return parts["y"], np.moveaxis(eps_y, -1, axis % x.ndim)
 
 
-def op_bound(node, arrays, model: FpModel, fma=False):
+def op_bound(node, arrays, model: FpModel, fma=False, profile=None):
     """bounds.py:176-218 -> (y float32, eps float64)."""
     kind = node.kind
+    fma = _fma(profile, fma)
     if kind == "softmax":
-        return softmax_bound_parts(arrays[0], int(node.attr("axis", -1)), model)
+        return softmax_bound_parts(arrays[0], int(node.attr("axis", -1)), model, profile)
     if kind == "layernorm":
         return layernorm_bound_parts(arrays[0], int(node.attr("axis", -1)),
-                                     float(node.attr("eps", 1e-5)), model)
-    out = apply_op(node, arrays, fma)
+                                     float(node.attr("eps", 1e-5)), model, profile)
+    out = apply_op(node, arrays, fma, profile)
     u = model.u
     if kind in DATA_MOVEMENT_KINDS or kind in EXT_DATA_MOVEMENT_KINDS or kind in (
             "relu", "max", "min"):

@@ -46,6 +46,15 @@ class CheckResult(ctypes.Structure):
 
 CHECK_RESULT_BYTES = ctypes.sizeof(CheckResult)
 
+ORDER = {"sequential": 0, "pairwise": 1, "blocked": 2, "permuted": 3}
+
+
+class Profile(ctypes.Structure):
+    """nao_profile: a DeviceProfile's reduction order for the value kernels."""
+    _fields_ = [("order", ctypes.c_int32), ("block_size", ctypes.c_int32),
+                ("perm", ctypes.c_void_p), ("perm_n", ctypes.c_int64),
+                ("fma", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
 
 class CheckDesc(ctypes.Structure):
     """nao_check_desc: the check fused into nao_commit_check_tensors."""
@@ -83,18 +92,18 @@ _SIGS = {
     "nao_percentile_profile": (c_int, [c_vp, c_i64, ctypes.POINTER(c_dbl), c_int, c_vp, c_vp,
                                        c_sz, c_vp]),
     "nao_softmax_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_dbl, c_dbl, c_dbl,
-                                  c_vp]),
+                                  ctypes.POINTER(Profile), c_vp]),
     "nao_layernorm_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, ctypes.c_float,
-                                    c_dbl, c_dbl, c_dbl, c_vp]),
+                                    c_dbl, c_dbl, c_dbl, ctypes.POINTER(Profile), c_vp]),
     "nao_reduce_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_int, c_dbl, c_dbl,
-                                 c_dbl, c_vp]),
+                                 c_dbl, ctypes.POINTER(Profile), c_vp]),
     "nao_unary_fp64": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
     "nao_scaled_abs_bound": (c_int, [c_vp, c_vp, c_int, c_i64, c_dbl, c_vp]),
     "nao_abs_gemm_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64,
                                    c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_dbl, c_vp, c_dbl,
                                    c_dbl, c_int, c_vp]),
     "nao_matmul_profile": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
-                                   c_i64, c_i64, c_i64, c_int, c_int, c_vp]),
+                                   c_i64, c_i64, c_i64, c_int, ctypes.POINTER(Profile), c_vp]),
     "nao_tf32_split_cols": (c_i64, [c_i64]),
     "nao_abs_gemm_tc_kchunk": (c_int, []),
     "nao_tf32_split": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_vp]),

@@ -27,7 +27,7 @@ import torch
 
 from . import _lib
 from .engine import (ExecutionError, fma_of, matmul_value, parse_shape_attr, relu,
-                     require_supported, to_device, unary, _batch_view)
+                     profile_arg, require_supported, to_device, unary, _batch_view)
 from .graph import DATA_MOVEMENT_KINDS, parse_ref
 from .tensor import Tensor
 
@@ -257,18 +257,20 @@ def _rows_last(x: torch.Tensor, axis: int):
     return xm, ax, rows, n
 
 
-def softmax_device(x: torch.Tensor, axis: int, model: FpModel, eps_f64=True):
+def softmax_device(x: torch.Tensor, axis: int, model: FpModel, eps_f64=True, profile=None):
     xm, ax, rows, n = _rows_last(x, axis)
     if n == 0:
         raise ValueError("cannot reduce an empty axis")
     y = torch.empty_like(xm)
     eps = _eps_buffer(xm.shape, x.device, eps_f64)
     _lib.call("nao_softmax_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64), rows,
-              n, model.u, model.reduction_const(n - 1), sum_slack(n), _lib.stream_ptr(x.device))
+              n, model.u, model.reduction_const(n - 1), sum_slack(n),
+              profile_arg(profile, n, x.device), _lib.stream_ptr(x.device))
     return y.movedim(-1, ax), eps.movedim(-1, ax)
 
 
-def layernorm_device(x: torch.Tensor, axis: int, ln_eps: float, model: FpModel, eps_f64=True):
+def layernorm_device(x: torch.Tensor, axis: int, ln_eps: float, model: FpModel, eps_f64=True,
+                     profile=None):
     xm, ax, rows, n = _rows_last(x, axis)
     if n == 0:
         raise ValueError("cannot reduce an empty axis")
@@ -276,14 +278,15 @@ def layernorm_device(x: torch.Tensor, axis: int, ln_eps: float, model: FpModel, 
     eps = _eps_buffer(xm.shape, x.device, eps_f64)
     _lib.call("nao_layernorm_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64),
               rows, n, float(np.float32(ln_eps)), model.u, model.reduction_const(n - 1),
-              sum_slack(n), _lib.stream_ptr(x.device))
+              sum_slack(n), profile_arg(profile, n, x.device), _lib.stream_ptr(x.device))
     return y.movedim(-1, ax), eps.movedim(-1, ax)
 
 
 _RED = {"sum": _lib.RED_SUM, "mean": _lib.RED_MEAN, "max": _lib.RED_MAX, "min": _lib.RED_MIN}
 
 
-def reduce_device(kind: str, x: torch.Tensor, axis: int, model: FpModel, eps_f64=True):
+def reduce_device(kind: str, x: torch.Tensor, axis: int, model: FpModel, eps_f64=True,
+                  profile=None):
     xm, ax, rows, n = _rows_last(x, axis)
     if n == 0:
         raise ValueError("cannot reduce an empty axis")
@@ -291,7 +294,7 @@ def reduce_device(kind: str, x: torch.Tensor, axis: int, model: FpModel, eps_f64
     eps = _eps_buffer(xm.shape[:-1], x.device, eps_f64)
     _lib.call("nao_reduce_bound", xm.data_ptr(), y.data_ptr(), eps.data_ptr(), int(eps_f64), rows,
               n, _RED[kind], model.u, model.reduction_const(n - 1), sum_slack(n),
-              _lib.stream_ptr(x.device))
+              profile_arg(profile, n, x.device), _lib.stream_ptr(x.device))
     return y, eps
 
 
@@ -326,7 +329,7 @@ def softmax_bound_parts(x, axis, model: FpModel, profile=None):
     """bounds.py:114-135 -> (y float32, eps float64) on the original axis layout."""
     require_supported(profile)
     host = not isinstance(x, torch.Tensor)
-    y, eps = softmax_device(to_device(x), int(axis), model)
+    y, eps = softmax_device(to_device(x), int(axis), model, profile=profile)
     return _to_host_pair(y, eps) if host else (y, eps)
 
 
@@ -339,7 +342,7 @@ def layernorm_bound_parts(x, axis, eps_attr, model: FpModel, profile=None):
     """bounds.py:143-169."""
     require_supported(profile)
     host = not isinstance(x, torch.Tensor)
-    y, eps = layernorm_device(to_device(x), int(axis), float(eps_attr), model)
+    y, eps = layernorm_device(to_device(x), int(axis), float(eps_attr), model, profile=profile)
     return _to_host_pair(y, eps) if host else (y, eps)
 
 
@@ -408,14 +411,14 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
     u = model.u
     if kind == "softmax":
         require_supported(profile)
-        return softmax_device(xs[0], int(node.attr("axis", -1)), model, f64)
+        return softmax_device(xs[0], int(node.attr("axis", -1)), model, f64, profile)
     if kind == "layernorm":
         require_supported(profile)
         return layernorm_device(xs[0], int(node.attr("axis", -1)), float(node.attr("eps", 1e-5)),
-                                model, f64)
+                                model, f64, profile)
     if kind in ("sum", "mean", "max", "min"):
         require_supported(profile)
-        y, eps = reduce_device(kind, xs[0], int(node.attr("axis", -1)), model, f64)
+        y, eps = reduce_device(kind, xs[0], int(node.attr("axis", -1)), model, f64, profile)
         if lazy and kind in ("max", "min"):
             return y, ("zero",)
         return y, eps

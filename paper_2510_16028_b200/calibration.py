@@ -209,12 +209,12 @@ def calibrate(g, dataset, profiles, grid=PERCENTILE_GRID, epsilon: float = DEFAU
     def value(node, xs, prof):
         k = node.kind
         if k == "softmax":
-            return softmax_device(xs[0], int(node.attr("axis", -1)), model, False)[0]
+            return softmax_device(xs[0], int(node.attr("axis", -1)), model, False, prof)[0]
         if k == "layernorm":
             return layernorm_device(xs[0], int(node.attr("axis", -1)),
-                                    float(node.attr("eps", 1e-5)), model, False)[0]
+                                    float(node.attr("eps", 1e-5)), model, False, prof)[0]
         if k in ("sum", "mean", "max", "min"):
-            return reduce_device(k, xs[0], int(node.attr("axis", -1)), model, False)[0]
+            return reduce_device(k, xs[0], int(node.attr("axis", -1)), model, False, prof)[0]
         return apply_value(node, xs, prof)
 
     for sample in dataset:

@@ -14,6 +14,7 @@
 // the bit-exact profile mode: products rounded to FP32, left fold over k (or
 // the FP64-fma emulation of the "+fma" profiles).
 #include "common.cuh"
+#include "profile_fold.cuh"
 
 namespace nao {
 
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(256, 1) k_absgemm_ffma(const __grid_constant__
 __global__ void k_matmul_seq(const float* __restrict__ A, const float* __restrict__ B,
                              float* __restrict__ C, int64_t M, int64_t N, int64_t K, int64_t lda,
                              int64_t ldb, int64_t sA, int64_t sB, int64_t sC, int transpose_b,
-                             int fma) {
+                             int fma, const Prof prof) {
     const int64_t b = blockIdx.z;
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = (int64_t)blockIdx.y;
@@ -147,6 +148,15 @@ __global__ void k_matmul_seq(const float* __restrict__ A, const float* __restric
     const float* a = A + b * sA + m * lda;
     const float* bp = B + b * sB;
     float acc = 0.f;
+    if (!fma && prof.order != NAO_ORDER_SEQUENTIAL) {
+        // FP32 products (rounded) reduced over K in the profile's order
+        auto at = [&](int64_t k) {
+            const float bv = transpose_b ? __ldg(bp + n * ldb + k) : __ldg(bp + k * ldb + n);
+            return __fmul_rn(__ldg(a + k), bv);
+        };
+        C[b * sC + m * N + n] = fold_profile(at, K, prof);
+        return;
+    }
     for (int64_t k = 0; k < K; k++) {
         const float bv = transpose_b ? __ldg(bp + n * ldb + k) : __ldg(bp + k * ldb + n);
         const float av = __ldg(a + k);
@@ -193,15 +203,18 @@ int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, i
 
 int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, int64_t M,
                        int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t stride_a,
-                       int64_t stride_b, int64_t stride_c, int transpose_b, int fma,
-                       void* stream) {
+                       int64_t stride_b, int64_t stride_c, int transpose_b,
+                       const nao_profile* profile, void* stream) {
+    const int fma = profile ? profile->fma : 0;
     NAO_REQUIRE(A && B && C, "matmul: null pointer");
     NAO_REQUIRE(K >= 1, "cannot reduce an empty axis");
     if (batch == 0 || M == 0 || N == 0) return NAO_OK;
     NAO_REQUIRE(M <= 65535 && batch <= 65535, "matmul_profile: shape too large");
+    if (!fma) NAO_CHECK_PROFILE(profile, K);
     dim3 grid((unsigned)ceil_div(N, 128), (unsigned)M, (unsigned)batch);
     k_matmul_seq<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        A, B, C, M, N, K, lda, ldb, stride_a, stride_b, stride_c, transpose_b, fma);
+        A, B, C, M, N, K, lda, ldb, stride_a, stride_b, stride_c, transpose_b, fma,
+        make_prof(profile));
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

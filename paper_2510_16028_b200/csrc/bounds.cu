@@ -13,6 +13,7 @@
 // folds its own row left to right -- 32 independent sequential folds per warp.
 #include <cmath>
 #include "common.cuh"
+#include "profile_fold.cuh"
 
 namespace nao {
 
@@ -327,6 +328,9 @@ static int row_grid(int64_t rows) { return (int)ceil_div(rows, 32 * kRowWarps); 
 namespace nao { namespace rowb {
 static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                   int kind, float ln_eps, double u, double rc, double slack, cudaStream_t st);
+static int launch_profile(const float* x, float* y, void* eps, int eps_f64, int64_t rows,
+                          int64_t n, int kind, float ln_eps, double u, double rc, double slack,
+                          const Prof& prof, cudaStream_t st);
 static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                      double u, double rc, double slack, cudaStream_t st);
 } }
@@ -336,10 +340,15 @@ using namespace nao;
 extern "C" {
 
 int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                      double u, double rc, double slack, void* stream) {
+                      double u, double rc, double slack, const nao_profile* profile,
+                      void* stream) {
     NAO_REQUIRE(rows >= 0 && n > 0, "softmax: cannot reduce an empty axis");
     NAO_REQUIRE(x && y && eps, "softmax: null pointer");
+    NAO_CHECK_PROFILE(profile, n);
     if (rows == 0) return NAO_OK;
+    if (profile && profile->order != NAO_ORDER_SEQUENTIAL)
+        return rowb::launch_profile(x, y, eps, eps_f64, rows, n, 0, 0.f, u, rc, slack,
+                                    make_prof(profile), static_cast<cudaStream_t>(stream));
     {
         int rc_c = rowb::softmax_c(x, y, eps, eps_f64, rows, n, u, rc, slack,
                                    static_cast<cudaStream_t>(stream));
@@ -355,10 +364,15 @@ int nao_softmax_bound(const float* x, float* y, void* eps, int eps_f64, int64_t 
 }
 
 int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                        float ln_eps, double u, double rc, double slack, void* stream) {
+                        float ln_eps, double u, double rc, double slack,
+                        const nao_profile* profile, void* stream) {
     NAO_REQUIRE(rows >= 0 && n > 0, "layernorm: cannot reduce an empty axis");
     NAO_REQUIRE(x && y && eps, "layernorm: null pointer");
+    NAO_CHECK_PROFILE(profile, n);
     if (rows == 0) return NAO_OK;
+    if (profile && profile->order != NAO_ORDER_SEQUENTIAL)
+        return rowb::launch_profile(x, y, eps, eps_f64, rows, n, 1, ln_eps, u, rc, slack,
+                                    make_prof(profile), static_cast<cudaStream_t>(stream));
     {
         int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 1, ln_eps, u, rc, slack,
                                 static_cast<cudaStream_t>(stream));
@@ -371,10 +385,15 @@ int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_
 }
 
 int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
-                     int kind, double u, double rc, double slack, void* stream) {
+                     int kind, double u, double rc, double slack, const nao_profile* profile,
+                     void* stream) {
     NAO_REQUIRE(rows >= 0 && n > 0, "cannot reduce an empty axis");
     NAO_REQUIRE(kind >= NAO_RED_SUM && kind <= NAO_RED_MIN, "bad reduce kind %d", kind);
+    NAO_CHECK_PROFILE(profile, n);
     if (rows == 0) return NAO_OK;
+    if (profile && profile->order != NAO_ORDER_SEQUENTIAL && kind <= NAO_RED_MEAN)
+        return rowb::launch_profile(x, y, eps, eps_f64, rows, n, 2 + kind, 0.f, u, rc, slack,
+                                    make_prof(profile), static_cast<cudaStream_t>(stream));
     {
         int rc_b = rowb::launch(x, y, eps, eps_f64, rows, n, 2 + kind, 0.f, u, rc, slack,
                                 static_cast<cudaStream_t>(stream));
@@ -490,7 +509,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // kind: 0 softmax, 1 layernorm, 2 sum, 3 mean, 4 max, 5 min
 __global__ void __launch_bounds__(kThreads) k_rows_smem(
     const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
-    int64_t rows, int64_t n, int R, int kind, float ln_eps, double u, double rc, double slack) {
+    int64_t rows, int64_t n, int R, int kind, float ln_eps, double u, double rc, double slack,
+    const Prof prof) {
     extern __shared__ __align__(16) float sx[];       // [R][n] x, then [R][n] e (softmax)
     __shared__ double red[kThreads / 32];
     __shared__ float s_a[32], s_b[32];                // per-row FP32 scalars
@@ -556,7 +576,22 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
     }
     __syncthreads();
     // serial profile folds: thread r owns row r
-    if (threadIdx.x < nr) {
+    if (threadIdx.x < nr && prof.order != NAO_ORDER_SEQUENTIAL) {
+        // another device profile's order (engine.py:95-113): generic fold
+        const int r = threadIdx.x;
+        const float* row = (kind == 0 ? se : sx) + (size_t)r * n;
+        const float acc = fold_profile([&](int64_t k) { return row[k]; }, n, prof);
+        if (kind == 1) {  // mu, then the profile fold over sq = (x - mu)^2
+            const float mu = __fdiv_rn(acc, (float)n);
+            s_a[r] = mu;
+            s_b[r] = fold_profile([&](int64_t k) {
+                const float xc = __fsub_rn(row[k], mu);
+                return __fmul_rn(xc, xc);
+            }, n, prof);
+        } else {
+            s_a[r] = acc;
+        }
+    } else if (threadIdx.x < nr) {
         const int r = threadIdx.x;
         const float* row = (kind == 0 ? se : sx) + (size_t)r * n;
         float acc = row[0];
@@ -917,7 +952,33 @@ static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows
         attr = true;
     }
     k_rows_smem<<<(unsigned)ceil_div(rows, R), kThreads, smem, st>>>(x, y, eps, eps_f64, rows, n, R,
-                                                                     kind, ln_eps, u, rc, slack);
+                                                                     kind, ln_eps, u, rc, slack,
+                                                                     Prof{NAO_ORDER_SEQUENTIAL, 32,
+                                                                          nullptr});
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
+// Non-sequential device profiles: always the shared-memory row kernel (the
+// fold thread walks the staged row in the profile's order).
+static int launch_profile(const float* x, float* y, void* eps, int eps_f64, int64_t rows,
+                          int64_t n, int kind, float ln_eps, double u, double rc, double slack,
+                          const Prof& prof, cudaStream_t st) {
+    const int64_t per_row = (kind == 0 ? 2 : 1) * n * 4;
+    NAO_REQUIRE(per_row <= 96 * 1024, "profile-order emulation supports rows of up to %lld "
+                "elements", (long long)(96 * 1024 / (kind == 0 ? 8 : 4)));
+    int64_t R = (96 * 1024) / per_row;
+    if (R > 32) R = 32;
+    while (R > 1 && ceil_div(rows, R) < 2 * kNumSMs) R >>= 1;
+    static bool attr = false;
+    if (!attr) {
+        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            200 * 1024));
+        attr = true;
+    }
+    const size_t smem = (size_t)(kind == 0 ? 2 : 1) * R * n * 4;
+    k_rows_smem<<<(unsigned)ceil_div(rows, R), kThreads, smem, st>>>(
+        x, y, eps, eps_f64, rows, n, (int)R, kind, ln_eps, u, rc, slack, prof);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

@@ -8,12 +8,15 @@ This B200 build executes
     nao_matmul_profile, softmax/layernorm/sum/mean via the fused bound kernels);
   * "native": GEMMs on cuBLAS FP32 (TF32 off), the production forward whose
     values are *not* any simulated profile (the B200 is its own device).
-Other reduction orders (pairwise / blocked / permuted) are SURVEY.md 8(f)
-row 3 ("next") and raise NotImplementedError.
+  * "pairwise" / "blocked" / "permuted": the same
+    kernels fold in that profile's order (csrc/profile_fold.cuh), bit-exact
+    with the reference (tests/golden/ref_profiles.npz); the permuted order's
+    Philox permutation is computed on the host exactly as engine.py:75-77.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -72,10 +75,41 @@ class ExecutionError(RuntimeError):
 
 def require_supported(profile) -> str:
     red = "sequential" if profile is None else profile.reduction
-    if red not in ("sequential", "native"):
-        raise NotImplementedError(
-            f"reduction order {red!r} is not emulated on the B200 path yet (SURVEY.md 8(f) row 3)")
+    if red not in REDUCTIONS:
+        raise ValueError(f"unknown reduction strategy {red!r}")
     return red
+
+
+_PERMS: dict = {}
+
+
+def permutation_device(seed: int, n: int, device) -> torch.Tensor:
+    """engine.py:75-77: the permuted profile's order (numpy Philox, computed
+    once per (seed, n) on the host -- it is data independent -- and kept on the
+    device as int64)."""
+    dev = torch.device(device)
+    key = (int(seed), int(n), dev.index)
+    t = _PERMS.get(key)
+    if t is None:
+        gen = np.random.Generator(np.random.Philox(key=int(seed), counter=int(n) << 128))
+        t = torch.from_numpy(gen.permutation(int(n)).astype(np.int64)).to(dev)
+        _PERMS[key] = t
+    return t
+
+
+def profile_arg(profile, n: int, device):
+    """ctypes nao_profile* for a DeviceProfile reducing length n (None for
+    sequential without fma and for the native profile)."""
+    if profile is None or profile.reduction == "native":
+        return None
+    if profile.reduction == "sequential" and not profile.fma:
+        return None
+    p = _lib.Profile(_lib.ORDER[profile.reduction], int(profile.block_size), None, 0,
+                     int(bool(profile.fma)), 0)
+    if profile.reduction == "permuted":
+        perm = permutation_device(profile.perm_seed, n, device)
+        p.perm, p.perm_n = perm.data_ptr(), int(n)
+    return ctypes.pointer(p)
 
 
 def fma_of(profile) -> bool:
@@ -141,7 +175,7 @@ def matmul_value(a: torch.Tensor, b: torch.Tensor, profile, transpose_b=False) -
     out = torch.empty(out_shape, dtype=torch.float32, device=a.device)
     ldb = K if transpose_b else N
     _lib.call("nao_matmul_profile", a3.data_ptr(), b3.data_ptr(), out.data_ptr(), nb, M, N, K, K,
-              ldb, sa, sb, M * N, int(transpose_b), int(fma_of(profile)),
+              ldb, sa, sb, M * N, int(transpose_b), profile_arg(profile, K, a.device),
               _lib.stream_ptr(a.device))
     return out
 
