@@ -82,6 +82,15 @@ def inject_drift(y: torch.Tensor, seed: int, period: int = 16, fault_scale: floa
     return out
 
 
+def _materialise_eps(eps, y: torch.Tensor) -> torch.Tensor:
+    """FP64 bound tensor of a node for a bound dump (lazy templates expanded)."""
+    if isinstance(eps, tuple):
+        if eps[0] == "scaled":
+            return torch.abs(y.double()) * float(eps[1])
+        return torch.zeros(y.shape, dtype=torch.float64, device=y.device)
+    return eps.double().reshape(y.shape)
+
+
 class _RunState:
     """Carry-over between the stream segments of one run."""
 
@@ -177,6 +186,10 @@ class StreamingVerifier:
         # (nao_commit_check_tensors: the ALU-bound Keccak hides its HBM read);
         # False: a separate nao_check launch per node on its own side stream
         self.fuse_check = bool(fuse_check)
+        # optional streaming dumps (traceio.TraceWriter / BoundWriter): the claimed
+        # trace and the bounds leave the device on a copy stream as nodes finish
+        self.trace_writer = None
+        self.bound_writer = None
         self._specs = None  # (device blob, {node index: byte offset}) of verdict specs
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
@@ -318,6 +331,10 @@ class StreamingVerifier:
                                      node_index=node.index, node_name=node.name) from exc
             y = y.contiguous()
             yc = claimed_fn(node, y)
+            if self.trace_writer is not None:
+                self.trace_writer.write(node.index, yc)
+            if self.bound_writer is not None:
+                self.bound_writer.write(node.index, _materialise_eps(eps, y))
             tau_a, tau_r = self._taus(node.name)
             kind, eps_ptr, scale, lo_f = _lib.EPS_ZERO, None, 0.0, 1.0
             if isinstance(eps, tuple):
