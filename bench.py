@@ -182,7 +182,16 @@ def run_ours(args):
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
                            chunk_bytes=args.chunk, fuse_check=not args.separate_check)
 
+    harness_ev = []  # (start, end) events around the proposer harness (serial pass only)
+
     def claimed_fn(node, y):
+        if harness_ev is not None and _lib._timer is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = drift_claim(node, y, 1, args.drift_period, fault)
+            e1.record()
+            harness_ev.append((e0, e1))
+            return out
         return drift_claim(node, y, 1, args.drift_period, fault)
 
     ids_dev = None  # the graphs' static input buffer (refilled in place for e2e)
@@ -292,6 +301,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     _lib.set_timer(timers, units, stream)
     t_serial = timed(verified_step, 1)
+    harness_ms = sum(a.elapsed_time(b) for a, b in harness_ev)
     _lib.set_timer(None, None, None)
     sv.overlap, (sv._s_chk, sv._s_com) = True, keep
     if gv is not None:
@@ -468,6 +478,10 @@ def run_ours(args):
                    "l2": "inputs/weights (32.8 GB) far larger than L2 (126 MB)"},
         "plain_fwd_ms": round(t_plain, 2), "verified_fwd_ms": round(t_ver, 2),
         "host_enqueue_ms": {k: round(v, 2) for k, v in host_ms.items()},
+        # the proposer harness (claimed trace: +-1-ulp drift on reduction nodes,
+        # copies of deterministic ones) runs inside the timed region and is
+        # counted against us; this is its serial share
+        "proposer_harness_ms": round(harness_ms, 2),
         "merkle_gbs": round(merkle_gbs, 1) if merkle_gbs else None,
         "committed_gb_per_step": round(commit_bytes_per_step / 1e9, 2),
         "gemm_tflop_per_step": round(stats.gemm_flops / 1e12, 2),

@@ -127,6 +127,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// One lane of a converged warp (the lowest): the MMA issuer loops run on the
+// whole warp so descriptors / TMEM addresses stay in uniform registers, and
+// only the tcgen05.mma / commit instructions are issued by the elected lane
+// (an `if (lane == 0)` issuer costs ~20 R2UR/ELECT instructions per MMA).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+                 : "=r"(p));
+    return p != 0;
+}
 __device__ __forceinline__ void fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -388,23 +398,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tma_load_3d(st + 3 * TILE_BYTES, &map_blo, &full[s], kb * KBE, n0, zb);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t acc1 = tmem + 2 * BN;
-            for (int kb = 0; kb < nkb; kb++) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                const int chunk = kb / KCHUNK_KB, buf = chunk & 1;
-                const bool first = (kb % KCHUNK_KB) == 0;
-                if (first) mbar_wait(&tempty[buf], ((chunk >> 1) & 1) ^ 1);
+    } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t acc1 = tmem + 2 * BN;
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            const int chunk = kb / KCHUNK_KB, buf = chunk & 1;
+            const bool first = (kb % KCHUNK_KB) == 0;
+            if (first) mbar_wait(&tempty[buf], ((chunk >> 1) & 1) ^ 1);
 #ifdef NAO_TC_NOWAIT  // timing probe only (wrong results): MMA rate without the TMA feed
-                if (kb < STAGES) mbar_wait(&full[s], ph);
+            if (kb < STAGES) mbar_wait(&full[s], ph);
 #else
-                mbar_wait(&full[s], ph);
+            mbar_wait(&full[s], ph);
 #endif
-                fence_after();
-                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
-                const uint32_t acc0 = tmem + buf * BN;
+            fence_after();
+            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t acc0 = tmem + buf * BN;
+            if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < BK / 8; j++) {
                     const uint64_t ahi = make_desc(st + j * 32);
@@ -418,8 +428,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 umma_commit(&empty[s]);
                 if ((kb % KCHUNK_KB) == KCHUNK_KB - 1 || kb == nkb - 1) umma_commit(&tfull[buf]);
             }
-            umma_commit(acc1_full);
+            __syncwarp();
         }
+        if (elect_one()) umma_commit(acc1_full);
+        __syncwarp();
     } else if (warp >= 4) {  // ---------------- epilogue
         const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
@@ -557,20 +569,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            int kg = 0, i = 0;
-            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, i++) {
-                const int slot = i & 1;
-                mbar_wait(&tempty[slot], ((i >> 1) & 1) ^ 1);
+    } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        int kg = 0, i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, i++) {
+            const int slot = i & 1;
+            mbar_wait(&tempty[slot], ((i >> 1) & 1) ^ 1);
+            fence_after();
+            const uint32_t acc0 = tmem + slot * 256, acc1 = acc0 + BN;
+            for (int kb = 0; kb < nkb; kb++, kg++) {
+                const int s = kg % shortk::STAGES;
+                const uint32_t ph = (kg / shortk::STAGES) & 1;
+                mbar_wait(&full[s], ph);
                 fence_after();
-                const uint32_t acc0 = tmem + slot * 256, acc1 = acc0 + BN;
-                for (int kb = 0; kb < nkb; kb++, kg++) {
-                    const int s = kg % shortk::STAGES;
-                    const uint32_t ph = (kg / shortk::STAGES) & 1;
-                    mbar_wait(&full[s], ph);
-                    fence_after();
-                    const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                if (elect_one()) {
 #pragma unroll
                     for (int j = 0; j < BK / 8; j++) {
                         const uint64_t ahi = make_desc(st + j * 32);
@@ -584,8 +596,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                     umma_commit(&empty[s]);
                 }
-                umma_commit(&tfull[slot]);
+                __syncwarp();
             }
+            if (elect_one()) umma_commit(&tfull[slot]);
+            __syncwarp();
         }
     } else if (warp >= 4) {  // ---------------- epilogue
         const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
@@ -710,6 +724,8 @@ constexpr uint32_t TMEM_COLS = 512;
 // kind::tf32, D=F32, K-major A/B, N=128, M=256 (cta_group::2)
 constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t kIdesc2F16 = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                ((uint32_t)(256 >> 4) << 24);
 }  // namespace pair
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -767,6 +783,22 @@ __device__ __forceinline__ void umma_tf32_pair(uint32_t d_tmem, uint64_t adesc, 
         : "memory");
 }
 
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+template <int FMT>
+__device__ __forceinline__ void umma_pair_fmt(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+    if constexpr (FMT == kFmtF16) umma_f16_pair(d, a, b, pair::kIdesc2F16, acc);
+    else umma_tf32_pair(d, a, b, pair::kIdesc2, acc);
+}
+
+template <int FMT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1)
     k_absgemm_tc2(const __grid_constant__ CUtensorMap map_ahi,
                   const __grid_constant__ CUtensorMap map_alo,
@@ -831,10 +863,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1
                 uint8_t* st = smem + s * pair::STAGE_BYTES;
                 const uint32_t fb = mapa_rank(smem_u32(&full[s]), 0);
                 if (leader) mbar_expect_tx(&full[s], 2 * pair::STAGE_BYTES);
-                tma_load_3d_pair(st, &map_ahi, fb, kb * pair::BK, m0, za);
-                tma_load_3d_pair(st + pair::A_BYTES, &map_alo, fb, kb * pair::BK, m0, za);
-                tma_load_3d_pair(st + 2 * pair::A_BYTES, &map_bhi, fb, kb * pair::BK, nb, zb);
-                tma_load_3d_pair(st + 2 * pair::A_BYTES + pair::B_BYTES, &map_blo, fb, kb * pair::BK, nb, zb);
+                constexpr int KBE = FmtK<FMT>::kb;
+                tma_load_3d_pair(st, &map_ahi, fb, kb * KBE, m0, za);
+                tma_load_3d_pair(st + pair::A_BYTES, &map_alo, fb, kb * KBE, m0, za);
+                tma_load_3d_pair(st + 2 * pair::A_BYTES, &map_bhi, fb, kb * KBE, nb, zb);
+                tma_load_3d_pair(st + 2 * pair::A_BYTES + pair::B_BYTES, &map_blo, fb, kb * KBE, nb, zb);
             }
         }
     } else if (warp == 1) {
@@ -856,9 +889,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1
                     const uint64_t alo = make_desc(st + pair::A_BYTES + j * 32);
                     const uint64_t bhi = make_desc(st + 2 * pair::A_BYTES + j * 32);
                     const uint64_t blo = make_desc(st + 2 * pair::A_BYTES + pair::B_BYTES + j * 32);
-                    umma_tf32_pair(acc0, ahi, bhi, pair::kIdesc2, (first && j == 0) ? 0u : 1u);
-                    umma_tf32_pair(acc1, ahi, blo, pair::kIdesc2, (kb == 0 && j == 0) ? 0u : 1u);
-                    umma_tf32_pair(acc1, alo, bhi, pair::kIdesc2, 1u);
+                    umma_pair_fmt<FMT>(acc0, ahi, bhi, (first && j == 0) ? 0u : 1u);
+                    umma_pair_fmt<FMT>(acc1, ahi, blo, (kb == 0 && j == 0) ? 0u : 1u);
+                    umma_pair_fmt<FMT>(acc1, alo, bhi, 1u);
                 }
                 umma_commit_pair(&empty[s]);
                 if ((kb % pair::KCHUNK_KB) == pair::KCHUNK_KB - 1 || kb == nkb - 1) umma_commit_pair(&tfull[buf]);
@@ -896,7 +929,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::NUM_THREADS, 1
         fence_after();
         const uint32_t col1 = tmem + lane_addr + 2 * pair::BN + half * 64;
         double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
-        tile_epilogue<kFmtTF32>(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+        tile_epilogue<FMT>(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
     }
     fence_before();
     cluster_sync_all();
@@ -1325,7 +1358,7 @@ static int launch_tc(const void* a_hi, const void* a_lo, const int32_t* a_exp, c
                 "abs-gemm tc: grid too large");
     const int64_t Kp = FMT == kFmtF16 ? (K + 7) / 8 * 8 : (K + 3) / 4 * 4;
     const int bk = FMT == kFmtF16 ? 32 : BK;  // elements per 64-byte k-block
-    const bool use_pair = FMT == kFmtTF32 && tc_use_pair();
+    const bool use_pair = FMT == kFmtTF32 && tc_use_pair();  // pair: TF32 only (slower, kept for A/B)
     CUtensorMap mah, mal, mbh, mbl;
     int rc;
     const int b_box = use_pair ? pair::BNH : BN;
@@ -1385,15 +1418,15 @@ static int launch_tc(const void* a_hi, const void* a_lo, const int32_t* a_exp, c
     } else if (use_pair) {
         static bool attr2_set = false;
         if (!attr2_set) {
-            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc2,
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc2<FMT>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 pair::SMEM_BYTES));
             attr2_set = true;
         }
         dim3 grid2((unsigned)(2 * ceil_div(N, pair::BN) * ceil_div(M, 2 * pair::BM)), 1,
                    (unsigned)batch);
-        k_absgemm_tc2<<<grid2, pair::NUM_THREADS, pair::SMEM_BYTES, stream>>>(mah, mal, mbh, mbl,
-                                                                             g);
+        k_absgemm_tc2<FMT><<<grid2, pair::NUM_THREADS, pair::SMEM_BYTES, stream>>>(mah, mal, mbh,
+                                                                                  mbl, g);
         NAO_CHECK_LAUNCH();
     } else {
     static bool attr_set = false;
