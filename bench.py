@@ -145,6 +145,8 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.main_priority:
+        torch.cuda.set_stream(torch.cuda.Stream(dev, priority=args.main_priority))
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -180,7 +182,8 @@ def run_ours(args):
 
     fault = args.fault_node
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
-                           chunk_bytes=args.chunk, fuse_check=not args.separate_check)
+                           chunk_bytes=args.chunk, fuse_check=not args.separate_check,
+                           max_lag=args.max_lag)
 
     harness_ev = []  # (start, end) events around the proposer harness (serial pass only)
 
@@ -635,6 +638,11 @@ def main(argv=None):
     ap.add_argument("--calib-samples", type=int, default=4)
     ap.add_argument("--debug-exceed", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--main-priority", type=int, default=-1,
+                    help="run both arms on a stream of this priority (negative = higher than "
+                         "the verifier's side streams)")
+    ap.add_argument("--max-lag", type=int, default=4,
+                    help="main waits for commit flush k-LAG (bounded side-stream lag)")
     ap.add_argument("--separate-check", action="store_true",
                     help="standalone nao_check per node instead of the check fused into commit")
     ap.add_argument("--graphs", type=int, default=0, metavar="SEG",

@@ -170,7 +170,8 @@ class StreamingVerifier:
     def __init__(self, graph, model: FpModel | None = None, profile=NATIVE, thresholds=None,
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
-                 grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True):
+                 grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
+                 max_lag: int = 0):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -190,6 +191,11 @@ class StreamingVerifier:
         # trace and the bounds leave the device on a copy stream as nodes finish
         self.trace_writer = None
         self.bound_writer = None
+        # max_lag > 0: the main stream waits for commit flush k - max_lag before
+        # issuing more work (bounds the claimed / local tensors pinned by a
+        # side stream that runs behind, e.g. under a high-priority main stream)
+        self.max_lag = int(max_lag)
+        self._com_events = []
         self._specs = None  # (device blob, {node index: byte offset}) of verdict specs
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
@@ -308,6 +314,12 @@ class StreamingVerifier:
                 side_use(t, s_com)
             if self.overlap and capturing:
                 keep.append(r)
+            if self.overlap and self.max_lag > 0 and not capturing:
+                ev = torch.cuda.Event()
+                ev.record(s_com)
+                self._com_events.append(ev)
+                if len(self._com_events) > self.max_lag:
+                    main.wait_event(self._com_events.pop(0))
             st.pending, st.pend_idx, st.pend_bytes = [], [], 0
             st.pend_checks, st.pend_keep = [], []
 
