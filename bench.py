@@ -485,6 +485,8 @@ def run_ours(args):
         # copies of deterministic ones) runs inside the timed region and is
         # counted against us; this is its serial share
         "proposer_harness_ms": round(harness_ms, 2),
+        # approximate: overhead with the proposer's serial share removed
+        "overhead_excl_proposer_pct": round(100.0 * (t_ver - harness_ms - t_plain) / t_plain, 2),
         "merkle_gbs": round(merkle_gbs, 1) if merkle_gbs else None,
         "committed_gb_per_step": round(commit_bytes_per_step / 1e9, 2),
         "gemm_tflop_per_step": round(stats.gemm_flops / 1e12, 2),
