@@ -24,6 +24,7 @@ namespace nao {
 
 constexpr int kMaxSegs = 128;
 constexpr int kTreeThreads = 256;  // a CTA folds up to 512 nodes
+constexpr uint64_t kFlatLevelMin = 1u << 16;  // live nodes from which levels run flat
 
 struct ChunkTable {
     int n;
@@ -481,6 +482,29 @@ __global__ void __launch_bounds__(kTreeThreads) k_tree_reduce(const __grid_const
     }
 }
 
+// One tree level for many segments at once, one parent hash per thread (the
+// large lower levels: every lane busy; k_tree_reduce takes over once the
+// levels are small).  parent j of a segment = H(0x01 || in[2j] || in[2j+1]),
+// an odd last node pairing with itself (commitments.py:119-127).
+template <int ALG>
+__global__ void __launch_bounds__(128) k_tree_level(const __grid_constant__ TreeTable tab,
+                                                   const uint32_t* __restrict__ in,
+                                                   uint32_t* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= tab.group_prefix[tab.n]) return;
+    const int s = find_seg(tab.group_prefix, tab.n, t);
+    const uint64_t j = t - tab.group_prefix[s];
+    const uint64_t a = 2 * j, b = (2 * j + 1 < tab.n_in[s]) ? 2 * j + 1 : 2 * j;
+    const uint4* pa = reinterpret_cast<const uint4*>(in + 8 * (tab.in_index[s] + a));
+    const uint4* pb = reinterpret_cast<const uint4*>(in + 8 * (tab.in_index[s] + b));
+    const uint4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1);
+    const uint32_t L[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const uint32_t R[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t res[8];
+    hash_node<ALG>(L, R, res);
+    store_digest(out + 8 * (tab.out_index[s] + j), res);
+}
+
 // ----------------------------------------------------------------- host side
 
 static int launch_chunk_leaves(int alg, ChunkTable& tab, uint32_t* digests, cudaStream_t st) {
@@ -529,21 +553,25 @@ static int reduce_trees(int alg, int nseg, const uint64_t* in_index, const uint6
                                            cudaMemcpyDeviceToDevice, st));
     for (int iter = 0; iter < 64; iter++) {
         std::vector<int> live;
+        uint64_t live_nodes = 0;
         for (int k = 0; k < nseg; k++)
-            if (cur_n[k] > 1) live.push_back(k);
+            if (cur_n[k] > 1) { live.push_back(k); live_nodes += cur_n[k]; }
         if (live.empty()) break;
         uint32_t* dst = levels_out ? levels_out : bufs[which];
         uint64_t dst_base = levels_out ? level_store_off : 0;
         std::vector<uint64_t> next_n(nseg), next_idx(nseg);
+        // big levels: one flat launch per level (all lanes busy)
+        const int lg_it = (live_nodes >= kFlatLevelMin || levels_out) ? 1 : lg;
         for (size_t b0 = 0; b0 < live.size(); b0 += kMaxSegs) {
             TreeTable tab;
             memset(&tab, 0, sizeof tab);
             tab.lg = lg;
             int cnt = 0;
             tab.group_prefix[0] = 0;
+            tab.lg = lg_it;
             for (size_t q = b0; q < live.size() && cnt < kMaxSegs; q++, cnt++) {
                 int k = live[q];
-                uint64_t groups = (cur_n[k] + (1ull << lg) - 1) >> lg;
+                uint64_t groups = (cur_n[k] + (1ull << lg_it) - 1) >> lg_it;
                 tab.full_levels[cnt] = groups > 1 ? 1 : 0;
                 tab.in_index[cnt] = cur_idx[k];
                 tab.n_in[cnt] = cur_n[k];
@@ -555,7 +583,13 @@ static int reduce_trees(int alg, int nseg, const uint64_t* in_index, const uint6
             }
             tab.n = cnt;
             uint64_t blocks = tab.group_prefix[cnt];
-            if (alg == kSHA256)
+            if (lg_it == 1 && !levels_out) {  // flat level: thread per parent
+                const uint64_t fb = (blocks + 127) / 128;
+                if (alg == kSHA256)
+                    k_tree_level<kSHA256><<<(unsigned)fb, 128, 0, st>>>(tab, cur, dst);
+                else
+                    k_tree_level<kKECCAK256><<<(unsigned)fb, 128, 0, st>>>(tab, cur, dst);
+            } else if (alg == kSHA256)
                 k_tree_reduce<kSHA256><<<(unsigned)blocks, kTreeThreads, 0, st>>>(tab, cur, dst);
             else
                 k_tree_reduce<kKECCAK256><<<(unsigned)blocks, kTreeThreads, 0, st>>>(tab, cur, dst);
@@ -588,8 +622,8 @@ size_t nao_merkle_commit_workspace(int64_t n_tensors, const uint64_t* payload_by
     if (n_tensors <= 0 || chunk_bytes == 0) return 0;
     uint64_t leaves = 0;
     for (int64_t i = 0; i < n_tensors; i++) leaves += 1 + seg_chunks(payload_bytes[i], chunk_bytes);
-    // level-0 digests + two ping-pong level buffers (each <= leaves/512 + n)
-    uint64_t lvl = leaves / 256 + 2 * (uint64_t)n_tensors + 16;
+    // level-0 digests + two ping-pong level buffers (each <= leaves/2 + 2n)
+    uint64_t lvl = leaves / 2 + 2 * (uint64_t)n_tensors + 16;  // flat first levels: n/2
     return (size_t)(32 * (leaves + 2 * lvl) + 3 * 256);
 }
 
@@ -639,7 +673,7 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
     Workspace ws(workspace, workspace_bytes);
     uint32_t* lvl0 = leaf_digests_out ? reinterpret_cast<uint32_t*>(leaf_digests_out)
                                       : ws.take<uint32_t>(8 * leaves);
-    uint64_t lvl = leaves / 256 + 2 * (uint64_t)n_tensors + 16;
+    uint64_t lvl = leaves / 2 + 2 * (uint64_t)n_tensors + 16;  // flat first levels: n/2
     uint32_t* sa = ws.take<uint32_t>(8 * lvl);
     uint32_t* sb = ws.take<uint32_t>(8 * lvl);
     NAO_REQUIRE(lvl0 && sa && sb, "workspace too small (%zu bytes)", workspace_bytes);
@@ -764,7 +798,7 @@ int nao_merkle_hash_leaves(const uint8_t* data, const int64_t* offsets, int64_t 
 
 size_t nao_merkle_root_workspace(int64_t n_leaves) {
     if (n_leaves <= 0) return 0;
-    return (size_t)(2 * 32 * ((uint64_t)n_leaves / 256 + 16) + 512);
+    return (size_t)(2 * 32 * ((uint64_t)n_leaves / 2 + 16) + 512);
 }
 
 int nao_merkle_root_of(const uint8_t* leaf_digests, int64_t n_leaves, int hash_alg,
@@ -774,7 +808,7 @@ int nao_merkle_root_of(const uint8_t* leaf_digests, int64_t n_leaves, int hash_a
     NAO_REQUIRE(n_leaves > 0, "merkle tree requires at least one leaf");
     NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg");
     Workspace ws(workspace, workspace_bytes);
-    uint64_t lvl = (uint64_t)n_leaves / 256 + 16;
+    uint64_t lvl = (uint64_t)n_leaves / 2 + 16;
     uint32_t* sa = ws.take<uint32_t>(8 * lvl);
     uint32_t* sb = ws.take<uint32_t>(8 * lvl);
     if (levels_out == nullptr) NAO_REQUIRE(sa && sb, "workspace too small");
