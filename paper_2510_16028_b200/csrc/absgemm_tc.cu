@@ -1527,7 +1527,9 @@ int nao_f16_split(const float* x, void* hi, void* lo, int32_t* row_info, int64_t
         if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
         const bool vec = (K % 8) == 0 && (ld % 4) == 0 && (stride_batch % 4) == 0 &&
                          (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-        if (vec && K * 4 <= 96 * 1024) {
+        // rows of <= 2048 elements: warp per row (the row stays in L1 for the
+        // second pass); longer rows: CTA per row staged in shared memory
+        if (vec && K > 2048 && K * 4 <= 96 * 1024) {
             static bool attr = false;
             if (!attr) {
                 NAO_CHECK_CUDA(cudaFuncSetAttribute(tc::k_split_f16_rows_smem,
