@@ -98,6 +98,9 @@ __global__ void __launch_bounds__(128) k_chunk_leaves(const __grid_constant__ Ch
 // A CTA covers 128 consecutive chunks of ONE tensor; the last CTA of a tensor
 // decides its verdict (histogram verdict + rare exact second pass).
 
+#ifndef NAO_CC_PROBE
+#define NAO_CC_PROBE 0
+#endif
 constexpr int kLeafThreads = 128;
 
 struct CheckDesc {  // == nao_check_desc (include/nao_b200.h)
@@ -149,7 +152,11 @@ struct CheckedWords {
     const uint32_t* __restrict__ q;  // local
     unsigned long long* mask;        // this thread's mask words (stride kLeafThreads)
     __device__ __forceinline__ void cmp(uint32_t c, uint32_t y, uint32_t i) const {
+#if NAO_CC_PROBE == 2  // timing probe: no compare at all (wrong verdicts)
+        (void)c; (void)y; (void)i;
+#else
         if (word_needs_check(c, y)) mask[(i >> 6) * kLeafThreads] |= 1ull << (i & 63);
+#endif
     }
     __device__ __forceinline__ uint4 v4(uint32_t i) const {
         const uint4 c = __ldg(reinterpret_cast<const uint4*>(p) + i);
@@ -290,7 +297,9 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
     const uint64_t lane_base = c * cw;  // element index of this lane's word 0
     int qn = 0;                         // warp-uniform
     unsigned long long nflag = 0;
-    for (uint32_t g = 0; g < groups; g++) {
+    // NAO_CC_PROBE >= 1: timing probe, flagged words are not processed (wrong verdicts)
+    const uint32_t groups_proc = NAO_CC_PROBE >= 1 ? 0u : groups;
+    for (uint32_t g = 0; g < groups_proc; g++) {
         unsigned long long m = s_mask[g * kLeafThreads + threadIdx.x];
         for (;;) {
             const bool has = m != 0ull;
