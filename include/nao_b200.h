@@ -143,8 +143,22 @@ typedef struct nao_check_desc {
     double eps_scale;            /* NAO_EPS_SCALED_LOCAL */
     double lo_factor;            /* borderline band (see nao_check) */
     int32_t eps_kind;
-    int32_t reserved;
+    int32_t flags;               /* NAO_CHECK_PARTIAL: `result` is a nao_check_partial */
 } nao_check_desc;
+/* A shard's combinable check state (batch-sharded verification):
+ * counts per threshold interval (bucket b = keys with b sorted thresholds
+ * strictly below them; b = G holds non-finite elements) and the smallest /
+ * largest FP64 key per bucket, so the exact p_max > 1 verdict of the whole
+ * tensor -- including numpy's interpolation between order statistics -- is
+ * decided from the shards' partials alone (paper_2510_16028_b200.dispute.
+ * combine_partials).  Empty buckets: min = +inf, max = 0. */
+enum { NAO_CHECK_PARTIAL = 1 };
+typedef struct nao_check_partial {
+    uint64_t n, n_violations, n_borderline, n_nonfinite;
+    double max_ratio;
+    uint64_t hist_abs[33], hist_rel[33];
+    double min_abs[33], max_abs[33], min_rel[33], max_rel[33];
+} nao_check_partial;
 /* nao_merkle_commit_tensors + nao_check of every tensor in the SAME pass:
  * payloads are the claimed tensors; checks[i] (host array, n_tensors entries)
  * compares payload i with checks[i].local (the reference's leaf route,

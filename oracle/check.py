@@ -127,3 +127,30 @@ def calibrate(graph, dataset, fmas, grid=PERCENTILE_GRID, epsilon=DEFAULT_EPSILO
                     np.maximum(rel_env[i], profs[:, 1], out=rel_env[i])
                     np.maximum(rel_env[i], profs[:, 2], out=rel_env[i])
     return abs_env, rel_env
+
+
+def shard_partial(local, claimed, eps, tau_abs, tau_rel, grid=PERCENTILE_GRID,
+                  epsilon=DEFAULT_EPSILON) -> dict:
+    """A shard's combinable check state (the nao_check_partial the GPU emits for
+    batch-sharded verification; not a reference function -- it restates the
+    pieces of dispute.py:130-141 / :641-648 that add up across shards): exact
+    FP64 keys bucketed by the number of sorted effective thresholds strictly
+    below them, bucket counts and key ranges, violation counts, max ratio."""
+    G = len(grid)
+    a, r = elementwise_errors(local, claimed, epsilon)
+    out = {"n": int(a.size)}
+    lc = leaf_check(local, claimed, eps)
+    out["n_violations"], out["max_ratio"] = lc["n_violations"], lc["max_ratio"]
+    out["n_borderline"], out["n_nonfinite"] = 0, 0
+    for key, vals, taus in (("abs", a, tau_abs), ("rel", r, tau_rel)):
+        srt = np.sort(np.maximum(np.asarray(taus, dtype=np.float64), 0.0))
+        b = np.searchsorted(srt, vals, side="left")  # #{t < key}
+        hist = np.bincount(b, minlength=33)[:33].astype(np.uint64)
+        mn = np.full(33, np.inf)
+        mx = np.zeros(33)
+        for k in range(G + 1):
+            sel = vals[b == k]
+            if sel.size:
+                mn[k], mx[k] = sel.min(), sel.max()
+        out[f"hist_{key}"], out[f"min_{key}"], out[f"max_{key}"] = hist, mn, mx
+    return out

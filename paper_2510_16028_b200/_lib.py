@@ -60,7 +60,23 @@ class CheckDesc(ctypes.Structure):
     """nao_check_desc: the check fused into nao_commit_check_tensors."""
     _fields_ = [("local", c_vp), ("eps", c_vp), ("spec", c_vp), ("result", c_vp),
                 ("eps_scale", ctypes.c_double), ("lo_factor", ctypes.c_double),
-                ("eps_kind", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("eps_kind", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+CHECK_PARTIAL = 1  # NAO_CHECK_PARTIAL
+
+
+class CheckPartial(ctypes.Structure):
+    """nao_check_partial: a shard's combinable check state."""
+    _fields_ = [("n", ctypes.c_uint64), ("n_violations", ctypes.c_uint64),
+                ("n_borderline", ctypes.c_uint64), ("n_nonfinite", ctypes.c_uint64),
+                ("max_ratio", ctypes.c_double),
+                ("hist_abs", ctypes.c_uint64 * 33), ("hist_rel", ctypes.c_uint64 * 33),
+                ("min_abs", ctypes.c_double * 33), ("max_abs", ctypes.c_double * 33),
+                ("min_rel", ctypes.c_double * 33), ("max_rel", ctypes.c_double * 33)]
+
+
+CHECK_PARTIAL_BYTES = ctypes.sizeof(CheckPartial)
 
 # name -> (restype, argtypes)
 _SIGS = {

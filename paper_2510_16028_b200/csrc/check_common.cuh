@@ -33,6 +33,10 @@ struct CheckAccum {
     unsigned long long max_ratio_bits;        // non-negative double
     unsigned long long amb_lo[2 * kMaxGrid];  // max key <= tau (double bits)
     unsigned long long amb_hi[2 * kMaxGrid];  // min key >  tau (double bits)
+    // partial mode (combinable records): per-bucket key range; min stored as
+    // max of ~bits so that the zero state means "empty"
+    unsigned long long bmax[2][kMaxGrid + 1];
+    unsigned long long bmin_inv[2][kMaxGrid + 1];
     unsigned int blocks_done;
     unsigned int pad_;
 };

@@ -111,9 +111,10 @@ struct CheckDesc {  // == nao_check_desc (include/nao_b200.h)
     double eps_scale;
     double lo_factor;
     int32_t eps_kind;
-    int32_t reserved;
+    int32_t flags;
 };
 static_assert(sizeof(CheckDesc) == sizeof(nao_check_desc), "nao_check_desc layout");
+static_assert(sizeof(nao_check_partial) == 8 * (5 + 2 * 33 + 4 * 33), "nao_check_partial layout");
 
 struct CCTable {
     int n;
@@ -134,6 +135,8 @@ struct LeafCheckSmem {
     float f_rel[kMaxGrid], f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];
     unsigned int wc[kLeafWarps][2][kMaxGrid + 1];  // warp-private interval counters
     unsigned long long q[kLeafWarps][96];           // warp queue of flagged element indices
+    unsigned long long bmax[2][kMaxGrid + 1];       // partial mode: per-bucket key range
+    unsigned long long bmin_inv[2][kMaxGrid + 1];
     unsigned long long viol, border, nonfin, nslow;
     unsigned long long maxr_bits;
     int is_last;
@@ -218,7 +221,17 @@ __device__ __forceinline__ void process_flagged(const CheckDesc& d, const Flagge
         lc.best_inf = true;
     }
     int pa = 0, q = 0;
-    if (diff != 0.0) {
+    if (d.flags & NAO_CHECK_PARTIAL) {  // exact keys + per-bucket key ranges
+        const double rel = rel_key(diff, y, epsilon);
+        if (diff != 0.0) {
+            pa = bsearch_pos(sm.t_abs, G, diff);
+            q = bsearch_pos(sm.t_rel, G, rel);
+        }
+        const unsigned long long ba = (unsigned long long)__double_as_longlong(diff);
+        const unsigned long long br = (unsigned long long)__double_as_longlong(rel);
+        atomicMax(&sm.bmax[0][pa], ba); atomicMax(&sm.bmin_inv[0][pa], ~ba);
+        atomicMax(&sm.bmax[1][q], br); atomicMax(&sm.bmin_inv[1][q], ~br);
+    } else if (diff != 0.0) {
         pa = bsearch_pos(sm.t_abs, G, diff);
         const float d32 = (float)diff;
         const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)epsilon));
@@ -264,6 +277,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         }
         for (int b = lane; b <= kMaxGrid; b += 32) { sm.wc[w][0][b] = 0u; sm.wc[w][1][b] = 0u; }
         if (threadIdx.x < 2 * kMaxGrid) sm.vs.amb[threadIdx.x] = 0;
+        for (int b = threadIdx.x; b < 2 * (kMaxGrid + 1); b += blockDim.x) {
+            (&sm.bmax[0][0])[b] = 0ull;
+            (&sm.bmin_inv[0][0])[b] = 0ull;
+        }
         if (threadIdx.x == 0) {
             sm.viol = sm.border = sm.nonfin = sm.nslow = 0ull;
             sm.maxr_bits = 0ull;
@@ -362,6 +379,20 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         }
         if (ha) atomicAdd(&acc->hist_abs[threadIdx.x], ha);
         if (hr) atomicAdd(&acc->hist_rel[threadIdx.x], hr);
+        if (d.flags & NAO_CHECK_PARTIAL) {
+            const int b = threadIdx.x;
+            unsigned long long mx0 = sm.bmax[0][b], mn0 = sm.bmin_inv[0][b];
+            unsigned long long mx1 = sm.bmax[1][b], mn1 = sm.bmin_inv[1][b];
+            if (b == 0) {  // the equal words: key 0 in bucket 0 of both arrays
+                const uint64_t c1 = c0 + kLeafThreads < nchunks ? c0 + kLeafThreads : nchunks;
+                const uint64_t w1 = c1 * cw < total_w ? c1 * cw : total_w;
+                if ((w1 - c0 * cw) > sm.nslow) { mn0 = ~0ull; mn1 = ~0ull; }
+            }
+            if (mx0) atomicMax(&acc->bmax[0][b], mx0);
+            if (mn0) atomicMax(&acc->bmin_inv[0][b], mn0);
+            if (mx1) atomicMax(&acc->bmax[1][b], mx1);
+            if (mn1) atomicMax(&acc->bmin_inv[1][b], mn1);
+        }
     }
     if (threadIdx.x == 0) {
         if (sm.viol) atomicAdd(&acc->n_viol, sm.viol);
@@ -377,6 +408,31 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
     __threadfence();
     const VerdictSpec& v = *d.spec;
     const int64_t n = (int64_t)total_w;
+    if (d.flags & NAO_CHECK_PARTIAL) {  // combinable shard record, no verdict here
+        nao_check_partial* out = reinterpret_cast<nao_check_partial*>(d.result);
+        const volatile CheckAccum* va = acc;
+        if (threadIdx.x <= kMaxGrid) {
+            const int b = threadIdx.x;
+            out->hist_abs[b] = va->hist_abs[b];
+            out->hist_rel[b] = va->hist_rel[b];
+            out->max_abs[b] = __longlong_as_double((long long)va->bmax[0][b]);
+            out->max_rel[b] = __longlong_as_double((long long)va->bmax[1][b]);
+            const unsigned long long i0 = va->bmin_inv[0][b], i1 = va->bmin_inv[1][b];
+            out->min_abs[b] = i0 ? __longlong_as_double((long long)~i0) : INFINITY;
+            out->min_rel[b] = i1 ? __longlong_as_double((long long)~i1) : INFINITY;
+        }
+        if (threadIdx.x == 0) {
+            out->n = (uint64_t)n;
+            out->n_violations = va->n_viol;
+            out->n_borderline = va->n_border;
+            out->n_nonfinite = va->n_nonfinite;
+            out->max_ratio = __longlong_as_double((long long)va->max_ratio_bits);
+        }
+        __syncthreads();
+        unsigned long long* zp = reinterpret_cast<unsigned long long*>(acc);
+        for (int i = threadIdx.x; i < (int)(sizeof(CheckAccum) / 8); i += blockDim.x) zp[i] = 0ull;
+        return;
+    }
     decide_targets(v, n, acc->hist_abs, acc->hist_rel, sm.vs, false);
     if (sm.vs.n_amb > 0) {
         settle_ambiguous(v, d.local, claimed, n, sm.vs);

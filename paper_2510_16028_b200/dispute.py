@@ -125,7 +125,8 @@ def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel
 
 
 def commit_check_nodes(claimed, local, eps, taus, chunk_bytes: int = 4096, alg="keccak256",
-                       grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON):
+                       grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON,
+                       partial: bool = False):
     """Merkle-commit every claimed tensor and check it against its local
     recomputation in the same pass (nao_commit_check_tensors).  eps[i] as in
     check_node; taus[i] = (tau_abs, tau_rel).  Returns (roots [n,32],
@@ -135,7 +136,8 @@ def commit_check_nodes(claimed, local, eps, taus, chunk_bytes: int = 4096, alg="
     if not (len(local) == len(eps) == len(taus) == n):
         raise ValueError("claimed/local/eps/taus lengths differ")
     dev = to_device(claimed[0]).device
-    recs = new_result_buffer(dev, n)
+    recs = (torch.zeros((n, _lib.CHECK_PARTIAL_BYTES), dtype=torch.uint8, device=dev) if partial
+            else new_result_buffer(dev, n))
     blobs, descs, keep = [], [], []
     for i in range(n):
         a = to_device(local[i]).contiguous()
@@ -166,12 +168,82 @@ def commit_check_nodes(claimed, local, eps, taus, chunk_bytes: int = 4096, alg="
     checks = []
     for i, (a, b, kind, eps_ptr, scale, lo) in enumerate(descs):
         checks.append(_lib.CheckDesc(a.data_ptr(), eps_ptr, spec.data_ptr() + i * size,
-                                     recs[i].data_ptr(), scale, lo, kind, 0)
+                                     recs[i].data_ptr(), scale, lo, kind,
+                                     _lib.CHECK_PARTIAL if partial else 0)
                       if a.numel() else None)
     roots = commit_tensors([d[1] for d in descs], chunk_bytes, alg, checks=checks)
     for t in keep + [spec]:
         t.record_stream(torch.cuda.current_stream(dev))
     return roots, recs
+
+
+def partial_from_bytes(raw: bytes) -> dict:
+    """Decode one nao_check_partial row."""
+    r = _lib.CheckPartial.from_buffer_copy(bytes(raw)[:_lib.CHECK_PARTIAL_BYTES])
+    out = {f: getattr(r, f) for f in ("n", "n_violations", "n_borderline", "n_nonfinite",
+                                      "max_ratio")}
+    for f in ("hist_abs", "hist_rel", "min_abs", "max_abs", "min_rel", "max_rel"):
+        out[f] = np.array(getattr(r, f)[:])
+    return out
+
+
+def _np_lerp(a, b, t):
+    """numpy _lerp (_function_base_impl.py:4657-4679)."""
+    d = b - a
+    r = a + d * t
+    if t >= 0.5:
+        r = b - d * (1.0 - t)
+    return r
+
+
+def combine_partials(partials, tau_abs, tau_rel, grid=PERCENTILE_GRID) -> dict:
+    """Merge shard partials of one tensor (nao_check_partial: interval counts +
+    per-interval key ranges) into the whole tensor's record: violation counts
+    add, max ratios max, and the threshold verdict observed_p_max > 1
+    (dispute.py:114-141) is decided exactly -- including numpy's interpolation
+    between order statistics, from the interval key ranges."""
+    G = len(grid)
+    n = int(sum(p["n"] for p in partials))
+    rec = {"n": n, "n_violations": int(sum(p["n_violations"] for p in partials)),
+           "n_borderline": int(sum(p["n_borderline"] for p in partials)),
+           "n_nonfinite": int(sum(p["n_nonfinite"] for p in partials)),
+           "max_ratio": float(max(p["max_ratio"] for p in partials)) if partials else 0.0}
+    exceeded, first = False, -1
+    for arr, (taus, key) in enumerate(((tau_abs, "abs"), (tau_rel, "rel"))):
+        eff = np.array([t if t > 0.0 else 0.0 for t in np.asarray(taus, dtype=np.float64)])
+        srt = np.sort(eff)
+        hist = np.sum([p[f"hist_{key}"][:G + 1] for p in partials], axis=0).astype(np.int64)
+        cnt = np.sum([(p[f"hist_{key}"][:G + 1] > 0) for p in partials], axis=0)
+        with np.errstate(invalid="ignore"):
+            mx = np.max([np.where(p[f"hist_{key}"][:G + 1] > 0, p[f"max_{key}"][:G + 1], -np.inf)
+                         for p in partials], axis=0)
+            mn = np.min([np.where(p[f"hist_{key}"][:G + 1] > 0, p[f"min_{key}"][:G + 1], np.inf)
+                         for p in partials], axis=0)
+        del cnt
+        for i in range(G):
+            tau = float(eff[i])
+            L = int(np.searchsorted(srt, tau, side="left"))  # #{sorted t < tau}
+            cle = int(hist[:L + 1].sum())
+            q = np.float64(grid[i]) / 100.0
+            vi = (n - 1) * q
+            if vi >= n - 1:
+                ex = cle < n
+            else:
+                prev = int(np.floor(vi))
+                g = vi - np.floor(vi)
+                if cle <= prev:
+                    ex = True
+                elif cle >= prev + 2:
+                    ex = False
+                else:  # exactly prev+1 keys <= tau: the prev-th / next order statistics
+                    a = float(np.max(mx[:L + 1]))
+                    b = float(np.min(mn[L + 1:])) if L + 1 <= G else np.inf
+                    ex = _np_lerp(a, b, g) > tau
+            if ex and not exceeded:
+                exceeded, first = True, arr * G + i
+    rec["threshold_exceeded"] = int(exceeded)
+    rec["first_exceeded"] = first
+    return rec
 
 
 def leaf_check(claimed, y_ref, eps) -> dict:
@@ -192,5 +264,6 @@ def to_device_eps(eps) -> torch.Tensor:
 
 
 __all__ = ["p_max", "observed_p_max", "screen", "select_offending", "check_node", "leaf_check",
-           "CheckRecord", "new_result_buffer", "commit_check_nodes"]
+           "CheckRecord", "new_result_buffer", "commit_check_nodes", "combine_partials",
+           "partial_from_bytes"]
 _ = ctypes

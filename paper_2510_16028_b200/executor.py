@@ -171,7 +171,7 @@ class StreamingVerifier:
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
                  grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
-                 max_lag: int = 0):
+                 max_lag: int = 0, partial: bool = False):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -196,6 +196,11 @@ class StreamingVerifier:
         # side stream that runs behind, e.g. under a high-priority main stream)
         self.max_lag = int(max_lag)
         self._com_events = []
+        # partial: records are combinable nao_check_partial rows (a batch shard of
+        # every node; shard.combine_shard_records decides the whole-tensor verdicts)
+        self.partial = bool(partial)
+        if self.partial and not self.fuse_check:
+            raise ValueError("partial (batch-shard) records need the fused check")
         self._specs = None  # (device blob, {node index: byte offset}) of verdict specs
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
@@ -256,7 +261,11 @@ class StreamingVerifier:
         st.inputs, st.start, st.end = inputs, start, end
         st.roots = roots if roots is not None else torch.empty((n, 32), dtype=torch.uint8,
                                                                 device=self.dev)
-        st.records = records if records is not None else new_result_buffer(self.dev, n)
+        if records is None:
+            records = (torch.zeros((n, _lib.CHECK_PARTIAL_BYTES), dtype=torch.uint8,
+                                   device=self.dev) if self.partial
+                       else new_result_buffer(self.dev, n))
+        st.records = records
         st.last = last_uses(g, start, end)
         st.values = dict(frontier or {})
         st.all_idx = torch.arange(n, device=self.dev)
@@ -361,7 +370,8 @@ class StreamingVerifier:
             if y.numel() and self.fuse_check:
                 blob, offs = st.specs
                 desc = _lib.CheckDesc(y.data_ptr(), eps_ptr, blob.data_ptr() + offs[node.index],
-                                      st.records[i].data_ptr(), scale, lo_f, kind, 0)
+                                      st.records[i].data_ptr(), scale, lo_f, kind,
+                                      _lib.CHECK_PARTIAL if self.partial else 0)
                 st.pend_keep.append(y)
                 if not isinstance(eps, tuple):
                     st.pend_keep.append(eps)

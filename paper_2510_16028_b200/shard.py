@@ -1,5 +1,13 @@
 """Multi-GPU sharding of the verified forward.
 
+Two unit kinds, both without a data-path collective:
+  * layer slices (below) for single-sequence models (Qwen3-8B, S=2048);
+  * batch shards (batch_rows, combine_shard_records) for the batched configs
+    (GPT-2 B=8, SD-UNet B=8): samples are independent, every rank verifies the
+    whole graph on its samples, commits each node's shard as its own tensor
+    (per-shard roots, north_star (5)) and emits combinable check partials, from
+    which rank 0 decides every node's verdict exactly as on the whole tensor.
+
 Units are contiguous canonical-order op slices -- the reference's partition
 unit (graph.py:275-293) -- aligned to layer boundaries so that each rank's
 frontier is the residual stream (the reference re-executes a child slice from
@@ -77,3 +85,52 @@ def gather_node_records(roots: torch.Tensor, records: torch.Tensor, group=None, 
     dist.all_gather(out, row, group=group)
     full = torch.cat([o[:s] for o, s in zip(out, sizes)])
     return full[:, :32].contiguous(), full[:, 32:].contiguous()
+
+
+# ------------------------------------------------------------ batch shards
+
+def batch_range(batch: int, rank: int, world: int):
+    """[lo, hi) samples of rank (contiguous, sizes differ by <= 1, larger first)."""
+    base, extra = divmod(int(batch), int(world))
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def batch_rows(t: torch.Tensor, batch: int, rank: int, world: int) -> torch.Tensor:
+    """The rank's samples of a batch-major tensor (leading extent = batch x k)."""
+    lo, hi = batch_range(batch, rank, world)
+    per = t.shape[0] // batch
+    return t[lo * per:hi * per]
+
+
+def combine_shard_records(partials_by_rank, thresholds_by_node, grid=None) -> list:
+    """Rank 0 after the gather: per node, combine the shards' nao_check_partial
+    rows (dispute.combine_partials) into the whole tensor's record.
+    partials_by_rank[r][i] = decoded partial dict of node i on rank r;
+    thresholds_by_node[i] = (tau_abs, tau_rel)."""
+    from .calibration import PERCENTILE_GRID
+    from .dispute import combine_partials
+    grid = PERCENTILE_GRID if grid is None else grid
+    n_nodes = len(partials_by_rank[0])
+    out = []
+    for i in range(n_nodes):
+        parts = [partials_by_rank[r][i] for r in range(len(partials_by_rank))
+                 if partials_by_rank[r][i]["n"] > 0]
+        ta, tr = thresholds_by_node[i]
+        out.append(combine_partials(parts, ta, tr, grid) if parts else
+                   {"n": 0, "n_violations": 0, "n_borderline": 0, "n_nonfinite": 0,
+                    "max_ratio": 0.0, "threshold_exceeded": 0, "first_exceeded": -1})
+    return out
+
+
+def shard_trace_root(roots_by_rank, alg="keccak256") -> bytes:
+    """Trace root of a batch-sharded run: Merkle tree over the per-(node, shard)
+    roots in node-major, rank-minor order (leaf = H(0x00 || root))."""
+    from .commitments import build_tree
+    leaves = []
+    n_nodes = roots_by_rank[0].shape[0]
+    host = [r.cpu().numpy() for r in roots_by_rank]
+    for i in range(n_nodes):
+        for h in host:
+            leaves.append(bytes(h[i]))
+    return build_tree(leaves, alg).root

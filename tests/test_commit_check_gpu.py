@@ -142,3 +142,40 @@ def test_fused_many_tensors_and_empty():
             ref = OC.leaf_check(y, yc, 2.0 ** -23 * np.abs(y.astype(np.float64)))
             assert got[i]["n"] == y.size
             assert got[i]["n_violations"] == ref["n_violations"], (rep, i)
+
+
+@pytest.mark.parametrize("pieces", [1, 2, 3, 5])
+def test_partial_records_combine_to_whole_tensor_verdict(pieces):
+    """Batch-sharded checks: each shard emits a combinable
+    nao_check_partial; combine_partials reproduces the whole tensor's record
+    from the pieces -- violations, borderline, max ratio and the exact
+    percentile verdict incl. thresholds AT the true percentiles (numpy's
+    interpolation between order statistics, decided from the key ranges)."""
+    from paper_2510_16028_b200 import dispute
+    rng = np.random.default_rng(pieces)
+    for mode, kind, tm in (("drift", "scaled", "exact"), ("heavy", "f32", "exact"),
+                           ("heavy", "f64", "scaled"), ("drift", "zero", "inf"),
+                           ("equal", "scaled", "exact"), ("heavy", "scaled", "exact")):
+        y, yc, eps, ref_eps, taus = _case(rng, 12000 + 7 * pieces, mode, kind, tm)
+        want = dispute.check_node(torch.from_numpy(y).cuda(), torch.from_numpy(yc).cuda(), eps,
+                                  taus[0], taus[1]).host()
+        cuts = np.linspace(0, y.size, pieces + 1).astype(int)
+        claimed = [torch.from_numpy(yc[a:b]).cuda() for a, b in zip(cuts[:-1], cuts[1:])]
+        local = [torch.from_numpy(y[a:b]).cuda() for a, b in zip(cuts[:-1], cuts[1:])]
+        if isinstance(eps, tuple):
+            epss = [eps] * pieces
+        else:
+            epss = [eps[a:b] for a, b in zip(cuts[:-1], cuts[1:])]
+        _, recs = dispute.commit_check_nodes(claimed, local, epss, [taus] * pieces, 256,
+                                             "keccak256", partial=True)
+        torch.cuda.synchronize()
+        parts = [dispute.partial_from_bytes(recs[i].cpu().numpy().tobytes())
+                 for i in range(pieces)]
+        got = dispute.combine_partials(parts, taus[0], taus[1])
+        for f in ("n", "n_violations", "n_borderline", "n_nonfinite", "threshold_exceeded",
+                  "first_exceeded"):
+            assert got[f] == want[f], (mode, kind, tm, f, got[f], want[f])
+        assert got["max_ratio"] == want["max_ratio"], (mode, kind, tm)
+        with np.errstate(invalid="ignore"):
+            pm = OC.observed_p_max(y, yc, taus[0], taus[1])
+        assert bool(got["threshold_exceeded"]) == (pm > 1.0)

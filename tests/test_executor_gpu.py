@@ -233,3 +233,78 @@ def test_layer_sharded_verification_matches_single_run(world):
     assert torch.equal(r_cat, r_all)
     assert torch.equal(c_cat, c_all)
     assert torch.equal(sv.trace_root(r_cat), t_all)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_batch_sharded_verification_matches_whole_batch(world):
+    """Batch shards (SURVEY 8(e), GPT-2-style B-major graph, sequential profile):
+    each "rank" verifies the whole graph on its samples from the claimed trace's
+    batch rows, commits its shard of every node (per-shard roots) and emits
+    combinable partials; combine_shard_records gives, node by node, the
+    unsharded run's violations, max ratio and exact percentile verdicts --
+    with thresholds placed at, below and above the true percentiles."""
+    from paper_2510_16028_b200 import shard
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.calibration import (PERCENTILE_GRID, OpThresholds, ThresholdSet,
+                                                   error_profiles_device)
+    from paper_2510_16028_b200.commitments import commit_tensors
+    from paper_2510_16028_b200.dispute import CheckRecord, partial_from_bytes
+    from paper_2510_16028_b200.engine import DeviceProfile
+    from paper_2510_16028_b200.executor import StreamingVerifier, drift_claim
+    from paper_2510_16028_b200.lowerings import DecoderShape, build_decoder
+    from paper_2510_16028_b200.tensor import Rng, Tensor
+    B = 6
+    base = DecoderShape("tiny-gpt2", layers=2, hidden=64, heads=2, kv_heads=2, head_dim=32,
+                        inter=128, vocab=300, seq=32, batch=B, norm="ln", qk_norm=False,
+                        rope=False, act="gelu", bias=True, eps=1e-5)
+    seq = DeviceProfile("seq", "sequential")
+    spec = build_decoder(base, seed=4)
+    g = spec.graph
+    ids = spec.make_inputs(Rng(8))
+    claimed, local = {}, {}
+
+    def claim_full(node, y):
+        yc = drift_claim(node, y, seed=6, period=3, fault_node="l1_fc")
+        claimed[node.index], local[node.index] = yc, y
+        return yc
+
+    StreamingVerifier(g, FpModel(), seq, hash_alg="keccak256", chunk_bytes=256).run(ids, claim_full)
+    ops = []
+    for k, node in enumerate(g.nodes):  # thresholds: at / below / above the true percentiles
+        pa, pr = error_profiles_device(local[node.index], claimed[node.index])
+        f = (1.0, 0.5, 3.0)[k % 3]
+        ops.append(OpThresholds(node.name, pa.cpu().numpy() * f, pr.cpu().numpy() * f))
+    ts = ThresholdSet(alpha=3.0, epsilon=1e-12, grid=PERCENTILE_GRID, ops=ops)
+    sv = StreamingVerifier(g, FpModel(), seq, ts, hash_alg="keccak256", chunk_bytes=256)
+    _, recs_full = sv.run(ids, lambda node, y: claimed[node.index])
+    want = [CheckRecord(recs_full[i]).host() for i in range(g.n_nodes)]
+
+    parts_by_rank, roots_by_rank = [], []
+    ids_full = torch.from_numpy(np.array(ids["ids"].array)).reshape(B, -1)
+    for r in range(world):
+        lo, hi = shard.batch_range(B, r, world)
+        shp = DecoderShape(**{**base.__dict__, "batch": hi - lo})
+        spec_r = build_decoder(shp, seed=4)
+        ids_r = {"ids": Tensor((hi - lo, base.seq), ids_full[lo:hi].float().cuda().reshape(-1))}
+        svr = StreamingVerifier(spec_r.graph, FpModel(), seq, ts, hash_alg="keccak256",
+                                chunk_bytes=256, partial=True)
+        roots, recs = svr.run(ids_r, lambda node, y: shard.batch_rows(
+            claimed[node.index], B, r, world).clone().reshape(y.shape))
+        torch.cuda.synchronize()
+        parts_by_rank.append([partial_from_bytes(recs[i].cpu().numpy().tobytes())
+                              for i in range(g.n_nodes)])
+        roots_by_rank.append(roots)
+        # per-shard roots are the roots of the claimed trace's batch rows
+        for i in (0, 5, g.n_nodes - 1):
+            sl = shard.batch_rows(claimed[i], B, r, world).contiguous()
+            assert torch.equal(roots[i], commit_tensors([sl], 256, "keccak256")[0])
+    got = shard.combine_shard_records(
+        parts_by_rank, [(ts.lookup(n.name).tau_abs, ts.lookup(n.name).tau_rel) for n in g.nodes])
+    exceeded = 0
+    for i, node in enumerate(g.nodes):
+        for f in ("n", "n_violations", "n_borderline", "n_nonfinite", "threshold_exceeded",
+                  "first_exceeded", "max_ratio"):
+            assert got[i][f] == want[i][f], (node.name, f, got[i][f], want[i][f])
+        exceeded += got[i]["threshold_exceeded"]
+    assert exceeded > 0 and got[[n.name for n in g.nodes].index("l1_fc")]["n_violations"] > 0
+    assert len(shard.shard_trace_root(roots_by_rank)) == 32
