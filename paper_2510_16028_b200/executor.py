@@ -201,7 +201,10 @@ class StreamingVerifier:
         self.partial = bool(partial)
         if self.partial and not self.fuse_check:
             raise ValueError("partial (batch-shard) records need the fused check")
-        self._specs = None  # (device blob, {node index: byte offset}) of verdict specs
+        # device verdict specs: {node index: device address}; every uploaded blob
+        # stays alive with the verifier (in-flight commits may still read it)
+        self._spec_addr: dict = {}
+        self._spec_blobs: list = []
         # side streams: the memory-bound check and the ALU-bound hashing run
         # concurrently with the next nodes' GEMMs / bound kernels
         # (equal priorities: a low-priority side stream starves and the memory its
@@ -226,20 +229,21 @@ class StreamingVerifier:
         return t
 
     def _spec_table(self, start, end):
-        """Device nao_verdict_spec of every node in [start, end) (one upload)."""
-        have = self._specs[1] if self._specs is not None else {}
-        nodes = self.g.nodes[start:end]
-        if self._specs is not None and all(n.index in have for n in nodes):
-            return self._specs
-        blob, offs = [], {}
-        size = int(_lib.load().nao_verdict_spec_bytes())
-        for k, node in enumerate(nodes):
-            tau_a, tau_r = self._taus(node.name)
-            blob.append(_lib.verdict_spec(self.grid, tau_a, tau_r, self.epsilon))
-            offs[node.index] = k * size
-        dev_blob = torch.frombuffer(bytearray(b"".join(blob)), dtype=torch.uint8).to(self.dev)
-        self._specs = (dev_blob, offs)
-        return self._specs
+        """Device address of every node's nao_verdict_spec in [start, end); the
+        missing ones are uploaded in one copy."""
+        if getattr(self, "_spec_for", None) is not self.thresholds:  # thresholds replaced
+            self._spec_addr, self._tau_cache = {}, {}
+            self._spec_for = self.thresholds
+        missing = [n for n in self.g.nodes[start:end] if n.index not in self._spec_addr]
+        if missing:
+            size = int(_lib.load().nao_verdict_spec_bytes())
+            blob = b"".join(_lib.verdict_spec(self.grid, *self._taus(n.name), self.epsilon)
+                            for n in missing)
+            dev_blob = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(self.dev)
+            self._spec_blobs.append(dev_blob)
+            for k, n in enumerate(missing):
+                self._spec_addr[n.index] = dev_blob.data_ptr() + k * size
+        return self._spec_addr
 
     # ----------------------------------------------------------------- run
     def run(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
@@ -368,8 +372,7 @@ class StreamingVerifier:
             i = node.index - start
             desc = None
             if y.numel() and self.fuse_check:
-                blob, offs = st.specs
-                desc = _lib.CheckDesc(y.data_ptr(), eps_ptr, blob.data_ptr() + offs[node.index],
+                desc = _lib.CheckDesc(y.data_ptr(), eps_ptr, st.specs[node.index],
                                       st.records[i].data_ptr(), scale, lo_f, kind,
                                       _lib.CHECK_PARTIAL if self.partial else 0)
                 st.pend_keep.append(y)
