@@ -154,11 +154,18 @@ struct CheckedWords {
     const uint32_t* __restrict__ p;  // claimed (hashed)
     const uint32_t* __restrict__ q;  // local
     unsigned long long* mask;        // this thread's mask words (stride kLeafThreads)
+    const char* eps;                 // bound tensor of this chunk (NAO_EPS_TENSOR_*), or null
+    int eps_shift;                   // log2 of its element size
     __device__ __forceinline__ void cmp(uint32_t c, uint32_t y, uint32_t i) const {
 #if NAO_CC_PROBE == 2  // timing probe: no compare at all (wrong verdicts)
         (void)c; (void)y; (void)i;
 #else
-        if (word_needs_check(c, y)) mask[(i >> 6) * kLeafThreads] |= 1ull << (i & 63);
+        if (word_needs_check(c, y)) {
+            mask[(i >> 6) * kLeafThreads] |= 1ull << (i & 63);
+            // the check reads this element's bound after the chunk is hashed:
+            // start pulling it into L2 now (nothing else touches it before)
+            if (eps) asm volatile("prefetch.global.L2 [%0];" ::"l"(eps + ((size_t)i << eps_shift)));
+        }
 #endif
     }
     __device__ __forceinline__ uint4 v4(uint32_t i) const {
@@ -294,9 +301,12 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         const uint32_t nw = (uint32_t)(total_w - off_w < cw ? total_w - off_w : cw);
         uint32_t dg[8];
         if (check) {
+            const bool et = d.eps_kind == NAO_EPS_TENSOR_F32 || d.eps_kind == NAO_EPS_TENSOR_F64;
+            const int esh = d.eps_kind == NAO_EPS_TENSOR_F64 ? 3 : 2;
             CheckedWords ld{tab.payload[s] + off_w,
                             reinterpret_cast<const uint32_t*>(d.local) + off_w,
-                            s_mask + threadIdx.x};
+                            s_mask + threadIdx.x,
+                            et ? static_cast<const char*>(d.eps) + (off_w << esh) : nullptr, esh};
             hash_tagged_words<ALG>(ld, nw, 0u, dg);
         } else {
             GlobalWords ld{tab.payload[s] + off_w};
