@@ -143,12 +143,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only knobs: run N ranks on one GPU over gloo to exercise the
+    # multi-rank path (NAO_BENCH_DEVICE=0 NAO_BENCH_BACKEND=gloo)
+    local = int(os.environ.get("NAO_BENCH_DEVICE", local))
+    backend = os.environ.get("NAO_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     if args.main_priority:
         torch.cuda.set_stream(torch.cuda.Stream(dev, priority=args.main_priority))
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
@@ -238,7 +246,7 @@ def run_ours(args):
             dist.barrier()
         ms = e0.elapsed_time(e1) / k
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -323,7 +331,8 @@ def run_ours(args):
     for _ in range(args.steps):
         roots, recs, troot = verified_step(e2e=True)
         if world > 1:
-            roots, recs = shard.gather_node_records(roots, recs)
+            roots, recs = shard.gather_node_records(roots.to(coll_dev), recs.to(coll_dev))
+            roots, recs = roots.to(dev), recs.to(dev)
             if rank == 0:
                 troot = sv.trace_root(roots)
         host_roots, host_recs = roots.cpu(), recs.cpu()
@@ -331,7 +340,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
@@ -369,7 +378,13 @@ def run_ours(args):
 
     overhead = 100.0 * (t_ver - t_plain) / t_plain
     peaks = _peaks()
-    commit_bytes_per_step = stats.bytes_committed * (world if world > 1 else 1)
+    # whole-job totals (every rank's slice)
+    tot_bytes, tot_flops = float(stats.bytes_committed), float(stats.gemm_flops)
+    if world > 1:
+        t = torch.tensor([tot_bytes, tot_flops], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        tot_bytes, tot_flops = float(t[0]), float(t[1])
+    commit_bytes_per_step = tot_bytes
 
     # roofline of the dominant kernel (largest share of event-timed launch time)
     shares = {k: sum(v["ms"]) for k, v in timers.items()}
@@ -489,7 +504,7 @@ def run_ours(args):
         "overhead_excl_proposer_pct": round(100.0 * (t_ver - harness_ms - t_plain) / t_plain, 2),
         "merkle_gbs": round(merkle_gbs, 1) if merkle_gbs else None,
         "committed_gb_per_step": round(commit_bytes_per_step / 1e9, 2),
-        "gemm_tflop_per_step": round(stats.gemm_flops / 1e12, 2),
+        "gemm_tflop_per_step": round(tot_flops / 1e12, 2),
         "verdicts": {"nodes": n_nodes, "bound_violation_nodes": viol_nodes[:10],
                      "threshold_exceeded_nodes": exceed_nodes[:10],
                      "borderline_elements": int(n_border), "planted_fault": fault},
