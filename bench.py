@@ -472,6 +472,13 @@ def run_ours(args):
     commit_ms = (shares.get("nao_merkle_commit_tensors", 0.0) +
                  shares.get("nao_commit_check_tensors", 0.0))
     merkle_gbs = (stats.bytes_committed / (commit_ms * 1e-3) / 1e9) if commit_ms else None
+    # whole job: every rank's committed bytes over the slowest rank's commit time
+    commit_ms_max = commit_ms
+    if world > 1:
+        t = torch.tensor([commit_ms], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        commit_ms_max = float(t.item())
+    merkle_gbs_job = (tot_bytes / (commit_ms_max * 1e-3) / 1e9) if commit_ms_max else None
 
     if rank != 0:
         if world > 1:
@@ -503,6 +510,7 @@ def run_ours(args):
         # approximate: overhead with the proposer's serial share removed
         "overhead_excl_proposer_pct": round(100.0 * (t_ver - harness_ms - t_plain) / t_plain, 2),
         "merkle_gbs": round(merkle_gbs, 1) if merkle_gbs else None,
+        "merkle_gbs_whole_job": round(merkle_gbs_job, 1) if merkle_gbs_job else None,
         "committed_gb_per_step": round(commit_bytes_per_step / 1e9, 2),
         "gemm_tflop_per_step": round(tot_flops / 1e12, 2),
         "verdicts": {"nodes": n_nodes, "bound_violation_nodes": viol_nodes[:10],

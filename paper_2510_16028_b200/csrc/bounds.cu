@@ -718,6 +718,157 @@ __global__ void __launch_bounds__(kThreads) k_rows_smem(
 }
 
 // ---------------------------------------------------------------------------
+// Rows too long for shared memory (layernorm / sum / mean / max / min with
+// n > 24576, e.g. GroupNorm rows C/G*H*W of a 64x64 UNet level): one CTA per
+// row streams the row through a double-buffered smem tile.  While thread 0
+// runs the profile's serial FP32 fold over tile t (the critical path: one
+// dependent FADD per element), warps 1-7 load tile t+1 and accumulate the
+// order-free FP64 template sums.  Layernorm makes a second pass for the fold
+// over sq = (x - mu)^2 (the loaders write sq into the tile) and a third,
+// all-thread elementwise pass for y and eps.  DRAM traffic = 2-3 reads of x +
+// writes of y and eps; time ~ passes x n x FADD latency per row, rows in parallel.
+constexpr int kStreamTile = 8192;  // floats per tile (2 tiles = 64 KB smem)
+
+__device__ __forceinline__ float fold_tile(float acc, const float* t, int L, bool first, int kind) {
+    int c = 0;
+    if (first) { acc = t[0]; c = 1; }
+    if (kind >= 4) {
+        for (; c < L; c++) acc = kind == 4 ? fmaxf(acc, t[c]) : fminf(acc, t[c]);
+        return acc;
+    }
+    for (; c < L && (c & 3); c++) acc = __fadd_rn(acc, t[c]);
+    const float4* t4 = reinterpret_cast<const float4*>(t + c);
+    const int n4 = (L - c) >> 2;
+    int k = 0;
+    for (; k + 8 <= n4; k += 8) {
+        float4 b[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) b[j] = t4[k + j];
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, b[j].x), b[j].y), b[j].z), b[j].w);
+    }
+    for (; k < n4; k++) {
+        const float4 v = t4[k];
+        acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v.x), v.y), v.z), v.w);
+    }
+    for (c += 4 * n4; c < L; c++) acc = __fadd_rn(acc, t[c]);
+    return acc;
+}
+
+// kind: 1 layernorm, 2 sum, 3 mean, 4 max, 5 min
+__global__ void __launch_bounds__(kThreads) k_rows_stream(
+    const float* __restrict__ x, float* __restrict__ y, void* __restrict__ eps, int eps_f64,
+    int64_t rows, int64_t n, int kind, float ln_eps, double u, double rc, double slack) {
+    extern __shared__ __align__(16) float sbuf[];     // [2][kStreamTile]
+    __shared__ double red[kThreads / 32];
+    __shared__ float s_fold;
+    const int64_t r = blockIdx.x;
+    const float* xr = x + r * n;
+    const int ntiles = (int)((n + kStreamTile - 1) / kStreamTile);
+    const bool vec = ((reinterpret_cast<uintptr_t>(xr) | (uintptr_t)(n * 4)) & 15) == 0;
+    const double nd = (double)n;
+    float mu = 0.f;
+    double eps_mu = 0.0, ssq = 0.0, seps = 0.0, sabs = 0.0;
+
+    // loader: tile t -> buf, transformed (pass 0: x, pass 1: sq), FP64 sums on the way
+    auto load = [&](int t, int pass, int tid0, int nthr) {
+        float* b = sbuf + (t & 1) * kStreamTile;
+        const int64_t base = (int64_t)t * kStreamTile;
+        const int L = (int)(n - base < kStreamTile ? n - base : kStreamTile);
+        auto one = [&](float v) -> float {
+            if (pass == 0) {
+                if (kind <= 3) sabs = __dadd_rn(sabs, fabs((double)v));
+                return v;
+            }
+            const float xc = __fsub_rn(v, mu);
+            const float sq = __fmul_rn(xc, xc);
+            const double xc64 = fabs((double)xc), sq64 = (double)sq;
+            const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
+            ssq = __dadd_rn(ssq, sq64);
+            seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(__dmul_rn(2.0, xc64), eps_xc),
+                                             __dmul_rn(u, sq64)));
+            return sq;
+        };
+        if (vec) {
+            const float4* s4 = reinterpret_cast<const float4*>(xr + base);
+            float4* b4 = reinterpret_cast<float4*>(b);
+            for (int i = tid0; i < (L >> 2); i += nthr) {
+                float4 v = __ldg(s4 + i);
+                v.x = one(v.x); v.y = one(v.y); v.z = one(v.z); v.w = one(v.w);
+                b4[i] = v;
+            }
+            for (int i = 4 * (L >> 2) + tid0; i < L; i += nthr) b[i] = one(__ldg(xr + base + i));
+        } else {
+            for (int i = tid0; i < L; i += nthr) b[i] = one(__ldg(xr + base + i));
+        }
+    };
+
+    const int passes = kind == 1 ? 2 : 1;
+    for (int pass = 0; pass < passes; pass++) {
+        float acc = 0.f;
+        load(0, pass, threadIdx.x, kThreads);
+        __syncthreads();
+        for (int t = 0; t < ntiles; t++) {
+            if (threadIdx.x == 0) {
+                const int64_t base = (int64_t)t * kStreamTile;
+                const int L = (int)(n - base < kStreamTile ? n - base : kStreamTile);
+                acc = fold_tile(acc, sbuf + (t & 1) * kStreamTile, L, t == 0, kind);
+            } else if (threadIdx.x >= 32 && t + 1 < ntiles) {
+                load(t + 1, pass, threadIdx.x - 32, kThreads - 32);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) s_fold = acc;
+        if (pass == 0) {
+            sabs = block_sum(sabs, red);  // (syncs; publishes s_fold)
+            if (kind == 1) {
+                mu = __fdiv_rn(s_fold, (float)n);
+                eps_mu = __dadd_rn(__ddiv_rn(__dmul_rn(rc, sabs), nd), __dmul_rn(u, fabs((double)mu)));
+            }
+        } else {
+            ssq = block_sum(ssq, red);
+            seps = block_sum(seps, red);
+        }
+    }
+    if (kind >= 2) {
+        if (threadIdx.x == 0) {
+            float out = s_fold;
+            if (kind == 3) out = __fdiv_rn(out, (float)n);
+            y[r] = out;
+            double e = 0.0;
+            if (kind <= 3) {
+                e = __dmul_rn(rc, sabs);
+                if (kind == 3) e = __dadd_rn(__ddiv_rn(e, nd), __dmul_rn(u, fabs((double)out)));
+            }
+            if (eps) store_eps(eps, eps_f64, r, e, kind <= 3 ? slack : 0.0);
+        }
+        return;
+    }
+    // layernorm epilogue (bounds.py:159-168), same expressions as k_rows_smem
+    const float var = __fdiv_rn(s_fold, (float)n);
+    const float sp = __fadd_rn(var, ln_eps);
+    const float sigma = __fsqrt_rn(sp);
+    const double eps_ssq = __dadd_rn(__dmul_rn(rc, ssq), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+    const double eps_var = __dadd_rn(__ddiv_rn(eps_ssq, nd), __dmul_rn(u, fabs((double)var)));
+    const double eps_sp = __dadd_rn(eps_var, __dmul_rn(u, fabs((double)sp)));
+    const double sg64 = fabs((double)sigma), sg2 = __dmul_rn(sg64, sg64);
+    const double esg = __dadd_rn(__ddiv_rn(eps_sp, __dmul_rn(2.0, sg64)), __dmul_rn(u, sg64));
+    const double inv_sg = __ddiv_rn(1.0, sg64), k_sg2 = __ddiv_rn(esg, sg2);
+    float* yr = y + r * n;
+    for (int64_t c = threadIdx.x; c < n; c += kThreads) {
+        const float xc = __fsub_rn(__ldg(xr + c), mu);
+        const float yv = __fdiv_rn(xc, sigma);
+        yr[c] = yv;
+        const double xc64 = fabs((double)xc);
+        const double eps_xc = __dadd_rn(eps_mu, __dmul_rn(u, xc64));
+        const double v = __dadd_rn(__dadd_rn(__dmul_rn(eps_xc, inv_sg), __dmul_rn(xc64, k_sg2)),
+                                   __dmul_rn(u, fabs((double)yv)));
+        store_eps(eps, eps_f64, r * n + c, v, slack);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Softmax, design C (many long rows): three launches, each at full occupancy.
 //   K1 warp per row : m = max, e = fp32(exp64(x - m)) -> y, FP64 eps sums
 //   K2 lane per row : the profile's sequential FP32 fold S of e (32 rows per
@@ -943,6 +1094,19 @@ static int rows_per_cta(int64_t rows, int64_t n, int kind) {
 static int launch(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                   int kind, float ln_eps, double u, double rc, double slack, cudaStream_t st) {
     const int R = rows_per_cta(rows, n, kind);
+    if (R == 0 && kind >= 1 && n * 4 > 96 * 1024) {  // rows beyond shared memory
+        const size_t sm = 2 * kStreamTile * sizeof(float);
+        static bool attr_s = false;
+        if (!attr_s) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_rows_stream,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr_s = true;
+        }
+        k_rows_stream<<<(unsigned)rows, kThreads, sm, st>>>(x, y, eps, eps_f64, rows, n, kind, ln_eps,
+                                                            u, rc, slack);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     if (R == 0) return -1;
     const size_t smem = (size_t)(kind == 0 ? 2 : 1) * R * n * 4;
     static bool attr = false;

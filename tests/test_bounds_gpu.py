@@ -215,6 +215,27 @@ def test_softmax_layernorm_large_rows(B):
     assert_bound(e, e_ref, "layernorm")
 
 
+@pytest.mark.parametrize("shape", [(3, 81920), (2, 100003), (5, 24577)])
+@pytest.mark.parametrize("kind", ["layernorm", "sum", "mean", "max", "min"])
+def test_rows_beyond_shared_memory(B, kind, shape):
+    """GroupNorm-length rows (C/G*H*W up to 122880 in the SD UNet) stream
+    through the double-buffered one-CTA-per-row kernel: values bit-exact to the
+    sequential fold, bounds within [ref, ref(1+1e-5)]; odd n exercises the
+    unaligned (scalar) loader."""
+    from paper_2510_16028_b200.engine import DeviceProfile
+    rng = np.random.default_rng(shape[1] + len(kind))
+    x = (rng.standard_normal(shape) * 2 + 0.75).astype(np.float32)
+    attrs = {"axis": -1, "eps": 1e-5}
+    y_ref, e_ref = OB.op_bound(_Node(kind, attrs), [x], OB.FpModel())
+    y, e = B.op_bound(_Node(kind, attrs), [x], B.FpModel(), DeviceProfile("seq", "sequential"))
+    assert np.array_equal(np.asarray(y, np.float32).view(np.uint32),
+                          np.asarray(y_ref, np.float32).view(np.uint32)), kind
+    if kind in ("max", "min"):
+        assert not np.any(e)
+    else:
+        assert_bound(e, e_ref, kind)
+
+
 def test_mlp_co_execute_matches_reference(B, ref_mlp):
     """Full reference MLP (784-256-10, B=64) under the sequential profile:
     every node value bit-exact (digest), bounds within [ref, ref(1+1e-5)]."""
