@@ -260,6 +260,12 @@ int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, 
                        int64_t stride_b, int64_t stride_c, int transpose_b,
                        const nao_profile* profile, void* stream);
 
+/* conv2d lowering (SURVEY.md 2.3 extension): patch rows of an NCHW FP32 input,
+ * col[b, oh*OW + ow, (c*k + kh)*k + kw] (torch unfold's K order, zero padding
+ * included in K), row-major [batch, OH*OW, C*k*k].  OH = (H + 2 pad - k)/stride + 1. */
+int nao_im2col_rows(const float* x, float* col, int64_t batch, int64_t C, int64_t H, int64_t W,
+                    int64_t k, int64_t stride, int64_t pad, void* stream);
+
 /* Additive fault / drift hook on a node output (engine.py:325-351 `inject`):
  * out = y with +-1-ulp flips on ~n/period elements and a relative fault
  * `fault_scale` on ~n/fault_period elements (0 disables either).  Used to

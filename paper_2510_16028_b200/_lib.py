@@ -114,6 +114,8 @@ _SIGS = {
     "nao_reduce_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_int, c_dbl, c_dbl,
                                  c_dbl, ctypes.POINTER(Profile), c_vp]),
     "nao_unary_fp64": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
+    "nao_im2col_rows": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+                                c_vp]),
     "nao_scaled_abs_bound": (c_int, [c_vp, c_vp, c_int, c_i64, c_dbl, c_vp]),
     "nao_abs_gemm_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_i64, c_i64, c_i64,
                                    c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_dbl, c_vp, c_dbl,

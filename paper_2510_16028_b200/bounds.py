@@ -181,13 +181,15 @@ def tf32_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool
     return hi, lo
 
 
-def f16_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool):
+def f16_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool, owner=None):
     """|x| -> (hi, lo, row_exp): K-major [batch, rows, Kp] FP16 parts with
-    |x| <= 2^e (hi + 2^-10 lo) per row (nao_f16_split)."""
-    key = ("f16", id(x3))
+    |x| <= 2^e (hi + 2^-10 lo) per row (nao_f16_split).  `owner` (default x3)
+    is the tensor the cache entry is keyed on (a weight whose view x3 is)."""
+    owner = x3 if owner is None else owner
+    key = ("f16", id(owner))
     if cache:
         hit = _SPLITS.get(key)
-        if hit is not None and hit[0]() is x3 and hit[1] == x3._version:
+        if hit is not None and hit[0]() is owner and hit[1] == owner._version:
             return hit[2], hit[3], hit[4]
     batch = x3.numel() // (rows * K) if rows * K else 1
     if transpose and not cache:
@@ -204,15 +206,17 @@ def f16_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool)
     _lib.call("nao_f16_split", x3.data_ptr(), hi.data_ptr(), lo.data_ptr(), ex.data_ptr(), batch,
               rows, K, ld, rows * K, int(transpose), _lib.stream_ptr(x3.device))
     if cache:
-        _SPLITS[key] = (weakref.ref(x3, lambda _r, k=key: _SPLITS.pop(k, None)), x3._version,
-                        hi, lo, ex)
+        _SPLITS[key] = (weakref.ref(owner, lambda _r, k=key: _SPLITS.pop(k, None)),
+                        owner._version, hi, lo, ex)
     return hi, lo, ex
 
 
 def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
                    y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
-                   path: int | None = None, cache_b: bool = False) -> torch.Tensor:
-    """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors)."""
+                   path: int | None = None, cache_b: bool = False,
+                   a_owner: torch.Tensor | None = None) -> torch.Tensor:
+    """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors).
+    a_owner: A is a (2-D view of a) static weight -- cache its split on it."""
     a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
     path = default_gemm_path(K) if path is None else path
     eps = _eps_buffer(out_shape, a.device, eps_f64)
@@ -223,7 +227,8 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
             raise ValueError("linear bound: output shape mismatch")
     if path == _lib.GEMM_TC_F16X3:
         cb = cache_b and b3.data_ptr() == b.data_ptr()
-        ahi, alo, aex = f16_split(a3, M, K, False, False)
+        ca = a_owner is not None and a3.data_ptr() == a.data_ptr()
+        ahi, alo, aex = f16_split(a3, M, K, False, ca, a_owner if ca else None)
         bhi, blo, bex = f16_split(b if cb else b3, N, K, not transpose_b, cb)
         fix = _lib.gemm_fix_workspace(a.device)
         bsrc = b if cb else b3
@@ -440,14 +445,16 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
         return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64,
                                  cache_b=static_b)
     if kind == "conv2d":
+        # eps[b] = const |W| @ |col_b|^T: the weight is the (cached) A operand and
+        # the patch rows are K-major B rows, so the GEMM writes NCHW directly
         x, w = xs
         col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
                                   int(node.attr("pad", 0)))
         K = col.shape[-1]
         count = K if fma_of(profile) else 2 * K - 1
-        eps = abs_gemm_bound(col, w.reshape(w.shape[0], -1), model.reduction_const(count), True,
-                             eps_f64=f64, cache_b=True)
-        return y, eps.reshape(B, OH, OW, w.shape[0]).permute(0, 3, 1, 2).contiguous()
+        eps = abs_gemm_bound(w.reshape(w.shape[0], -1), col, model.reduction_const(count), True,
+                             eps_f64=f64, a_owner=w)
+        return y, eps.reshape(B, w.shape[0], OH, OW)
     raise ValueError(f"no bound template for kind {kind!r}")
 
 
@@ -455,10 +462,13 @@ def im2col(x: torch.Tensor, k: int, stride: int, pad: int):
     """[B, C, H, W] -> [B, OH*OW, C*k*k] patches (zero padding included in K,
     SURVEY.md 2.3), K ordered (c, kh, kw) as torch.nn.functional.unfold."""
     B, C, H, W = x.shape
-    col = torch.nn.functional.unfold(x, k, padding=pad, stride=stride)  # [B, C*k*k, L]
     OH = (H + 2 * pad - k) // stride + 1
     OW = (W + 2 * pad - k) // stride + 1
-    return col.transpose(1, 2).contiguous(), (B, OH, OW)
+    xc = x.contiguous()
+    col = torch.empty((B, OH * OW, C * k * k), dtype=torch.float32, device=x.device)
+    _lib.call("nao_im2col_rows", xc.data_ptr(), col.data_ptr(), B, C, H, W, k, stride, pad,
+              _lib.stream_ptr(x.device))
+    return col, (B, OH, OW)
 
 
 def op_bound(node, arrays, model: FpModel, profile=None):

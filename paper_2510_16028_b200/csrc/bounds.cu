@@ -424,6 +424,54 @@ int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, doub
 
 }  // extern "C"
 
+// ------------------------------------------------------------ conv2d lowering
+// Patch rows of an NCHW input for the implicit-GEMM conv bound (SURVEY.md 2.3
+// extension): col[b, oh*OW + ow, (c*k + kh)*k + kw] = x[b, c, oh*s-p+kh, ow*s-p+kw]
+// (0 outside), i.e. torch unfold's K order, written row-major [B, OH*OW, K]
+// in one launch (consecutive threads -> consecutive K: coalesced stores; the
+// ~k*k-fold re-reads of x hit L1/L2).
+namespace nao {
+__global__ void k_im2col_rows(const float* __restrict__ x, float* __restrict__ col, int C, int H,
+                              int W, int k, int stride, int pad, int OH, int OW) {
+    const int b = blockIdx.y;
+    const int L = OH * OW, K = C * k * k;
+    const int64_t per_b = (int64_t)L * K;
+    const float* xb = x + (int64_t)b * C * H * W;
+    float* cb = col + (int64_t)b * per_b;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_b;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)(i / K), kk = (int)(i - (int64_t)p * K);
+        const int c = kk / (k * k), r = kk - c * k * k;
+        const int kh = r / k, kw = r - kh * k;
+        const int oh = p / OW, ow = p - oh * OW;
+        const int ih = oh * stride - pad + kh, iw = ow * stride - pad + kw;
+        float v = 0.f;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = __ldg(xb + ((int64_t)c * H + ih) * W + iw);
+        cb[i] = v;
+    }
+}
+}  // namespace nao
+
+extern "C" int nao_im2col_rows(const float* x, float* col, int64_t batch, int64_t C, int64_t H,
+                               int64_t W, int64_t k, int64_t stride, int64_t pad, void* stream) {
+    NAO_REQUIRE(batch >= 0 && C > 0 && H > 0 && W > 0 && k > 0 && stride > 0 && pad >= 0,
+                "im2col: bad geometry");
+    NAO_REQUIRE(batch <= 65535, "im2col: batch %lld > 65535", (long long)batch);
+    const int64_t OH = (H + 2 * pad - k) / stride + 1, OW = (W + 2 * pad - k) / stride + 1;
+    NAO_REQUIRE(OH > 0 && OW > 0, "im2col: empty output");
+    NAO_REQUIRE(OH * OW * C * k * k < (int64_t)1 << 31, "im2col: per-sample patch matrix too large");
+    if (batch == 0) return NAO_OK;
+    const int64_t per_b = OH * OW * C * k * k;
+    int64_t gx = (per_b + 255) / 256;
+    const int64_t cap = (int64_t)nao::kNumSMs * 16 / batch + 1;
+    if (gx > cap) gx = cap;
+    nao::k_im2col_rows<<<dim3((unsigned)gx, (unsigned)batch), 256, 0,
+                         static_cast<cudaStream_t>(stream)>>>(x, col, (int)C, (int)H, (int)W, (int)k,
+                                                              (int)stride, (int)pad, (int)OH, (int)OW);
+    NAO_CHECK_LAUNCH();
+    return NAO_OK;
+}
+
 // ------------------------------------------------------------ fault / drift hook
 // Mirrors the reference's additive `inject` hook on node outputs
 // (engine.py:325-351): the claimed value of element i is y_i moved by

@@ -309,3 +309,16 @@ def test_abs_gemm_tc_short_k_persistent(B, K, path):
                            y=torch.from_numpy(y).cuda(), u=u, eps_f64=False, path=path,
                            cache_b=True).cpu().numpy()
     assert_bound(got, ref, "linear")
+
+
+@pytest.mark.parametrize("geom", [(2, 3, 17, 13, 7, 2, 3), (3, 5, 8, 8, 3, 1, 1),
+                                  (1, 4, 9, 6, 1, 1, 0), (2, 2, 5, 7, 3, 2, 0)])
+def test_im2col_rows_matches_unfold(B, geom):
+    """nao_im2col_rows == torch unfold (K order c, kh, kw; zero padding) transposed
+    to [B, OH*OW, K]: the patch-row operand of the conv2d abs-GEMM bound."""
+    b, c, h, w, k, st, pd = geom
+    x = torch.randn((b, c, h, w), device="cuda")
+    col, (nb, oh, ow) = B.im2col(x, k, st, pd)
+    ref = torch.nn.functional.unfold(x, k, padding=pd, stride=st).transpose(1, 2)
+    assert (nb, oh * ow) == (b, ref.shape[1])
+    assert torch.equal(col, ref)
