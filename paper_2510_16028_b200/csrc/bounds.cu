@@ -431,23 +431,33 @@ int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, doub
 // in one launch (consecutive threads -> consecutive K: coalesced stores; the
 // ~k*k-fold re-reads of x hit L1/L2).
 namespace nao {
-__global__ void k_im2col_rows(const float* __restrict__ x, float* __restrict__ col, int C, int H,
-                              int W, int k, int stride, int pad, int OH, int OW) {
+// warp per patch row (oh, ow decoded once), lanes over K; KS = compile-time
+// kernel side (1/3/7 cover the configs) so the K decode is multiply-shift
+template <int KS>
+__global__ void __launch_bounds__(256) k_im2col_rows(const float* __restrict__ x,
+                                                     float* __restrict__ col, int C, int H, int W,
+                                                     int k_rt, int stride, int pad, int OH, int OW) {
+    const int k = KS > 0 ? KS : k_rt;
+    const int kk2 = k * k;
     const int b = blockIdx.y;
-    const int L = OH * OW, K = C * k * k;
-    const int64_t per_b = (int64_t)L * K;
+    const int L = OH * OW, K = C * kk2;
     const float* xb = x + (int64_t)b * C * H * W;
-    float* cb = col + (int64_t)b * per_b;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_b;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int p = (int)(i / K), kk = (int)(i - (int64_t)p * K);
-        const int c = kk / (k * k), r = kk - c * k * k;
-        const int kh = r / k, kw = r - kh * k;
+    float* cb = col + (int64_t)b * L * K;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < L; p += nw) {
         const int oh = p / OW, ow = p - oh * OW;
-        const int ih = oh * stride - pad + kh, iw = ow * stride - pad + kw;
-        float v = 0.f;
-        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = __ldg(xb + ((int64_t)c * H + ih) * W + iw);
-        cb[i] = v;
+        const int ih0 = oh * stride - pad, iw0 = ow * stride - pad;
+        float* crow = cb + (int64_t)p * K;
+        for (int kk = lane; kk < K; kk += 32) {
+            const int c = kk / kk2, r = kk - c * kk2;
+            const int kh = r / k, kw = r - kh * k;
+            const int ih = ih0 + kh, iw = iw0 + kw;
+            float v = 0.f;
+            if ((unsigned)ih < (unsigned)H && (unsigned)iw < (unsigned)W)
+                v = __ldg(xb + ((int64_t)c * H + ih) * W + iw);
+            crow[kk] = v;
+        }
     }
 }
 }  // namespace nao
@@ -461,13 +471,18 @@ extern "C" int nao_im2col_rows(const float* x, float* col, int64_t batch, int64_
     NAO_REQUIRE(OH > 0 && OW > 0, "im2col: empty output");
     NAO_REQUIRE(OH * OW * C * k * k < (int64_t)1 << 31, "im2col: per-sample patch matrix too large");
     if (batch == 0) return NAO_OK;
-    const int64_t per_b = OH * OW * C * k * k;
-    int64_t gx = (per_b + 255) / 256;
-    const int64_t cap = (int64_t)nao::kNumSMs * 16 / batch + 1;
+    int64_t gx = (OH * OW + 7) / 8;  // 8 warps (rows) per CTA
+    const int64_t cap = (int64_t)nao::kNumSMs * 8 / batch + 1;
     if (gx > cap) gx = cap;
-    nao::k_im2col_rows<<<dim3((unsigned)gx, (unsigned)batch), 256, 0,
-                         static_cast<cudaStream_t>(stream)>>>(x, col, (int)C, (int)H, (int)W, (int)k,
-                                                              (int)stride, (int)pad, (int)OH, (int)OW);
+    const dim3 grid((unsigned)gx, (unsigned)batch);
+    auto st = static_cast<cudaStream_t>(stream);
+#define NAO_IM2COL(KS) nao::k_im2col_rows<KS><<<grid, 256, 0, st>>>( \
+        x, col, (int)C, (int)H, (int)W, (int)k, (int)stride, (int)pad, (int)OH, (int)OW)
+    if (k == 1) NAO_IM2COL(1);
+    else if (k == 3) NAO_IM2COL(3);
+    else if (k == 7) NAO_IM2COL(7);
+    else NAO_IM2COL(0);
+#undef NAO_IM2COL
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }
@@ -1100,12 +1115,155 @@ __global__ void __launch_bounds__(256) k_smc_epi(const float* __restrict__ x, fl
     }
 }
 
+// ---------------------------------------------------------------------------
+// Softmax, design G (many rows, 16-byte aligned, R rows of e fit in ~64 KB):
+// one CTA per group of R rows, persistent over groups, e kept in shared memory
+// so HBM sees read x + write y + write eps (12-16 B/element; the epilogue's
+// re-read of x hits L2).  Phase 1 warp per row (max, e = fp32(exp64(x-m)) ->
+// smem, FP64 eps sums); phase 2 lane r of warp 0 runs row r's sequential fold
+// from smem (conflict-free: rows padded to n+4 floats); phase 3 warp per row
+// epilogue.  2-3 CTAs per SM overlap one CTA's serial fold with the others'
+// memory phases.
+constexpr int kSmgBudget = 72 * 1024;
+
+__global__ void __launch_bounds__(256) k_smg(const float* __restrict__ x, float* __restrict__ y,
+                                             void* __restrict__ eps, int eps_f64, int64_t rows,
+                                             int n, int R, double u, double rc, double slack) {
+    extern __shared__ __align__(16) float s_e[];  // [R][n + 4]
+    __shared__ float s_m[32], s_S[32];
+    __shared__ double s_epsS[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ns = n + 4, n4 = n >> 2;
+    const double two_u = __dmul_rn(2.0, u);
+    const double sl = __dadd_rn(1.0, slack);
+    for (int64_t g0 = (int64_t)blockIdx.x * R; g0 < rows; g0 += (int64_t)gridDim.x * R) {
+        const int nr = (int)(rows - g0 < R ? rows - g0 : R);
+        // phase 1
+        for (int r = w; r < nr; r += 8) {
+            const float4* x4 = reinterpret_cast<const float4*>(x + (g0 + r) * n);
+            float m = -INFINITY;
+            for (int c = lane; c < n4; c += 32) {
+                const float4 v = __ldg(x4 + c);
+                m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const double m64a = fabs((double)m);
+            double se = 0.0, seps = 0.0;
+            auto one = [&](float xv) -> float {
+                const float ev = (float)exp((double)__fsub_rn(xv, m));
+                const double e64 = (double)ev;
+                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
+                se = __dadd_rn(se, e64);
+                seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64)));
+                return ev;
+            };
+            float4* e4 = reinterpret_cast<float4*>(s_e + (size_t)r * ns);
+            for (int c = lane; c < n4; c += 32) {
+                const float4 v = __ldg(x4 + c);
+                float4 e;
+                e.x = one(v.x); e.y = one(v.y); e.z = one(v.z); e.w = one(v.w);
+                e4[c] = e;
+            }
+            se = warp_sum(se);
+            seps = warp_sum(seps);
+            if (lane == 0) {
+                s_m[r] = m;
+                s_epsS[r] = __dadd_rn(__dmul_rn(rc, se), __dmul_rn(__dadd_rn(rc, 1.0), seps));
+            }
+        }
+        __syncthreads();
+        // phase 2: S = (((e0 + e1) + e2) + ...)
+        if (threadIdx.x < nr) {
+            const float4* e4 = reinterpret_cast<const float4*>(s_e + (size_t)threadIdx.x * ns);
+            float4 v = e4[0];
+            float acc = __fadd_rn(__fadd_rn(__fadd_rn(v.x, v.y), v.z), v.w);
+            int c = 1;
+            for (; c + 8 <= n4; c += 8) {
+                float4 b[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) b[k] = e4[c + k];
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, b[k].x), b[k].y), b[k].z),
+                                    b[k].w);
+            }
+            for (; c < n4; c++) {
+                v = e4[c];
+                acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v.x), v.y), v.z), v.w);
+            }
+            s_S[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        // phase 3
+        for (int r = w; r < nr; r += 8) {
+            const float S = s_S[r];
+            const double S64 = (double)S, S2 = __dmul_rn(S64, S64);
+            const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(s_epsS[r], S2);
+            const double m64a = fabs((double)s_m[r]);
+            const int64_t ob = (g0 + r) * n;
+            const float4* x4 = reinterpret_cast<const float4*>(x + ob);
+            const float4* e4 = reinterpret_cast<const float4*>(s_e + (size_t)r * ns);
+            float4* y4 = reinterpret_cast<float4*>(y + ob);
+            for (int c = lane; c < n4; c += 32) {
+                const float4 xv = __ldg(x4 + c);
+                const float4 ev = e4[c];
+                const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, es[4] = {ev.x, ev.y, ev.z, ev.w};
+                float ys[4];
+                double vs[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    ys[k] = __fdiv_rn(es[k], S);
+                    const double e64 = (double)es[k];
+                    const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xs[k]), m64a));
+                    const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
+                    vs[k] = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
+                                      __dmul_rn(u, fabs((double)ys[k])));
+                }
+                __stcs(y4 + c, make_float4(ys[0], ys[1], ys[2], ys[3]));
+                if (eps_f64) {
+                    double2* e2 = reinterpret_cast<double2*>(static_cast<double*>(eps) + ob) + 2 * c;
+                    __stcs(e2, make_double2(__dmul_rn(vs[0], sl), __dmul_rn(vs[1], sl)));
+                    __stcs(e2 + 1, make_double2(__dmul_rn(vs[2], sl), __dmul_rn(vs[3], sl)));
+                } else {
+                    __stcs(reinterpret_cast<float4*>(static_cast<float*>(eps) + ob) + c, make_float4(
+                        __double2float_ru(__dmul_rn(vs[0], sl)), __double2float_ru(__dmul_rn(vs[1], sl)),
+                        __double2float_ru(__dmul_rn(vs[2], sl)), __double2float_ru(__dmul_rn(vs[3], sl))));
+                }
+            }
+        }
+        __syncthreads();  // s_e / s_S reused by the next group
+    }
+}
+
 // design C for many long rows (returns -1 when it does not apply)
 static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                      double u, double rc, double slack, cudaStream_t st) {
     if (n < 128 || rows < 1024) return -1;
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
                        reinterpret_cast<uintptr_t>(eps)) & 15) == 0 && (n & 3) == 0;
+    static const int design = [] {
+        const char* e = getenv("NAO_SOFTMAX_DESIGN");
+        return e && e[0] == 'C' ? 0 : 1;
+    }();
+    const int64_t row_bytes = (n + 4) * 4;
+    if (vec && design == 1 && row_bytes <= kSmgBudget && n < (1 << 30)) {
+        int R = (int)(kSmgBudget / row_bytes);
+        if (R > 32) R = 32;
+        if (R > 8) R &= ~7;
+        const size_t smem = (size_t)R * row_bytes;
+        static bool attr = false;
+        if (!attr) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_smg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                kSmgBudget));
+            attr = true;
+        }
+        const int64_t groups = ceil_div(rows, (int64_t)R);
+        const int64_t grid = std::min<int64_t>(groups, (int64_t)kNumSMs * 3);
+        k_smg<<<(unsigned)grid, 256, smem, st>>>(x, y, eps, eps_f64, rows, (int)n, R, u, rc, slack);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     const int64_t wblocks = std::min<int64_t>(ceil_div(rows, 8), (int64_t)kNumSMs * 8);
     if (vec) {
         k_smc_rows<true><<<(unsigned)wblocks, 256, 0, st>>>(x, y, eps, eps_f64, rows, n, u, rc);

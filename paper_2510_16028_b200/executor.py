@@ -396,6 +396,8 @@ class StreamingVerifier:
                 stats.bytes_committed += y.numel() * 4
                 if node.kind in ("matmul", "linear"):
                     stats.gemm_flops += 2 * y.numel() * xs[0].shape[-1]
+                elif node.kind == "conv2d":  # implicit GEMM, K = C k k
+                    stats.gemm_flops += 2 * y.numel() * xs[1][0].numel()
             del eps, y
             yc = yc.contiguous()
             values[node.index] = yc

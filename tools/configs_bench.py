@@ -40,7 +40,7 @@ def _build(name):
     raise ValueError(name)
 
 
-def run_config(name, steps, warmup, drift_period=16, profile=False):
+def run_config(name, steps, warmup, drift_period=16, profile=False, flush_mb=2048, graphs=0):
     from paper_2510_16028_b200.calibration import (PERCENTILE_GRID, OpThresholds, ThresholdSet,
                                                    error_profiles_device)
     from paper_2510_16028_b200.dispute import CheckRecord
@@ -66,35 +66,49 @@ def run_config(name, steps, warmup, drift_period=16, profile=False):
     th = ThresholdSet(alpha=3.0, epsilon=1e-12, grid=PERCENTILE_GRID,
                       ops=[OpThresholds(n, 3.0 * a.cpu().numpy(), 3.0 * r.cpu().numpy())
                            for n, (a, r) in env.items()])
-    sv = StreamingVerifier(g, None, thresholds=th, max_lag=4)
+    sv = StreamingVerifier(g, None, thresholds=th, max_lag=4, flush_bytes=flush_mb << 20)
 
     def claimed(node, y):
         return drift_claim(node, y, 1, drift_period, fault)
 
+    graphed = {}
+    host = {}
+
     def plain():
+        if "plain" in graphed:
+            return graphed["plain"].replay()
         return plain_forward(g, x, dev)
 
     def ver():
+        if "ver" in graphed:
+            return graphed["ver"].replay()
         return sv.run(x, claimed)
 
-    def timed(fn):
+    def timed(fn, key):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        h0 = time.perf_counter()
         for _ in range(steps):
             out = fn()
             del out
+        host[key] = (time.perf_counter() - h0) * 1e3 / steps
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / steps
 
     stats = NodeStats()
     _, recs = sv.run(x, claimed, stats=stats)
+    plain_forward(g, x, dev)
     torch.cuda.synchronize()
-    t_plain = timed(plain)
-    t_ver = timed(ver)
+    if graphs:
+        from paper_2510_16028_b200.executor import GraphedRun
+        graphed["plain"] = GraphedRun.record_plain(g, x, dev, 0, None, None, seg_nodes=graphs)
+        graphed["ver"] = sv.capture(x, claimed, seg_nodes=graphs)
+    t_plain = timed(plain, "plain")
+    t_ver = timed(ver, "verified")
     _, recs = ver()
     torch.cuda.synchronize()
     if profile:  # top device kernels of one verified step (torch.profiler / CUPTI)
@@ -116,6 +130,12 @@ def run_config(name, steps, warmup, drift_period=16, profile=False):
             "overhead_pct": round(100.0 * (t_ver - t_plain) / t_plain, 1),
             "committed_gb_per_step": round(stats.bytes_committed / 1e9, 3),
             "gemm_tflop_per_step": round(stats.gemm_flops / 1e12, 3),
+            "host_enqueue_ms": {k: round(v, 2) for k, v in host.items()},
+            "mem_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+            "mem_reserved_gb": round(torch.cuda.memory_reserved() / 1e9, 1),
+            "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0),
+            "cuda_mallocs": torch.cuda.memory_stats().get("num_device_alloc", 0),
+            "dispatch": f"cuda graphs ({graphs}-node segments)" if graphs else "eager",
             "flagged_nodes": flagged, "planted_fault": fault, "steps": steps,
             "warmup": warmup}
 
@@ -126,16 +146,21 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--graphs", type=int, default=0, metavar="SEG")
+    ap.add_argument("--flush-mb", default="2048", help="comma list: commit batch sizes to try")
     a = ap.parse_args()
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     for name in a.configs.split(","):
-        t0 = time.perf_counter()
-        line = run_config(name, a.steps, a.warmup, profile=a.profile)
-        line["wall_s"] = round(time.perf_counter() - t0, 1)
-        print(json.dumps(line), flush=True)
-        torch.cuda.empty_cache()
+        for fmb in (int(v) for v in a.flush_mb.split(",")):
+            t0 = time.perf_counter()
+            line = run_config(name, a.steps, a.warmup, profile=a.profile, flush_mb=fmb,
+                              graphs=a.graphs)
+            line["flush_mb"] = fmb
+            line["wall_s"] = round(time.perf_counter() - t0, 1)
+            print(json.dumps(line), flush=True)
+            torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

@@ -40,6 +40,22 @@ def timeit(fn, reps=10, warm=3):
     return e0.elapsed_time(e1) / reps
 
 
+def calltime(fn, reps=10, warm=3):
+    """Sum of the library calls' event-timed durations (excludes Python-side
+    preparation between calls, e.g. per-tensor verdict specs)."""
+    from paper_2510_16028_b200 import _lib
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    store = {}
+    _lib.set_timer(store, lambda n, a: 0.0, torch.cuda.current_stream())
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    _lib.set_timer(None, None, None)
+    return sum(sum(v["ms"]) for v in store.values()) / reps
+
+
 def report(name, ms, bytes_=None, flops=None, **kw):
     d = {"kernel": name, "ms": round(ms, 4)}
     if bytes_:
@@ -97,6 +113,40 @@ def main():
                                                                          "keccak256"), a.reps), nb)
         report("commit_only_keccak", timeit(lambda: commit_tensors(ycs, 4096, "keccak256"),
                                             a.reps), nb)
+        # every tensor drifting, FP32 eps tensors (GEMM / conv outputs)
+        ycs2 = [inject_drift(y, 1, 16) for y in ys]
+        eps2 = [(y.abs() * 2 ** -20).float() for y in ys]
+        report("commit_check_keccak_alldrift_epsT",
+               timeit(lambda: commit_check_nodes(ycs2, ys, eps2, taus, 4096, "keccak256"), a.reps),
+               nb)
+        ycs3 = [y.clone() for y in ys]
+        report("commit_check_keccak_nodrift_epsT",
+               timeit(lambda: commit_check_nodes(ycs3, ys, eps2, taus, 4096, "keccak256"), a.reps),
+               nb)
+        # many small tensors (UNet-like: 1M-element node outputs)
+        sm = [torch.randn(1 << 20, device=dev) for _ in range(256)]
+        smc = [inject_drift(y, 1, 16) for y in sm]
+        report("commit_check_keccak_256x4MB",
+               timeit(lambda: commit_check_nodes(smc, sm, [("scaled", 2 ** -23)] * 256,
+                                                 [(tau, tau)] * 256, 4096, "keccak256"), a.reps),
+               256 * 4 << 20)
+        report("commit_check_keccak_256x4MB_calls",
+               calltime(lambda: commit_check_nodes(smc, sm, [("scaled", 2 ** -23)] * 256,
+                                                   [(tau, tau)] * 256, 4096, "keccak256"), a.reps),
+               256 * 4 << 20)
+        report("commit_only_keccak_256x4MB", timeit(lambda: commit_tensors(smc, 4096, "keccak256"),
+                                                    a.reps), 256 * 4 << 20)
+        inf = np.full(23, np.inf)
+        report("commit_check_keccak_256x4MB_inf_tau",
+               timeit(lambda: commit_check_nodes(smc, sm, [("scaled", 2 ** -23)] * 256,
+                                                 [(inf, inf)] * 256, 4096, "keccak256"), a.reps),
+               256 * 4 << 20)
+        big = [torch.cat(sm)]
+        bigc = [torch.cat(smc)]
+        report("commit_check_keccak_1x1GB",
+               timeit(lambda: commit_check_nodes(bigc, big, [("scaled", 2 ** -23)],
+                                                 [(tau, tau)], 4096, "keccak256"), a.reps),
+               256 * 4 << 20)
     if want("softmax"):
         x = torch.randn((NH, S, S), device=dev) * 3
         n = x.numel()
