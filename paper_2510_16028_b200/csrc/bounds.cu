@@ -1148,14 +1148,14 @@ __global__ void __launch_bounds__(256) k_smg(const float* __restrict__ x, float*
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            const double m64a = fabs((double)m);
-            double se = 0.0, seps = 0.0;
+            // sum eps_e = sum e (u(|x| + |m|) + 2u) = u sum e|x| + (u|m| + 2u) sum e:
+            // two order-free FP64 sums (re-association covered by `slack`)
+            double se = 0.0, sex = 0.0;
             auto one = [&](float xv) -> float {
                 const float ev = (float)exp((double)__fsub_rn(xv, m));
                 const double e64 = (double)ev;
-                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
                 se = __dadd_rn(se, e64);
-                seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64)));
+                sex = __fma_rn(e64, fabs((double)xv), sex);
                 return ev;
             };
             float4* e4 = reinterpret_cast<float4*>(s_e + (size_t)r * ns);
@@ -1166,8 +1166,10 @@ __global__ void __launch_bounds__(256) k_smg(const float* __restrict__ x, float*
                 e4[c] = e;
             }
             se = warp_sum(se);
-            seps = warp_sum(seps);
+            sex = warp_sum(sex);
             if (lane == 0) {
+                const double um2 = __dadd_rn(__dmul_rn(u, fabs((double)m)), two_u);
+                const double seps = __dadd_rn(__dmul_rn(u, sex), __dmul_rn(um2, se));
                 s_m[r] = m;
                 s_epsS[r] = __dadd_rn(__dmul_rn(rc, se), __dmul_rn(__dadd_rn(rc, 1.0), seps));
             }
@@ -1197,10 +1199,17 @@ __global__ void __launch_bounds__(256) k_smg(const float* __restrict__ x, float*
         __syncthreads();
         // phase 3
         for (int r = w; r < nr; r += 8) {
+            // eps_y = e (u(|x|+|m|) + 2u)/S + e epsS/S^2 + u|y| = e (A|x| + B) + u|y|,
+            // A = u/S, B = (u|m| + 2u)/S + epsS/S^2, all terms >= 0 (a few FP64
+            // ulps from bounds.py's order, covered by `slack`); the (1 + slack)
+            // factor is folded into A, B and u
             const float S = s_S[r];
-            const double S64 = (double)S, S2 = __dmul_rn(S64, S64);
-            const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(s_epsS[r], S2);
-            const double m64a = fabs((double)s_m[r]);
+            const double S64 = (double)S;
+            const double A = __dmul_rn(__ddiv_rn(u, S64), sl);
+            const double B = __dmul_rn(__dadd_rn(
+                __ddiv_rn(__dadd_rn(__dmul_rn(u, fabs((double)s_m[r])), two_u), S64),
+                __ddiv_rn(s_epsS[r], __dmul_rn(S64, S64))), sl);
+            const double us = __dmul_rn(u, sl);
             const int64_t ob = (g0 + r) * n;
             const float4* x4 = reinterpret_cast<const float4*>(x + ob);
             const float4* e4 = reinterpret_cast<const float4*>(s_e + (size_t)r * ns);
@@ -1214,21 +1223,18 @@ __global__ void __launch_bounds__(256) k_smg(const float* __restrict__ x, float*
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     ys[k] = __fdiv_rn(es[k], S);
-                    const double e64 = (double)es[k];
-                    const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xs[k]), m64a));
-                    const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
-                    vs[k] = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
-                                      __dmul_rn(u, fabs((double)ys[k])));
+                    const double t = __fma_rn(A, fabs((double)xs[k]), B);
+                    vs[k] = __fma_rn((double)es[k], t, __dmul_rn(us, fabs((double)ys[k])));
                 }
                 __stcs(y4 + c, make_float4(ys[0], ys[1], ys[2], ys[3]));
                 if (eps_f64) {
                     double2* e2 = reinterpret_cast<double2*>(static_cast<double*>(eps) + ob) + 2 * c;
-                    __stcs(e2, make_double2(__dmul_rn(vs[0], sl), __dmul_rn(vs[1], sl)));
-                    __stcs(e2 + 1, make_double2(__dmul_rn(vs[2], sl), __dmul_rn(vs[3], sl)));
+                    __stcs(e2, make_double2(vs[0], vs[1]));
+                    __stcs(e2 + 1, make_double2(vs[2], vs[3]));
                 } else {
                     __stcs(reinterpret_cast<float4*>(static_cast<float*>(eps) + ob) + c, make_float4(
-                        __double2float_ru(__dmul_rn(vs[0], sl)), __double2float_ru(__dmul_rn(vs[1], sl)),
-                        __double2float_ru(__dmul_rn(vs[2], sl)), __double2float_ru(__dmul_rn(vs[3], sl))));
+                        __double2float_ru(vs[0]), __double2float_ru(vs[1]),
+                        __double2float_ru(vs[2]), __double2float_ru(vs[3])));
                 }
             }
         }
@@ -1247,8 +1253,13 @@ static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t r
         return e && e[0] == 'C' ? 0 : 1;
     }();
     const int64_t row_bytes = (n + 4) * 4;
-    if (vec && design == 1 && row_bytes <= kSmgBudget && n < (1 << 30)) {
-        int R = (int)(kSmgBudget / row_bytes);
+    static const int budget = [] {
+        const char* e = getenv("NAO_SMG_BUDGET");
+        const int b = e ? atoi(e) : kSmgBudget;
+        return b > 0 && b <= kSmgBudget ? b : kSmgBudget;
+    }();
+    if (vec && design == 1 && row_bytes <= budget && n < (1 << 30)) {
+        int R = (int)(budget / row_bytes);
         if (R > 32) R = 32;
         if (R > 8) R &= ~7;
         const size_t smem = (size_t)R * row_bytes;
@@ -1259,7 +1270,7 @@ static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t r
             attr = true;
         }
         const int64_t groups = ceil_div(rows, (int64_t)R);
-        const int64_t grid = std::min<int64_t>(groups, (int64_t)kNumSMs * 3);
+        const int64_t grid = std::min<int64_t>(groups, (int64_t)kNumSMs * (kSmgBudget * 3 / budget));
         k_smg<<<(unsigned)grid, 256, smem, st>>>(x, y, eps, eps_f64, rows, (int)n, R, u, rc, slack);
         NAO_CHECK_LAUNCH();
         return NAO_OK;
