@@ -322,3 +322,35 @@ def test_im2col_rows_matches_unfold(B, geom):
     ref = torch.nn.functional.unfold(x, k, padding=pd, stride=st).transpose(1, 2)
     assert (nb, oh * ow) == (b, ref.shape[1])
     assert torch.equal(col, ref)
+
+
+def test_softmax_design_g_parity():
+    """The opt-in shared-memory softmax (NAO_SOFTMAX_DESIGN=G, read once per
+    process) against the oracle, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from oracle import bounds as OB\n"
+        "from paper_2510_16028_b200 import bounds as B\n"
+        "for shape in ((1030, 2048), (2048, 1024), (1500, 516)):\n"
+        "    rng = np.random.default_rng(shape[1])\n"
+        "    x = (rng.standard_normal(shape) * 4).astype(np.float32)\n"
+        "    x[3, :7] = -np.inf\n"
+        "    y_ref, e_ref = OB.softmax_bound_parts(x, -1, OB.FpModel())\n"
+        "    for f64 in (True, False):\n"
+        "        y, e = B.softmax_device(torch.from_numpy(x).cuda(), -1, B.FpModel(), eps_f64=f64)\n"
+        "        y, e = y.cpu().numpy(), e.cpu().numpy().astype(np.float64)\n"
+        "        assert np.array_equal(y.view(np.uint32), y_ref.view(np.uint32))\n"
+        "        ok = ~np.isnan(e_ref)\n"
+        "        assert np.array_equal(np.isnan(e), ~ok)\n"
+        "        assert np.all(e[ok] >= e_ref[ok])\n"
+        "        sp = 0 if f64 else 2 * np.spacing(e_ref[ok].astype(np.float32))\n"
+        "        assert np.all(e[ok] <= e_ref[ok] * (1 + 1e-5) + sp)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, NAO_SOFTMAX_DESIGN="G", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
