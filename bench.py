@@ -35,6 +35,10 @@ from pathlib import Path
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
+# many distinct large tensor sizes per step (node outputs, bounds, splits):
+# expandable segments keep the caching allocator from fragmenting into
+# cudaMalloc retries (device syncs) on the UNet-sized graphs
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 METRIC = "bounds+check+commit overhead % vs FP32 fwd (Qwen3-8B shape); Merkle GB/s"
 UNIT = "%"
 PCT = (0.0, 1.0) + tuple(float(p) for p in range(5, 100, 5)) + (99.0, 100.0)

@@ -15,11 +15,16 @@ from __future__ import annotations
 import argparse
 import dataclasses
 import json
+import os
 import sys
 import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+# many distinct large tensor sizes per step (node outputs, bounds, splits):
+# expandable segments keep the caching allocator from fragmenting into
+# cudaMalloc retries (device syncs) on the UNet-sized graphs
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 import torch  # noqa: E402
 
@@ -133,6 +138,8 @@ def run_config(name, steps, warmup, drift_period=16, profile=False, flush_mb=204
             "host_enqueue_ms": {k: round(v, 2) for k, v in host.items()},
             "mem_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
             "mem_reserved_gb": round(torch.cuda.memory_reserved() / 1e9, 1),
+            "mem_peak_reserved_gb": round(torch.cuda.max_memory_reserved() / 1e9, 1),
+            "device_free_total_gb": [round(v / 1e9, 1) for v in torch.cuda.mem_get_info()],
             "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0),
             "cuda_mallocs": torch.cuda.memory_stats().get("num_device_alloc", 0),
             "dispatch": f"cuda graphs ({graphs}-node segments)" if graphs else "eager",
@@ -161,6 +168,7 @@ def main():
             line["wall_s"] = round(time.perf_counter() - t0, 1)
             print(json.dumps(line), flush=True)
             torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
 
 
 if __name__ == "__main__":
