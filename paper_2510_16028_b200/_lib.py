@@ -238,12 +238,19 @@ def dbl_array(values):
 _ws: dict = {}
 
 
+_ws_captured: list = []  # scratch buffers baked into captured CUDA graphs
+
+
 def workspace(nbytes: int, device) -> torch.Tensor:
-    """Per (device, stream) growable scratch buffer."""
+    """Per (device, stream) growable scratch buffer.  A buffer outgrown while
+    a CUDA graph is being captured stays alive: the graph's earlier kernels
+    keep its address (replaying them after it was freed faults)."""
     dev = torch.device(device)
     key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
+        if buf is not None and torch.cuda.is_current_stream_capturing():
+            _ws_captured.append(buf)
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
         _ws[key] = buf
     return buf

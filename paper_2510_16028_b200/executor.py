@@ -196,6 +196,7 @@ class StreamingVerifier:
         # side stream that runs behind, e.g. under a high-priority main stream)
         self.max_lag = int(max_lag)
         self._com_events = []
+        self._host_events = []
         # partial: records are combinable nao_check_partial rows (a batch shard of
         # every node; shard.combine_shard_records decides the whole-tensor verdicts)
         self.partial = bool(partial)
@@ -332,7 +333,16 @@ class StreamingVerifier:
                 ev.record(s_com)
                 self._com_events.append(ev)
                 if len(self._com_events) > self.max_lag:
-                    main.wait_event(self._com_events.pop(0))
+                    old_ev = self._com_events.pop(0)
+                    main.wait_event(old_ev)
+                    # the host may not run more than 4 x max_lag further flushes
+                    # ahead of the GPU: blocks freed while a side stream still uses
+                    # them stay reserved until it passes, so unbounded run-ahead
+                    # turns into allocator OOM retries (device syncs) on large
+                    # graphs (a tighter bound starves host-heavy graphs: GPT-2)
+                    self._host_events.append(old_ev)
+                    if len(self._host_events) > 4 * self.max_lag:
+                        self._host_events.pop(0).synchronize()
             st.pending, st.pend_idx, st.pend_bytes = [], [], 0
             st.pend_checks, st.pend_keep = [], []
 

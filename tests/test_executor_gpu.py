@@ -308,3 +308,35 @@ def test_batch_sharded_verification_matches_whole_batch(world):
         exceeded += got[i]["threshold_exceeded"]
     assert exceeded > 0 and got[[n.name for n in g.nodes].index("l1_fc")]["n_violations"] > 0
     assert len(shard.shard_trace_root(roots_by_rank)) == 32
+
+
+def test_graphed_replay_survives_workspace_growth():
+    """Scratch grown between captured segments (small nodes first, a large one
+    later; 1 MiB minimum workspace) must not free the buffer earlier segments
+    were recorded with (regression: SD-UNet batch 1, illegal address on replay)."""
+    from paper_2510_16028_b200 import _lib
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.executor import StreamingVerifier, drift_claim
+    from paper_2510_16028_b200.graph import build_graph, input_ref
+    from paper_2510_16028_b200.lowerings import _Builder
+    b = _Builder()
+    h = b.add("a0", "exp", [input_ref("x")])
+    for i in range(1, 6):
+        h = b.add(f"a{i}", "tanh", [h])
+    big = b.add("wide", "concat", [h] * 4096, {"axis": 1})
+    out = b.add("out", "relu", [big])
+    g = build_graph(b.nodes, [("x", (64, 64))], b.weights, [out])
+    x = {"x": torch.randn((64, 64), device="cuda") * 0.1}
+    sv = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=64)
+    claimed = lambda node, y: drift_claim(node, y, seed=1, period=4)  # noqa: E731
+    r0, c0 = sv.run(x, claimed)
+    r0, c0 = r0.clone(), c0.clone()
+    _lib._ws.clear()  # force growth inside the capture
+    kept = len(_lib._ws_captured)
+    gr = sv.capture(x, claimed, seg_nodes=2)
+    assert len(_lib._ws_captured) > kept  # the outgrown buffer stays alive with the graph
+    torch.cuda.empty_cache()
+    for _ in range(3):
+        r1, c1 = gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(r1, r0) and torch.equal(c1, c0)

@@ -39,9 +39,13 @@ def _build(name):
     if name == "resnet18":
         return (L.build_resnet18(batch=32, side=224), "layer3.0.conv2",
                 "ResNet-18 FP32 batch 32 224x224")
-    if name == "unet":
+    if name == "unet":  # the 8-GPU batch-sharded config: one sample per GPU
+        return (L.build_unet(dataclasses.replace(L.SD15_UNET, batch=1)), "down1.res0.conv2",
+                "SD-1.5 UNet-shaped FP32 step, 64x64 latent, batch 8 over 8 GPUs "
+                "(per-GPU shard: batch 1)")
+    if name == "unet8":  # the whole batch on one GPU
         return (L.build_unet(L.SD15_UNET), "down1.res0.conv2",
-                "SD-1.5 UNet-shaped FP32 step, 64x64 latent, batch 8 (one GPU)")
+                "SD-1.5 UNet-shaped FP32 step, 64x64 latent, batch 8 on one GPU")
     raise ValueError(name)
 
 
@@ -113,6 +117,9 @@ def run_config(name, steps, warmup, drift_period=16, profile=False, flush_mb=204
         graphed["plain"] = GraphedRun.record_plain(g, x, dev, 0, None, None, seg_nodes=graphs)
         graphed["ver"] = sv.capture(x, claimed, seg_nodes=graphs)
     t_plain = timed(plain, "plain")
+    if t_plain * steps < 500.0:  # short steps: time >= ~0.5 s of work
+        steps = int(500.0 / max(t_plain, 1e-3)) + 1
+        t_plain = timed(plain, "plain")
     t_ver = timed(ver, "verified")
     _, recs = ver()
     torch.cuda.synchronize()
