@@ -211,6 +211,21 @@ def f16_split(x3: torch.Tensor, rows: int, K: int, transpose: bool, cache: bool,
     return hi, lo, ex
 
 
+_ACT_MEMO: list = []  # [(weakref(x3), version, M, K, hi, lo, ex)]: the last activation split
+
+
+def _act_split(x3: torch.Tensor, M: int, K: int):
+    """f16_split of a per-call A operand, memoised for the most recent tensor:
+    consecutive GEMMs reading the same activation (q/k/v, gate/up) split it once."""
+    if _ACT_MEMO:
+        ref, ver, m, k, hi, lo, ex = _ACT_MEMO[0]
+        if ref() is x3 and ver == x3._version and (m, k) == (M, K):
+            return hi, lo, ex
+    hi, lo, ex = f16_split(x3, M, K, False, False)
+    _ACT_MEMO[:] = [(weakref.ref(x3), x3._version, M, K, hi, lo, ex)]
+    return hi, lo, ex
+
+
 def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
                    y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
                    path: int | None = None, cache_b: bool = False,
@@ -228,7 +243,10 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
     if path == _lib.GEMM_TC_F16X3:
         cb = cache_b and b3.data_ptr() == b.data_ptr()
         ca = a_owner is not None and a3.data_ptr() == a.data_ptr()
-        ahi, alo, aex = f16_split(a3, M, K, False, ca, a_owner if ca else None)
+        if ca:
+            ahi, alo, aex = f16_split(a3, M, K, False, True, a_owner)
+        else:
+            ahi, alo, aex = _act_split(a3, M, K)
         bhi, blo, bex = f16_split(b if cb else b3, N, K, not transpose_b, cb)
         fix = _lib.gemm_fix_workspace(a.device)
         bsrc = b if cb else b3

@@ -165,6 +165,9 @@ def main():
     a = ap.parse_args()
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
+    # autotuned cuDNN algorithms for the conv values of both arms (the default
+    # heuristics pick slow FP32 algorithms for some batch-1 UNet shapes)
+    torch.backends.cudnn.benchmark = True
     torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     for name in a.configs.split(","):
         for fmb in (int(v) for v in a.flush_mb.split(",")):
