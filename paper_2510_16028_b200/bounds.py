@@ -226,6 +226,10 @@ def _act_split(x3: torch.Tensor, M: int, K: int):
     return hi, lo, ex
 
 
+def release_activation_split() -> None:
+    _ACT_MEMO.clear()
+
+
 def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=False,
                    y: torch.Tensor | None = None, u: float = 0.0, eps_f64=True,
                    path: int | None = None, cache_b: bool = False,

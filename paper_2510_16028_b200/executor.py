@@ -31,7 +31,7 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .bounds import FpModel, apply_value, op_bound_device
+from .bounds import FpModel, apply_value, op_bound_device, release_activation_split
 from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID
 from .commitments import DEFAULT_CHUNK_BYTES, alg_id, commit_tensors, root_of_digests
 from .dispute import new_result_buffer
@@ -428,6 +428,7 @@ class StreamingVerifier:
             main.wait_stream(s_chk)
             main.wait_stream(s_com)
         keep.clear()
+        release_activation_split()  # the memo must not pin a split past the segment
 
     # ------------------------------------------------------------ graphs
     def capture(self, inputs: dict, claimed_fn, start: int = 0, end: int | None = None,
