@@ -550,6 +550,7 @@ def co_execute(g, inputs, profile, model: FpModel, with_trace: bool = False):
                                  node_index=node.index, node_name=node.name)
         values.append(y)
         bounds.append(BoundTensor(tuple(y.shape), eps))
+    release_activation_split()
     outputs = [Tensor(values[parse_ref(r)[1]].shape, values[parse_ref(r)[1]]) for r in g.outputs]
     if not with_trace:
         return outputs, bounds
