@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .graph import parse_ref
 
 SHA256 = "sha256"
 KECCAK256 = "keccak256"
@@ -74,7 +75,10 @@ def canon_header(shape, dtype=np.float32) -> bytes:
 
 
 def canon_tensor(t) -> bytes:
-    arr = t.array if hasattr(t, "array") and not isinstance(t, np.ndarray) else np.asarray(t)
+    if isinstance(t, torch.Tensor):
+        arr = t.detach().cpu().numpy()
+    else:
+        arr = t.array if hasattr(t, "array") and not isinstance(t, np.ndarray) else np.asarray(t)
     if arr.dtype not in (np.float32, np.float64):
         raise ValueError(f"unsupported dtype {arr.dtype}")
     dt = np.dtype("<f4") if arr.dtype == np.float32 else np.dtype("<f8")
@@ -377,3 +381,71 @@ def verify_commitment(c: Commitment, input_tensors=None, output_tensors=None) ->
         return sha256(c.r_w + c.r_g + h_x + h_y + _meta_bytes(c.meta)) == c.c0
     except ValueError:
         return False
+
+
+# ------------------------------------------------- dispute-time records
+# (commitments.py:250-323 restated on this package's
+# MerkleTree / prove / verify; per-tensor digests come from tensor_digest,
+# device tensors included)
+
+def thresholds_tree(threshold_doc: dict, alg=SHA256) -> "MerkleTree":
+    """commitments.py:250-256: r_e over the canonical threshold file, one
+    header chunk (version, alpha, epsilon, grid), then one chunk per operator."""
+    header = {k: threshold_doc[k] for k in ("version", "alpha", "epsilon", "grid")}
+    chunks = [canonical_json_bytes(header)]
+    chunks += [canonical_json_bytes(entry) for entry in threshold_doc["ops"]]
+    return build_tree(chunks, alg)
+
+
+@dataclass(frozen=True)
+class SubgraphRecord:
+    """commitments.py:259-271: a child slice's indices, interface hashes and
+    inclusion proofs of every referenced weight and node signature."""
+    start: int
+    end: int
+    h_in: bytes
+    h_out: bytes
+    weight_proofs: tuple
+    sig_proofs: tuple
+
+
+def _frontier_tensors(fr, g, trace_tensors, inputs):
+    ins = ([inputs[n] for n in fr.in_inputs] + [g.weights[n] for n in fr.in_weights]
+           + [trace_tensors[i] for i in fr.in_nodes])
+    return ins, [trace_tensors[i] for i in fr.out_nodes]
+
+
+def make_subgraph_record(g, s, trace_tensors, inputs, wtree, wnames, gtree) -> SubgraphRecord:
+    """commitments.py:283-304."""
+    from .graph import frontiers
+    fr = frontiers(g, s)
+    ins, outs = _frontier_tensors(fr, g, trace_tensors, inputs)
+    referenced = set()
+    for i in range(s.start, s.end):
+        for ref in g.nodes[i].inputs:
+            cat, key = parse_ref(ref)
+            if cat == "weight":
+                referenced.add(key)
+    leaf_of = {n: i for i, n in enumerate(wnames)}
+    weight_proofs = tuple((name, prove(wtree, leaf_of[name])) for name in sorted(referenced))
+    sig_proofs = tuple((i, prove(gtree, i)) for i in range(s.start, s.end))
+    return SubgraphRecord(start=s.start, end=s.end, h_in=interface_hash(ins),
+                          h_out=interface_hash(outs), weight_proofs=weight_proofs,
+                          sig_proofs=sig_proofs)
+
+
+def verify_subgraph_record(record: SubgraphRecord, g, r_w: bytes, r_g: bytes, in_tensors,
+                           out_tensors) -> bool:
+    """commitments.py:307-323: weight membership, signature membership, then
+    the interface hashes recomputed from the observed tensors."""
+    for name, proof in record.weight_proofs:
+        if name not in g.weights or not verify(r_w, canon_tensor(g.weights[name]), proof):
+            return False
+    for index, proof in record.sig_proofs:
+        if not (0 <= index < g.n_nodes):
+            return False
+        if not verify(r_g, op_signature(g.nodes[index]), proof):
+            return False
+    if interface_hash(in_tensors) != record.h_in:
+        return False
+    return interface_hash(out_tensors) == record.h_out

@@ -267,3 +267,89 @@ __all__ = ["p_max", "observed_p_max", "screen", "select_offending", "check_node"
            "CheckRecord", "new_result_buffer", "commit_check_nodes", "combine_partials",
            "partial_from_bytes"]
 _ = ctypes
+
+
+# ------------------------------------------- challenger child re-execution
+# Challenger._child_offense (dispute.py:544-559) on the
+# GPU.  The child slice runs straight from the parent graph (no extracted
+# sub-graph object): boundary tensors keyed by the parent refs the reference's
+# SubgraphModule.placeholder_refs use ("input:<name>", "node:<i>"), weights
+# from the graph, values under the challenger's DeviceProfile.
+
+_FLOP_WEIGHTS = {"add": 1, "sub": 1, "mul": 1, "div": 1, "neg": 1, "relu": 1,
+                 "exp": 4, "log": 4, "sqrt": 2, "rsqrt": 3, "tanh": 4, "gelu": 8, "silu": 6}
+
+
+def node_flops(node, out_shape, in_shapes) -> int:
+    """engine.py:409-429 analytic FLOP model (+ the extension kinds: conv2d as
+    its implicit GEMM, the other extensions as data movement)."""
+    from .graph import DATA_MOVEMENT_KINDS
+    kind = node.kind
+    out_size = int(np.prod(out_shape, dtype=np.int64)) if out_shape else 1
+    if kind in DATA_MOVEMENT_KINDS or kind in ("transpose", "maxpool2d", "upsample2x"):
+        return 0
+    if kind in _FLOP_WEIGHTS:
+        return _FLOP_WEIGHTS[kind] * out_size
+    if kind in ("sum", "mean", "max", "min"):
+        return int(np.prod(in_shapes[0], dtype=np.int64))
+    if kind == "softmax":
+        return 4 * int(np.prod(in_shapes[0], dtype=np.int64))
+    if kind == "layernorm":
+        return 8 * int(np.prod(in_shapes[0], dtype=np.int64))
+    if kind == "matmul":
+        return 2 * in_shapes[0][-1] * out_size
+    if kind == "linear":
+        return 2 * in_shapes[0][-1] * out_size + out_size
+    if kind == "conv2d":
+        return 2 * int(np.prod(in_shapes[1][1:], dtype=np.int64)) * out_size
+    raise ValueError(f"no flop model for kind {kind!r}")
+
+
+def run_slice(g, s, boundary: dict, profile=None, device=None):
+    """engine.py:393-400 run_subgraph for nodes [s.start, s.end) of g on the
+    GPU.  Returns ({node index: value}, flops) -- flops as graph_flops
+    (engine.py:432-446) over the slice."""
+    from .bounds import FpModel, apply_value, op_bound_device
+    from .engine import DeviceProfile, ExecutionError
+    from .graph import parse_ref
+    profile = profile or DeviceProfile("seq", "sequential")
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    values, flops, model = {}, 0, FpModel()
+    for i in range(s.start, s.end):
+        node = g.nodes[i]
+        xs, from_boundary = [], []
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            if cat == "node" and s.contains(key):
+                xs.append(values[key])
+            elif cat == "weight":
+                xs.append(to_device(g.weights[key], dev))
+            else:
+                if ref not in boundary:
+                    raise ExecutionError(f"missing boundary tensor for {ref}")
+                xs.append(to_device(boundary[ref], dev))
+            from_boundary.append(cat != "weight" and not (cat == "node" and s.contains(key)))
+        if node.kind in ("softmax", "layernorm", "sum", "mean", "max", "min"):
+            y, _ = op_bound_device(node, xs, model, profile, eps_f64=None)
+        else:
+            y = apply_value(node, xs, profile)
+        values[i] = y.contiguous()
+        # graph_flops sees boundary tensors as the sub-graph's inputs, whose
+        # shape it takes from the node's own output (engine.py:435-444)
+        flops += node_flops(node, tuple(y.shape), [tuple(y.shape) if fb else tuple(x.shape)
+                                                   for x, fb in zip(xs, from_boundary)])
+    return values, flops
+
+
+def child_offense(g, child, boundary: dict, claimed_outputs: dict, thresholds, profile=None,
+                  device=None):
+    """dispute.py:544-559: re-execute one child from its committed inputs and
+    return (worst live-out p_max against the claimed tensors, FLOPs spent).
+    claimed_outputs: {parent node index: claimed tensor} for the live-outs."""
+    from .graph import frontiers
+    values, flops = run_slice(g, child, boundary, profile, device)
+    worst = 0.0
+    for i in frontiers(g, child).out_nodes:
+        worst = max(worst, observed_p_max(values[i], claimed_outputs[i], thresholds,
+                                          g.nodes[i].name))
+    return worst, flops
