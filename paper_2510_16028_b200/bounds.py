@@ -528,7 +528,7 @@ def _check_declared_inputs(g, inputs):
 def co_execute(g, inputs, profile, model: FpModel, with_trace: bool = False):
     """bounds.py:221-262 on the GPU: returns (outputs, bounds[, trace]) with
     device-resident Tensors / BoundTensors (numpy views materialise lazily)."""
-    from .commitments import tensor_digest
+    from .commitments import tensor_digest, weight_digests
     from .engine_trace import Trace
 
     _check_declared_inputs(g, inputs)
@@ -557,7 +557,7 @@ def co_execute(g, inputs, profile, model: FpModel, with_trace: bool = False):
     trace = Trace(tensors=[Tensor(v.shape, v) for v in values],
                   profile_id=getattr(profile, "id", "seq"),
                   input_digests={k: tensor_digest(v) for k, v in sorted(inputs.items())},
-                  weight_digests={k: tensor_digest(v) for k, v in sorted(g.weights.items())})
+                  weight_digests=weight_digests(g.weights))
     return outputs, bounds, trace
 
 

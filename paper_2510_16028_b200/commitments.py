@@ -89,6 +89,38 @@ def tensor_digest(t) -> str:
     return sha256(canon_tensor(t)).hex()
 
 
+_WEIGHT_DIGESTS: dict = {}
+
+
+def weight_digests(weights: dict) -> dict:
+    """{name: tensor_digest} of a graph's weights, each computed once per
+    weight object (engine.py:362-363 re-hashes all weights on every call --
+    32.8 GB for Qwen3-8B; cache them).  Torch weights
+    are re-hashed when their version counter moves; reference Tensors are
+    immutable.  Misses hash on a thread pool (one SHA-256 stream per tensor)."""
+    import weakref
+    out, miss = {}, []
+    for name in sorted(weights):
+        t = weights[name]
+        hit = _WEIGHT_DIGESTS.get(id(t))
+        ver = t._version if isinstance(t, torch.Tensor) else 0
+        if hit is not None and hit[0]() is t and hit[1] == ver:
+            out[name] = hit[2]
+        else:
+            miss.append(name)
+    if miss:
+        for name, d in zip(miss, _digests([weights[n] for n in miss])):
+            t = weights[name]
+            ver = t._version if isinstance(t, torch.Tensor) else 0
+            try:
+                ref = weakref.ref(t, lambda _r, k=id(t): _WEIGHT_DIGESTS.pop(k, None))
+                _WEIGHT_DIGESTS[id(t)] = (ref, ver, d.hex())
+            except TypeError:  # not weak-referenceable: no caching
+                pass
+            out[name] = d.hex()
+    return {k: out[k] for k in sorted(out)}
+
+
 def _device(device=None):
     return torch.device(device if device is not None else "cuda", torch.cuda.current_device()
                         if device is None else torch.device(device).index)

@@ -107,3 +107,20 @@ def test_streaming_verifier_dumps_the_claimed_trace(tmp_path):
     tw.close(spec.graph.n_nodes)
     assert json.loads((tmp_path / "t" / "manifest.json").read_text()) == man
     assert _digests(tmp_path / "t") == GOLD["trace/probabilistic"]
+
+
+def test_weight_digests_cached_and_invalidated():
+    """co_execute's per-call weight digests (engine.py:362-363) are computed
+    once per weight object; a torch weight changed in place is re-hashed."""
+    import torch
+    from paper_2510_16028_b200 import commitments as CM
+    from paper_2510_16028_b200.tensor import Tensor
+    w = {"b": Tensor((3,), np.arange(3, dtype=np.float32)),
+         "a": torch.ones((2, 2), dtype=torch.float32)}
+    d1 = CM.weight_digests(w)
+    assert list(d1) == ["a", "b"]
+    assert d1 == {k: CM.tensor_digest(v) for k, v in w.items()}
+    assert CM.weight_digests(w) == d1
+    w["a"].mul_(2.0)
+    d2 = CM.weight_digests(w)
+    assert d2["a"] == CM.tensor_digest(w["a"]) != d1["a"] and d2["b"] == d1["b"]
