@@ -968,14 +968,14 @@ __global__ void __launch_bounds__(256) k_smc_rows(const float* __restrict__ x, f
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const double m64a = fabs((double)m);
-        double se = 0.0, seps = 0.0;
+        // sum eps_e = sum e (u(|x| + |m|) + 2u) = u sum e|x| + (u|m| + 2u) sum e:
+        // two order-free FP64 sums (re-association covered by `slack`)
+        double se = 0.0, sex = 0.0;
         auto one = [&](float xv) -> float {
             const float ev = (float)exp((double)__fsub_rn(xv, m));
             const double e64 = (double)ev;
-            const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
             se = __dadd_rn(se, e64);
-            seps = __dadd_rn(seps, __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64)));
+            sex = __fma_rn(e64, fabs((double)xv), sex);
             return ev;
         };
         if (VEC) {
@@ -991,8 +991,10 @@ __global__ void __launch_bounds__(256) k_smc_rows(const float* __restrict__ x, f
             for (int64_t c = lane; c < n; c += 32) er[c] = one(__ldg(xr + c));
         }
         se = warp_sum(se);
-        seps = warp_sum(seps);
+        sex = warp_sum(sex);
         if (lane == 0) {
+            const double um2 = __dadd_rn(__dmul_rn(u, fabs((double)m)), two_u);
+            const double seps = __dadd_rn(__dmul_rn(u, sex), __dmul_rn(um2, se));
             const double epsS = __dadd_rn(__dmul_rn(rc, se), __dmul_rn(__dadd_rn(rc, 1.0), seps));
             uint32_t* st = stats_ptr(eps, eps_f64, r, n);
             const unsigned long long b = (unsigned long long)__double_as_longlong(epsS);
@@ -1061,11 +1063,17 @@ __global__ void __launch_bounds__(256) k_smc_epi(const float* __restrict__ x, fl
             __longlong_as_double((long long)(((unsigned long long)st[1] << 32) | st[0]));
         const float m = __uint_as_float(st[2]), S = __uint_as_float(st[3]);
         __syncwarp();  // every lane holds the stats before the slot is overwritten
-        const double S64 = (double)S, S2 = __dmul_rn(S64, S64);
-        // divisions by per-row constants as reciprocal multiplies: <= 2 ulp FP64,
-        // covered by `slack` (>= 2^-50)
-        const double invS = __ddiv_rn(1.0, S64), kS2 = __ddiv_rn(epsS, S2);
-        const double m64a = fabs((double)m), two_u = __dmul_rn(2.0, u);
+        // eps_y = e (u(|x|+|m|) + 2u)/S + e epsS/S^2 + u|y| = e (A|x| + B) + u|y|
+        // with A = u/S, B = (u|m| + 2u)/S + epsS/S^2: every term >= 0, a few
+        // FP64 ulps from bounds.py's order (covered by `slack` >= 2^-50), and
+        // the (1 + slack) factor folded into A, B and u
+        const double S64 = (double)S;
+        const double sl = __dadd_rn(1.0, slack), two_u = __dmul_rn(2.0, u);
+        const double A = __dmul_rn(__ddiv_rn(u, S64), sl);
+        const double B = __dmul_rn(__dadd_rn(
+            __ddiv_rn(__dadd_rn(__dmul_rn(u, fabs((double)m)), two_u), S64),
+            __ddiv_rn(epsS, __dmul_rn(S64, S64))), sl);
+        const double us = __dmul_rn(u, sl);
         const float* xr = x + r * n;
         float* yr = y + r * n;
         const int64_t ob = r * n;
@@ -1081,22 +1089,18 @@ __global__ void __launch_bounds__(256) k_smc_epi(const float* __restrict__ x, fl
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     ys[k] = __fdiv_rn(es[k], S);
-                    const double e64 = (double)es[k];
-                    const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xs[k]), m64a));
-                    const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
-                    vs[k] = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
-                                      __dmul_rn(u, fabs((double)ys[k])));
+                    const double t = __fma_rn(A, fabs((double)xs[k]), B);
+                    vs[k] = __fma_rn((double)es[k], t, __dmul_rn(us, fabs((double)ys[k])));
                 }
                 y4[c] = make_float4(ys[0], ys[1], ys[2], ys[3]);
-                const double sl = __dadd_rn(1.0, slack);
                 if (eps_f64) {
                     double2* e2 = reinterpret_cast<double2*>(static_cast<double*>(eps) + ob) + 2 * c;
-                    e2[0] = make_double2(__dmul_rn(vs[0], sl), __dmul_rn(vs[1], sl));
-                    e2[1] = make_double2(__dmul_rn(vs[2], sl), __dmul_rn(vs[3], sl));
+                    e2[0] = make_double2(vs[0], vs[1]);
+                    e2[1] = make_double2(vs[2], vs[3]);
                 } else {
                     reinterpret_cast<float4*>(static_cast<float*>(eps) + ob)[c] = make_float4(
-                        __double2float_ru(__dmul_rn(vs[0], sl)), __double2float_ru(__dmul_rn(vs[1], sl)),
-                        __double2float_ru(__dmul_rn(vs[2], sl)), __double2float_ru(__dmul_rn(vs[3], sl)));
+                        __double2float_ru(vs[0]), __double2float_ru(vs[1]),
+                        __double2float_ru(vs[2]), __double2float_ru(vs[3]));
                 }
             }
         } else {
@@ -1104,12 +1108,10 @@ __global__ void __launch_bounds__(256) k_smc_epi(const float* __restrict__ x, fl
                 const float xv = __ldg(xr + c), ev = yr[c];
                 const float yv = __fdiv_rn(ev, S);
                 yr[c] = yv;
-                const double e64 = (double)ev;
-                const double eps_z = __dmul_rn(u, __dadd_rn(fabs((double)xv), m64a));
-                const double eps_e = __dadd_rn(__dmul_rn(e64, eps_z), __dmul_rn(two_u, e64));
-                const double v = __dadd_rn(__dadd_rn(__dmul_rn(eps_e, invS), __dmul_rn(e64, kS2)),
-                                           __dmul_rn(u, fabs((double)yv)));
-                store_eps(eps, eps_f64, ob + c, v, slack);
+                const double t = __fma_rn(A, fabs((double)xv), B);
+                const double v = __fma_rn((double)ev, t, __dmul_rn(us, fabs((double)yv)));
+                if (eps_f64) static_cast<double*>(eps)[ob + c] = v;
+                else static_cast<float*>(eps)[ob + c] = __double2float_ru(v);
             }
         }
     }
