@@ -440,6 +440,19 @@ def run_ours(args):
                     "peak_source": "derived integer-ALU roofline of Keccak-256: 148 SM x 64 "
                                    "lanes/clk x SM clock / (24 x 180 ops per 136 B block)",
                     "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
+        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
+            # SHA-256 is integer-ALU bound too: ~1253 ALU-pipe ops per 64-byte
+            # compression (cuobjdump of k_chunk_leaves<sha256>: 660 SHF + 350 LOP3
+            # + 243 IADD3 per compression; ~130 IMAD go to the FMA pipe)
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
+            sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+            peak = 148 * 64 * sm_mhz * 1e6 / (1253 / 64.0) / 1e9
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
+                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "derived integer-ALU roofline of SHA-256: 148 SM x 64 "
+                                   "lanes/clk x SM clock / (1253 ops per 64 B block)",
+                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
         else:
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
             peak = peaks.get("hbm_gbs", 6650.0)
