@@ -195,7 +195,7 @@ def run_ours(args):
     fault = args.fault_node
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
                            chunk_bytes=args.chunk, fuse_check=not args.separate_check,
-                           max_lag=args.max_lag)
+                           max_lag=args.max_lag, flush_bytes=args.flush_mb << 20)
 
     harness_ev = []  # (start, end) events around the proposer harness (serial pass only)
 
@@ -537,6 +537,7 @@ def run_ours(args):
                 "ms_per_step": round(e2e_ms, 2), "h2d_bytes_per_step": int(ids_host.numel() * 4),
                 "d2h_bytes_per_step": int(n_nodes * (32 + _lib.CHECK_RESULT_BYTES) + 32)},
         "gpu_launches": n_launch,
+        "mem_peak_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
         "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
     }
     print(json.dumps(line))
@@ -685,6 +686,8 @@ def main(argv=None):
                          "the verifier's side streams)")
     ap.add_argument("--max-lag", type=int, default=4,
                     help="main waits for commit flush k-LAG (bounded side-stream lag)")
+    ap.add_argument("--flush-mb", type=int, default=2048,
+                    help="claimed bytes per fused commit launch (StreamingVerifier flush_bytes)")
     ap.add_argument("--separate-check", action="store_true",
                     help="standalone nao_check per node instead of the check fused into commit")
     ap.add_argument("--graphs", type=int, default=0, metavar="SEG",

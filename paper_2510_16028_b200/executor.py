@@ -196,7 +196,8 @@ class StreamingVerifier:
         # side stream that runs behind, e.g. under a high-priority main stream)
         self.max_lag = int(max_lag)
         self._com_events = []
-        self._host_events = []
+        self._host_events = []  # commit-flush events the host has not waited for
+        self.host_lag_bytes = 32 << 30
         # partial: records are combinable nao_check_partial rows (a batch shard of
         # every node; shard.combine_shard_records decides the whole-tensor verdicts)
         self.partial = bool(partial)
@@ -335,13 +336,17 @@ class StreamingVerifier:
                 if len(self._com_events) > self.max_lag:
                     old_ev = self._com_events.pop(0)
                     main.wait_event(old_ev)
-                    # the host may not run more than 4 x max_lag further flushes
-                    # ahead of the GPU: blocks freed while a side stream still uses
-                    # them stay reserved until it passes, so unbounded run-ahead
-                    # turns into allocator OOM retries (device syncs) on large
-                    # graphs (a tighter bound starves host-heavy graphs: GPT-2)
+                    # the host may run at most ~host_lag_bytes of claimed tensors
+                    # (in flushes) further ahead: blocks freed while a side stream
+                    # still uses them stay reserved until it passes (claimed + local
+                    # + eps per node), so unbounded run-ahead fills HBM and turns
+                    # into allocator OOM retries (device syncs).  The bound must stay
+                    # loose: the host enqueues only ~8 % faster than the GPU runs,
+                    # and a tight one (6 flushes) left the main stream starved
+                    # (77 -> 90-130 % on the bench)
                     self._host_events.append(old_ev)
-                    if len(self._host_events) > 4 * self.max_lag:
+                    n_host = max(self.max_lag, int(self.host_lag_bytes // max(1, self.flush_bytes)))
+                    while len(self._host_events) > n_host:
                         self._host_events.pop(0).synchronize()
             st.pending, st.pend_idx, st.pend_bytes = [], [], 0
             st.pend_checks, st.pend_keep = [], []
