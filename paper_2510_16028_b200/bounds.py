@@ -27,7 +27,8 @@ import torch
 
 from . import _lib
 from .engine import (ExecutionError, fma_of, matmul_value, parse_shape_attr, relu,
-                     profile_arg, require_supported, to_device, unary, _batch_view)
+                     profile_arg, require_f32, require_supported, to_device, unary,
+                     _batch_view)
 from .graph import DATA_MOVEMENT_KINDS, parse_ref
 from .tensor import Tensor
 
@@ -236,6 +237,7 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
                    a_owner: torch.Tensor | None = None) -> torch.Tensor:
     """const * (|A| @ |B|) (* (1+slack)) [+ u|y|] on the GPU (device tensors).
     a_owner: A is a (2-D view of a) static weight -- cache its split on it."""
+    require_f32(a, b, y)
     a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
     path = default_gemm_path(K) if path is None else path
     eps = _eps_buffer(out_shape, a.device, eps_f64)
@@ -277,6 +279,7 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
 
 
 def _rows_last(x: torch.Tensor, axis: int):
+    require_f32(x)
     ax = axis % x.dim()
     xm = x.movedim(ax, -1).contiguous()
     n = xm.shape[-1]

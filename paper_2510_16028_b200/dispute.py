@@ -93,6 +93,8 @@ def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel
                out: torch.Tensor | None = None) -> CheckRecord:
     """One-pass check of a node.  eps: FP32/FP64 CUDA tensor, ("scaled", c)
     for c|local| templates, or ("zero",).  No host sync."""
+    from .engine import require_f32
+    require_f32(local, claimed)
     a = to_device(local).reshape(-1).contiguous()
     b = to_device(claimed).reshape(-1).contiguous()
     if a.numel() != b.numel():

@@ -130,8 +130,18 @@ def to_device(a, device=None) -> torch.Tensor:
     return torch.from_numpy(arr).to(device or "cuda")
 
 
+def require_f32(*ts) -> None:
+    """The kernels read FP32 words: any other dtype is rejected at the boundary
+    (ValueError, the reference's error type for bad inputs) instead of being
+    reinterpreted -- e.g. a float64 array from float32 / np.float64 promotion."""
+    for t in ts:
+        if isinstance(t, torch.Tensor) and t.dtype != torch.float32:
+            raise ValueError(f"expected a float32 tensor, got {t.dtype}")
+
+
 def unary(kind: str, x: torch.Tensor) -> torch.Tensor:
     """engine.py:133-154 (FP64 evaluation rounded once)."""
+    require_f32(x)
     x = x.contiguous()
     y = torch.empty_like(x)
     _lib.call("nao_unary_fp64", x.data_ptr(), y.data_ptr(), x.numel(), _lib.UNARY[kind],

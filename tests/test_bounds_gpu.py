@@ -354,3 +354,45 @@ def test_softmax_design_g_parity():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("MKN", [(2048, 4096, 4096), (2048, 4096, 12288), (2048, 12288, 4096),
+                                 (2048, 4096, 1024)])
+def test_abs_gemm_full_qwen_shapes(B, MKN):
+    """Qwen3-8B projection shapes at full size on the default (FP16 3-split)
+    path: 24 sampled output rows against the FP64 reference template, and two
+    size-independent properties over the whole output -- exact power-of-two
+    homogeneity eps(8A) == 8 eps(A) (the split, the MMAs, the FP64 drains and
+    the round-up all commute with 2^3) and eps(A) == eps(A) over a row
+    permutation of A (rows are independent)."""
+    M, K, N = MKN
+    rng = np.random.default_rng(K + N)
+    a = torch.from_numpy((rng.standard_normal((M, K)) * 0.5).astype(np.float32)).cuda()
+    w = torch.from_numpy((rng.uniform(-1, 1, (K, N)) / np.sqrt(K)).astype(np.float32)).cuda()
+    c = B.FpModel().reduction_const(2 * K - 1)
+    eps = B.abs_gemm_bound(a, w, c, False, eps_f64=False)
+    rows = np.r_[0, M - 1, rng.choice(M, 22, replace=False)]
+    ref = OB.matmul_bound(a[rows].cpu().numpy(), w.cpu().numpy(), OB.FpModel())
+    assert_bound(eps[rows].cpu().numpy().astype(np.float64), ref, str(MKN))
+    eps8 = B.abs_gemm_bound(a * 8.0, w, c, False, eps_f64=False)
+    assert torch.equal(eps8, eps * 8.0)
+    perm = torch.from_numpy(rng.permutation(M)).cuda()
+    epsp = B.abs_gemm_bound(a[perm].contiguous(), w, c, False, eps_f64=False)
+    assert torch.equal(epsp, eps[perm])
+
+
+def test_non_fp32_inputs_rejected(B):
+    """A float64 operand (e.g. float32 / np.float64 promotion) is a ValueError at
+    the boundary, never reinterpreted as FP32 words by the kernels."""
+    from paper_2510_16028_b200.dispute import check_node
+    a32 = torch.ones((4, 8), device="cuda")
+    a64 = torch.ones((4, 8), device="cuda", dtype=torch.float64)
+    c = B.FpModel().reduction_const(15)
+    with pytest.raises(ValueError):
+        B.abs_gemm_bound(a32, a64.T.contiguous(), c)
+    with pytest.raises(ValueError):
+        B.softmax_device(a64, -1, B.FpModel())
+    with pytest.raises(ValueError):
+        B.reduce_device("sum", a64, -1, B.FpModel())
+    with pytest.raises(ValueError):
+        check_node(a32, a64, ("zero",), np.full(23, np.inf), np.full(23, np.inf))
