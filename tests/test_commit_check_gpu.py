@@ -179,3 +179,42 @@ def test_partial_records_combine_to_whole_tensor_verdict(pieces):
         with np.errstate(invalid="ignore"):
             pm = OC.observed_p_max(y, yc, taus[0], taus[1])
         assert bool(got["threshold_exceeded"]) == (pm > 1.0)
+
+
+def test_fused_full_qwen_scores_tensor():
+    """One Qwen3-8B attention-scores-sized tensor (32 x 2048 x 2048 FP32, 537 MB)
+    with 1/16 of the elements drifted by one ulp, an FP32 bound tensor and
+    thresholds at the exact percentile profile of its own errors (every grid
+    point on the boundary: the exact second pass runs): the fused record equals
+    the standalone check's, the verdicts equal the oracle's numpy ones, and the
+    Keccak root equals the C restatement's."""
+    from paper_2510_16028_b200 import dispute
+    from paper_2510_16028_b200.commitments import commit_tensors
+    rng = np.random.default_rng(2048)
+    n = 32 * 2048 * 2048
+    y = (rng.standard_normal(n, dtype=np.float32) * 3.0).astype(np.float32)
+    yc = _drift(y, 1 / 16, 1, rng)
+    c = 3.3 * 2.0 ** -24
+    e32 = (c * np.abs(y.astype(np.float64))).astype(np.float32)
+    e32[rng.integers(0, n, size=64)] = 0.0  # a few zero bounds: violations where drifted
+    with np.errstate(invalid="ignore"):
+        a, r = OC.elementwise_errors(y, yc)
+    pa, pr = OC.percentile_profile(a), OC.percentile_profile(r)
+    del a, r
+    local, claimed = torch.from_numpy(y).cuda(), torch.from_numpy(yc).cuda()
+    eps = torch.from_numpy(e32).cuda()
+    roots, recs = dispute.commit_check_nodes([claimed], [local], [eps], [(pa, pr)], 4096,
+                                             "keccak256")
+    plain = commit_tensors([claimed], 4096, "keccak256")
+    want = dispute.check_node(local, claimed, eps, pa, pr).host()
+    got = _records(recs)[0]
+    torch.cuda.synchronize()
+    assert torch.equal(roots, plain)
+    for f in FIELDS:
+        assert got[f] == want[f], (f, got[f], want[f])
+    ref = OC.leaf_check(y, yc, e32.astype(np.float64))
+    assert got["n_violations"] == ref["n_violations"] > 0
+    assert bool(got["threshold_exceeded"]) == (OC.observed_p_max(y, yc, pa, pr) > 1.0)
+    import os
+    assert bytes(roots[0].cpu().numpy()) == OM.tensor_root(yc, 4096, OM.KECCAK256,
+                                                           n_threads=os.cpu_count() or 1)
