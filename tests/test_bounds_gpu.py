@@ -396,3 +396,27 @@ def test_non_fp32_inputs_rejected(B):
         B.reduce_device("sum", a64, -1, B.FpModel())
     with pytest.raises(ValueError):
         check_node(a32, a64, ("zero",), np.full(23, np.inf), np.full(23, np.inf))
+
+
+def test_softmax_full_qwen_scores(B):
+    """Qwen3-8B attention probabilities at full size (32 x 2048 x 2048, causal
+    -1e9 mask as in the lowering): 16 sampled rows bit-exact / within tolerance
+    against the oracle, and the whole output equivariant under a permutation of
+    the 65536 rows (rows are independent in every design)."""
+    S, H = 2048, 32
+    rng = np.random.default_rng(S)
+    x = torch.randn((H, S, S), device="cuda") * 4.0
+    mask = torch.triu(torch.full((S, S), -1e9, device="cuda"), diagonal=1)
+    x = (x + mask).contiguous()
+    y, e = B.softmax_device(x, -1, B.FpModel(), eps_f64=False)
+    flat_x, flat_y, flat_e = x.reshape(-1, S), y.reshape(-1, S), e.reshape(-1, S)
+    rows = np.r_[0, S - 1, rng.choice(H * S, 14, replace=False)]
+    xr = flat_x[rows].cpu().numpy()
+    y_ref, e_ref = OB.softmax_bound_parts(xr, -1, OB.FpModel())
+    got_y, got_e = flat_y[rows].cpu().numpy(), flat_e[rows].cpu().numpy().astype(np.float64)
+    assert np.array_equal(got_y.view(np.uint32), y_ref.view(np.uint32))
+    assert np.all(got_e >= e_ref)
+    assert np.all(got_e <= e_ref * (1 + RTOL) + 2 * np.spacing(e_ref.astype(np.float32)))
+    perm = torch.from_numpy(rng.permutation(H * S)).cuda()
+    yp, ep = B.softmax_device(flat_x[perm].contiguous(), -1, B.FpModel(), eps_f64=False)
+    assert torch.equal(yp, flat_y[perm]) and torch.equal(ep, flat_e[perm])
