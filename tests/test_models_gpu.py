@@ -119,3 +119,14 @@ def test_unet_sd15_shape_flags_only_the_fault():
     from paper_2510_16028_b200.lowerings import SD15_UNET, build_unet
     spec = build_unet(dataclasses.replace(SD15_UNET, batch=1, latent=32))
     assert _flagged(spec, "down1.res0.conv2") == ["down1.res0.conv2"]
+
+
+def test_qwen3_8b_full_width_layers_flag_only_the_fault():
+    """Two Qwen3-8B-shaped layers at full width and sequence (S=2048, H=4096,
+    32/8 heads, I=12288) plus the LM head, through the streaming verifier with
+    +-1-ulp drift on every reduction output: no bound violation anywhere but the
+    node carrying the planted fault (BASELINE configs[3], bench.py's workload)."""
+    import dataclasses
+    from paper_2510_16028_b200.lowerings import QWEN3_8B, build_decoder
+    spec = build_decoder(dataclasses.replace(QWEN3_8B, seq=2048), layers=2)
+    assert _flagged(spec, "l1_down") == ["l1_down"]
