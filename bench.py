@@ -63,10 +63,19 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index, self.samples, self._stop = index, [], threading.Event()
         self._t = None
+        # NVML is loaded and initialised here, on the caller's thread and before
+        # the timed region, so the sampler thread only issues cheap queries
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
 
     def _run_nvml(self, nv):
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        h, mx = self._h, self._mx
         bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
         while not self._stop.is_set():
@@ -80,11 +89,7 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-        except Exception:
-            nv = None
+        nv = self._nv
         if nv is not None:
             try:
                 self._run_nvml(nv)
