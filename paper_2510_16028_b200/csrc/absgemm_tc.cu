@@ -1529,7 +1529,11 @@ int nao_f16_split(const float* x, void* hi, void* lo, int32_t* row_info, int64_t
                          (reinterpret_cast<uintptr_t>(x) % 16) == 0;
         // rows of <= 2048 elements: warp per row (the row stays in L1 for the
         // second pass); longer rows: CTA per row staged in shared memory
-        if (vec && K > 2048 && K * 4 <= 96 * 1024) {
+        static const int64_t smem_min_k = [] {  // experiment knob
+            const char* e = getenv("NAO_SPLIT_SMEM_MIN_K");
+            return (int64_t)(e ? atoll(e) : 2049);
+        }();
+        if (vec && K >= smem_min_k && K * 4 <= 96 * 1024) {
             static bool attr = false;
             if (!attr) {
                 NAO_CHECK_CUDA(cudaFuncSetAttribute(tc::k_split_f16_rows_smem,
