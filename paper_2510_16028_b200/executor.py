@@ -24,6 +24,7 @@ TF32 off, torch eager ops) -- the baseline the overhead is measured against.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -197,7 +198,7 @@ class StreamingVerifier:
         self.max_lag = int(max_lag)
         self._com_events = []
         self._host_events = []  # commit-flush events the host has not waited for
-        self.host_lag_bytes = 32 << 30
+        self.host_lag_bytes = int(float(os.environ.get("NAO_HOST_LAG_GB", "32")) * (1 << 30))
         # partial: records are combinable nao_check_partial rows (a batch shard of
         # every node; shard.combine_shard_records decides the whole-tensor verdicts)
         self.partial = bool(partial)
