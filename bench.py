@@ -744,10 +744,11 @@ def main(argv=None):
                     help="claimed bytes per fused commit launch (StreamingVerifier flush_bytes)")
     ap.add_argument("--separate-check", action="store_true",
                     help="standalone nao_check per node instead of the check fused into commit")
-    ap.add_argument("--graphs", type=int, default=300, metavar="SEG",
-                    help="replay both arms as CUDA graphs of SEG-node segments (default 300: "
-                         "80.1-80.2 %% at 124 GB peak; 96: 81.1-81.4 %%; >= 1000 runs out of "
-                         "HBM during capture -- side-stream tensors live until the segment joins; "
+    ap.add_argument("--graphs", type=int, default=96, metavar="SEG",
+                    help="replay both arms as CUDA graphs of SEG-node segments (default 96: "
+                         "81.1-81.4 %% and e2e alike over six runs; 300: 80.2-80.6 %% at 124 GB "
+                         "peak but one e2e outlier in two runs; >= 1000 runs out of HBM during "
+                         "capture -- side-stream tensors live until the segment joins; "
                          "0 = eager dispatch: ~1.5 %% faster at best, but the host enqueues "
                          "only ~7 %% ahead of the GPU and some runs lose the overlap "
                          "(90-240 %%); graph replay measured 81.1-81.4 %% over six runs)")
