@@ -121,10 +121,15 @@ typedef struct nao_check_result {
  * is a dedicated accumulator that must be zero before its first use; every
  * call leaves it zeroed again (do not share it with other entry points). */
 size_t nao_check_workspace(void);
+/* Borderline list (optional, device): uint64 [1 + border_cap]; word 0 counts
+ * the borderline elements, words 1.. hold the flat indices of the first
+ * border_cap of them (nao_refine_borderline settles them exactly and resets
+ * the count).  NULL: borderline elements are only counted. */
 int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind, const void* eps,
               double eps_scale, double lo_factor, const double* grid, const double* tau_abs,
               const double* tau_rel, int n_grid, double epsilon, nao_check_result* result,
-              void* workspace, size_t workspace_bytes, void* stream);
+              void* workspace, size_t workspace_bytes, uint64_t* border_list,
+              int64_t border_cap, void* stream);
 /* Per-node verdict spec: grid + thresholds prepared once on the host
  * (ThresholdSet.lookup(name), calibration.py:117-191) and kept in device
  * memory; nao_verdict_spec_bytes() bytes, filled by nao_verdict_spec_fill
@@ -144,6 +149,8 @@ typedef struct nao_check_desc {
     double lo_factor;            /* borderline band (see nao_check) */
     int32_t eps_kind;
     int32_t flags;               /* NAO_CHECK_PARTIAL: `result` is a nao_check_partial */
+    uint64_t* border_list;       /* optional borderline list (see nao_check) */
+    int64_t border_cap;
 } nao_check_desc;
 /* A shard's combinable check state (batch-sharded verification):
  * counts per threshold interval (bucket b = keys with b sorted thresholds
@@ -199,8 +206,18 @@ int nao_layernorm_bound(const float* x, float* y, void* eps, int eps_f64, int64_
 int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t rows, int64_t n,
                      int kind, double u, double rc, double slack, const nao_profile* profile,
                      void* stream);
-/* _unary_intrinsic values, engine.py:133-154 (FP64 evaluation, one rounding) */
-int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* stream);
+/* _unary_intrinsic values, engine.py:133-154 (FP64 evaluation, one rounding).
+ * The reference's FP64 libm (numpy SIMD exp/log/tanh/pow) is not correctly
+ * rounded and differs across CPUs, so each element also gets the range of
+ * FP32 results any evaluation within the libm error envelope can produce
+ * (exp/log/tanh: 16 FP64 ulps; gelu: its x**3, tanh and the cancellation in
+ * 1+tanh propagated).  y = the value of this evaluation; elements whose range
+ * holds more than one FP32 value are "value-ambiguous": their flat indices go
+ * to amb_list (same layout as the check's borderline list, may be NULL).
+ * eps (optional): the intrinsic template eps_scale*|y| (bounds.py:198-199)
+ * taken at the largest |candidate|, so eps >= the reference's on every element. */
+int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* eps, int eps_f64,
+                   double eps_scale, uint64_t* amb_list, int64_t amb_cap, void* stream);
 /* eps = scale*|y|: single-rounding (u) / intrinsic (2u) templates, bounds.py:196-199 */
 int nao_scaled_abs_bound(const float* y, void* eps, int eps_f64, int64_t n, double scale,
                          void* stream);
@@ -265,6 +282,60 @@ int nao_matmul_profile(const float* A, const float* B, float* C, int64_t batch, 
  * included in K), row-major [batch, OH*OW, C*k*k].  OH = (H + 2 pad - k)/stride + 1. */
 int nao_im2col_rows(const float* x, float* col, int64_t batch, int64_t C, int64_t H, int64_t W,
                     int64_t k, int64_t stride, int64_t pad, void* stream);
+
+/* ---------------------------------------------- exact re-adjudication */
+/* Settles the borderline elements a check recorded (nao_check /
+ * nao_check_desc border_list) against the reference's own bound: the
+ * streaming bounds over-estimate the reference's by a certified factor R
+ * (DESIGN.md 5), so an element with eps/R < diff <= eps is undecided until
+ * the reference's eps is recomputed for it.  GEMM / conv: the abs-dot
+ * sum_k |a||b| exactly (FP64 products, double-double sum), then the
+ * reference's interval eps_ref in const*S*(1 +- (K+4) 2^-53) [+ u|y|] --
+ * numpy's BLAS order is unknown, nothing narrower is reproducible.  UNARY:
+ * value-ambiguous elements (nao_unary_fp64) -- the verdict
+ * |c - y| > scale|y| is evaluated over every candidate y.  Each settled
+ * element leaves n_borderline; a certain violation is added to n_violations;
+ * a verdict that differs between candidates is moved out of n_violations
+ * into n_borderline.  After the pass n_violations counts certain reference
+ * violations and n_borderline the undecided rest.  The list count is reset
+ * to 0 (graph replay).  One launch for up to 64 descriptors (host array). */
+enum nao_refine_kind { NAO_REFINE_GEMM = 0, NAO_REFINE_CONV = 1, NAO_REFINE_UNARY = 2 };
+typedef struct nao_refine_desc {
+    int32_t kind;               /* NAO_REFINE_* */
+    int32_t unary_kind;         /* NAO_UN_* (UNARY) */
+    uint64_t* list;             /* border / ambiguity list of the node */
+    int64_t cap;
+    nao_check_result* result;   /* the node's check record */
+    const float* local;         /* recomputed output y */
+    const double* local64;      /* GEMM / CONV: FP64 y instead (the leaf route's FP64 oracle
+                                   recheck, dispute.py:648-656), else NULL */
+    const float* claimed;       /* claimed output y' */
+    const float* a;             /* GEMM: A [batch_a, M, K]; CONV: W [N=Cout, C, k, k]; UNARY: x */
+    const float* b;             /* GEMM: B [batch_b, K, N] / [batch_b, N, K]; CONV: x [batch, C, H, W] */
+    int64_t batch, M, N, K;     /* GEMM output [batch, M, N]; CONV: batch, M=OH*OW, N=Cout, K=C k k */
+    int64_t stride_a, stride_b; /* batch strides (0 = broadcast) */
+    int32_t transpose_b, has_y; /* has_y: linear's + u|y| */
+    int64_t C, H, W, k, stride, pad, OW; /* CONV geometry */
+    double gamma_const, u;      /* reduction_const(count); u (linear) / eps_scale (UNARY) */
+} nao_refine_desc;
+int nao_refine_borderline(const nao_refine_desc* descs, int n_descs, void* stream);
+
+/* ------------------------------------------- FP64 theoretical oracle path */
+/* The reference's FP64 execution of one operator (apply_op(fp64=True),
+ * engine.py:220-285 via execute_fp64 :369-390; the leaf route's theoretical
+ * recheck, dispute.py:648-656): FP32 inputs promoted to FP64, every
+ * reduction a sequential FP64 fold (reduce_last_axis(profile=None),
+ * engine.py:95-113), so results are bit-identical to numpy's except the
+ * transcendentals' last FP64 ulps.  C is FP64 [batch, M, N]. */
+int nao_matmul_fp64(const float* A, const float* B, double* C, int64_t batch, int64_t M,
+                    int64_t N, int64_t K, int64_t stride_a, int64_t stride_b, int transpose_b,
+                    void* stream);
+/* rows [rows, n] FP32 -> FP64: kind 0 softmax (engine.py:185-194), 1 layernorm
+ * (:197-213, ln_eps as the attribute's double), 2 sum, 3 mean (y: [rows]). */
+int nao_rows_fp64(int kind, const float* x, double* y, int64_t rows, int64_t n, double ln_eps,
+                  void* stream);
+/* _unary_intrinsic(fp64=True): FP64 results of FP32 inputs. */
+int nao_unary_f64out(const float* x, double* y, int64_t n, int kind, void* stream);
 
 /* Additive fault / drift hook on a node output (engine.py:325-351 `inject`):
  * out = y with +-1-ulp flips on ~n/period elements and a relative fault

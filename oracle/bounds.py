@@ -411,3 +411,50 @@ def co_execute(graph, inputs: dict, model: FpModel, fma=False, inject=None):
         values.append(out)
         bounds.append(np.asarray(eps, dtype=np.float64))
     return values, bounds
+
+
+# ------------------------------------------- FP64 oracle (theoretical path)
+
+def matmul_fp64(a, b, transpose_b=False) -> np.ndarray:
+    """engine.py:173-177 (fp64=True): FP64 products, sequential fold over K
+    (reduce_last_axis(profile=None), engine.py:95-103).  Folded k-slice by
+    k-slice instead of materialising the (M, K, N) product array -- the same
+    additions in the same order."""
+    a = np.asarray(a, np.float32).astype(np.float64)
+    b = np.asarray(b, np.float32).astype(np.float64)
+    if transpose_b:
+        b = np.swapaxes(b, -1, -2)
+    acc = a[..., :, 0:1] * b[..., 0:1, :]
+    for k in range(1, a.shape[-1]):
+        acc = acc + a[..., :, k:k + 1] * b[..., k:k + 1, :]
+    return acc
+
+
+def apply_op_fp64(node, arrays) -> np.ndarray:
+    """apply_op(node, args64, None, fp64=True) (engine.py:220-285) for the
+    reduction kinds and matmul (the leaf route's FP64 oracle recheck,
+    dispute.py:648-656): sequential FP64 folds."""
+    kind = node.kind
+    x = np.asarray(arrays[0], np.float32).astype(np.float64)
+    if kind == "matmul":
+        return matmul_fp64(arrays[0], arrays[1], bool(node.attr("transpose_b", 0)))
+    if kind == "linear":
+        return matmul_fp64(arrays[0], arrays[1]) + np.asarray(arrays[2], np.float32).astype(np.float64)
+    axis = int(node.attr("axis", -1)) % x.ndim
+    xm = np.moveaxis(x, axis, -1)
+    n = xm.shape[-1]
+    if kind in ("sum", "mean"):
+        red = fold_last(xm)
+        return red if kind == "sum" else red / np.float64(n)
+    if kind == "softmax":  # engine.py:185-194
+        m = np.max(xm, axis=-1, keepdims=True)
+        e = np.exp(xm - m)
+        y = e / fold_last(e)[..., None]
+        return np.moveaxis(y, -1, axis)
+    if kind == "layernorm":  # engine.py:197-213 (eps as the attribute's double)
+        mu = (fold_last(xm) / np.float64(n))[..., None]
+        xc = xm - mu
+        var = (fold_last(xc * xc) / np.float64(n))[..., None]
+        y = xc / np.sqrt(var + np.float64(float(node.attr("eps", 1e-5))))
+        return np.moveaxis(y, -1, axis)
+    raise ValueError(f"oracle apply_op_fp64: kind {kind!r} not restated")

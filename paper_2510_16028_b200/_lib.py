@@ -34,6 +34,7 @@ EPS_TENSOR_F32, EPS_TENSOR_F64, EPS_SCALED_LOCAL, EPS_ZERO = 0, 1, 2, 3
 RED_SUM, RED_MEAN, RED_MAX, RED_MIN = 0, 1, 2, 3
 UNARY = {"exp": 0, "log": 1, "sqrt": 2, "rsqrt": 3, "tanh": 4, "gelu": 5, "silu": 6}
 GEMM_FFMA_RU, GEMM_TC_TF32X3, GEMM_TC_F16X3 = 0, 1, 2
+BORDER_CAP = 1023  # borderline / ambiguity list entries per node (word 0 = count)
 
 
 class CheckResult(ctypes.Structure):
@@ -60,7 +61,24 @@ class CheckDesc(ctypes.Structure):
     """nao_check_desc: the check fused into nao_commit_check_tensors."""
     _fields_ = [("local", c_vp), ("eps", c_vp), ("spec", c_vp), ("result", c_vp),
                 ("eps_scale", ctypes.c_double), ("lo_factor", ctypes.c_double),
-                ("eps_kind", ctypes.c_int32), ("flags", ctypes.c_int32)]
+                ("eps_kind", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("border_list", c_vp), ("border_cap", ctypes.c_int64)]
+
+
+REFINE_GEMM, REFINE_CONV, REFINE_UNARY = 0, 1, 2
+
+
+class RefineDesc(ctypes.Structure):
+    """nao_refine_desc: one node's borderline list and what recomputes its bound."""
+    _fields_ = [("kind", ctypes.c_int32), ("unary_kind", ctypes.c_int32),
+                ("list", c_vp), ("cap", ctypes.c_int64), ("result", c_vp),
+                ("local", c_vp), ("local64", c_vp), ("claimed", c_vp), ("a", c_vp), ("b", c_vp),
+                ("batch", ctypes.c_int64), ("M", ctypes.c_int64), ("N", ctypes.c_int64),
+                ("K", ctypes.c_int64), ("stride_a", ctypes.c_int64), ("stride_b", ctypes.c_int64),
+                ("transpose_b", ctypes.c_int32), ("has_y", ctypes.c_int32),
+                ("C", ctypes.c_int64), ("H", ctypes.c_int64), ("W", ctypes.c_int64),
+                ("k", ctypes.c_int64), ("stride", ctypes.c_int64), ("pad", ctypes.c_int64),
+                ("OW", ctypes.c_int64), ("gamma_const", ctypes.c_double), ("u", ctypes.c_double)]
 
 
 CHECK_PARTIAL = 1  # NAO_CHECK_PARTIAL
@@ -101,7 +119,7 @@ _SIGS = {
                                          c_vp, c_sz, c_vp]),
     "nao_check": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_dbl, c_dbl,
                           ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
-                          c_int, c_dbl, c_vp, c_vp, c_sz, c_vp]),
+                          c_int, c_dbl, c_vp, c_vp, c_sz, c_vp, c_i64, c_vp]),
     "nao_percentile_workspace": (c_sz, [c_i64]),
     "nao_error_profiles": (c_int, [c_vp, c_vp, c_i64, c_dbl, ctypes.POINTER(c_dbl), c_int,
                                    c_vp, c_vp, c_vp, c_sz, c_vp]),
@@ -113,7 +131,12 @@ _SIGS = {
                                     c_dbl, c_dbl, c_dbl, ctypes.POINTER(Profile), c_vp]),
     "nao_reduce_bound": (c_int, [c_vp, c_vp, c_vp, c_int, c_i64, c_i64, c_int, c_dbl, c_dbl,
                                  c_dbl, ctypes.POINTER(Profile), c_vp]),
-    "nao_unary_fp64": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
+    "nao_unary_fp64": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_int, c_dbl, c_vp, c_i64, c_vp]),
+    "nao_refine_borderline": (c_int, [ctypes.POINTER(RefineDesc), c_int, c_vp]),
+    "nao_matmul_fp64": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int,
+                                c_vp]),
+    "nao_rows_fp64": (c_int, [c_int, c_vp, c_vp, c_i64, c_i64, c_dbl, c_vp]),
+    "nao_unary_f64out": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp]),
     "nao_im2col_rows": (c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                                 c_vp]),
     "nao_scaled_abs_bound": (c_int, [c_vp, c_vp, c_int, c_i64, c_dbl, c_vp]),
@@ -249,10 +272,12 @@ def workspace(nbytes: int, device) -> torch.Tensor:
     key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
     buf = _ws.get(key)
     if buf is None or buf.numel() < nbytes:
-        if buf is not None and torch.cuda.is_current_stream_capturing():
-            _ws_captured.append(buf)
         buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
         _ws[key] = buf
+    if torch.cuda.is_current_stream_capturing() and not any(b is buf for b in _ws_captured):
+        # every buffer a graph records stays alive, also one handed out before
+        # the capture and outgrown by a later eager call
+        _ws_captured.append(buf)
     return buf
 
 

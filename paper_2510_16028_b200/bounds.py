@@ -91,6 +91,48 @@ def gemm_slack(k: int) -> float:
     return (int(k) + int(k) // 32 + 16) * 2.0 ** -52
 
 
+# Certified over-estimates R: eps_ref <= eps_gpu <= R * eps_ref for every
+# element, per bound path.  A check counts eps_gpu/R < diff <=
+# eps_gpu as borderline (its lo_factor is 1/R); those elements are settled
+# exactly by nao_refine_borderline.
+def _tc_overestimate(K: int, f16: bool) -> float:
+    """tcgen05 3-split: split excess (hi+lo < |x|(1+2^-20), per operand),
+    the dropped-lo compensation, the acc0 chunk compensation (the MMA
+    accumulation is modelled as losing <= 3*2^-23 per instruction, never
+    gaining), the acc1 compensation on its <= 2^-8 share, FP16 tiny parts
+    (<= 2^-20) and the epilogue's slack."""
+    kchunk = int(_lib.load(require_cuda=False).nao_abs_gemm_tc_kchunk())
+    bk = 32 if f16 else 16
+    kp = (K + 7) // 8 * 8 if f16 else (K + 3) // 4 * 4
+    nkb = -(-kp // bk)
+    mma = 3.0 * 2.0 ** -23
+    comp0 = 1.0 / (1.0 - (kchunk // 16) * 2 * mma)  # KCHUNK_KB k-blocks of 64 B, 2 MMAs each
+    comp1 = 1.0 / (1.0 - 2.0 * nkb * 2 * mma)
+    comp_split = 1.0 / (1.0 - 1.002 * 2.0 ** -20)
+    r = comp_split * comp0 * (1.0 + (comp1 - 1.0) * 2.0 ** -8) * (1.0 + 2.0 ** -20) ** 2
+    if f16:
+        r *= 1.0 + 2.0 ** -20
+    return r * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -50) * (1.0 + 2.0 ** -48)
+
+
+def certified_overestimate(kind: str, K: int = 0, n: int = 0, path: int | None = None,
+                           eps_f32: bool = True) -> float:
+    """R of one node's bound.  kind: matmul/linear/conv2d (K = reduced length,
+    path = the abs-GEMM path), softmax/layernorm/sum/mean (n = row length),
+    anything else 1.0 (templates evaluated exactly as the reference does)."""
+    store = 1.0 + 2.0 ** -23 if eps_f32 else 1.0  # FP32 rounded up
+    if kind in ("matmul", "linear", "conv2d"):
+        path = default_gemm_path(K) if path is None else path
+        if path == _lib.GEMM_FFMA_RU:  # every partial rounds up, chains of 32
+            r = (1.0 + 2.0 ** -23) ** 34 * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -48)
+        else:
+            r = _tc_overestimate(K, path == _lib.GEMM_TC_F16X3)
+        return r * store
+    if kind in ("softmax", "layernorm", "sum", "mean"):
+        return (1.0 + sum_slack(n)) ** 2 * (1.0 + 2.0 ** -48) * store
+    return 1.0
+
+
 class BoundTensor:
     """Same-shape non-negative cap (bounds.py:69-93); eps is FP64, flat,
     held on the GPU or the host."""
@@ -431,13 +473,18 @@ def apply_value(node, xs, profile) -> torch.Tensor:
     raise ExecutionError(f"unsupported op kind {kind!r}")
 
 
-def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
+ROW_KINDS = frozenset({"softmax", "layernorm", "sum", "mean"})
+
+
+def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True, amb=None):
     """(y, eps) for one node on device tensors.  eps is a tensor, or a
     ("scaled", c) / ("zero",) tag when eps_f64 is None (lazy: the check
-    kernel recomputes c|y| on the fly and nothing is materialised)."""
+    kernel recomputes c|y| on the fly and nothing is materialised; row
+    kernels then write FP64 bounds, GEMMs FP32 rounded up).  amb: the
+    value-ambiguity list of an intrinsic node (csrc/unary.cuh)."""
     kind = node.kind
     lazy = eps_f64 is None
-    f64 = bool(eps_f64) if not lazy else False
+    f64 = bool(eps_f64) if not lazy else kind in ROW_KINDS
     u = model.u
     if kind == "softmax":
         require_supported(profile)
@@ -452,13 +499,16 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True):
         if lazy and kind in ("max", "min"):
             return y, ("zero",)
         return y, eps
+    if kind in INTRINSIC_KINDS:
+        if lazy:
+            return unary(kind, xs[0], amb=amb), ("scaled", 2.0 * u)
+        return unary(kind, xs[0], amb=amb, eps_scale=2.0 * u, eps_f64=f64)
     y = apply_value(node, xs, profile)
     if kind in ZERO_BOUND_KINDS:
         return y, (("zero",) if lazy else torch.zeros(y.shape, dtype=torch.float64 if f64 else
                                                       torch.float32, device=y.device))
-    if kind in SINGLE_ROUNDING_KINDS or kind in INTRINSIC_KINDS:
-        c = u if kind in SINGLE_ROUNDING_KINDS else 2.0 * u
-        return y, (("scaled", c) if lazy else scaled_abs(y, c, f64))
+    if kind in SINGLE_ROUNDING_KINDS:
+        return y, (("scaled", u) if lazy else scaled_abs(y, u, f64))
     if kind in ("matmul", "linear"):
         tb = bool(node.attr("transpose_b", 0)) if kind == "matmul" else False
         k_dim = xs[0].shape[-1]

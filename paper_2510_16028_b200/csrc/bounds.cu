@@ -13,6 +13,7 @@
 // folds its own row left to right -- 32 independent sequential folds per warp.
 #include <cmath>
 #include "common.cuh"
+#include "unary.cuh"
 #include "profile_fold.cuh"
 
 namespace nao {
@@ -278,30 +279,23 @@ __global__ void __launch_bounds__(32 * kRowWarps) k_reduce_rows(
 
 // ------------------------------------------------------ elementwise pieces
 
-// engine.py:133-154: FP64 evaluation rounded once to FP32.
-// kind: 0 exp 1 log 2 sqrt 3 rsqrt 4 tanh 5 gelu 6 silu
-__global__ void k_unary(const float* __restrict__ x, float* __restrict__ y, int64_t n, int kind) {
-    const double kS = 0.7978845608028654;  // sqrt(2/pi)  (engine.py:23)
-    const double kC = 0.044715;            // engine.py:24
+// engine.py:133-154: FP64 evaluation rounded once to FP32 (csrc/unary.cuh),
+// plus the value-ambiguity list and the optional intrinsic bound 2u|y| taken
+// at the largest candidate (never below the reference's).
+__global__ void k_unary(const float* __restrict__ x, float* __restrict__ y, int64_t n, int kind,
+                        void* __restrict__ eps, int eps_f64, double eps_scale,
+                        unsigned long long* __restrict__ amb, long long amb_cap) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const double v = (double)__ldg(x + i);
-        double o;
-        switch (kind) {
-            case 0: o = exp(v); break;
-            case 1: o = log(v); break;
-            case 2: o = sqrt(v); break;
-            case 3: o = __ddiv_rn(1.0, sqrt(v)); break;
-            case 4: o = tanh(v); break;
-            case 5: {  // 0.5 * x * (1 + tanh(S * (x + C * x**3)))
-                const double x3 = __dmul_rn(__dmul_rn(v, v), v);
-                const double inner = __dmul_rn(kS, __dadd_rn(v, __dmul_rn(kC, x3)));
-                o = __dmul_rn(__dmul_rn(0.5, v), __dadd_rn(1.0, tanh(inner)));
-                break;
-            }
-            default: o = __ddiv_rn(v, __dadd_rn(1.0, exp(-v))); break;
+        const UnaryOut o = unary_eval(kind, __ldg(x + i));
+        y[i] = o.y;
+        if (eps) {
+            const double m = fmax(fabs((double)o.lo), fabs((double)o.hi));
+            const double e = __dmul_rn(eps_scale, m);
+            if (eps_f64) static_cast<double*>(eps)[i] = e;
+            else static_cast<float*>(eps)[i] = __double2float_ru(e);
         }
-        y[i] = (float)o;
+        if (amb && fbits_differ(o.lo, o.hi)) list_push(amb, amb_cap, (unsigned long long)i);
     }
 }
 
@@ -405,10 +399,14 @@ int nao_reduce_bound(const float* x, float* y, void* eps, int eps_f64, int64_t r
     return NAO_OK;
 }
 
-int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* stream) {
+int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* eps, int eps_f64,
+                   double eps_scale, uint64_t* amb_list, int64_t amb_cap, void* stream) {
     NAO_REQUIRE(kind >= NAO_UN_EXP && kind <= NAO_UN_SILU, "bad unary kind %d", kind);
+    NAO_REQUIRE(amb_list == nullptr || amb_cap >= 0, "bad ambiguity list capacity");
     if (n == 0) return NAO_OK;
-    k_unary<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, n, kind);
+    k_unary<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, y, n, kind, eps, eps_f64, eps_scale,
+        reinterpret_cast<unsigned long long*>(amb_list), (long long)amb_cap);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "check_common.cuh"
+#include "unary.cuh"
 
 namespace nao {
 
@@ -35,6 +36,8 @@ struct CheckParams {
     int eps_kind;       // NAO_EPS_*
     double eps_scale;   // NAO_EPS_SCALED_LOCAL: eps = scale*|local|
     double lo_factor;   // borderline band
+    unsigned long long* border;  // optional borderline list [1 + cap] (include/nao_b200.h)
+    long long border_cap;
     VerdictSpec v;      // grid, thresholds, epsilon
 };
 
@@ -47,6 +50,7 @@ struct CheckSmem {
     uint32_t wc[kCheckWarps][2][kMaxGrid + 1];   // warp-private interval counters
     float qy[kCheckWarps][kQ], qc[kCheckWarps][kQ];  // warp compaction queue of
     double qe[kCheckWarps][kQ];                      // non-zero differences
+    unsigned long long qi[kCheckWarps][kQ];          // and their flat indices
     unsigned long long viol, border, nonfin;
     double maxr;
     int is_last;
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
     uint32_t nzero = 0;  // y' == y exactly: diff 0 -> bucket 0, never a violation
 
     // exact processing of one non-zero difference (all lanes busy: no divergence)
-    auto process = [&](float y, float yc, double eps) {
+    auto process = [&](float y, float yc, double eps, unsigned long long idx) {
         if (!isfinite(y) || !isfinite(yc)) {
             nonfin++; viol++;
             atomicAdd(&sm.wc[w][0][G], 1u); atomicAdd(&sm.wc[w][1][G], 1u);
@@ -98,7 +102,10 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         }
         const double diff = abs_key(y, yc);
         if (diff > eps) viol++;
-        else if (diff > eps * p.lo_factor) border++;
+        else if (diff > eps * p.lo_factor) {
+            border++;
+            if (p.border) list_push(p.border, p.border_cap, idx);
+        }
         if (eps > 0.0) {
             if (!best_inf && diff * best_den > best_num * eps) { best_num = diff; best_den = eps; }
         } else if (diff > 0.0) {
@@ -119,22 +126,23 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         atomicAdd(&sm.wc[w][1][q], 1u);
     };
     int qn = 0;  // warp-uniform queue length
-    auto push = [&](bool flag, float y, float yc, double e) {
+    auto push = [&](bool flag, float y, float yc, double e, unsigned long long idx) {
         const unsigned m = __ballot_sync(0xffffffffu, flag);
         if (m == 0) return;
         if (flag) {
             const int pos = qn + __popc(m & ((1u << lane) - 1u));
-            sm.qy[w][pos] = y; sm.qc[w][pos] = yc; sm.qe[w][pos] = e;
+            sm.qy[w][pos] = y; sm.qc[w][pos] = yc; sm.qe[w][pos] = e; sm.qi[w][pos] = idx;
         }
         qn += __popc(m);
         if (qn >= 32) {
             __syncwarp();
-            process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane]);
+            process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane], sm.qi[w][lane]);
             __syncwarp();
             if (lane < qn - 32) {
                 sm.qy[w][lane] = sm.qy[w][32 + lane];
                 sm.qc[w][lane] = sm.qc[w][32 + lane];
                 sm.qe[w][lane] = sm.qe[w][32 + lane];
+                sm.qi[w][lane] = sm.qi[w][32 + lane];
             }
             __syncwarp();
             qn -= 32;
@@ -182,10 +190,11 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
             if (z3) nzero++;
         }
         const bool live = ok && !all_eq;
-        push(live && !z0, a.x, c.x, e0);
-        push(live && !z1, a.y, c.y, e1);
-        push(live && !z2, a.z, c.z, e2);
-        push(live && !z3, a.w, c.w, e3);
+        const unsigned long long i0 = 4ull * (unsigned long long)v;
+        push(live && !z0, a.x, c.x, e0, i0);
+        push(live && !z1, a.y, c.y, e1, i0 + 1);
+        push(live && !z2, a.z, c.z, e2, i0 + 2);
+        push(live && !z3, a.w, c.w, e3, i0 + 3);
     };
     for (; wb < nvec; wb += stride) {  // warp-uniform trip count (ballots)
         const float4 a0 = na0, c0 = nc0, a1 = na1, c1 = nc1;
@@ -204,10 +213,10 @@ __global__ void __launch_bounds__(kCheckThreads, 3) k_check(const __grid_constan
         if (ok) { y = p.local[i]; c = p.claimed[i]; e = load_eps<EPSK>(p, i, y); }
         const bool z = (y == c) && isfinite(y);
         if (ok && z) nzero++;
-        push(ok && !z, y, c, e);
+        push(ok && !z, y, c, e, (unsigned long long)i);
     }
     __syncwarp();
-    if (lane < qn) process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane]);
+    if (lane < qn) process(sm.qy[w][lane], sm.qc[w][lane], sm.qe[w][lane], sm.qi[w][lane]);
     __syncwarp();
     if (nzero) { atomicAdd(&sm.wc[w][0][0], nzero); atomicAdd(&sm.wc[w][1][0], nzero); }
 
@@ -390,7 +399,8 @@ int nao_verdict_spec_fill(void* spec_host, const double* grid, const double* tau
 int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind, const void* eps,
               double eps_scale, double lo_factor, const double* grid, const double* tau_abs,
               const double* tau_rel, int n_grid, double epsilon, nao_check_result* result,
-              void* workspace, size_t workspace_bytes, void* stream) {
+              void* workspace, size_t workspace_bytes, uint64_t* border_list,
+              int64_t border_cap, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     NAO_REQUIRE(n > 0, "percentile profile of empty input");
     NAO_REQUIRE(local && claimed && result, "null pointer argument");
@@ -411,6 +421,10 @@ int nao_check(const float* local, const float* claimed, int64_t n, int eps_kind,
     memset(&p, 0, sizeof p);
     p.local = local; p.claimed = claimed; p.eps = eps; p.n = n; p.eps_kind = eps_kind;
     p.eps_scale = eps_scale; p.lo_factor = lo_factor;
+    NAO_REQUIRE(lo_factor > 0.0 && lo_factor <= 1.0, "lo_factor %g out of (0, 1]", lo_factor);
+    NAO_REQUIRE(border_list == nullptr || border_cap >= 0, "bad borderline list capacity");
+    p.border = reinterpret_cast<unsigned long long*>(border_list);
+    p.border_cap = (long long)border_cap;
     int rc = fill_verdict_spec(p.v, grid, tau_abs, tau_rel, n_grid, epsilon);
     if (rc) return rc;
     // one resident wave: 3 CTAs per SM (launch bounds), each warp 64 float4 per step

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "check_common.cuh"
+#include "unary.cuh"
 #include "hash.cuh"
 
 namespace nao {
@@ -112,6 +113,8 @@ struct CheckDesc {  // == nao_check_desc (include/nao_b200.h)
     double lo_factor;
     int32_t eps_kind;
     int32_t flags;
+    unsigned long long* border_list;
+    long long border_cap;
 };
 static_assert(sizeof(CheckDesc) == sizeof(nao_check_desc), "nao_check_desc layout");
 static_assert(sizeof(nao_check_partial) == 8 * (5 + 2 * 33 + 4 * 33), "nao_check_partial layout");
@@ -195,11 +198,12 @@ struct LaneCheck {
     bool best_inf = false;
 };
 
-struct Flagged { float y, c; double eps; };
+struct Flagged { float y, c; double eps; unsigned long long idx; };
 
 __device__ __forceinline__ Flagged load_flagged(const CheckDesc& d, const float* claimed,
                                                 uint64_t idx) {
     Flagged f;
+    f.idx = idx;
     f.y = __ldg(d.local + idx);
     f.c = __ldg(claimed + idx);
     f.eps = 0.0;
@@ -221,7 +225,10 @@ __device__ __forceinline__ void process_flagged(const CheckDesc& d, const Flagge
     if (d.eps_kind == NAO_EPS_SCALED_LOCAL) eps = __dmul_rn(d.eps_scale, fabs((double)y));
     const double diff = abs_key(y, c);
     if (diff > eps) lc.viol++;
-    else if (diff > eps * d.lo_factor) lc.border++;
+    else if (diff > eps * d.lo_factor) {
+        lc.border++;
+        if (d.border_list) list_push(d.border_list, d.border_cap, f.idx);
+    }
     if (eps > 0.0) {
         if (!lc.best_inf && diff * lc.best_den > lc.best_num * eps) { lc.best_num = diff; lc.best_den = eps; }
     } else if (diff > 0.0) {

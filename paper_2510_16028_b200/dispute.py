@@ -90,9 +90,10 @@ def new_result_buffer(device, n: int = 1) -> torch.Tensor:
 
 def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel,
                grid=PERCENTILE_GRID, epsilon: float = DEFAULT_EPSILON, lo_factor: float = 1.0,
-               out: torch.Tensor | None = None) -> CheckRecord:
+               out: torch.Tensor | None = None, border: torch.Tensor | None = None) -> CheckRecord:
     """One-pass check of a node.  eps: FP32/FP64 CUDA tensor, ("scaled", c)
-    for c|local| templates, or ("zero",).  No host sync."""
+    for c|local| templates, or ("zero",).  border: int64 [1 + cap] list that
+    receives the borderline elements (for nao_refine_borderline).  No host sync."""
     from .engine import require_f32
     require_f32(local, claimed)
     a = to_device(local).reshape(-1).contiguous()
@@ -121,8 +122,8 @@ def check_node(local: torch.Tensor, claimed: torch.Tensor, eps, tau_abs, tau_rel
     ws = _lib.check_accumulator(a.device)
     _lib.call("nao_check", a.data_ptr(), b.data_ptr(), n, kind, eps_ptr, scale, float(lo_factor),
               _lib.dbl_array(grid), _lib.dbl_array(tau_abs), _lib.dbl_array(tau_rel), len(grid),
-              float(epsilon), res.data_ptr(), ws.data_ptr(), ws.numel(),
-              _lib.stream_ptr(a.device))
+              float(epsilon), res.data_ptr(), ws.data_ptr(), ws.numel(), _lib.ptr(border),
+              (border.numel() - 1) if border is not None else 0, _lib.stream_ptr(a.device))
     return CheckRecord(res)
 
 
@@ -171,7 +172,7 @@ def commit_check_nodes(claimed, local, eps, taus, chunk_bytes: int = 4096, alg="
     for i, (a, b, kind, eps_ptr, scale, lo) in enumerate(descs):
         checks.append(_lib.CheckDesc(a.data_ptr(), eps_ptr, spec.data_ptr() + i * size,
                                      recs[i].data_ptr(), scale, lo, kind,
-                                     _lib.CHECK_PARTIAL if partial else 0)
+                                     _lib.CHECK_PARTIAL if partial else 0, None, 0)
                       if a.numel() else None)
     roots = commit_tensors([d[1] for d in descs], chunk_bytes, alg, checks=checks)
     for t in keep + [spec]:
@@ -249,12 +250,194 @@ def combine_partials(partials, tau_abs, tau_rel, grid=PERCENTILE_GRID) -> dict:
 
 
 def leaf_check(claimed, y_ref, eps) -> dict:
-    """dispute.py:641-648 on the GPU: any(|claimed - y_ref| > eps) and its count.
-    Thresholds are irrelevant here (grid of one point, tau = +inf)."""
+    """dispute.py:641-648 on the GPU for a given bound: any(|claimed - y_ref| > eps)
+    and its count (thresholds are irrelevant: grid of one point, tau = +inf).
+    With a bound computed by this package prefer leaf_bound_check, which also
+    settles the elements inside the bound's certified over-estimate."""
     e = eps if isinstance(eps, tuple) else to_device_eps(eps)
     rec = check_node(y_ref, claimed, e, [np.inf], [np.inf], grid=(100.0,)).host()
-    return {"n_violations": int(rec["n_violations"]), "max_ratio": float(rec["max_ratio"]),
-            "any_violation": rec["n_violations"] > 0}
+    return {"n_violations": int(rec["n_violations"]), "n_borderline": int(rec["n_borderline"]),
+            "max_ratio": float(rec["max_ratio"]), "any_violation": rec["n_violations"] > 0}
+
+
+def _node_args(args):
+    from .engine import to_device
+    xs = []
+    for a in args:
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            xs.append(a)
+        elif isinstance(a, np.ndarray) and a.dtype.kind in "iu":
+            xs.append(torch.from_numpy(np.ascontiguousarray(a)).cuda())
+        else:
+            xs.append(to_device(a))
+    return xs
+
+
+def leaf_bound_check(node, args, claimed, model=None, profile=None) -> dict:
+    """The leaf's bound check exactly as the reference decides it
+    (Challenger.leaf_payload, dispute.py:639-648: y_ref, eps = op_bound(...);
+    any(|claimed - y_ref| > eps)).  The GPU bound over-estimates eps_ref by at
+    most its certified factor R; elements in (eps/R, eps] are recorded by the
+    check and settled by nao_refine_borderline (GEMM / conv: the reference's
+    eps recomputed for that element; intrinsics: every FP32 value numpy's libm
+    could give).  Returns counts of certain violations, the undecided rest
+    (n_borderline; the reference's own FP64 summation order is the only
+    source left), y and eps (device)."""
+    from .bounds import FpModel, INTRINSIC_KINDS, SINGLE_ROUNDING_KINDS, op_bound_device
+    from .executor import check_band, refine_desc, run_refine
+    model = model or FpModel()
+    xs = _node_args(args)
+    c = claimed._dev if getattr(claimed, "_dev", None) is not None else claimed
+    c = _node_args([c])[0]
+    border = torch.zeros(1 + _lib.BORDER_CAP, dtype=torch.int64, device=xs[0].device)
+    intrinsic = node.kind in INTRINSIC_KINDS
+    y, eps = op_bound_device(node, xs, model, profile, eps_f64=True,
+                             amb=border if intrinsic else None)
+    y = y.contiguous()
+    if tuple(c.shape) != tuple(y.shape):
+        raise ValueError(f"claimed shape {tuple(c.shape)} differs from the output {tuple(y.shape)}")
+    c = c.contiguous()
+    eps_chk = eps
+    if intrinsic:
+        eps_chk = ("scaled", 2.0 * model.u)
+    elif node.kind in SINGLE_ROUNDING_KINDS:
+        eps_chk = ("scaled", model.u)
+    rec = new_result_buffer(y.device)
+    if y.numel() == 0:
+        return {"n_violations": 0, "n_borderline": 0, "max_ratio": 0.0, "any_violation": False,
+                "certain": True, "y": y, "eps": eps}
+    kind, _, scale, lo, listed = check_band(node, xs, eps_chk)
+    check_node(y, c, eps_chk, [np.inf], [np.inf], grid=(100.0,), lo_factor=lo, out=rec,
+               border=border if listed else None)
+    if listed or intrinsic:
+        d, keep = refine_desc(node, xs, y, c, rec.data_ptr(), border, model, profile,
+                              eps_scale=scale)
+        run_refine([d])
+        del keep
+    h = CheckRecord(rec).host()
+    return {"n_violations": int(h["n_violations"]), "n_borderline": int(h["n_borderline"]),
+            "max_ratio": float(h["max_ratio"]), "any_violation": h["n_violations"] > 0,
+            "certain": h["n_borderline"] == 0, "y": y, "eps": eps}
+
+
+def oracle_recheck(node, args, claimed, eps, model=None, profile=None) -> dict:
+    """The theoretical path (dispute.py:649-656): y_oracle = apply_op(node,
+    args64, None, fp64=True) on the GPU (engine.apply_op_fp64: sequential FP64
+    folds, bit-identical to numpy's except transcendental last ulps), then
+    all(|claimed - y_oracle| <= eps).  Against the GPU's eps (>= eps_ref) the
+    elements inside its certified band are re-adjudicated for GEMM / conv
+    nodes with the reference's eps recomputed (nao_refine_borderline on the
+    FP64 oracle values)."""
+    from .bounds import FpModel
+    from .engine import apply_op_fp64
+    from .executor import GEMM_KINDS, check_band, refine_desc, run_refine
+    model = model or FpModel()
+    xs = _node_args(args)
+    c = claimed._dev if getattr(claimed, "_dev", None) is not None else claimed
+    c = _node_args([c])[0].contiguous()
+    y_or = apply_op_fp64(node, xs).contiguous()
+    e = eps.double().reshape(y_or.shape) if isinstance(eps, torch.Tensor) else \
+        to_device_eps(eps).reshape(y_or.shape)
+    diff = (c.double() - y_or).abs()
+    excess = diff - e
+    fail = diff > e
+    n_fail = int(fail.sum())
+    n_border = 0
+    if node.kind in GEMM_KINDS and diff.numel():
+        _, _, _, lo, _ = check_band(node, xs, eps if isinstance(eps, torch.Tensor) else e)
+        band = (~fail) & (diff > e * lo)
+        idx = torch.nonzero(band.reshape(-1)).reshape(-1)
+        n_border = int(idx.numel())
+        if n_border:
+            y32 = None
+            if node.kind == "linear":  # the u|y| term takes the FP32 value
+                from .bounds import op_bound_device
+                y32, _ = op_bound_device(node, xs, model, profile, eps_f64=None)
+                y32 = y32.contiguous()
+            cap = _lib.BORDER_CAP
+            border = torch.zeros(1 + cap, dtype=torch.int64, device=y_or.device)
+            border[0] = n_border
+            border[1:1 + min(cap, n_border)] = idx[:cap]
+            rec = new_result_buffer(y_or.device)
+            r = torch.zeros(2, dtype=torch.int64, device=y_or.device)
+            r[0], r[1] = n_fail, n_border
+            rec.view(torch.int64)[0, 1:3].copy_(r)
+            d, keep = refine_desc(node, xs, y32 if y32 is not None else c, c, rec.data_ptr(),
+                                  border, model, profile)
+            d.local64 = y_or.data_ptr()
+            if y32 is None:
+                d.local = None
+            run_refine([d])
+            h = CheckRecord(rec).host()
+            n_fail, n_border = int(h["n_violations"]), int(h["n_borderline"])
+            del keep
+    return {"ok": n_fail == 0, "n_fail": n_fail, "n_borderline": n_border,
+            "max_excess": float(excess.max()) if excess.numel() else float("-inf"),
+            "y_oracle": y_or}
+
+
+def sample_committee(pool, size: int, seed: int):
+    """dispute.py:675-682: committee members without replacement (Rng(seed))."""
+    from .tensor import Rng
+    if size % 2 == 0:
+        raise ValueError("committee size must be odd")
+    if size > len(pool):
+        raise ValueError(f"committee size {size} exceeds profile pool {len(pool)}")
+    order = Rng(seed).permutation(len(pool))
+    return [pool[i] for i in order[:size]]
+
+
+def member_value(node, xs, member) -> torch.Tensor:
+    """apply_op(node, args, member, fp64=False) on the GPU (the member's
+    DeviceProfile emulated bit-exactly, csrc/profile_fold.cuh)."""
+    from .bounds import FpModel, ROW_KINDS, apply_value, op_bound_device
+    if node.kind in ROW_KINDS:
+        y, _ = op_bound_device(node, xs, FpModel(), member, eps_f64=False)
+        return y
+    return apply_value(node, xs, member)
+
+
+def leaf_route(node, args, claimed, thresholds=None, committee_pool=None, committee_size=3,
+               committee_seed=0, model=None, profile=None, leaf=None) -> dict:
+    """Challenger.leaf_payload's verdict (dispute.py:639-671) on the GPU, from
+    the leaf's arguments on: the bound check (leaf_bound_check, exact), then
+    either the theoretical FP64-oracle recheck or the committee vote -- each
+    member re-executes the node under its DeviceProfile and votes
+    observed_p_max <= 1 against the claimed tensor; majority wins.  Returns
+    {"path", "winner", "evidence", "flops"} like the reference (evidence adds
+    the undecided-element counts)."""
+    from .bounds import FpModel
+    from .commitments import tensor_digest
+    from .tensor import Tensor
+    model = model or FpModel()
+    xs = _node_args(args)
+    res = leaf_bound_check(node, xs, claimed, model, profile)
+    y = res["y"]
+    flops = node_flops(node, tuple(y.shape), [tuple(a.shape) for a in xs])
+    c = claimed._dev if getattr(claimed, "_dev", None) is not None else claimed
+    c = _node_args([c])[0]
+    evidence = {"leaf": leaf if leaf is not None else getattr(node, "index", None),
+                "leaf_name": node.name,
+                "claimed_digest": tensor_digest(Tensor(tuple(c.shape), c.cpu().numpy().reshape(-1))),
+                "undecided_bound_elements": res["n_borderline"]}
+    if res["any_violation"]:
+        orc = oracle_recheck(node, xs, c, res["eps"], model, profile)
+        evidence["max_excess"] = orc["max_excess"]
+        evidence["undecided_oracle_elements"] = orc["n_borderline"]
+        return {"path": "theoretical", "winner": "proposer" if orc["ok"] else "challenger",
+                "evidence": evidence, "flops": flops}
+    if thresholds is None or committee_pool is None:
+        raise ValueError("committee path needs thresholds and a profile pool")
+    members = sample_committee(committee_pool, committee_size, committee_seed)
+    votes = []
+    for member in members:
+        ym = member_value(node, xs, member)
+        votes.append(observed_p_max(ym, c, thresholds, node.name) <= 1.0)
+    within = sum(votes)
+    evidence["votes_within"] = within
+    evidence["committee"] = ",".join(m.id for m in members)
+    return {"path": "committee", "winner": "proposer" if within * 2 > len(votes) else "challenger",
+            "evidence": evidence, "flops": flops}
 
 
 def to_device_eps(eps) -> torch.Tensor:
@@ -266,6 +449,7 @@ def to_device_eps(eps) -> torch.Tensor:
 
 
 __all__ = ["p_max", "observed_p_max", "screen", "select_offending", "check_node", "leaf_check",
+           "leaf_bound_check", "oracle_recheck", "leaf_route", "sample_committee",
            "CheckRecord", "new_result_buffer", "commit_check_nodes", "combine_partials",
            "partial_from_bytes"]
 _ = ctypes

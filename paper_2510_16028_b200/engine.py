@@ -139,14 +139,22 @@ def require_f32(*ts) -> None:
             raise ValueError(f"expected a float32 tensor, got {t.dtype}")
 
 
-def unary(kind: str, x: torch.Tensor) -> torch.Tensor:
-    """engine.py:133-154 (FP64 evaluation rounded once)."""
+def unary(kind: str, x: torch.Tensor, amb: torch.Tensor | None = None, eps_scale: float = 0.0,
+          eps_f64: bool | None = None):
+    """engine.py:133-154 (FP64 evaluation rounded once).  amb: the node's
+    value-ambiguity list (int64 [1 + cap], csrc/unary.cuh); eps_f64 not None:
+    also return the intrinsic bound eps_scale*|y| at the largest candidate."""
     require_f32(x)
     x = x.contiguous()
     y = torch.empty_like(x)
+    eps = None
+    if eps_f64 is not None:
+        eps = torch.empty(x.shape, dtype=torch.float64 if eps_f64 else torch.float32,
+                          device=x.device)
     _lib.call("nao_unary_fp64", x.data_ptr(), y.data_ptr(), x.numel(), _lib.UNARY[kind],
-              _lib.stream_ptr(x.device))
-    return y
+              _lib.ptr(eps), int(bool(eps_f64)), float(eps_scale), _lib.ptr(amb),
+              (amb.numel() - 1) if amb is not None else 0, _lib.stream_ptr(x.device))
+    return y if eps_f64 is None else (y, eps)
 
 
 def _batch_view(a: torch.Tensor, b: torch.Tensor, transpose_b: bool):
@@ -197,3 +205,80 @@ def relu(x: torch.Tensor) -> torch.Tensor:
 
 def parse_shape_attr(spec) -> tuple:
     return tuple(int(tok) for tok in str(spec).split(",") if tok != "")
+
+
+# ------------------------------------------------ FP64 oracle (theoretical path)
+
+def _rows_fp64(kind: int, x: torch.Tensor, axis: int, ln_eps: float = 0.0) -> torch.Tensor:
+    """nao_rows_fp64 over `axis` (moved last and back)."""
+    require_f32(x)
+    ax = axis % x.dim()
+    xm = x.movedim(ax, -1).contiguous()
+    n = xm.shape[-1]
+    if n == 0:
+        raise ValueError("cannot reduce an empty axis")
+    rows = xm.numel() // n
+    out_shape = xm.shape[:-1] if kind >= 2 else xm.shape
+    y = torch.empty(out_shape, dtype=torch.float64, device=x.device)
+    _lib.call("nao_rows_fp64", kind, xm.data_ptr(), y.data_ptr(), rows, n, float(ln_eps),
+              _lib.stream_ptr(x.device))
+    return y if kind >= 2 else y.movedim(-1, ax)
+
+
+def matmul_fp64(a: torch.Tensor, b: torch.Tensor, transpose_b: bool = False) -> torch.Tensor:
+    """matmul_op(fp64=True) (engine.py:173-177): exact FP64 products folded
+    sequentially -- bit-identical to the reference."""
+    require_f32(a, b)
+    a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
+    out = torch.empty(out_shape, dtype=torch.float64, device=a.device)
+    _lib.call("nao_matmul_fp64", a3.data_ptr(), b3.data_ptr(), out.data_ptr(), nb, M, N, K, sa, sb,
+              int(transpose_b), _lib.stream_ptr(a.device))
+    return out
+
+
+def apply_op_fp64(node, xs) -> torch.Tensor:
+    """apply_op(node, args64, None, fp64=True) (engine.py:220-285) on the GPU:
+    the reference's FP64 oracle of one operator (execute_fp64 :369-390; the
+    leaf route's theoretical recheck, dispute.py:648-656).  xs: FP32 CUDA
+    tensors (the node's arguments, promoted to FP64 as args64 is)."""
+    k = node.kind
+    if k in ("add", "sub", "mul", "div"):
+        a, b = xs[0].double(), xs[1].double()
+        return {"add": torch.add, "sub": torch.sub, "mul": torch.mul, "div": torch.div}[k](a, b)
+    if k == "neg":
+        return torch.neg(xs[0].double())
+    if k == "relu":
+        return relu(xs[0].double())
+    if k in UNARY_F64:
+        x = xs[0].contiguous()
+        require_f32(x)
+        y = torch.empty(x.shape, dtype=torch.float64, device=x.device)
+        _lib.call("nao_unary_f64out", x.data_ptr(), y.data_ptr(), x.numel(), _lib.UNARY[k],
+                  _lib.stream_ptr(x.device))
+        return y
+    if k in ("sum", "mean"):
+        return _rows_fp64(2 if k == "sum" else 3, xs[0], int(node.attr("axis", -1)))
+    if k in ("max", "min"):
+        ax = int(node.attr("axis", -1)) % xs[0].dim()
+        return (torch.amax if k == "max" else torch.amin)(xs[0].double(), dim=ax)
+    if k == "matmul":
+        return matmul_fp64(xs[0], xs[1], bool(node.attr("transpose_b", 0)))
+    if k == "linear":
+        return torch.add(matmul_fp64(xs[0], xs[1]), xs[2].double())
+    if k == "softmax":
+        return _rows_fp64(0, xs[0], int(node.attr("axis", -1)))
+    if k == "layernorm":
+        return _rows_fp64(1, xs[0], int(node.attr("axis", -1)), float(node.attr("eps", 1e-5)))
+    if k == "conv2d":  # extension: the implicit-im2col GEMM in FP64
+        from .bounds import im2col
+        x, w = xs
+        col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
+                                  int(node.attr("pad", 0)))
+        out = matmul_fp64(w.reshape(w.shape[0], -1).contiguous(), col, transpose_b=True)
+        return out.reshape(B, w.shape[0], OH, OW)
+    # data movement: exact in any precision
+    from .bounds import apply_value
+    return apply_value(node, list(xs), DeviceProfile("seq", "sequential")).double()
+
+
+UNARY_F64 = frozenset({"exp", "log", "sqrt", "rsqrt", "tanh", "gelu", "silu"})

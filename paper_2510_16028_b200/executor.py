@@ -32,11 +32,12 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .bounds import FpModel, apply_value, op_bound_device, release_activation_split
+from .bounds import (INTRINSIC_KINDS, ROW_KINDS, FpModel, apply_value, certified_overestimate,
+                     default_gemm_path, op_bound_device, release_activation_split)
 from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID
 from .commitments import DEFAULT_CHUNK_BYTES, alg_id, commit_tensors, root_of_digests
 from .dispute import new_result_buffer
-from .engine import NATIVE, ExecutionError, to_device
+from .engine import NATIVE, ExecutionError, _batch_view, fma_of, to_device
 from .graph import parse_ref
 
 INF_TAU = np.full(len(PERCENTILE_GRID), np.inf)
@@ -98,6 +99,75 @@ class _RunState:
     def __init__(self):
         self.pending, self.pend_idx, self.pend_bytes = [], [], 0
         self.pend_checks, self.pend_keep = [], []  # fused check descriptors / their operands
+        self.pend_refine = []  # nao_refine_desc of the flush's GEMM / conv / intrinsic nodes
+
+
+GEMM_KINDS = frozenset({"matmul", "linear", "conv2d"})
+
+
+def check_band(node, xs, eps):
+    """(eps kind, eps pointer, scale, lo_factor, uses the borderline list) of a
+    node's check.  lo_factor = 1/R with R the certified over-estimate of the
+    node's bound path (bounds.certified_overestimate): diff in (eps/R, eps] is
+    borderline -- recorded for GEMM / conv nodes (settled exactly by
+    nao_refine_borderline), only counted for row kernels (FP64 bounds, band
+    ~1e-12: numpy's own summation order)."""
+    if isinstance(eps, tuple):
+        if eps[0] == "scaled":  # u|y|, 2u|y|: the reference's FP64 product, exactly
+            return _lib.EPS_SCALED_LOCAL, None, float(eps[1]), 1.0, False
+        return _lib.EPS_ZERO, None, 0.0, 1.0, False
+    f32 = eps.dtype == torch.float32
+    kind = _lib.EPS_TENSOR_F32 if f32 else _lib.EPS_TENSOR_F64
+    if node.kind in GEMM_KINDS:
+        K = xs[1][0].numel() if node.kind == "conv2d" else xs[0].shape[-1]
+        R = certified_overestimate(node.kind, K=K, path=default_gemm_path(K), eps_f32=f32)
+        return kind, eps.data_ptr(), 0.0, 1.0 / R, True
+    if node.kind in ROW_KINDS:
+        ax = int(node.attr("axis", -1)) % xs[0].dim()
+        R = certified_overestimate(node.kind, n=xs[0].shape[ax], eps_f32=f32)
+        return kind, eps.data_ptr(), 0.0, 1.0 / R, False
+    return kind, eps.data_ptr(), 0.0, (1.0 / (1.0 + 2.0 ** -22) if f32 else 1.0), False
+
+
+def refine_desc(node, xs, y, yc, record_ptr, border, model, profile=None, eps_scale=0.0):
+    """nao_refine_desc of one node (None when its check needs no settling) and
+    the operand tensors it reads (keep them alive until the refine ran)."""
+    k = node.kind
+    d = _lib.RefineDesc()
+    d.list, d.cap, d.result = border.data_ptr(), border.numel() - 1, record_ptr
+    d.local, d.claimed = y.data_ptr(), yc.data_ptr()
+    if k in INTRINSIC_KINDS:
+        x = xs[0].contiguous()
+        d.kind, d.unary_kind, d.a, d.u = _lib.REFINE_UNARY, _lib.UNARY[k], x.data_ptr(), eps_scale
+        return d, [x]
+    if k in ("matmul", "linear"):
+        tb = bool(node.attr("transpose_b", 0)) if k == "matmul" else False
+        a3, b3, sa, sb, nb, M, N, K, _ = _batch_view(xs[0], xs[1], tb)
+        d.kind, d.a, d.b = _lib.REFINE_GEMM, a3.data_ptr(), b3.data_ptr()
+        d.batch, d.M, d.N, d.K, d.stride_a, d.stride_b = nb, M, N, K, sa, sb
+        d.transpose_b, d.has_y = int(tb), int(k == "linear")
+        d.gamma_const = model.reduction_const(K if fma_of(profile) else 2 * K - 1)
+        d.u = model.u
+        return d, [a3, b3]
+    if k == "conv2d":
+        x, w = xs[0].contiguous(), xs[1].contiguous()
+        B, C, H, W = x.shape
+        kk, st, pd = w.shape[-1], int(node.attr("stride", 1)), int(node.attr("pad", 0))
+        OH, OW = (H + 2 * pd - kk) // st + 1, (W + 2 * pd - kk) // st + 1
+        K = C * kk * kk
+        d.kind, d.a, d.b = _lib.REFINE_CONV, w.data_ptr(), x.data_ptr()
+        d.batch, d.M, d.N, d.K = B, OH * OW, w.shape[0], K
+        d.C, d.H, d.W, d.k, d.stride, d.pad, d.OW = C, H, W, kk, st, pd, OW
+        d.gamma_const = model.reduction_const(K if fma_of(profile) else 2 * K - 1)
+        return d, [x, w]
+    return None, []
+
+
+def run_refine(descs) -> None:
+    """One nao_refine_borderline launch on the current stream."""
+    if descs:
+        arr = (_lib.RefineDesc * len(descs))(*descs)
+        _lib.call("nao_refine_borderline", arr, len(descs), _lib.stream_ptr())
 
 
 def _segments(lo: int, hi: int, size: int):
@@ -172,11 +242,14 @@ class StreamingVerifier:
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
                  grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
-                 max_lag: int = 0, partial: bool = False):
+                 max_lag: int = 0, partial: bool = False, missing_thresholds: str = "raise"):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
         self.thresholds = thresholds
+        if missing_thresholds not in ("raise", "inf"):
+            raise ValueError("missing_thresholds must be 'raise' or 'inf'")
+        self.missing_thresholds = missing_thresholds
         self.alg = alg_id(hash_alg)
         self.chunk = int(chunk_bytes)
         self.flush_bytes = int(flush_bytes)
@@ -218,15 +291,28 @@ class StreamingVerifier:
         self._s_main = None
 
     # ---------------------------------------------------------- thresholds
+    def _sync_thresholds(self):
+        """Drop the cached taus / device specs when `thresholds` was replaced."""
+        if getattr(self, "_spec_for", None) is not self.thresholds:
+            self._spec_addr, self._tau_cache = {}, {}
+            self._spec_for = self.thresholds
+
     def _taus(self, name):
+        """(tau_abs, tau_rel) of a node.  Without a ThresholdSet the threshold
+        verdict is off (tau = +inf); with one, a node it does not cover raises
+        KeyError like the reference's ThresholdSet.lookup (calibration.py:189-191),
+        unless the verifier was built with missing_thresholds="inf"."""
         if self.thresholds is None:
             return INF_TAU, INF_TAU
+        self._sync_thresholds()
         t = self._tau_cache.get(name)
         if t is None:
             try:
                 op = self.thresholds.lookup(name)
                 t = (op.tau_abs, op.tau_rel)
             except KeyError:
+                if self.missing_thresholds != "inf":
+                    raise
                 t = (INF_TAU, INF_TAU)
             self._tau_cache[name] = t
         return t
@@ -234,9 +320,7 @@ class StreamingVerifier:
     def _spec_table(self, start, end):
         """Device address of every node's nao_verdict_spec in [start, end); the
         missing ones are uploaded in one copy."""
-        if getattr(self, "_spec_for", None) is not self.thresholds:  # thresholds replaced
-            self._spec_addr, self._tau_cache = {}, {}
-            self._spec_for = self.thresholds
+        self._sync_thresholds()
         missing = [n for n in self.g.nodes[start:end] if n.index not in self._spec_addr]
         if missing:
             size = int(_lib.load().nao_verdict_spec_bytes())
@@ -276,6 +360,9 @@ class StreamingVerifier:
         st.last = last_uses(g, start, end)
         st.values = dict(frontier or {})
         st.all_idx = torch.arange(n, device=self.dev)
+        # per-node borderline / value-ambiguity lists (word 0 = count, reset by
+        # the refine pass that consumes them)
+        st.border = torch.zeros((n, 1 + _lib.BORDER_CAP), dtype=torch.int64, device=self.dev)
         st.grid_arr = _lib.dbl_array(self.grid)
         if self.fuse_check:
             st.specs = self._spec_table(start, end)
@@ -321,6 +408,8 @@ class StreamingVerifier:
             with torch.cuda.stream(s_com):
                 r = commit_tensors(st.pending, self.chunk, self.alg,
                                    checks=st.pend_checks if self.fuse_check else None)
+                if self.fuse_check:
+                    run_refine(st.pend_refine)  # settle the flush's borderline elements
                 lo_i, hi_i = st.pend_idx[0], st.pend_idx[-1] + 1
                 if hi_i - lo_i == len(st.pend_idx):
                     st.roots[lo_i:hi_i].copy_(r)
@@ -350,7 +439,7 @@ class StreamingVerifier:
                     while len(self._host_events) > n_host:
                         self._host_events.pop(0).synchronize()
             st.pending, st.pend_idx, st.pend_bytes = [], [], 0
-            st.pend_checks, st.pend_keep = [], []
+            st.pend_checks, st.pend_keep, st.pend_refine = [], [], []
 
         values, last = st.values, st.last
         for node in g.nodes[lo:hi]:
@@ -363,8 +452,11 @@ class StreamingVerifier:
                     xs.append(to_device(st.inputs[key], self.dev))
                 else:
                     xs.append(to_device(g.weights[key], self.dev))
+            i = node.index - start
+            border = st.border[i]
             try:
-                y, eps = op_bound_device(node, xs, self.model, self.profile, eps_f64=None)
+                y, eps = op_bound_device(node, xs, self.model, self.profile, eps_f64=None,
+                                         amb=border if node.kind in INTRINSIC_KINDS else None)
             except (ExecutionError, NotImplementedError):
                 raise
             except Exception as exc:
@@ -372,28 +464,40 @@ class StreamingVerifier:
                                      node_index=node.index, node_name=node.name) from exc
             y = y.contiguous()
             yc = claimed_fn(node, y)
+            if not (isinstance(yc, torch.Tensor) and yc.dtype == torch.float32
+                    and tuple(yc.shape) == tuple(y.shape) and yc.device == y.device):
+                # the reference raises on a claimed tensor of another shape
+                # (elementwise_errors / leaf_payload broadcasting); the kernels
+                # would read the local tensor out of bounds
+                raise ExecutionError(
+                    f"node {node.index} ({node.name!r}): claimed tensor "
+                    f"{getattr(yc, 'dtype', type(yc))} {tuple(getattr(yc, 'shape', ()))} does not "
+                    f"match the recomputed float32 {tuple(y.shape)} on {y.device}",
+                    node_index=node.index, node_name=node.name)
+            yc = yc.contiguous()
             if self.trace_writer is not None:
                 self.trace_writer.write(node.index, yc)
             if self.bound_writer is not None:
                 self.bound_writer.write(node.index, _materialise_eps(eps, y))
             tau_a, tau_r = self._taus(node.name)
-            kind, eps_ptr, scale, lo_f = _lib.EPS_ZERO, None, 0.0, 1.0
-            if isinstance(eps, tuple):
-                if eps[0] == "scaled":
-                    kind, scale = _lib.EPS_SCALED_LOCAL, float(eps[1])
-            else:
-                kind = _lib.EPS_TENSOR_F64 if eps.dtype == torch.float64 else _lib.EPS_TENSOR_F32
-                lo_f = 1.0 if eps.dtype == torch.float64 else 1.0 / (1.0 + 2.0 ** -22)
-                eps_ptr = eps.data_ptr()
-            i = node.index - start
+            kind, eps_ptr, scale, lo_f, listed = check_band(node, xs, eps)
+            blist = border.data_ptr() if listed else None
+            rdesc, rkeep = (None, [])
+            if y.numel() and (listed or node.kind in INTRINSIC_KINDS):
+                rdesc, rkeep = refine_desc(node, xs, y, yc, st.records[i].data_ptr(), border,
+                                           self.model, self.profile, eps_scale=scale)
             desc = None
             if y.numel() and self.fuse_check:
                 desc = _lib.CheckDesc(y.data_ptr(), eps_ptr, st.specs[node.index],
                                       st.records[i].data_ptr(), scale, lo_f, kind,
-                                      _lib.CHECK_PARTIAL if self.partial else 0)
+                                      _lib.CHECK_PARTIAL if self.partial else 0,
+                                      blist, _lib.BORDER_CAP)
                 st.pend_keep.append(y)
                 if not isinstance(eps, tuple):
                     st.pend_keep.append(eps)
+                if rdesc is not None:
+                    st.pend_refine.append(rdesc)
+                    st.pend_keep.extend(rkeep)
             elif y.numel():
                 if self.overlap:
                     s_chk.wait_stream(main)
@@ -401,12 +505,16 @@ class StreamingVerifier:
                     side_use(yc, s_chk)
                     if not isinstance(eps, tuple):
                         side_use(eps, s_chk)
+                    for t in rkeep:
+                        side_use(t, s_chk)
                 with torch.cuda.stream(s_chk):
                     _lib.call("nao_check", y.data_ptr(), yc.data_ptr(), y.numel(), kind, eps_ptr,
                               scale, lo_f, st.grid_arr, _lib.dbl_array(tau_a),
                               _lib.dbl_array(tau_r), len(self.grid), self.epsilon,
                               st.records[i].data_ptr(), ws_chk.data_ptr(), ws_chk.numel(),
-                              chk_ptr)
+                              blist, _lib.BORDER_CAP, chk_ptr)
+                    if rdesc is not None:
+                        run_refine([rdesc])
             if stats is not None:
                 stats.elements_checked += y.numel()
                 stats.bytes_committed += y.numel() * 4
@@ -415,7 +523,6 @@ class StreamingVerifier:
                 elif node.kind == "conv2d":  # implicit GEMM, K = C k k
                     stats.gemm_flops += 2 * y.numel() * xs[1][0].numel()
             del eps, y
-            yc = yc.contiguous()
             values[node.index] = yc
             st.pending.append(yc)
             st.pend_checks.append(desc)

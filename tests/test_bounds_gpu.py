@@ -59,21 +59,23 @@ def test_op_bound_matches_reference(B, ref_ops, tag):
     yu, ru = y.view(np.int32).astype(np.int64), y_ref.astype(np.float32).view(np.int32)
     same = yu == ru
     if kind in INTRINSIC_TRANSCENDENTAL:
-        # FP64 exp/log/tanh differ from numpy's libm in the last FP64 ulp; after the
-        # single FP32 rounding that shows up as a rare 1-ulp value difference
-        # (engine.py:4-8 "2-ULP budget").  Bound = template on our own value.
-        if kind == "gelu":
-            # 0.5x(1+tanh(.)) cancels for x << 0: a 1-ulp FP64 tanh difference moves the
-            # result by ~|x| 2^-52 absolute -- the reference formula's own noise floor.
-            x64 = np.abs(ins[0].astype(np.float64))
-            ulp = np.spacing(np.abs(y_ref.astype(np.float32))).astype(np.float64)
-            tol = 2 * ulp + x64 * 2.0 ** -51
-            assert np.all(np.abs(y.astype(np.float64) - y_ref) <= tol), tag
-        else:
-            assert np.all(np.abs(yu - ru) <= 1), tag
-        assert same.mean() >= 0.95, (tag, same.mean())
-        np.testing.assert_array_equal(eps, 2 * 2.0 ** -24 * np.abs(y.astype(np.float64)))
-        assert_bound(eps.reshape(-1)[same.reshape(-1)], eps_ref.reshape(-1)[same.reshape(-1)], tag)
+        # numpy's FP64 libm is not correctly rounded: the GPU value equals the
+        # reference's on every element except the flagged value-ambiguous ones
+        # (csrc/unary.cuh), and the bound (taken at the largest candidate) is
+        # never below the reference's anywhere
+        import torch
+        from paper_2510_16028_b200 import _lib
+        from paper_2510_16028_b200.engine import unary
+        amb = torch.zeros(1 + _lib.BORDER_CAP, dtype=torch.int64, device="cuda")
+        unary(kind, torch.from_numpy(np.ascontiguousarray(ins[0])).cuda(), amb=amb)
+        a = amb.cpu().numpy()
+        flagged = np.zeros(y.size, bool)
+        flagged[a[1:1 + min(int(a[0]), _lib.BORDER_CAP)]] = True
+        assert np.all(flagged[~same.reshape(-1)]), (tag, int((~same).sum()))
+        assert flagged.mean() <= 0.05, (tag, flagged.mean())
+        e, er = eps.reshape(-1), eps_ref.reshape(-1)
+        assert np.all(e >= er), tag
+        assert_bound(e[~flagged], er[~flagged], tag)
     else:
         assert same.all(), tag
         assert_bound(eps, eps_ref, tag)

@@ -1,0 +1,183 @@
+"""GPU: accept/reject decisions identical to the reference at the bound boundary.
+
+The GPU bounds over-estimate the reference's eps by a certified factor R
+(up to ~1e-5 on the tcgen05 abs-GEMM).  Claims are planted with
+|claimed - y| within 1e-5 of eps_ref on both sides -- exactly the band where
+the unrefined GPU check would accept what the reference rejects -- on the
+MLP's fc0 (linear 784->256), a Qwen3 q-projection-shaped matmul
+(2048x4096x4096, sampled rows) and a ResNet-style conv.  The GPU verdict
+(leaf_bound_check: check + nao_refine_borderline) must count exactly the
+oracle's violations with nothing left undecided, and the leaf route must
+match the reference's (dispute.py:639-671)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import bounds as OB
+from oracle import check as OC
+
+pytestmark = pytest.mark.gpu
+
+
+class _Node:
+    def __init__(self, kind, attrs=None, name="op"):
+        self.kind, self.attrs, self.index, self.name, self.inputs = kind, attrs or {}, 0, name, ()
+
+    def attr(self, k, d=None):
+        return self.attrs.get(k, d)
+
+
+def plant_in_band(y, eps, rng, n_max=400, band=1e-5):
+    """claimed = y except on up to n_max elements whose FP32 grid is fine enough
+    (|y| small vs eps) to put |claimed - y| / eps inside (1-band, 1+band);
+    half just above 1, half just below."""
+    y = np.asarray(y, np.float32)
+    c = y.copy().reshape(-1)
+    yf, ef = y.reshape(-1).astype(np.float64), np.asarray(eps, np.float64).reshape(-1)
+    cand = np.nonzero((np.abs(yf) < 20 * ef) & (ef > 0))[0]
+    rng.shuffle(cand)
+    above = below = 0
+    for i in cand[:n_max]:
+        sgn = 1.0 if rng.random() < 0.5 else -1.0
+        want_above = above <= below
+        t = np.float32(yf[i] + sgn * ef[i])
+        # walk the FP32 grid until the ratio is on the wanted side, inside the band
+        for _ in range(64):
+            r = abs(float(t) - yf[i]) / ef[i]
+            if want_above and r <= 1.0:
+                t = np.nextafter(t, np.float32(sgn * np.inf))
+            elif not want_above and r > 1.0:
+                t = np.nextafter(t, np.float32(-sgn * np.inf))
+            else:
+                break
+        r = abs(float(t) - yf[i]) / ef[i]
+        if abs(r - 1.0) < band and (r > 1.0) == want_above:
+            c[i] = t
+            above += want_above
+            below += not want_above
+    assert above >= 10 and below >= 10, (above, below)
+    return c.reshape(y.shape), above, below
+
+
+def _check(node, args, claimed, y_ref, eps_ref, profile=None):
+    from paper_2510_16028_b200 import dispute
+    ref = OC.leaf_check(y_ref, claimed, eps_ref)
+    got = dispute.leaf_bound_check(node, args, claimed, profile=profile)
+    assert got["n_borderline"] == 0, got["n_borderline"]
+    assert got["n_violations"] == ref["n_violations"], (got["n_violations"], ref["n_violations"])
+    return got, ref
+
+
+def test_linear_fc0_in_band(ref_mlp):
+    from paper_2510_16028_b200.engine import DeviceProfile
+    from paper_2510_16028_b200.lowerings import build_mlp
+    from paper_2510_16028_b200.tensor import Rng
+    c = ref_mlp["config"]
+    spec = build_mlp(c["seed"], c["batch"], c["in_dim"], c["hidden"], c["n_classes"])
+    x = spec.make_inputs(Rng(*c["input_rng"]))["x"].array
+    g = spec.graph
+    node = next(n for n in g.nodes if n.kind == "linear")
+    args = [x] + [g.weights[r.split(":", 1)[1]].array for r in node.inputs[1:]]
+    y_ref, eps_ref = OB.op_bound(node, args, OB.FpModel())
+    claimed, above, below = plant_in_band(y_ref, eps_ref, np.random.default_rng(0))
+    prof = DeviceProfile("seq", "sequential")
+    got, ref = _check(node, args, claimed, y_ref, eps_ref, prof)
+    assert ref["n_violations"] == above
+    # the unrefined check (no band) would have missed them: eps_gpu > eps_ref there
+    from paper_2510_16028_b200 import dispute
+    raw = dispute.leaf_check(claimed, got["y"], got["eps"])
+    assert raw["n_violations"] < ref["n_violations"]
+
+
+@pytest.mark.parametrize("path", ["f16", "tf32", "ffma"])
+def test_qproj_matmul_in_band(monkeypatch, path):
+    """Qwen3-8B q-projection shape: y = x @ W (2048x4096 @ 4096x4096); eps_ref
+    from FP64 BLAS on 48 sampled rows, claims planted there."""
+    monkeypatch.setenv("NAO_GEMM_PATH", path)
+    from paper_2510_16028_b200 import dispute
+    from paper_2510_16028_b200.bounds import FpModel
+    rng = np.random.default_rng(11)
+    M, K, N = 2048, 4096, 4096
+    x = rng.standard_normal((M, K)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (K, N)) / np.sqrt(K)).astype(np.float32)
+    node = _Node("matmul")
+    xs, ws = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    y = (xs @ ws).cpu().numpy()  # native value; the band is about eps only
+    rows = np.sort(rng.choice(M, 48, replace=False))
+    eps_rows = OB.matmul_bound(x[rows], w, OB.FpModel())
+    claimed = y.copy()
+    cr, above, below = plant_in_band(y[rows], eps_rows, rng)
+    claimed[rows] = cr
+    ref = OC.leaf_check(y[rows], claimed[rows], eps_rows)
+    # GPU: the same leaf check on the GPU's own y (op_bound's value is cuBLAS here)
+    from paper_2510_16028_b200.engine import NATIVE
+    got = dispute.leaf_bound_check(node, [xs, ws], torch.from_numpy(claimed).cuda(),
+                                   FpModel(), NATIVE)
+    assert np.array_equal(got["y"].cpu().numpy(), y)
+    assert got["n_borderline"] == 0
+    assert got["n_violations"] == ref["n_violations"] == above
+
+
+def test_conv_in_band():
+    from paper_2510_16028_b200 import dispute
+    from paper_2510_16028_b200.engine import DeviceProfile
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 64, 14, 14)).astype(np.float32)
+    w = (rng.standard_normal((64, 64, 3, 3)) * 0.05).astype(np.float32)
+    node = _Node("conv2d", {"stride": 1, "pad": 1})
+    y_ref, eps_ref = OB.op_bound(node, [x, w], OB.FpModel())
+    claimed, above, below = plant_in_band(y_ref, eps_ref, rng)
+    got, ref = _check(node, [x, w], claimed, y_ref, eps_ref, DeviceProfile("seq", "sequential"))
+    assert ref["n_violations"] == above
+
+
+def test_leaf_route_matches_reference_route(ref_mlp):
+    """Both routes of dispute.py:639-671: an in-band claim goes theoretical (and
+    the FP64 oracle decides exactly as numpy's execute_fp64 would); an honest
+    drift claim goes to the committee of emulated profiles."""
+    from paper_2510_16028_b200 import calibration, dispute
+    from paper_2510_16028_b200.engine import DeviceProfile, default_profiles
+    from paper_2510_16028_b200.lowerings import build_mlp
+    from paper_2510_16028_b200.tensor import Rng
+    c = ref_mlp["config"]
+    spec = build_mlp(c["seed"], c["batch"], c["in_dim"], c["hidden"], c["n_classes"])
+    x = spec.make_inputs(Rng(*c["input_rng"]))["x"].array
+    g = spec.graph
+    node = next(n for n in g.nodes if n.kind == "linear")
+    args = [x] + [g.weights[r.split(":", 1)[1]].array for r in node.inputs[1:]]
+    th = calibration.ThresholdSet.from_json(ref_mlp["thresholds"])
+    y_ref, eps_ref = OB.op_bound(node, args, OB.FpModel())
+    claimed, _, _ = plant_in_band(y_ref, eps_ref, np.random.default_rng(3))
+    res = dispute.leaf_route(node, args, claimed, th, default_profiles(), 3, 7,
+                             profile=DeviceProfile("seq", "sequential"))
+    # reference: any(diff > eps) -> theoretical; FP64 oracle (products exact, sequential fold)
+    y64 = OB.matmul_fp64(args[0], args[1]) + args[2].astype(np.float64)
+    ok = bool(np.all(np.abs(claimed.astype(np.float64) - y64) <= eps_ref))
+    assert res["path"] == "theoretical"
+    assert res["winner"] == ("proposer" if ok else "challenger")
+    assert res["evidence"]["undecided_bound_elements"] == 0
+    # honest claim (the reference value): committee path, proposer wins
+    res2 = dispute.leaf_route(node, args, y_ref, th, default_profiles(), 3, 7,
+                              profile=DeviceProfile("seq", "sequential"))
+    assert res2["path"] == "committee" and res2["winner"] == "proposer"
+    assert res2["evidence"]["votes_within"] == 3
+
+
+def test_matmul_fp64_bit_exact():
+    from paper_2510_16028_b200.engine import apply_op_fp64
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((3, 37, 70)).astype(np.float32)
+    b = rng.standard_normal((3, 70, 19)).astype(np.float32)
+    got = apply_op_fp64(_Node("matmul"), [torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()])
+    ref = OB.matmul_fp64(a, b)
+    assert np.array_equal(got.cpu().numpy(), ref)
+    xs = rng.standard_normal((40, 33)).astype(np.float32)
+    for kind, attrs in (("softmax", {"axis": -1}), ("layernorm", {"axis": -1, "eps": 1e-5}),
+                        ("sum", {"axis": -1}), ("mean", {"axis": 0})):
+        got = apply_op_fp64(_Node(kind, attrs), [torch.from_numpy(xs).cuda()]).cpu().numpy()
+        ref = OB.apply_op_fp64(_Node(kind, attrs), [xs])
+        if kind == "softmax":  # FP64 exp: last-ulp libm differences only
+            np.testing.assert_allclose(got, ref, rtol=4e-16, atol=0)
+        else:
+            assert np.array_equal(got, ref), kind
