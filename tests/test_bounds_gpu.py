@@ -72,7 +72,9 @@ def test_op_bound_matches_reference(B, ref_ops, tag):
         flagged = np.zeros(y.size, bool)
         flagged[a[1:1 + min(int(a[0]), _lib.BORDER_CAP)]] = True
         assert np.all(flagged[~same.reshape(-1)]), (tag, int((~same).sum()))
-        assert flagged.mean() <= 0.05, (tag, flagged.mean())
+        # gelu on U(-6, 6): 1 + tanh cancels for x < ~-3 (its FP32 value there
+        # depends on the libm's last FP64 ulps); the others: ~never
+        assert flagged.mean() <= (0.15 if kind == "gelu" else 1e-3), (tag, flagged.mean())
         e, er = eps.reshape(-1), eps_ref.reshape(-1)
         assert np.all(e >= er), tag
         assert_bound(e[~flagged], er[~flagged], tag)

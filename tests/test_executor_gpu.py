@@ -99,7 +99,7 @@ def test_streaming_in_band_claims_match_oracle(ref_mlp):
         y_ref, eps = OB.op_bound(node, args, OB.FpModel())
         cl = y_ref
         if node.kind == "linear":
-            cl, _, _ = plant_in_band(y_ref, eps, rng, n_max=200)
+            cl, _, _ = plant_in_band(y_ref, eps, rng, n_max=200, min_each=3)
         expect[node.index] = OC.leaf_check(y_ref, cl, eps)["n_violations"]
         claimed[node.index] = torch.from_numpy(np.ascontiguousarray(cl)).cuda()
         return claimed[node.index].clone()

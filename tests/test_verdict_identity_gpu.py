@@ -28,7 +28,7 @@ class _Node:
         return self.attrs.get(k, d)
 
 
-def plant_in_band(y, eps, rng, n_max=400, band=1e-5):
+def plant_in_band(y, eps, rng, n_max=400, band=1e-5, min_each=10):
     """claimed = y except on up to n_max elements whose FP32 grid is fine enough
     (|y| small vs eps) to put |claimed - y| / eps inside (1-band, 1+band);
     half just above 1, half just below."""
@@ -56,7 +56,7 @@ def plant_in_band(y, eps, rng, n_max=400, band=1e-5):
             c[i] = t
             above += want_above
             below += not want_above
-    assert above >= 10 and below >= 10, (above, below)
+    assert above >= min_each and below >= min_each, (above, below)
     return c.reshape(y.shape), above, below
 
 
