@@ -1,0 +1,54 @@
+"""GPU: the reference's OWN tests, run against the unmodified reference package
+(baseline/_ref: `pip install --target` of /root/reference/pkg plus a copy of
+its tests, made by tools/install_reference.sh) with libnao_b200.so bound in
+by paper_2510_16028_b200.refbind:
+  test_bounds.py:22-228, test_commitments.py:20-193, test_calibration.py:24-101,
+  and the leaf routing of test_dispute.py:246-297 (TestLeafRouting) plus the
+  whole dispute game that ends in it.
+Every one must pass with the hot-path calls counted through the binding and
+the in-tree library mapped into the process."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+REF = ROOT / "baseline" / "_ref"
+REF_TESTS = REF / "ref_tests"
+
+SUITES = {
+    "bounds": (["test_bounds.py"], ("op_bound", "matmul_bound")),
+    "commitments": (["test_commitments.py"], ("build_tree",)),
+    "calibration": (["test_calibration.py"], ("percentile_profile", "calibrate")),
+    "dispute_leaf": (["test_dispute.py"], ("leaf_payload", "op_bound", "percentile_profile")),
+}
+
+
+@pytest.mark.parametrize("suite", sorted(SUITES))
+def test_reference_suite_through_b200(suite, tmp_path):
+    if not (REF / "fpverify").is_dir() or not REF_TESTS.is_dir():
+        pytest.skip("baseline/_ref not installed (tools/install_reference.sh)")
+    files, must_call = SUITES[suite]
+    report = tmp_path / "report.json"
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT / "tests"), str(ROOT),
+                                         env.get("PYTHONPATH", "")])
+    env["NAO_REF_REPORT"] = str(report)
+    cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "ref_plugin",
+           "-p", "no:cacheprovider", "--rootdir", str(REF_TESTS),
+           *[str(REF_TESTS / f) for f in files]]
+    res = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True,
+                         timeout=1800)
+    tail = (res.stdout + res.stderr)[-4000:]
+    assert res.returncode == 0, tail
+    doc = json.loads(report.read_text())
+    assert doc["native_loaded"], doc
+    for name in must_call:
+        assert doc["calls"].get(name, 0) > 0, (name, doc["calls"])
+    print(suite, doc["calls"], tail.splitlines()[-1])
