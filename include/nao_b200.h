@@ -64,7 +64,11 @@ typedef struct nao_profile {
     int32_t fma;
     int32_t reserved;
 } nao_profile;
-enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1, NAO_GEMM_TC_F16X3 = 2 };
+/* abs-GEMM bound paths: FFMA round-up chains, tcgen05 3-split (TF32 / FP16),
+ * and FP64 (the reference's own arithmetic; the API default, eps within
+ * ~1e-12 of numpy's -- the streaming verifier uses the tensor-core paths) */
+enum nao_gemm_path { NAO_GEMM_FFMA_RU = 0, NAO_GEMM_TC_TF32X3 = 1, NAO_GEMM_TC_F16X3 = 2,
+                     NAO_GEMM_FP64 = 3 };
 
 /* ------------------------------------------------------------ library */
 int nao_version(void);

@@ -33,7 +33,7 @@ HASH_SHA256, HASH_KECCAK256 = 0, 1
 EPS_TENSOR_F32, EPS_TENSOR_F64, EPS_SCALED_LOCAL, EPS_ZERO = 0, 1, 2, 3
 RED_SUM, RED_MEAN, RED_MAX, RED_MIN = 0, 1, 2, 3
 UNARY = {"exp": 0, "log": 1, "sqrt": 2, "rsqrt": 3, "tanh": 4, "gelu": 5, "silu": 6}
-GEMM_FFMA_RU, GEMM_TC_TF32X3, GEMM_TC_F16X3 = 0, 1, 2
+GEMM_FFMA_RU, GEMM_TC_TF32X3, GEMM_TC_F16X3, GEMM_FP64 = 0, 1, 2, 3
 BORDER_CAP = 1023  # borderline / ambiguity list entries per node (word 0 = count)
 
 

@@ -117,14 +117,18 @@ def _tc_overestimate(K: int, f16: bool) -> float:
 
 def certified_overestimate(kind: str, K: int = 0, n: int = 0, path: int | None = None,
                            eps_f32: bool = True) -> float:
+    # path None: the path abs_gemm_bound picks for this eps dtype
     """R of one node's bound.  kind: matmul/linear/conv2d (K = reduced length,
     path = the abs-GEMM path), softmax/layernorm/sum/mean (n = row length),
     anything else 1.0 (templates evaluated exactly as the reference does)."""
     store = 1.0 + 2.0 ** -23 if eps_f32 else 1.0  # FP32 rounded up
     if kind in ("matmul", "linear", "conv2d"):
-        path = default_gemm_path(K) if path is None else path
+        path = default_gemm_path(K, api=not eps_f32) if path is None else path
         if path == _lib.GEMM_FFMA_RU:  # every partial rounds up, chains of 32
             r = (1.0 + 2.0 ** -23) ** 34 * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -48)
+        elif path == _lib.GEMM_FP64:  # both FP64 sums within gamma_K of the exact one
+            g = (K + 2) * 2.0 ** -53
+            r = (1.0 + g) / (1.0 - g) * (1.0 + gemm_slack(K)) * (1.0 + 2.0 ** -48)
         else:
             r = _tc_overestimate(K, path == _lib.GEMM_TC_F16X3)
         return r * store
@@ -186,9 +190,12 @@ def _eps_buffer(shape, device, f64: bool) -> torch.Tensor:
 F16_MIN_K = 256  # short K is epilogue bound: the TF32 split wins there (kbench)
 
 
-def default_gemm_path(K: int | None = None) -> int:
-    """NAO_GEMM_PATH = auto (default: tcgen05 FP16 3-split for K > 256, 3xTF32
-    below), tc / tf32, f16, or ffma.  All are sound."""
+def default_gemm_path(K: int | None = None, api: bool = False) -> int:
+    """NAO_GEMM_PATH = auto (default), tc / tf32, f16, ffma or fp64.  auto:
+    the streaming verifier's FP32 bounds run on tcgen05 (FP16 3-split for
+    K > 256, 3xTF32 below); API calls returning the reference's FP64 bound
+    (api=True: matmul_bound, op_bound, co_execute) use the FP64 path, the
+    reference's own arithmetic.  All are sound."""
     env = os.environ.get("NAO_GEMM_PATH", "auto").lower()
     if env in ("ffma", "simt", "0"):
         return _lib.GEMM_FFMA_RU
@@ -196,6 +203,8 @@ def default_gemm_path(K: int | None = None) -> int:
         return _lib.GEMM_TC_F16X3
     if env in ("tc", "tf32", "1"):
         return _lib.GEMM_TC_TF32X3
+    if env in ("fp64", "3") or api:
+        return _lib.GEMM_FP64
     return _lib.GEMM_TC_F16X3 if (K is not None and K > F16_MIN_K) else _lib.GEMM_TC_TF32X3
 
 
@@ -281,7 +290,7 @@ def abs_gemm_bound(a: torch.Tensor, b: torch.Tensor, const: float, transpose_b=F
     a_owner: A is a (2-D view of a) static weight -- cache its split on it."""
     require_f32(a, b, y)
     a3, b3, sa, sb, nb, M, N, K, out_shape = _batch_view(a, b, transpose_b)
-    path = default_gemm_path(K) if path is None else path
+    path = default_gemm_path(K, api=bool(eps_f64)) if path is None else path
     eps = _eps_buffer(out_shape, a.device, eps_f64)
     yc = None
     if y is not None:

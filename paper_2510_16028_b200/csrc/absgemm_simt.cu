@@ -178,6 +178,66 @@ using namespace nao;
 
 extern "C" {
 
+}  // extern "C"
+
+namespace nao {
+// NAO_GEMM_FP64: the reference's own arithmetic -- |a||b| exact in FP64, an
+// FP64 running sum per output (error <= gamma_K in FP64, ~K 2^-53), then
+// const * S * (1 + slack) [+ u|y|].  The API path of matmul_bound / op_bound
+// (eps within ~1e-12 of numpy's, reference test tolerances of 1e-9 hold); the
+// streaming verifier uses the tensor-core paths.
+constexpr int kF64T = 64, kF64K = 16;
+__global__ void __launch_bounds__(256) k_absgemm_fp64(const __grid_constant__ GemmArgs g) {
+    __shared__ double As[kF64K][kF64T], Bs[kF64K][kF64T];
+    const int64_t bz = blockIdx.z;
+    const int64_t m0 = (int64_t)blockIdx.y * kF64T, n0 = (int64_t)blockIdx.x * kF64T;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const float* a = g.A + bz * g.sA;
+    const float* b = g.B + bz * g.sB;
+    double acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < g.K; k0 += kF64K) {
+        for (int t = threadIdx.x; t < kF64K * kF64T; t += 256) {
+            const int kk = t % kF64K, r = t / kF64K;
+            const int64_t gm = m0 + r, gk = k0 + kk;
+            As[kk][r] = (gm < g.M && gk < g.K) ? fabs((double)__ldg(a + gm * g.lda + gk)) : 0.0;
+            const int kb = t / kF64T, c = t % kF64T;
+            const int64_t gn = n0 + c, gk2 = k0 + kb;
+            float bv = 0.f;
+            if (gn < g.N && gk2 < g.K)
+                bv = g.transpose_b ? __ldg(b + gn * g.ldb + gk2) : __ldg(b + gk2 * g.ldb + gn);
+            Bs[kb][c] = fabs((double)bv);
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < kF64K; kk++) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    const double s = __dmul_ru(g.c, 1.0 + g.slack);
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
+            if (gm >= g.M || gn >= g.N) continue;
+            const int64_t o = bz * g.sC + gm * g.ldc + gn;
+            double e = __dmul_ru(s, acc[i][j]);
+            if (g.Y) e = __dadd_ru(e, __dmul_rn(g.u, fabs((double)__ldg(g.Y + o))));
+            if (g.out_f64) static_cast<double*>(g.C)[o] = e;
+            else static_cast<float*>(g.C)[o] = __double2float_ru(e);
+        }
+}
+}  // namespace nao
+
+extern "C" {
+
 int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, int64_t batch,
                        int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc,
                        int64_t stride_a, int64_t stride_b, int64_t stride_c, int transpose_b,
@@ -185,7 +245,8 @@ int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, i
                        int path, void* stream) {
     NAO_REQUIRE(A && B && eps, "abs-gemm: null pointer");
     NAO_REQUIRE(batch >= 0 && M >= 0 && N >= 0 && K >= 1, "abs-gemm: bad shape");
-    NAO_REQUIRE(path == NAO_GEMM_FFMA_RU, "abs-gemm: path %d not available in this build", path);
+    NAO_REQUIRE(path == NAO_GEMM_FFMA_RU || path == NAO_GEMM_FP64,
+                "abs-gemm: path %d not available through nao_abs_gemm_bound", path);
     NAO_REQUIRE(batch <= 65535, "abs-gemm: batch too large");
     if (batch == 0 || M == 0 || N == 0) return NAO_OK;
     GemmArgs g;
@@ -194,6 +255,13 @@ int nao_abs_gemm_bound(const float* A, const float* B, void* eps, int eps_f64, i
     g.sA = stride_a; g.sB = stride_b; g.sC = stride_c;
     g.transpose_b = transpose_b; g.out_f64 = eps_f64;
     g.c = gamma_const; g.slack = slack; g.u = u;
+    if (path == NAO_GEMM_FP64) {
+        dim3 grid64((unsigned)ceil_div(N, kF64T), (unsigned)ceil_div(M, kF64T), (unsigned)batch);
+        NAO_REQUIRE(grid64.y <= 65535, "abs-gemm: M too large");
+        k_absgemm_fp64<<<grid64, 256, 0, static_cast<cudaStream_t>(stream)>>>(g);
+        NAO_CHECK_LAUNCH();
+        return NAO_OK;
+    }
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
     NAO_REQUIRE(grid.y <= 65535, "abs-gemm: M too large");
     k_absgemm_ffma<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(g);

@@ -126,6 +126,8 @@ def to_device(a, device=None) -> torch.Tensor:
         return a.device_view(device)
     if hasattr(a, "cuda") and hasattr(a, "shape") and not isinstance(a, np.ndarray):
         return a.cuda(device).reshape(a.shape)
+    if not isinstance(a, np.ndarray) and hasattr(a, "array"):  # the reference's Tensor
+        a = a.array
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
     return torch.from_numpy(arr).to(device or "cuda")
 

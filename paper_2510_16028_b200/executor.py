@@ -33,7 +33,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .bounds import (INTRINSIC_KINDS, ROW_KINDS, FpModel, apply_value, certified_overestimate,
-                     default_gemm_path, op_bound_device, release_activation_split)
+                     op_bound_device, release_activation_split)
 from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID
 from .commitments import DEFAULT_CHUNK_BYTES, alg_id, commit_tensors, root_of_digests
 from .dispute import new_result_buffer
@@ -120,7 +120,7 @@ def check_band(node, xs, eps):
     kind = _lib.EPS_TENSOR_F32 if f32 else _lib.EPS_TENSOR_F64
     if node.kind in GEMM_KINDS:
         K = xs[1][0].numel() if node.kind == "conv2d" else xs[0].shape[-1]
-        R = certified_overestimate(node.kind, K=K, path=default_gemm_path(K), eps_f32=f32)
+        R = certified_overestimate(node.kind, K=K, eps_f32=f32)
         return kind, eps.data_ptr(), 0.0, 1.0 / R, True
     if node.kind in ROW_KINDS:
         ax = int(node.attr("axis", -1)) % xs[0].dim()

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parent.parent
 REF = ROOT / "baseline" / "_ref"
-REF_TESTS = REF / "ref_tests"
+REF_TESTS = REF / "tests"  # the reference tests read tests/golden/ relative to their package dir
 
 SUITES = {
     "bounds": (["test_bounds.py"], ("op_bound", "matmul_bound")),
@@ -41,9 +41,8 @@ def test_reference_suite_through_b200(suite, tmp_path):
                                          env.get("PYTHONPATH", "")])
     env["NAO_REF_REPORT"] = str(report)
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "ref_plugin",
-           "-p", "no:cacheprovider", "--rootdir", str(REF_TESTS),
-           *[str(REF_TESTS / f) for f in files]]
-    res = subprocess.run(cmd, cwd=str(tmp_path), env=env, capture_output=True, text=True,
+           "-p", "no:cacheprovider", "--rootdir", str(REF), *[f"tests/{f}" for f in files]]
+    res = subprocess.run(cmd, cwd=str(REF), env=env, capture_output=True, text=True,
                          timeout=1800)
     tail = (res.stdout + res.stderr)[-4000:]
     assert res.returncode == 0, tail

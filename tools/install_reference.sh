@@ -9,6 +9,6 @@ rm -rf /tmp/nao_refpkg baseline/_ref
 cp -r /root/reference/pkg /tmp/nao_refpkg
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target baseline/_ref /tmp/nao_refpkg
-mkdir -p baseline/_ref/ref_tests
-cp -r /root/reference/pkg/tests/* baseline/_ref/ref_tests/
+mkdir -p baseline/_ref/tests
+cp -r /root/reference/pkg/tests/* baseline/_ref/tests/
 echo "reference installed in baseline/_ref"
