@@ -161,7 +161,10 @@ def calibrate_thresholds(g, sv_cls, ids, dev, model, args, start=0, end=None, fr
             # is the ulp of the largest one
             per = 1 if y.numel() <= (1 << 16) else max(1, args.drift_period // 4)
             yc = drift_claim(node, y, seed=seed, period=per)
-            if y.numel():
+            if not y.numel():  # empty outputs: no errors, zero thresholds
+                z = torch.zeros(len(PERCENTILE_GRID), dtype=torch.float64, device=y.device)
+                env.setdefault(node.name, (z, z.clone()))
+            else:
                 pa, pr = error_profiles_device(y, yc)
                 if node.name in env:
                     torch.maximum(env[node.name][0], pa, out=env[node.name][0])
@@ -600,117 +603,335 @@ def run_ours(args):
     return line
 
 
-# ------------------------------------------------------------- CPU (oracle)
-def cpu_layer_sample(seq: int, layers_total: int, hash_name: str, threads: int):
-    """The reference algorithm on the host: one Qwen3-8B-shaped layer (full
-    hidden/heads/intermediate widths) at sequence length `seq`, node by node:
-    numpy FP32 forward (BLAS), oracle bound templates (FP64 BLAS abs-GEMM,
-    sequential-fold softmax/norm parts), leaf check + np.percentile p_max,
-    chunked Merkle commit (C restatement, `threads` threads).  Returns per-node
-    (kind, numel, gemm_flops, t_fwd, t_bound, t_check, t_commit)."""
+# ------------------------------------------------- the other BASELINE configs
+CONFIGS = {
+    # name: (BASELINE.json config, global batch, batch-sharded across ranks, planted fault)
+    "mlp": ("2-layer MLP 784-256-10 FP32 batch 64", 64, False, "fc1"),
+    "resnet18": ("ResNet-18 FP32 batch 32 224x224", 32, False, "layer3.0.conv2"),
+    "gpt2": ("GPT-2 small FP32 seq 1024 batch 8", 8, True, "l5_fc"),
+    "unet": ("Stable Diffusion UNet-shaped FP32 denoising step 64x64 latent batch 8 "
+             "(batch-sharded over the ranks)", 8, True, "down1.res0.conv2"),
+}
+
+
+def _config_model(name, batch, device):
     import dataclasses
+    from paper_2510_16028_b200 import lowerings as L
+    if name == "mlp":
+        return L.build_mlp(seed=0, batch=batch)
+    if name == "resnet18":
+        return L.build_resnet18(batch=batch, side=224, device=device)
+    if name == "gpt2":
+        return L.build_decoder(dataclasses.replace(L.GPT2_SMALL, batch=batch), device=device,
+                               seed=0)
+    if name == "unet":
+        return L.build_unet(dataclasses.replace(L.SD15_UNET, batch=batch), device=device)
+    raise ValueError(name)
+
+
+def run_config(args):
+    """bench.py --config {mlp,resnet18,gpt2,unet}: the same protocol as the
+    Qwen3 line on another BASELINE.json config -- plain forward (cuBLAS /
+    cuDNN FP32, TF32 off) vs the streaming verifier (bounds + check + exact
+    verdicts + chunked Keccak commit, proposer harness inside the timed
+    region), CUDA-graph dispatch, device-calibrated thresholds (alpha 3).
+    L2 is flushed (256 MB write) before every timed step, outside its events,
+    so small configs do not run from a warm L2.  Batch-sharded configs split
+    the global batch over the ranks (strong scaling); every rank verifies its
+    samples independently, one all_gather of the per-node records, timing =
+    max over ranks."""
     import torch
+    import torch.distributed as dist
+    from paper_2510_16028_b200 import _lib
+    from paper_2510_16028_b200.dispute import CheckRecord
+    from paper_2510_16028_b200.executor import (GraphedRun, NodeStats, StreamingVerifier,
+                                                drift_claim)
+    from paper_2510_16028_b200.tensor import Rng
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("NAO_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    backend = os.environ.get("NAO_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
+    if world > 1:
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cudnn.benchmark = True
+    torch.cuda.set_stream(torch.cuda.Stream(dev, priority=-1))
+    label, gbatch, sharded, fault = CONFIGS[args.config]
+    if sharded and gbatch % world:
+        raise ValueError(f"batch {gbatch} does not split over {world} ranks")
+    batch = gbatch // world if sharded else gbatch
+    spec = _config_model(args.config, batch, dev)
+    g = spec.graph
+    x = spec.make_inputs(Rng(2024 + rank))
+    for node in g.nodes:  # materialise the weights before timing
+        for ref in node.inputs:
+            if ref.startswith("weight:"):
+                g.weights[ref.split(":", 1)[1]]
+    thresholds = calibrate_thresholds(g, StreamingVerifier, x, dev, None, args)
+    sv = StreamingVerifier(g, None, thresholds=thresholds, hash_alg=args.hash,
+                           chunk_bytes=args.chunk, max_lag=args.max_lag,
+                           flush_bytes=args.flush_mb << 20)
+
+    def claimed_fn(node, y):
+        return drift_claim(node, y, 1, args.drift_period, fault)
+
+    stats = NodeStats()
+    sv.run(x, claimed_fn, stats=stats)
+    torch.cuda.synchronize()
+    seg = args.graphs or 96
+    plain = GraphedRun.record_plain(g, x, dev, 0, None, None, seg_nodes=seg)
+    ver = sv.capture(x, claimed_fn, seg_nodes=seg)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, k):
+        ms = 0.0
+        for _ in range(k):
+            flush.fill_(1)  # evict L2 (126 MB) between steps, outside the events
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        ms /= k
+        if world > 1:
+            t = torch.tensor([ms], device=coll_dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    import gc
+    gc.collect(); gc.freeze(); gc.disable()
+    for _ in range(args.warmup):
+        plain.replay()
+    t_plain = timed(plain.replay, args.steps)
+    for _ in range(args.warmup):
+        ver.replay()
+    with ClockSampler(local) as clocks:
+        t_ver = timed(ver.replay, args.steps)
+    # end to end: inputs H2D from pinned host into the graphs' input buffers,
+    # verified forward, D2H of the per-node roots + records
+    from paper_2510_16028_b200.engine import to_device
+    in_dev = {k: to_device(v, dev) for k, v in x.items()}
+    in_host = {k: v.detach().cpu().pin_memory() for k, v in in_dev.items()}
+    h2d = sum(v.numel() * v.element_size() for v in in_host.values())
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k, v in in_host.items():
+            in_dev[k].copy_(v, non_blocking=True)
+        roots, recs = ver.replay()
+        host_roots, host_recs = roots.cpu(), recs.cpu()
+        e2e_ms += (time.perf_counter() - t0) * 1000.0
+    e2e_ms /= args.steps
+    gc.enable()
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        parts = [torch.zeros_like(host_recs) for _ in range(world)]
+        dist.all_gather(parts, host_recs.to(coll_dev) if backend == "nccl" else host_recs)
+        all_recs = [p.cpu() for p in parts]
+        tot = torch.tensor([float(stats.bytes_committed), float(stats.gemm_flops)],
+                           dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        tot_bytes, tot_flops = float(tot[0]), float(tot[1])
+    else:
+        all_recs = [host_recs]
+        tot_bytes, tot_flops = float(stats.bytes_committed), float(stats.gemm_flops)
+    flagged = set()
+    n_border = 0
+    for recs_r in all_recs:
+        for i in range(recs_r.shape[0]):
+            r = CheckRecord(recs_r[i]).host()
+            n_border += int(r["n_borderline"])
+            if r["n_violations"] or r["threshold_exceeded"]:
+                flagged.add(g.nodes[i].name)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+    overhead = 100.0 * (t_ver - t_plain) / t_plain
+    line = {"metric": METRIC, "value": round(overhead, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ver, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 values / f64 bound math / u32 hash words", "data": "synthetic",
+            "config": {"workload": label, "model": f"{args.config} random-init",
+                       "global_batch": gbatch, "per_rank_batch": batch,
+                       "nodes": g.n_nodes, "dispatch": f"cuda graphs ({seg}-node segments)",
+                       "parallelism": f"batch-sharded x{world}" if sharded and world > 1
+                       else ("replicas" if world > 1 else "single"),
+                       "l2": "flushed (256 MB write) before every timed step, outside the events"},
+            "plain_fwd_ms": round(t_plain, 3), "verified_fwd_ms": round(t_ver, 3),
+            "merkle_gb_per_step": round(tot_bytes / 1e9, 3),
+            "gemm_tflop_per_step": round(tot_flops / 1e12, 4),
+            "verdicts": {"flagged_nodes": sorted(flagged)[:10], "planted_fault": fault,
+                         "borderline_elements": n_border},
+            "e2e": {"value": round(100.0 * (e2e_ms - t_plain) / t_plain, 2), "unit": UNIT,
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(host_roots.numel() + host_recs.numel())},
+            "gpu_launches": None, "roofline": None, "cpu_baseline": None,
+            "clocks": clocks.summary()}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+# ------------------------------------------------------------- CPU (oracle)
+def cpu_layer_prepare(seq: int):
+    """One Qwen3-8B-shaped decoder layer at the real shape (hidden 4096, 32/8
+    heads, intermediate 12288, S=seq) on the host: the graph, its weights and
+    every node's FP32 arguments from a numpy forward (setup, untimed -- the
+    inputs of the timed node work)."""
+    import dataclasses
     from oracle import bounds as OB
-    from oracle import check as OC
-    from oracle import commit as OM
     from paper_2510_16028_b200.graph import parse_ref
     from paper_2510_16028_b200.lowerings import QWEN3_8B, build_decoder
     shape = dataclasses.replace(QWEN3_8B, seq=seq)
     spec = build_decoder(shape, device="cpu", seed=0, layers=1, with_head=False)
     g = spec.graph
-    rng = np.random.default_rng(0)
-    ids = rng.integers(0, shape.vocab, size=(1, seq)).astype(np.float32)
-    model = OB.FpModel()
-    vals, out = {}, []
-    alg = OM.KECCAK256 if hash_name == "keccak256" else OM.SHA256
-    inf = np.full(len(OC.PERCENTILE_GRID), np.inf)
+    ids = np.random.default_rng(0).integers(0, shape.vocab, size=(1, seq)).astype(np.float32)
+    vals, work = {}, []
+    last = {}
+    for node in g.nodes:
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            if cat == "node":
+                last[key] = node.index
     for node in g.nodes:
         args = []
         for ref in node.inputs:
             cat, key = parse_ref(ref)
             args.append(vals[key] if cat == "node" else ids if cat == "input"
                         else g.weights[key].array)
-        t0 = time.perf_counter()
-        if node.kind in ("matmul", "linear"):
-            b = np.swapaxes(args[1], -1, -2) if node.attr("transpose_b", 0) else args[1]
-            y = np.matmul(args[0], b).astype(np.float32)
-            if node.kind == "linear":
-                y = y + args[2]
-            t1 = time.perf_counter()
-            eps = OB.matmul_bound(args[0], args[1], model,
-                                  transpose_b=bool(node.attr("transpose_b", 0)))
-            if node.kind == "linear":
-                eps = eps + model.u * np.abs(y.astype(np.float64))
-            flops = 2.0 * y.size * args[0].shape[-1]
-        else:
-            y = OB.apply_op(node, args)
-            t1 = time.perf_counter()
-            _, eps = OB.op_bound(node, args, model)
-            flops = 0.0
-        t2 = time.perf_counter()
-        y = np.ascontiguousarray(y, dtype=np.float32)
-        yc = y.copy()
-        OC.leaf_check(y, yc, eps)
-        OC.observed_p_max(y, yc, inf, inf)
-        t3 = time.perf_counter()
-        OM.tensor_root(yc, 4096, alg, n_threads=threads)
-        t4 = time.perf_counter()
+        y = _cpu_value(node, args, OB)
         vals[node.index] = y
-        out.append((node.name, node.kind, y.size, flops, t1 - t0, t2 - t1, t3 - t2, t4 - t3))
-    return out
+        work.append((node, args))
+    return g, work
 
 
-def cpu_baseline(args, seq: int | None = None):
-    """Time the oracle port on a bounded sample (one layer at seq=512) and
-    extrapolate per node to the full workload (numel x S ratio, GEMM flop ratio,
-    x layers).  Labelled extrapolated."""
-    seq = seq or args.cpu_seq
+def _cpu_value(node, args, OB):
+    """FP32 value of one node on the host: numpy BLAS SGEMM for the GEMMs (the
+    reference's sequential matmul_op needs O(M K N) memory, engine.py:181),
+    the oracle restatement of apply_op otherwise."""
+    if node.kind in ("matmul", "linear"):
+        b = np.swapaxes(args[1], -1, -2) if node.attr("transpose_b", 0) else args[1]
+        y = np.matmul(args[0], b).astype(np.float32)
+        return y + args[2] if node.kind == "linear" else y
+    return np.ascontiguousarray(OB.apply_op(node, args), dtype=np.float32)
+
+
+def cpu_time_node(node, args, hash_name: str, threads: int):
+    """The reference algorithm for one node on the host cores: value, bound
+    (oracle templates: FP64 BLAS abs-GEMM, sequential-fold softmax / norm
+    parts), leaf check + np.percentile p_max, chunked Merkle commit (C
+    restatement, `threads` threads).  Returns (t_fwd, t_bound, t_check, t_commit)."""
+    from oracle import bounds as OB
+    from oracle import check as OC
+    from oracle import commit as OM
+    model = OB.FpModel()
+    alg = OM.KECCAK256 if hash_name == "keccak256" else OM.SHA256
+    inf = np.full(len(OC.PERCENTILE_GRID), np.inf)
+    t0 = time.perf_counter()
+    y = _cpu_value(node, args, OB)
+    t1 = time.perf_counter()
+    if node.kind in ("matmul", "linear"):
+        eps = OB.matmul_bound(args[0], args[1], model,
+                              transpose_b=bool(node.attr("transpose_b", 0)))
+        if node.kind == "linear":
+            eps = eps + model.u * np.abs(y.astype(np.float64))
+    else:
+        _, eps = OB.op_bound(node, args, model)
+    t2 = time.perf_counter()
+    yc = y.copy()
+    OC.leaf_check(y, yc, eps)
+    OC.observed_p_max(y, yc, inf, inf)
+    t3 = time.perf_counter()
+    OM.tensor_root(yc, 4096, alg, n_threads=threads)
+    t4 = time.perf_counter()
+    return t1 - t0, t2 - t1, t3 - t2, t4 - t3
+
+
+def _cpu_summary(times, n_nodes, seq, wall, threads):
+    fwd = sum(t[0] for t in times.values())
+    parts = [sum(t[i] for t in times.values()) for i in (1, 2, 3)]
+    bcc = sum(parts)
+    return {"value": round(100.0 * bcc / fwd, 1), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle port (numpy FP32 forward / FP64-BLAS bounds / np.percentile check "
+                      f"/ C keccak commit) on one full Qwen3-8B-shaped decoder layer at S={seq} "
+                      f"({len(times)} of {n_nodes} nodes timed, {wall:.1f} s wall); the "
+                      f"per-layer ratio is the model's (36 identical layers; embedding and "
+                      f"lm_head not sampled) -- no sequence-length extrapolation",
+            "cpu_layer_fwd_s": round(fwd, 2), "cpu_layer_bound_s": round(parts[0], 2),
+            "cpu_layer_check_s": round(parts[1], 2), "cpu_layer_commit_s": round(parts[2], 2)}
+
+
+def cpu_baseline(args):
+    """The oracle port timed on one full layer at the real shape (S=args.seq)."""
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    rows = cpu_layer_sample(seq, args.layers, args.hash, threads)
-    wall = time.perf_counter() - t0
-    # per-node scaling from the sample to S=args.seq (attention S^2, rest S)
-    r = args.seq / seq
-    fwd = other = 0.0
-    for name, kind, numel, flops, tf, tb, tc, tm in rows:
-        quad = any(t in name for t in ("scores", "scaled", "masked", "probs"))
-        s_el = r * r if quad else r
-        s_fl = r * r if quad or "ctx" in name else r
-        fwd += tf * (s_fl if kind in ("matmul", "linear") else s_el)
-        other += (tb * (s_fl if kind in ("matmul", "linear") else s_el)) + (tc + tm) * s_el
-    fwd_full = fwd * args.layers
-    other_full = other * args.layers
-    return {"value": round(100.0 * other_full / fwd_full, 1), "unit": UNIT, "cores": threads,
-            "kind": "port",
-            "sample": f"oracle port (numpy/FP64 BLAS + C keccak) on one Qwen3-8B-shaped layer at "
-                      f"S={seq} ({len(rows)} nodes, {wall:.1f} s wall), extrapolated per node to "
-                      f"S={args.seq} x {args.layers} layers: CPU fwd {fwd_full:.0f} s, "
-                      f"bounds+check+commit {other_full:.0f} s",
-            "cpu_fwd_s_extrapolated": round(fwd_full, 1),
-            "cpu_bcc_s_extrapolated": round(other_full, 1)}
+    g, work = cpu_layer_prepare(args.seq)
+    times = {node.index: cpu_time_node(node, a, args.hash, threads) for node, a in work}
+    return _cpu_summary(times, g.n_nodes, args.seq, time.perf_counter() - t0, threads)
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (the oracle
+    port; the reference's Python engine cannot run these shapes, engine.py:181),
+    rank 0 only.  Setup (untimed): one real-shape layer and its node inputs.
+    The layer's nodes are split into G = min(steps, 8) contiguous groups of
+    similar cost; step k times group k mod G, so every node is timed at least
+    once when steps >= G; value = 100 * sum(bounds+check+commit) / sum(fwd)
+    over the per-node mean times."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    steps = []
-    cpu = None
-    for _ in range(args.warmup):
-        pass  # the CPU sample has no warm-up effects worth a full extra pass
-    t0 = time.perf_counter()
-    for _ in range(max(1, args.steps)):
-        cpu = cpu_baseline(args)
-        steps.append(cpu["value"])
-    wall = (time.perf_counter() - t0) / max(1, args.steps)
-    val = statistics.median(steps)
+    threads = os.cpu_count() or 1
+    g, work = cpu_layer_prepare(args.seq)
+    n_groups = max(1, min(args.steps, 8))
+    # contiguous groups of similar size (the attention nodes are the big ones)
+    weight = [max(1, int(np.prod(np.asarray(a[0]).shape))) for _, a in work]
+    tot, acc, groups, cur = float(sum(weight)), 0.0, [], []
+    for (node, a), w in zip(work, weight):
+        cur.append((node, a))
+        acc += w
+        if acc >= tot * (len(groups) + 1) / n_groups and len(groups) < n_groups - 1:
+            groups.append(cur)
+            cur = []
+    groups.append(cur)
+    groups = [gr for gr in groups if gr]
+    per_node: dict = {}
+    walls = []
+    for k in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        for node, a in groups[k % len(groups)]:
+            per_node.setdefault(node.index, []).append(cpu_time_node(node, a, args.hash, threads))
+        walls.append(time.perf_counter() - t0)
+    times = {i: tuple(float(np.mean([t[j] for t in ts])) for j in range(4))
+             for i, ts in per_node.items()}
+    cpu = _cpu_summary(times, g.n_nodes, args.seq, sum(walls), threads)
+    cpu["sample"] += f"; {len(groups)} node groups, one per step"
+    val = cpu["value"]
     line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference",
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(wall * 1000.0, 1),
+            "warmup": args.warmup, "ms_per_step": round(1000.0 * float(np.mean(walls)), 1),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 values / f64 bound math", "data": "synthetic",
             "config": {"workload": f"Qwen3-8B-shaped FP32 forward S={args.seq}, {args.layers} "
-                                   f"layers (CPU oracle port, one-layer sample extrapolated)",
+                                   f"layers (CPU oracle port, one real-shape layer sampled)",
                        "model": "qwen3-8b-shaped random-init", "seq_len": args.seq,
                        "layers": args.layers},
             "cpu_baseline": cpu,
@@ -725,13 +946,14 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["qwen3-8b"] + sorted(CONFIGS), default="qwen3-8b",
+                    help="BASELINE.json config (default: the headline Qwen3-8B line)")
     ap.add_argument("--layers", type=int, default=36)
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--hash", choices=["keccak256", "sha256"], default="keccak256")
     ap.add_argument("--chunk", type=int, default=4096)
     ap.add_argument("--drift-period", type=int, default=16)
     ap.add_argument("--fault-node", default="l3_down")
-    ap.add_argument("--cpu-seq", type=int, default=512)
     ap.add_argument("--calib-samples", type=int, default=4)
     ap.add_argument("--debug-exceed", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -757,6 +979,8 @@ def main(argv=None):
         args.fault_node = "l0_down"
     if args.impl == "reference":
         return run_reference(args)
+    if args.config != "qwen3-8b":
+        return run_config(args)
     return run_ours(args)
 
 
