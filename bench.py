@@ -467,12 +467,13 @@ def run_ours(args):
                     "traffic": None}
         elif dom == "nao_abs_gemm_tc16":
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
-            f16 = peaks.get("bf16_tflops", 1590.0)
+            f16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
             peak = f16 / 3.0
             roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
                     "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) = FP16 dense, / 3 "
-                                   "MMAs per product (FP16 3-split): algorithmic ceiling",
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (timed inside a "
+                                   "second-long step) = FP16 dense, / 3 MMAs per product "
+                                   "(FP16 3-split): algorithmic ceiling",
                     "mma_tflops": round(3 * achieved, 1), "f16_peak": round(f16, 1),
                     "traffic": None}
         elif dom == "nao_abs_gemm_bound":
@@ -490,12 +491,20 @@ def run_ours(args):
             # 64-lane/clk/SM ALU pipe (profiles/r1_keccak_pipe_balance.md)
             achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
             sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
-            peak = 148 * 64 * sm_mhz * 1e6 / (24 * 180 / 136.0) / 1e9
+            try:  # measured: compute-only keccak_f1600 rate (tools/alu_peak.cu)
+                alu = json.load(open(ROOT / "profiles" / "r2_alu_peak.json"))
+                peak = float(alu["keccak_rate_gbs"]) * sm_mhz / 1965.0
+                src = ("measured: profiles/r2_alu_peak.json keccak_rate_gbs (tools/alu_peak.cu, "
+                       "compute-only keccak_f1600 of csrc/hash.cuh on 148 SMs, CUDA events, "
+                       "1965 MHz), scaled to this run's median SM clock")
+            except Exception:
+                peak = 148 * 64 * sm_mhz * 1e6 / (24 * 180 / 136.0) / 1e9
+                src = ("derived integer-ALU roofline of Keccak-256: 148 SM x 64 lanes/clk x SM "
+                       "clock / (24 x 180 ops per 136 B block)")
             hbm = peaks.get("hbm_gbs", 6650.0)
             roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
                     "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "derived integer-ALU roofline of Keccak-256: 148 SM x 64 "
-                                   "lanes/clk x SM clock / (24 x 180 ops per 136 B block)",
+                    "peak_source": src,
                     "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
         elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
             # SHA-256 is integer-ALU bound too: ~1253 ALU-pipe ops per 64-byte
