@@ -154,6 +154,10 @@ class _LazyWeights(dict):
     def __contains__(self, k):
         return k in self.specs
 
+    def shape_of(self, k) -> tuple:
+        """Shape without materialising the weight."""
+        return tuple(self.specs[k][0])
+
     def __missing__(self, k):
         shape, kind, a = self.specs[k]
         gen = torch.Generator(device=self.device)

@@ -36,21 +36,71 @@ def layer_starts(graph) -> list:
     return starts
 
 
+def _weight_numel(graph, ref) -> int:
+    cat, key = parse_ref(ref)
+    if cat != "weight":
+        return 0
+    w = graph.weights
+    shp = w.shape_of(key) if hasattr(w, "shape_of") else tuple(w[key].shape)
+    n = 1
+    for d in shp:
+        n *= int(d)
+    return n
+
+
+def epilogue_cost(graph, starts) -> float:
+    """Verified-time weight of the nodes after the last layer (final norm +
+    lm_head), in layer units: the GEMM weight elements behind them relative to
+    one layer's, times the GEMM share of a verified layer's time (~0.5 on the
+    B200: the commit and the row kernels scale with activations, not weights).
+    Qwen3-8B: lm_head 622 M vs 193 M per layer -> ~1.6 layers."""
+    if len(starts) < 2:
+        return 0.0
+    mm = ("matmul", "linear", "conv2d")
+    layer = sum(_weight_numel(graph, r) for n in graph.nodes[starts[0]:starts[1]]
+                if n.kind in mm for r in n.inputs[1:2])
+    tail = sum(_weight_numel(graph, r) for n in graph.nodes[starts[-1]:]
+               if n.kind in mm for r in n.inputs[1:2]) - layer
+    return 0.5 * max(tail, 0) / layer if layer else 0.0
+
+
 def rank_slice(graph, n_layers: int, rank: int, world: int):
-    """[start, end) of rank's slice: layers split into contiguous groups whose
-    sizes differ by <= 1 (larger first, like partition); rank 0 also owns the
-    prologue, the last rank the epilogue."""
+    """[start, end) of rank's slice: contiguous groups of whole layers; rank 0
+    also owns the prologue, the last rank the epilogue.  Groups balance the
+    estimated verified time, with the epilogue (lm_head) weighted by
+    epilogue_cost, so the last rank takes fewer layers when the head is
+    heavy (Qwen3-8B on 8 ranks: 5,5,5,5,4,4,4,3 + head instead of 5,5,5,5,4,4,4,4 + head)."""
     if world <= 1:
         return 0, graph.n_nodes
     starts = layer_starts(graph)
     if len(starts) < world:
         raise ValueError(f"{len(starts)} layers cannot be split over {world} ranks")
-    base, extra = divmod(n_layers, world)
-    lo = rank * base + min(rank, extra)
-    hi = lo + base + (1 if rank < extra else 0)
+    n = len(starts)
+    cost = [1.0] * n
+    cost[-1] += epilogue_cost(graph, starts)
+    total = sum(cost)
+    # layer j goes to the rank whose share holds the midpoint of its cost
+    owner, acc = [], 0.0
+    for j in range(n):
+        mid = acc + cost[j] / 2.0
+        owner.append(min(world - 1, int(mid * world / total)))
+        acc += cost[j]
+    # every rank keeps at least one layer (contiguous, monotone owners)
+    for r in range(world):
+        if r not in owner:
+            return _even_slice(graph, starts, n, rank, world)
+    lo = owner.index(rank)
+    hi = len(owner) - owner[::-1].index(rank)
     start = 0 if rank == 0 else starts[lo]
     end = graph.n_nodes if rank == world - 1 else starts[hi]
     return start, end
+
+
+def _even_slice(graph, starts, n, rank, world):
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return (0 if rank == 0 else starts[lo]), (graph.n_nodes if rank == world - 1 else starts[hi])
 
 
 def frontier_refs(graph, start: int, end: int) -> list:
