@@ -177,12 +177,28 @@ typedef struct nao_check_partial {
  * accum: device scratch of nao_commit_check_accum_bytes(), zero before its
  * first use and left zeroed by every call (dedicated per stream).
  * Workspace as nao_merkle_commit_workspace. */
+/* Chunk-digest reuse (optional, host array of n_tensors entries or NULL): a
+ * tensor whose LOCAL recomputation is a data-movement copy of another claimed
+ * tensor of the same call (reshape: the same bytes; concat of one tensor with
+ * itself: blocks repeated) has chunk c equal, when its claimed chunk equals
+ * its local chunk word for word, to source chunk
+ *   (c / (block_chunks * repeats)) * block_chunks + c % block_chunks,
+ * so its digest is copied instead of re-hashed (leaf = H(0x00 || chunk) is a
+ * function of the bytes only; the header leaf and the tree are still built).
+ * Chunks that differ are hashed.  src = -1: no reuse.  Needs the fused check
+ * (checks[i].local).  Sources are processed in an earlier launch. */
+typedef struct nao_chunk_reuse {
+    int64_t src;
+    uint64_t block_chunks;
+    uint64_t repeats;
+} nao_chunk_reuse;
 size_t nao_commit_check_accum_bytes(void);
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
                              const uint64_t* payload_bytes, const uint8_t* const* headers,
                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
-                             const nao_check_desc* checks, uint8_t* roots_out, void* accum,
-                             void* workspace, size_t workspace_bytes, void* stream);
+                             const nao_check_desc* checks, const nao_chunk_reuse* reuse,
+                             uint8_t* roots_out, void* accum, void* workspace,
+                             size_t workspace_bytes, void* stream);
 /* Exact numpy method="linear" percentile profiles (calibration.py:33-37):
  * of |local-claimed| and |local-claimed|/(|local|+epsilon) (calibration.py:40-49),
  * or of an arbitrary FP64 array.  Outputs are device arrays of n_grid doubles. */

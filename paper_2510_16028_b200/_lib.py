@@ -65,6 +65,12 @@ class CheckDesc(ctypes.Structure):
                 ("border_list", c_vp), ("border_cap", ctypes.c_int64)]
 
 
+class ChunkReuse(ctypes.Structure):
+    """nao_chunk_reuse: a data-movement node's chunk digests copied from its source."""
+    _fields_ = [("src", ctypes.c_int64), ("block_chunks", ctypes.c_uint64),
+                ("repeats", ctypes.c_uint64)]
+
+
 REFINE_GEMM, REFINE_CONV, REFINE_UNARY = 0, 1, 2
 
 
@@ -115,8 +121,9 @@ _SIGS = {
     "nao_commit_check_accum_bytes": (c_sz, []),
     "nao_commit_check_tensors": (c_int, [c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_u64),
                                          ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_uint32),
-                                         c_u64, c_int, ctypes.POINTER(CheckDesc), c_vp, c_vp,
-                                         c_vp, c_sz, c_vp]),
+                                         c_u64, c_int, ctypes.POINTER(CheckDesc),
+                                         ctypes.POINTER(ChunkReuse), c_vp, c_vp, c_vp, c_sz,
+                                         c_vp]),
     "nao_check": (c_int, [c_vp, c_vp, c_i64, c_int, c_vp, c_dbl, c_dbl,
                           ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                           c_int, c_dbl, c_vp, c_vp, c_sz, c_vp, c_i64, c_vp]),

@@ -279,12 +279,14 @@ def _as_payload(t: torch.Tensor) -> torch.Tensor:
 
 def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
                    out: torch.Tensor | None = None, leaf_digests: torch.Tensor | None = None,
-                   checks=None):
+                   checks=None, reuse=None):
     """Chunked tensor roots for CUDA tensors, one batched launch set, no host
     sync.  Returns an (n, 32) uint8 CUDA tensor (row i = root of tensors[i]).
     checks: optional list of _lib.CheckDesc (or None entries), one per tensor:
     the acceptance check of tensor i against checks[i].local runs inside the
-    same hashing pass (nao_commit_check_tensors)."""
+    same hashing pass (nao_commit_check_tensors).  reuse: optional list of
+    (src, block_chunks, repeats) or None per tensor (nao_chunk_reuse: chunk
+    digests of data-movement nodes copied from their source; roots unchanged)."""
     tensors = [_as_payload(t) for t in tensors]
     n = len(tensors)
     if n == 0:
@@ -308,8 +310,13 @@ def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
             if c is not None:
                 descs[i] = c
         acc = _lib.commit_check_accumulator(dev)
+        reuse_arr = None
+        if reuse is not None and any(r is not None for r in reuse):
+            reuse_arr = (_lib.ChunkReuse * n)()
+            for i, r in enumerate(reuse):
+                reuse_arr[i] = _lib.ChunkReuse(*r) if r is not None else _lib.ChunkReuse(-1, 0, 0)
         _lib.call("nao_commit_check_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes,
-                  alg_id(alg), descs, roots.data_ptr(), acc.data_ptr(), ws.data_ptr(),
+                  alg_id(alg), descs, reuse_arr, roots.data_ptr(), acc.data_ptr(), ws.data_ptr(),
                   ws.numel(), _lib.stream_ptr(dev))
     else:
         _lib.call("nao_merkle_commit_tensors", n, ptrs, sizes, hptrs, hlens, chunk_bytes,

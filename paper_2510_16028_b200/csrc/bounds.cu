@@ -12,6 +12,7 @@
 // (lane = column), transposed through shared memory, and each lane then
 // folds its own row left to right -- 32 independent sequential folds per warp.
 #include <cmath>
+#include <algorithm>
 #include "common.cuh"
 #include "unary.cuh"
 #include "profile_fold.cuh"
@@ -502,21 +503,44 @@ __device__ __forceinline__ float drift_one(float v, int64_t i, uint32_t seed, ui
     return v;
 }
 
-// float4 per thread per step (16-byte aligned y/out); scalar tail
-__global__ void k_inject_drift(const float* __restrict__ y, float* __restrict__ out, int64_t n,
-                               uint32_t seed, uint32_t period, float fault_scale,
-                               uint32_t fault_period) {
+// 4 float4 per thread per step (16-byte aligned y/out; 64 B in flight per
+// thread keeps HBM busy), scalar tail.  period = fault_period = 0 is a pure
+// copy: the proposer harness's claim of a deterministic node.
+template <bool COPY>
+__global__ void __launch_bounds__(256) k_inject_drift(const float* __restrict__ y,
+                                                      float* __restrict__ out, int64_t n,
+                                                      uint32_t seed, uint32_t period,
+                                                      float fault_scale, uint32_t fault_period) {
     const int64_t nv = n >> 2;
     const float4* y4 = reinterpret_cast<const float4*>(y);
     float4* o4 = reinterpret_cast<float4*>(out);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
-        float4 a = __ldg(y4 + v);
-        const int64_t i = 4 * v;
-        a.x = drift_one(a.x, i, seed, period, fault_scale, fault_period);
-        a.y = drift_one(a.y, i + 1, seed, period, fault_scale, fault_period);
-        a.z = drift_one(a.z, i + 2, seed, period, fault_scale, fault_period);
-        a.w = drift_one(a.w, i + 3, seed, period, fault_scale, fault_period);
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v + 3 * stride < nv; v += 4 * stride) {
+        float4 a[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) a[u] = __ldcs(y4 + v + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (!COPY) {
+                const int64_t i = 4 * (v + u * stride);
+                a[u].x = drift_one(a[u].x, i, seed, period, fault_scale, fault_period);
+                a[u].y = drift_one(a[u].y, i + 1, seed, period, fault_scale, fault_period);
+                a[u].z = drift_one(a[u].z, i + 2, seed, period, fault_scale, fault_period);
+                a[u].w = drift_one(a[u].w, i + 3, seed, period, fault_scale, fault_period);
+            }
+            __stcs(o4 + v + u * stride, a[u]);
+        }
+    }
+    for (; v < nv; v += stride) {
+        float4 a = __ldcs(y4 + v);
+        if (!COPY) {
+            const int64_t i = 4 * v;
+            a.x = drift_one(a.x, i, seed, period, fault_scale, fault_period);
+            a.y = drift_one(a.y, i + 1, seed, period, fault_scale, fault_period);
+            a.z = drift_one(a.z, i + 2, seed, period, fault_scale, fault_period);
+            a.w = drift_one(a.w, i + 3, seed, period, fault_scale, fault_period);
+        }
         __stcs(o4 + v, a);
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
@@ -532,8 +556,15 @@ extern "C" int nao_inject_drift(const float* y, float* out, int64_t n, uint32_t 
     if (n == 0) return NAO_OK;
     NAO_REQUIRE((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(out)) % 16 == 0,
                 "y/out must be 16-byte aligned");
-    nao::k_inject_drift<<<nao::ew_grid((n + 3) / 4), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        y, out, n, seed, period, fault_scale, fault_period);
+    // one resident wave (8 CTAs of 256 per SM), 4 float4 in flight per thread
+    const int64_t want = ((n >> 2) + 255) / 256;
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, nao::kNumSMs * 8));
+    if (period == 0 && fault_period == 0)
+        nao::k_inject_drift<true><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            y, out, n, seed, period, fault_scale, fault_period);
+    else
+        nao::k_inject_drift<false><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            y, out, n, seed, period, fault_scale, fault_period);
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

@@ -127,6 +127,9 @@ struct CCTable {
     uint64_t out_index[kMaxSegs];
     uint64_t block_prefix[kMaxSegs + 1];
     CheckDesc chk[kMaxSegs];
+    uint64_t reuse_out[kMaxSegs];    // digest index of the source's chunk 0, or ~0 (none)
+    uint64_t reuse_block[kMaxSegs];  // chunks per source block
+    uint64_t reuse_span[kMaxSegs];   // block_chunks * repeats
 };
 
 constexpr int kLeafWarps = kLeafThreads / 32;
@@ -307,7 +310,33 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         const uint64_t off_w = c * cw;
         const uint32_t nw = (uint32_t)(total_w - off_w < cw ? total_w - off_w : cw);
         uint32_t dg[8];
-        if (check) {
+        bool reused = false;
+        if (check && tab.reuse_out[s] != ~0ull) {
+            // data-movement node: claimed chunk == local chunk (word for word,
+            // finite) means the source's chunk digest is this chunk's digest
+            const uint32_t* cp = tab.payload[s] + off_w;
+            const uint32_t* lp = reinterpret_cast<const uint32_t*>(d.local) + off_w;
+            bool eq = true;
+            uint32_t i = 0;
+            for (; i + 4 <= nw; i += 4) {
+                const uint4 a = __ldg(reinterpret_cast<const uint4*>(cp + i));
+                const uint4 b = __ldg(reinterpret_cast<const uint4*>(lp + i));
+                eq &= !(word_needs_check(a.x, b.x) | word_needs_check(a.y, b.y) |
+                        word_needs_check(a.z, b.z) | word_needs_check(a.w, b.w));
+            }
+            for (; i < nw; i++) eq &= !word_needs_check(__ldg(cp + i), __ldg(lp + i));
+            if (eq) {
+                const uint64_t span = tab.reuse_span[s], blk = tab.reuse_block[s];
+                const uint64_t sc = (c / span) * blk + c % blk;
+                const uint4* src = reinterpret_cast<const uint4*>(digests + 8 * (tab.reuse_out[s] + sc));
+                uint4* dst = reinterpret_cast<uint4*>(digests + 8 * (tab.out_index[s] + c));
+                dst[0] = src[0];
+                dst[1] = src[1];
+                reused = true;
+            }
+        }
+        if (reused) {
+        } else if (check) {
             const bool et = d.eps_kind == NAO_EPS_TENSOR_F32 || d.eps_kind == NAO_EPS_TENSOR_F64;
             const int esh = d.eps_kind == NAO_EPS_TENSOR_F64 ? 3 : 2;
             CheckedWords ld{tab.payload[s] + off_w,
@@ -319,7 +348,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             GlobalWords ld{tab.payload[s] + off_w};
             hash_tagged_words<ALG>(ld, nw, 0u, dg);
         }
-        store_digest(digests + 8 * (tab.out_index[s] + c), dg);
+        if (!reused) store_digest(digests + 8 * (tab.out_index[s] + c), dg);
     }
     if (!check) return;
     __syncwarp();
@@ -716,9 +745,9 @@ namespace nao {
 static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
                                const uint64_t* payload_bytes, const uint8_t* const* headers,
                                const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
-                               const nao_check_desc* checks, uint8_t* roots_out,
-                               uint8_t* leaf_digests_out, void* accum, void* workspace,
-                               size_t workspace_bytes, cudaStream_t st) {
+                               const nao_check_desc* checks, const nao_chunk_reuse* reuse,
+                               uint8_t* roots_out, uint8_t* leaf_digests_out, void* accum,
+                               void* workspace, size_t workspace_bytes, cudaStream_t st) {
     NAO_REQUIRE(n_tensors > 0, "n_tensors must be positive");
     NAO_REQUIRE(hash_alg == NAO_HASH_SHA256 || hash_alg == NAO_HASH_KECCAK256, "bad hash_alg %d",
                 hash_alg);
@@ -752,6 +781,26 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
         n_leaves[i] = 1 + seg_chunks(payload_bytes[i], chunk_bytes);
         leaves += n_leaves[i];
     }
+    // chunk-digest reuse: phase = 1 + the source's phase (sources hash first)
+    std::vector<int> phase(n_tensors, 0);
+    int n_phases = 1;
+    for (int64_t i = 0; reuse && i < n_tensors; i++) {
+        const nao_chunk_reuse& r = reuse[i];
+        if (r.src < 0 || payload_bytes[i] == 0) continue;
+        NAO_REQUIRE(r.src < i, "reuse %lld: source %lld must come earlier", (long long)i,
+                    (long long)r.src);
+        NAO_REQUIRE(checks && checks[i].local, "reuse %lld needs the fused check", (long long)i);
+        NAO_REQUIRE(r.repeats >= 1 && r.block_chunks >= 1, "reuse %lld: bad block", (long long)i);
+        const uint64_t sb = payload_bytes[r.src];
+        if (r.repeats == 1)
+            NAO_REQUIRE(payload_bytes[i] == sb && r.block_chunks == seg_chunks(sb, chunk_bytes),
+                        "reuse %lld: a reshape must have the source's bytes", (long long)i);
+        else
+            NAO_REQUIRE(sb % (r.block_chunks * chunk_bytes) == 0 && payload_bytes[i] == sb * r.repeats,
+                        "reuse %lld: repeated blocks must be whole chunks", (long long)i);
+        phase[i] = phase[r.src] + 1;
+        n_phases = std::max(n_phases, phase[i] + 1);
+    }
     Workspace ws(workspace, workspace_bytes);
     uint32_t* lvl0 = leaf_digests_out ? reinterpret_cast<uint32_t*>(leaf_digests_out)
                                       : ws.take<uint32_t>(8 * leaves);
@@ -776,14 +825,24 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
     for (int64_t i = 0; checks && i < n_tensors; i++) any_check |= checks[i].local != nullptr;
     NAO_REQUIRE(!any_check || chunk_bytes / 4 <= (uint64_t)kMaxFusedChunkWords,
                 "the fused check supports chunk_bytes <= %d", 4 * kMaxFusedChunkWords);
-    for (int64_t b0 = 0; b0 < n_tensors; b0 += kMaxSegs) {
+    std::vector<int64_t> order;  // tensors by phase, canonical order within a phase
+    std::vector<int64_t> phase_end;
+    for (int ph = 0; ph < n_phases; ph++) {
+        for (int64_t i = 0; i < n_tensors; i++)
+            if (phase[i] == ph) order.push_back(i);
+        phase_end.push_back((int64_t)order.size());
+    }
+    for (int64_t b0 = 0, ph = 0; b0 < n_tensors;) {
+        while (b0 >= phase_end[ph]) ph++;
+        const int64_t b1 = std::min<int64_t>(b0 + kMaxSegs, phase_end[ph]);
         if (!any_check) {
             ChunkTable ct;
             memset(&ct, 0, sizeof ct);
             ct.chunk_words = (uint32_t)(chunk_bytes / 4);
             int cnt = 0;
             ct.chunk_prefix[0] = 0;
-            for (int64_t i = b0; i < n_tensors && cnt < kMaxSegs; i++, cnt++) {
+            for (int64_t k = b0; k < b1; k++, cnt++) {
+                const int64_t i = order[k];
                 ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
                 ct.nbytes[cnt] = payload_bytes[i];
                 ct.out_index[cnt] = in_index[i] + 1;
@@ -791,6 +850,7 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
                     ct.chunk_prefix[cnt] + seg_chunks(payload_bytes[i], chunk_bytes);
             }
             ct.n = cnt;
+            b0 = b1;
             int rc = launch_chunk_leaves(hash_alg, ct, lvl0, st);
             if (rc) return rc;
             continue;
@@ -800,15 +860,24 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
         ct.chunk_words = (uint32_t)(chunk_bytes / 4);
         int cnt = 0;
         ct.block_prefix[0] = 0;
-        for (int64_t i = b0; i < n_tensors && cnt < kMaxSegs; i++, cnt++) {
+        for (int64_t k = b0; k < b1; k++, cnt++) {
+            const int64_t i = order[k];
             ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
             ct.nbytes[cnt] = payload_bytes[i];
             ct.out_index[cnt] = in_index[i] + 1;
             ct.block_prefix[cnt + 1] = ct.block_prefix[cnt] +
                 ceil_div((int64_t)seg_chunks(payload_bytes[i], chunk_bytes), kLeafThreads);
             if (checks && payload_bytes[i] > 0) memcpy(&ct.chk[cnt], &checks[i], sizeof(CheckDesc));
+            ct.reuse_out[cnt] = ~0ull;
+            if (phase[i] > 0) {
+                const nao_chunk_reuse& r = reuse[i];
+                ct.reuse_out[cnt] = in_index[r.src] + 1;
+                ct.reuse_block[cnt] = r.block_chunks;
+                ct.reuse_span[cnt] = r.block_chunks * r.repeats;
+            }
         }
         ct.n = cnt;
+        b0 = b1;
         uint64_t blocks = ct.block_prefix[cnt];
         if (blocks == 0) continue;
         static const uint64_t max_ctas = [] {
@@ -845,7 +914,7 @@ int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
                               uint8_t* roots_out, uint8_t* leaf_digests_out, void* workspace,
                               size_t workspace_bytes, void* stream) {
     return commit_tensors_impl(n_tensors, payloads, payload_bytes, headers, header_lens,
-                               chunk_bytes, hash_alg, nullptr, roots_out, leaf_digests_out,
+                               chunk_bytes, hash_alg, nullptr, nullptr, roots_out, leaf_digests_out,
                                nullptr, workspace, workspace_bytes,
                                static_cast<cudaStream_t>(stream));
 }
@@ -855,10 +924,11 @@ size_t nao_commit_check_accum_bytes(void) { return sizeof(CheckAccum) * kMaxSegs
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
                              const uint64_t* payload_bytes, const uint8_t* const* headers,
                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,
-                             const nao_check_desc* checks, uint8_t* roots_out, void* accum,
-                             void* workspace, size_t workspace_bytes, void* stream) {
+                             const nao_check_desc* checks, const nao_chunk_reuse* reuse,
+                             uint8_t* roots_out, void* accum, void* workspace,
+                             size_t workspace_bytes, void* stream) {
     return commit_tensors_impl(n_tensors, payloads, payload_bytes, headers, header_lens,
-                               chunk_bytes, hash_alg, checks, roots_out, nullptr, accum,
+                               chunk_bytes, hash_alg, checks, reuse, roots_out, nullptr, accum,
                                workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 

@@ -218,3 +218,57 @@ def test_fused_full_qwen_scores_tensor():
     import os
     assert bytes(roots[0].cpu().numpy()) == OM.tensor_root(yc, 4096, OM.KECCAK256,
                                                            n_threads=os.cpu_count() or 1)
+
+
+@pytest.mark.parametrize("chunk", [512, 4096])
+def test_chunk_digest_reuse_keeps_roots(chunk):
+    """nao_chunk_reuse (data-movement nodes copy their source's chunk digests):
+    a reshape chain and a GQA-style concat of one tensor with itself, with
+    claims equal to the local copy, with one differing word, and with an inf,
+    give the same roots as hashing every chunk and the same check records."""
+    from paper_2510_16028_b200 import _lib
+    from paper_2510_16028_b200.commitments import commit_tensors
+    from paper_2510_16028_b200.dispute import CheckRecord
+    rng = np.random.default_rng(3)
+    S, hd = 64, 32  # block = S*hd*4 = 8 KiB = whole chunks
+    src = torch.from_numpy(rng.standard_normal((2, 1, S, hd)).astype(np.float32)).cuda()
+    spec = torch.frombuffer(bytearray(_lib.verdict_spec(GRID, INF, INF, 1e-12)),
+                            dtype=torch.uint8).cuda()
+    for mode in ("equal", "word", "inf"):
+        # every local is the data movement of the CLAIMED inputs (as in the executor)
+        c0 = src.clone()
+        l1 = c0.reshape(2, S, hd)             # reshape node (a view of claim 0)
+        c1 = l1.clone()
+        l2 = torch.cat([c0] * 4, dim=1)       # GQA concat of claim 0 with itself
+        c2 = l2.clone()
+        if mode == "word":
+            c2.view(-1)[1000] += 1.0
+        elif mode == "inf":
+            c1.view(-1)[5] = float("inf")
+        l3 = c2.reshape(8, S, hd)             # reshape of the concat's claim (chain)
+        c3 = l3.clone()
+        if mode == "word":
+            c3.view(-1)[3000] -= 1.0
+        claims = [c0, c1, c2, c3]
+        locals_ = [None, l1, l2, l3]
+        recs = torch.zeros((4, _lib.CHECK_RESULT_BYTES), dtype=torch.uint8, device="cuda")
+        checks = [None] + [_lib.CheckDesc(l.data_ptr(), None, spec.data_ptr(), recs[i + 1].data_ptr(),
+                                          0.0, 1.0, _lib.EPS_ZERO, 0, None, 0)
+                           for i, l in enumerate(locals_[1:])]
+        nch = -(-src.numel() * 4 // chunk)
+        blk = S * hd * 4 // chunk
+        reuse = [None, (0, nch, 1), (0, blk, 4), (2, 4 * nch, 1)]
+        got = commit_tensors(claims, chunk, "keccak256", checks=checks, reuse=reuse)
+        plain = commit_tensors(claims, chunk, "keccak256")
+        torch.cuda.synchronize()
+        assert torch.equal(got, plain), mode
+        for i, t in enumerate(claims):
+            assert bytes(got[i].cpu().numpy()) == OM.tensor_root(t.cpu().numpy(), chunk,
+                                                                 OM.KECCAK256), (mode, i)
+        r = [CheckRecord(recs[i]).host() for i in range(1, 4)]
+        if mode == "equal":
+            assert all(x["n_violations"] == 0 for x in r)
+        elif mode == "word":
+            assert [x["n_violations"] for x in r] == [0, 1, 1]
+        else:
+            assert r[0]["n_violations"] == 1 and r[0]["n_nonfinite"] == 1
