@@ -305,9 +305,10 @@ __device__ __forceinline__ void keccak256_tagged(const Load& ld, uint32_t nw, ui
         uint32_t D[34];
 #pragma unroll
         for (int q = 0; q < 17; q++) {
-            uint2 v = ld.v2(17 * b + q);
+            uint2 v = ld.v2c(17 * b + q, q);  // q: compile-time pair index in the block
             D[2 * q] = v.x; D[2 * q + 1] = v.y;
         }
+        ld.block_end(b);
 #pragma unroll
         for (int i = 0; i < 17; i++) {
             uint32_t prev = (i == 0) ? carry : D[2 * i - 1];
@@ -324,10 +325,11 @@ __device__ __forceinline__ void keccak256_tagged(const Load& ld, uint32_t nw, ui
 #pragma unroll
     for (int k = 0; k < 34; k++) {
         uint32_t v = 0;
-        if ((uint32_t)k < rem) v = ld.w(base + k);
+        if ((uint32_t)k < rem) v = ld.wc(base + k, k);
         else if ((uint32_t)k == rem) v = 0x01u;
         E[k] = v;
     }
+    ld.block_end(nfull);
 #pragma unroll
     for (int i = 0; i < 17; i++) {
         uint32_t prev = (i == 0) ? carry : E[2 * i - 1];
@@ -343,6 +345,11 @@ __device__ __forceinline__ void keccak256_tagged(const Load& ld, uint32_t nw, ui
 
 // ------------------------------------------------------------ loaders
 
+// Loaders.  The Keccak sponge reads a 136-byte block as 17 word pairs
+// (v2c(i, q), q the compile-time pair index within the block) or, for the
+// last block, words (wc(i, k)), then calls block_end(b): hooks for loaders
+// that inspect what they load (the fused check's CheckedWords); plain
+// loaders forward to v2 / w and ignore block_end.
 struct GlobalWords {  // 16-byte aligned global payload, read-only path
     const uint32_t* __restrict__ p;
     __device__ __forceinline__ uint4 v4(uint32_t i) const {
@@ -352,6 +359,9 @@ struct GlobalWords {  // 16-byte aligned global payload, read-only path
         return __ldg(reinterpret_cast<const uint2*>(p) + i);
     }
     __device__ __forceinline__ uint32_t w(uint32_t i) const { return __ldg(p + i); }
+    __device__ __forceinline__ uint2 v2c(uint32_t i, int) const { return v2(i); }
+    __device__ __forceinline__ uint32_t wc(uint32_t i, int) const { return w(i); }
+    __device__ __forceinline__ void block_end(uint32_t) const {}
 };
 
 struct RegWords16 {  // two 32-byte digests held in registers (internal node)
@@ -363,6 +373,9 @@ struct RegWords16 {  // two 32-byte digests held in registers (internal node)
         return make_uint2(m[2 * i], m[2 * i + 1]);
     }
     __device__ __forceinline__ uint32_t w(uint32_t i) const { return m[i]; }
+    __device__ __forceinline__ uint2 v2c(uint32_t i, int) const { return v2(i); }
+    __device__ __forceinline__ uint32_t wc(uint32_t i, int) const { return w(i); }
+    __device__ __forceinline__ void block_end(uint32_t) const {}
 };
 
 // Digest of tag || words, written as 8 little-endian words = the digest bytes.

@@ -152,28 +152,76 @@ struct LeafCheckSmem {
 __device__ __forceinline__ bool word_needs_check(uint32_t c, uint32_t y) {
     return (c != y) | ((c & 0x7f800000u) == 0x7f800000u);  // differs, or inf/nan
 }
+// The check's filter as FP32 compares (FSETP, off the integer-ALU pipe the
+// sponge saturates): flags words that differ as floats or are inf / nan.
+// +0 / -0 pairs pass unflagged -- their difference is exactly 0, the same
+// verdict as equal words (the hash still absorbs the raw claimed bits).
+__device__ __forceinline__ bool word_needs_check_f(uint32_t c, uint32_t y) {
+    const float fc = __uint_as_float(c), fy = __uint_as_float(y);
+    return !((fc == fy) & (fabsf(fc) <= 3.402823466e38f));
+}
+// warp-aggregated increment of a per-warp shared counter (lanes hitting the
+// same bucket -- the common case -- add once instead of serialising)
+__device__ __forceinline__ void agg_inc(unsigned int* ctr, unsigned key, unsigned active) {
+    const unsigned peers = __match_any_sync(active, key);
+    if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(ctr, (unsigned)__popc(peers));
+}
 
 // Claimed payload words for the sponge; a word that differs from the local
 // word at the same offset (or is inf/nan) sets bit i%64 of this thread's
 // mask word i/64 in shared memory -- the check itself runs after the hash.
+// Check flags: one 64-bit mask entry per BW-word group of a thread's chunk
+// (bit j = word BW*g + j needs the exact check).  Keccak-256: BW = 34, one
+// entry per 136-byte sponge block, bit positions known at compile time (the
+// block loop is unrolled), so a word costs two FP32 compares and one
+// predicated LOP3 with an immediate -- no branch, no shifts.  SHA-256: BW = 64
+// groups filled word by word.
+template <int ALG> struct MaskGeom { static constexpr uint32_t BW = ALG == kKECCAK256 ? 34u : 64u; };
+
+template <int ALG>
 struct CheckedWords {
     const uint32_t* __restrict__ p;  // claimed (hashed)
     const uint32_t* __restrict__ q;  // local
-    unsigned long long* mask;        // this thread's mask words (stride kLeafThreads)
-    const char* eps;                 // bound tensor of this chunk (NAO_EPS_TENSOR_*), or null
-    int eps_shift;                   // log2 of its element size
+    unsigned long long* mask;        // this thread's mask entries (stride kLeafThreads)
+    mutable uint32_t lo = 0, hi = 0, grp = 0;
+    __device__ __forceinline__ void put(bool f, int bitpos) const {  // bitpos: compile time
+        if (bitpos < 32) lo |= f ? (1u << (bitpos & 31)) : 0u;
+        else hi |= f ? (1u << (bitpos & 31)) : 0u;
+    }
+    __device__ __forceinline__ void store(uint32_t g) const {
+        mask[g * kLeafThreads] = ((unsigned long long)hi << 32) | lo;
+        lo = hi = 0;
+    }
+    // Keccak hooks
+    __device__ __forceinline__ uint2 v2c(uint32_t i, int qp) const {
+        const uint2 c = __ldg(reinterpret_cast<const uint2*>(p) + i);
+#if NAO_CC_PROBE != 2
+        const uint2 y = __ldg(reinterpret_cast<const uint2*>(q) + i);
+        put(word_needs_check_f(c.x, y.x), 2 * qp);
+        put(word_needs_check_f(c.y, y.y), 2 * qp + 1);
+#endif
+        return c;
+    }
+    __device__ __forceinline__ uint32_t wc(uint32_t i, int k) const {
+        const uint32_t c = __ldg(p + i);
+#if NAO_CC_PROBE != 2
+        put(word_needs_check_f(c, __ldg(q + i)), k);
+#endif
+        return c;
+    }
+    __device__ __forceinline__ void block_end(uint32_t b) const { store(b); }
+    // SHA-256 path: word by word into 64-word groups
     __device__ __forceinline__ void cmp(uint32_t c, uint32_t y, uint32_t i) const {
-#if NAO_CC_PROBE == 2  // timing probe: no compare at all (wrong verdicts)
-        (void)c; (void)y; (void)i;
-#else
-        if (word_needs_check(c, y)) {
-            mask[(i >> 6) * kLeafThreads] |= 1ull << (i & 63);
-            // the check reads this element's bound after the chunk is hashed:
-            // start pulling it into L2 now (nothing else touches it before)
-            if (eps) asm volatile("prefetch.global.L2 [%0];" ::"l"(eps + ((size_t)i << eps_shift)));
-        }
+#if NAO_CC_PROBE != 2
+        const uint32_t g = i >> 6;
+        if (g != grp) { store(grp); grp = g; }
+        const uint32_t bit = 1u << (i & 31);
+        const bool f = word_needs_check_f(c, y);
+        if (i & 32) hi |= f ? bit : 0u;
+        else lo |= f ? bit : 0u;
 #endif
     }
+    __device__ __forceinline__ void finish() const { if (ALG != kKECCAK256) store(grp); }
     __device__ __forceinline__ uint4 v4(uint32_t i) const {
         const uint4 c = __ldg(reinterpret_cast<const uint4*>(p) + i);
         const uint4 y = __ldg(reinterpret_cast<const uint4*>(q) + i);
@@ -215,15 +263,30 @@ __device__ __forceinline__ Flagged load_flagged(const CheckDesc& d, const float*
     return f;
 }
 
+__device__ __forceinline__ void process_finite(const CheckDesc& d, const Flagged& f, int G,
+                                               double epsilon, LeafCheckSmem& sm, int w,
+                                               LaneCheck& lc, unsigned active_all);
+
+// `active`: the lanes calling (all of them in the full-queue path); the
+// histogram counters are incremented warp-aggregated over equal buckets
 __device__ __forceinline__ void process_flagged(const CheckDesc& d, const Flagged& f, int G,
                                                 double epsilon, LeafCheckSmem& sm, int w,
-                                                LaneCheck& lc) {
-    const float y = f.y, c = f.c;
-    if (!isfinite(y) || !isfinite(c)) {
+                                                LaneCheck& lc, unsigned active) {
+    const bool fin = isfinite(f.y) && isfinite(f.c);
+    const unsigned finm = __ballot_sync(active, fin);
+    if (!fin) {
         lc.nonfin++; lc.viol++;
-        atomicAdd(&sm.wc[w][0][G], 1u); atomicAdd(&sm.wc[w][1][G], 1u);
+        agg_inc(&sm.wc[w][0][G], (unsigned)G, active & ~finm);
+        agg_inc(&sm.wc[w][1][G], (unsigned)G, active & ~finm);
         return;
     }
+    process_finite(d, f, G, epsilon, sm, w, lc, finm);
+}
+
+__device__ __forceinline__ void process_finite(const CheckDesc& d, const Flagged& f, int G,
+                                               double epsilon, LeafCheckSmem& sm, int w,
+                                               LaneCheck& lc, unsigned active_all) {
+    const float y = f.y, c = f.c;
     double eps = f.eps;
     if (d.eps_kind == NAO_EPS_SCALED_LOCAL) eps = __dmul_rn(d.eps_scale, fabs((double)y));
     const double diff = abs_key(y, c);
@@ -257,8 +320,8 @@ __device__ __forceinline__ void process_flagged(const CheckDesc& d, const Flagge
                           (q == G || r32 < sm.f_rel_lo[q]) && (q == 0 || r32 > sm.f_rel_hi[q - 1]);
         if (!safe) q = bsearch_pos(sm.t_rel, G, rel_key(diff, y, epsilon));
     }
-    atomicAdd(&sm.wc[w][0][pa], 1u);
-    atomicAdd(&sm.wc[w][1][q], 1u);
+    agg_inc(&sm.wc[w][0][pa], (unsigned)pa, active_all);
+    agg_inc(&sm.wc[w][1][q], (unsigned)q, active_all);
 }
 
 template <int ALG>
@@ -271,7 +334,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t total_w = tab.nbytes[s] >> 2;
     const uint32_t cw = tab.chunk_words;
-    const uint32_t groups = (cw + 63) >> 6;
+    constexpr uint32_t BW = MaskGeom<ALG>::BW;
+    // mask entries per thread: Keccak one per sponge block (the tail block's
+    // entry always exists), SHA-256 one per 64 words
+    const uint32_t groups = ALG == kKECCAK256 ? cw / BW + 1 : (cw + 63) >> 6;
     const uint64_t nchunks = (total_w + cw - 1) / cw;
     const uint64_t c0 = (vb - tab.block_prefix[s]) * kLeafThreads;
     const uint64_t c = c0 + threadIdx.x;
@@ -337,13 +403,11 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         }
         if (reused) {
         } else if (check) {
-            const bool et = d.eps_kind == NAO_EPS_TENSOR_F32 || d.eps_kind == NAO_EPS_TENSOR_F64;
-            const int esh = d.eps_kind == NAO_EPS_TENSOR_F64 ? 3 : 2;
-            CheckedWords ld{tab.payload[s] + off_w,
-                            reinterpret_cast<const uint32_t*>(d.local) + off_w,
-                            s_mask + threadIdx.x,
-                            et ? static_cast<const char*>(d.eps) + (off_w << esh) : nullptr, esh};
+            CheckedWords<ALG> ld{tab.payload[s] + off_w,
+                                 reinterpret_cast<const uint32_t*>(d.local) + off_w,
+                                 s_mask + threadIdx.x};
             hash_tagged_words<ALG>(ld, nw, 0u, dg);
+            ld.finish();
         } else {
             GlobalWords ld{tab.payload[s] + off_w};
             hash_tagged_words<ALG>(ld, nw, 0u, dg);
@@ -371,7 +435,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             if (has) {
                 const int bit = __ffsll((long long)m) - 1;
                 m &= m - 1ull;
-                sm.q[w][qn + __popc(b & ((1u << lane) - 1u))] = lane_base + 64ull * g + bit;
+                sm.q[w][qn + __popc(b & ((1u << lane) - 1u))] = lane_base + (uint64_t)BW * g + bit;
             }
             qn += __popc(b);
             nflag += has;
@@ -379,8 +443,8 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
                 __syncwarp();
                 const Flagged f0 = load_flagged(d, claimed, sm.q[w][lane]);
                 const Flagged f1 = load_flagged(d, claimed, sm.q[w][32 + lane]);
-                process_flagged(d, f0, G, epsilon, sm, w, lc);
-                process_flagged(d, f1, G, epsilon, sm, w, lc);
+                process_flagged(d, f0, G, epsilon, sm, w, lc, 0xffffffffu);
+                process_flagged(d, f1, G, epsilon, sm, w, lc, 0xffffffffu);
                 __syncwarp();
                 if (lane < qn - 64) sm.q[w][lane] = sm.q[w][64 + lane];
                 __syncwarp();
@@ -390,9 +454,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
     }
     __syncwarp();
     for (int base = 0; base < qn; base += 32) {
+        const unsigned act = __ballot_sync(0xffffffffu, base + lane < qn);
         if (base + lane < qn) {
             const Flagged f = load_flagged(d, claimed, sm.q[w][base + lane]);
-            process_flagged(d, f, G, epsilon, sm, w, lc);
+            process_flagged(d, f, G, epsilon, sm, w, lc, act);
         }
     }
     __syncwarp();
@@ -886,7 +951,9 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
         }();
         if (max_ctas && blocks > max_ctas) blocks = max_ctas;
         CheckAccum* accs = static_cast<CheckAccum*>(accum);
-        const size_t dsm = (size_t)((ct.chunk_words + 63) / 64) * kLeafThreads * 8;
+        const uint32_t mgroups = hash_alg == kKECCAK256 ? ct.chunk_words / MaskGeom<kKECCAK256>::BW + 1
+                                                        : (ct.chunk_words + 63) / 64;
+        const size_t dsm = (size_t)mgroups * kLeafThreads * 8;
         if (hash_alg == kSHA256) {
             NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kSHA256>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
