@@ -497,7 +497,9 @@ __device__ __forceinline__ float drift_one(float v, int64_t i, uint32_t seed, ui
                                            float fault_scale, uint32_t fault_period) {
     uint32_t h = (uint32_t)i * 0x9E3779B1u ^ seed;
     h ^= h >> 16; h *= 0x85EBCA6Bu; h ^= h >> 13; h *= 0xC2B2AE35u; h ^= h >> 16;
-    if (period && (h % period) == 0 && v != 0.0f && isfinite(v))
+    // h % period without an integer division when period is a power of two
+    const uint32_t hm = (period & (period - 1)) == 0 ? (h & (period - 1)) : (period ? h % period : 1u);
+    if (period && hm == 0 && v != 0.0f && isfinite(v))
         v = __int_as_float(__float_as_int(v) + ((h >> 20) & 1 ? 1 : -1));
     if (fault_period && ((h >> 8) % fault_period) == 0) v = v * (1.0f + fault_scale);
     return v;
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(256) k_inject_drift(const float* __restrict__ 
     for (; v + 3 * stride < nv; v += 4 * stride) {
         float4 a[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) a[u] = __ldcs(y4 + v + u * stride);
+        for (int u = 0; u < 4; u++) a[u] = __ldg(y4 + v + u * stride);
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             if (!COPY) {
@@ -529,11 +531,11 @@ __global__ void __launch_bounds__(256) k_inject_drift(const float* __restrict__ 
                 a[u].z = drift_one(a[u].z, i + 2, seed, period, fault_scale, fault_period);
                 a[u].w = drift_one(a[u].w, i + 3, seed, period, fault_scale, fault_period);
             }
-            __stcs(o4 + v + u * stride, a[u]);
+            o4[v + u * stride] = a[u];  // default policy: the claim is read next
         }
     }
     for (; v < nv; v += stride) {
-        float4 a = __ldcs(y4 + v);
+        float4 a = __ldg(y4 + v);
         if (!COPY) {
             const int64_t i = 4 * v;
             a.x = drift_one(a.x, i, seed, period, fault_scale, fault_period);
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(256) k_inject_drift(const float* __restrict__ 
             a.z = drift_one(a.z, i + 2, seed, period, fault_scale, fault_period);
             a.w = drift_one(a.w, i + 3, seed, period, fault_scale, fault_period);
         }
-        __stcs(o4 + v, a);
+        o4[v] = a;
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
         const int64_t i = (nv << 2) + threadIdx.x;
