@@ -1281,12 +1281,14 @@ static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t r
     if (n < 128 || rows < 1024) return -1;
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
                        reinterpret_cast<uintptr_t>(eps)) & 15) == 0 && (n & 3) == 0;
-    // design G is ~25% faster in isolation but its 72 KB CTAs crowd the
-    // concurrently running commit kernel out of the SMs: in the overlapped
-    // verifier design C wins (profiles/README.md); G is opt-in
+    // design G (default since round 2): ~25% faster alone; in round 1 its 72 KB
+    // CTAs crowded the concurrently running commit out of the SMs, but with
+    // FP64 row bounds and the round-2 commit it wins in the overlapped verifier
+    // too (bench 76.0 -> 75.5 %, softmax 33.7 -> 26.7 ms per step);
+    // NAO_SOFTMAX_DESIGN=C selects design C
     static const int design = [] {
         const char* e = getenv("NAO_SOFTMAX_DESIGN");
-        return e && e[0] == 'G' ? 1 : 0;
+        return e && e[0] == 'C' ? 0 : 1;
     }();
     const int64_t row_bytes = (n + 4) * 4;
     static const int budget = [] {

@@ -328,9 +328,10 @@ def test_im2col_rows_matches_unfold(B, geom):
     assert torch.equal(col, ref)
 
 
-def test_softmax_design_g_parity():
-    """The opt-in shared-memory softmax (NAO_SOFTMAX_DESIGN=G, read once per
-    process) against the oracle, in a subprocess."""
+def test_softmax_design_c_parity():
+    """The opt-in three-kernel softmax (NAO_SOFTMAX_DESIGN=C, read once per
+    process; the default is the shared-memory design G) against the oracle,
+    in a subprocess."""
     import os
     import subprocess
     import sys
@@ -354,7 +355,7 @@ def test_softmax_design_g_parity():
         "        assert np.all(e[ok] <= e_ref[ok] * (1 + 1e-5) + sp)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, NAO_SOFTMAX_DESIGN="G", PYTHONPATH=root)
+    env = dict(os.environ, NAO_SOFTMAX_DESIGN="C", PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
