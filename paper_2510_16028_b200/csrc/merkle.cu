@@ -139,6 +139,7 @@ constexpr float kGuard32 = 1.0f / 524288.0f;  // 2^-19 guard of the FP32 relativ
 struct LeafCheckSmem {
     double t_abs[kMaxGrid], t_rel[kMaxGrid];
     float f_rel[kMaxGrid], f_rel_lo[kMaxGrid], f_rel_hi[kMaxGrid];
+    float f_abs[kMaxGrid], f_abs_lo[kMaxGrid], f_abs_hi[kMaxGrid];
     unsigned int wc[kLeafWarps][2][kMaxGrid + 1];  // warp-private interval counters
     unsigned long long q[kLeafWarps][96];           // warp queue of flagged element indices
     unsigned long long bmax[2][kMaxGrid + 1];       // partial mode: per-bucket key range
@@ -312,9 +313,14 @@ __device__ __forceinline__ void process_finite(const CheckDesc& d, const Flagged
         atomicMax(&sm.bmax[0][pa], ba); atomicMax(&sm.bmin_inv[0][pa], ~ba);
         atomicMax(&sm.bmax[1][q], br); atomicMax(&sm.bmin_inv[1][q], ~br);
     } else if (diff != 0.0) {
-        pa = bsearch_pos(sm.t_abs, G, diff);
+        // FP32 bucket searches with a 2^-19 guard band around every threshold;
+        // keys inside a band (or tiny) take the exact FP64 search
         const float d32 = (float)diff;
-        const float r32 = __fdiv_rn(d32, __fadd_rn(fabsf(y), (float)epsilon));
+        pa = bsearch_pos32(sm.f_abs, G, d32);
+        const bool safe_a = (d32 >= 1e-30f) && isfinite(d32) &&
+                            (pa == G || d32 < sm.f_abs_lo[pa]) && (pa == 0 || d32 > sm.f_abs_hi[pa - 1]);
+        if (!safe_a) pa = bsearch_pos(sm.t_abs, G, diff);
+        const float r32 = __fdividef(d32, __fadd_rn(fabsf(y), (float)epsilon));  // ~2 ulp
         q = bsearch_pos32(sm.f_rel, G, r32);
         const bool safe = (d32 >= 1e-30f) && (r32 >= 1e-30f) && isfinite(r32) &&
                           (q == G || r32 < sm.f_rel_lo[q]) && (q == 0 || r32 > sm.f_rel_hi[q - 1]);
@@ -350,6 +356,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         if (threadIdx.x < kMaxGrid) {
             const int i = threadIdx.x;
             const double ta = i < G ? v->t_abs[i] : INFINITY;
+            const float fa = (float)ta;
+            sm.f_abs[i] = fa;
+            sm.f_abs_lo[i] = fa * (1.0f - kGuard32);
+            sm.f_abs_hi[i] = fa * (1.0f + kGuard32);
             const double tr = i < G ? v->t_rel[i] : INFINITY;
             sm.t_abs[i] = ta;
             sm.t_rel[i] = tr;
