@@ -125,6 +125,10 @@ __global__ void __launch_bounds__(256) k_refine(const __grid_constant__ RefineTa
     const int64_t m = (int64_t)(count < (unsigned long long)d.cap ? count : (unsigned long long)d.cap);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     long long dv = 0, db = 0;
+    // ambiguous intrinsic values beyond the list were never examined: their
+    // verdict is uncertified (GEMM band entries beyond it are already borderline)
+    if (d.kind == NAO_REFINE_UNARY && threadIdx.x == 0 && count > (unsigned long long)d.cap)
+        db += (long long)(count - (unsigned long long)d.cap);
     for (int64_t e = w; e < m; e += nw) {
         const unsigned long long idx = d.list[1 + e];
         const float c = __ldg(d.claimed + idx);

@@ -297,6 +297,18 @@ def leaf_bound_check(node, args, claimed, model=None, profile=None) -> dict:
     if tuple(c.shape) != tuple(y.shape):
         raise ValueError(f"claimed shape {tuple(c.shape)} differs from the output {tuple(y.shape)}")
     c = c.contiguous()
+    if intrinsic or node.kind in ("matmul", "linear", "conv2d"):
+        # the API path sizes the list to the node (every listed element is settled)
+        cap = max(_lib.BORDER_CAP, min(int(y.numel()), 1 << 24))
+        if cap > _lib.BORDER_CAP:
+            big = torch.zeros(1 + cap, dtype=torch.int64, device=y.device)
+            if intrinsic:  # the ambiguity list was filled by the value kernel
+                n_amb = int(border[0])
+                if n_amb > _lib.BORDER_CAP:  # re-run the value pass into the big list
+                    _ = op_bound_device(node, xs, model, profile, eps_f64=True, amb=big)
+                else:
+                    big[:1 + _lib.BORDER_CAP].copy_(border)
+            border = big
     eps_chk = eps
     if intrinsic:
         eps_chk = ("scaled", 2.0 * model.u)

@@ -129,6 +129,8 @@ def to_device(a, device=None) -> torch.Tensor:
     if not isinstance(a, np.ndarray) and hasattr(a, "array"):  # the reference's Tensor
         a = a.array
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+    if not arr.flags.writeable:  # the reference freezes its arrays (tensor.py:36-37)
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device or "cuda")
 
 

@@ -189,3 +189,31 @@ def test_matmul_fp64_bit_exact():
             np.testing.assert_allclose(got, ref, rtol=4e-16, atol=0)
         else:
             assert np.array_equal(got, ref), kind
+
+
+def test_intrinsic_value_ambiguity_settled():
+    """gelu in its cancellation region (x << 0: 1 + tanh(inner) cancels, so the
+    FP32 value depends on the libm's last FP64 ulps) with the claim = numpy's
+    value on this host, plus real faults on well-conditioned elements: the GPU
+    reports exactly the oracle's (certain) violations; elements whose verdict
+    differs between the possible reference values are undecided
+    (n_borderline), never violations."""
+    from paper_2510_16028_b200 import _lib, dispute
+    from paper_2510_16028_b200.engine import DeviceProfile, unary
+    rng = np.random.default_rng(8)
+    x = np.concatenate([rng.uniform(-8.0, -3.0, 60000), rng.uniform(-2.0, 3.0, 40000)])
+    x = x.astype(np.float32)
+    node = _Node("gelu")
+    y_ref, eps_ref = OB.op_bound(node, [x], OB.FpModel())
+    claimed = y_ref.copy()
+    good = np.nonzero(x > 0.5)[0][:50]
+    claimed[good] = (claimed[good] * np.float32(1.001)).astype(np.float32)
+    ref = OC.leaf_check(y_ref, claimed, eps_ref)
+    got = dispute.leaf_bound_check(node, [x], claimed, profile=DeviceProfile("seq", "sequential"))
+    amb = torch.zeros(1 + _lib.BORDER_CAP, dtype=torch.int64, device="cuda")
+    y = unary("gelu", torch.from_numpy(x).cuda(), amb=amb).cpu().numpy()
+    n_amb = int(amb[0])
+    mism = int(np.count_nonzero(y.view(np.uint32) != y_ref.view(np.uint32)))
+    assert n_amb >= mism > 0  # the host's numpy and the GPU differ, always flagged
+    assert got["n_violations"] == ref["n_violations"] == 50
+    assert got["n_borderline"] <= n_amb
