@@ -520,7 +520,7 @@ def run_ours(args):
         # algorithmic unit in one `ncu --set full` capture of this bench command
         # (profiles/r1_traffic.json), applied to this run's per-launch units
         try:
-            tr = json.load(open(ROOT / "profiles" / "r1_traffic.json")).get(dom)
+            tr = json.load(open(ROOT / "profiles" / "r2_traffic.json")).get(dom)
             if tr and "ratio_dram_to_hashed" in tr:
                 roof["traffic"] = round(tr["ratio_dram_to_hashed"] * per_launch_units)
                 roof["traffic_unit"] = "bytes per launch (ncu dram read+write, ratio "
