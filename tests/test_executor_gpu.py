@@ -393,3 +393,55 @@ def test_graphed_replay_survives_workspace_growth():
         r1, c1 = gr.replay()
         torch.cuda.synchronize()
         assert torch.equal(r1, r0) and torch.equal(c1, c0)
+
+
+def test_streaming_conv_in_band_claims_match_oracle():
+    """A small ResNet (conv -> BN -> relu, maxpool, residual blocks) through the
+    streaming verifier with claims planted inside the certified band of every
+    conv node (FP32 tensor-core bounds, conv refine by implicit-im2col
+    double-double dots): per-node violation counts equal the oracle's exactly,
+    nothing undecided."""
+    from test_verdict_identity_gpu import plant_in_band
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.dispute import CheckRecord
+    from paper_2510_16028_b200.engine import DeviceProfile
+    from paper_2510_16028_b200.executor import StreamingVerifier
+    from paper_2510_16028_b200.graph import parse_ref
+    from paper_2510_16028_b200.lowerings import build_resnet18
+    from paper_2510_16028_b200.tensor import Rng
+    spec = build_resnet18(batch=2, side=32, n_classes=10, width=16)
+    g = spec.graph
+    x = spec.make_inputs(Rng(3))
+    sv = StreamingVerifier(g, FpModel(), DeviceProfile("seq", "sequential"), None,
+                           hash_alg="keccak256", chunk_bytes=1024)
+    claimed, expect = {}, {}
+    rng = np.random.default_rng(6)
+
+    def claimed_fn(node, y):
+        args = []
+        for ref in node.inputs:
+            cat, key = parse_ref(ref)
+            args.append(claimed[key].cpu().numpy() if cat == "node" else
+                        (x[key].array if cat == "input" else g.weights[key].array))
+        if node.kind == "conv2d":
+            y_ref, eps = OB.op_bound(node, args, OB.FpModel())
+            assert np.array_equal(y_ref.view(np.uint32), y.cpu().numpy().view(np.uint32))
+            cl, _, _ = plant_in_band(y_ref, eps, rng, n_max=100, min_each=0)
+            expect[node.index] = OC.leaf_check(y_ref, cl, eps)["n_violations"]
+        else:
+            cl = y.cpu().numpy()
+        claimed[node.index] = torch.from_numpy(np.ascontiguousarray(cl)).cuda()
+        return claimed[node.index].clone()
+
+    roots, recs = sv.run(x, claimed_fn)
+    torch.cuda.synchronize()
+    planted = 0
+    for node in g.nodes:
+        rec = CheckRecord(recs[node.index]).host()
+        assert rec["n_borderline"] == 0, node.name
+        if node.index in expect:
+            assert rec["n_violations"] == expect[node.index], node.name
+            planted += expect[node.index]
+        else:
+            assert rec["n_violations"] == 0, node.name
+    assert planted > 0
