@@ -787,6 +787,14 @@ def run_config(args):
                     "d2h_bytes_per_step": int(host_roots.numel() + host_recs.numel())},
             "gpu_launches": None, "roofline": None, "cpu_baseline": None,
             "clocks": clocks.summary()}
+    if args.config == "mlp" and world == 1 and not args.no_cpu:
+        res = cpu_mlp_reference(5)
+        if res is not None:
+            line["cpu_baseline"] = {
+                "value": round(res[0], 1), "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"the unmodified reference ({res[3]}): execute vs co_execute + "
+                          f"observed_p_max + chunked SHA-256 build_tree, median of 5",
+                "plain_ms": round(res[2], 2), "verified_ms": round(res[1], 2)}
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -891,6 +899,71 @@ def cpu_baseline(args):
     return _cpu_summary(times, g.n_nodes, args.seq, time.perf_counter() - t0, threads)
 
 
+def _import_reference():
+    """The unmodified reference package: baseline/_ref (tools/install_reference.sh;
+    travels to the GPU box) or, in the build container, /root/reference."""
+    for cand in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (cand / "fpverify").is_dir():
+            if str(cand) not in sys.path:
+                sys.path.insert(0, str(cand))
+            import fpverify  # noqa: F401
+            return cand
+    return None
+
+
+def cpu_mlp_reference(n_steps: int):
+    """The MLP config's full reference pipeline on the host, the reference's own
+    code (kind "reference"): plain forward = engine.execute; verified =
+    bounds.co_execute (bounds.py:221-262) + dispute.observed_p_max of every node
+    against a drifted claim (a second device profile's trace) + the chunked
+    SHA-256 Merkle commitment of every claimed tensor (commitments.build_tree
+    over canon-header + 4 KiB chunk leaves) and the trace tree.  Returns
+    (overhead %, ms per verified step, ms per plain step)."""
+    where = _import_reference()
+    if where is None:
+        return None
+    from fpverify import calibration as C, commitments as M, dispute as D, engine as E
+    from fpverify.bounds import FpModel, co_execute
+    from fpverify.models import build_mlp
+    from fpverify.tensor import Rng
+    spec = build_mlp(seed=0, batch=64, in_dim=784, hidden=256, n_classes=10)
+    g = spec.graph
+    x = spec.make_inputs(Rng(7))
+    seq, pair = E.DeviceProfile("seq", "sequential"), E.DeviceProfile("pair", "pairwise")
+    rng = Rng(101)
+    env = C.calibrate(g, [spec.make_inputs(rng) for _ in range(2)], [seq, pair])
+    th = C.build_thresholds(env, alpha=3.0)
+    _, claimed = E.execute(g, x, pair)
+    model = FpModel()
+
+    def plain():
+        E.execute(g, x, seq)
+
+    def verified():
+        _, _, trace = co_execute(g, x, seq, model, with_trace=True)
+        roots = []
+        for i, node in enumerate(g.nodes):
+            D.observed_p_max(trace.tensors[i], claimed.tensors[i], th, node.name)
+            canon = M.canon_tensor(claimed.tensors[i])
+            hl = 5 + 16 * len(claimed.tensors[i].shape)
+            head, pay = canon[:hl], canon[hl:]
+            roots.append(M.build_tree([head] + [pay[o:o + 4096]
+                                                for o in range(0, len(pay), 4096)]).root)
+        M.build_tree(roots)
+
+    def best(fn):
+        ts = []
+        for _ in range(max(1, n_steps)):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    plain(); verified()
+    tp, tv = best(plain), best(verified)
+    return 100.0 * (tv - tp) / tp, tv * 1000.0, tp * 1000.0, str(where)
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the host cores (the oracle
     port; the reference's Python engine cannot run these shapes, engine.py:181),
@@ -902,6 +975,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    if args.config == "mlp":
+        return run_reference_mlp(args)
     threads = os.cpu_count() or 1
     g, work = cpu_layer_prepare(args.seq)
     n_groups = max(1, min(args.steps, 8))
@@ -939,6 +1014,34 @@ def run_reference(args):
                        "layers": args.layers},
             "cpu_baseline": cpu,
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return line
+
+
+def run_reference_mlp(args):
+    """--impl reference --config mlp: the reference package itself (not a port)."""
+    res = cpu_mlp_reference(max(1, args.steps))
+    if res is None:
+        line = {"impl": "reference", "unavailable": "reference package not installed "
+                "(tools/install_reference.sh)"}
+        print(json.dumps(line))
+        return line
+    val, tv, tp, where = res
+    cpu = {"value": round(val, 1), "unit": UNIT, "cores": 1, "kind": "reference",
+           "sample": f"the unmodified reference ({where}): engine.execute vs co_execute + "
+                     f"observed_p_max per node + chunked SHA-256 build_tree commitment, MLP "
+                     f"784-256-10 batch 64, median of {max(1, args.steps)} steps "
+                     f"(numpy single-threaded except BLAS)",
+           "plain_ms": round(tp, 2), "verified_ms": round(tv, 2)}
+    line = {"metric": METRIC, "value": round(val, 1), "unit": UNIT, "impl": "reference",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(tv, 2), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 values / f64 bound math",
+            "data": "synthetic",
+            "config": {"workload": CONFIGS["mlp"][0], "model": "mlp (reference build_mlp)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(val, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return line
 
