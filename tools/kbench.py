@@ -156,7 +156,7 @@ def main():
         from paper_2510_16028_b200.bounds import reduce_device
         for shape in ((S, H), (S * NH, 128), (S * 8, 128)):
             x = torch.randn(shape, device=dev)
-            report("mean_bound_f32eps", timeit(lambda: reduce_device("mean", x, -1, model, False),
+            report("mean_bound_f64eps", timeit(lambda: reduce_device("mean", x, -1, model, True),
                                                a.reps), 4 * x.numel() + 8 * shape[0],
                    shape=list(shape))
     if want("drift"):
