@@ -332,12 +332,13 @@ __global__ void __launch_bounds__(128) k_reduce_lane(
 // engine.py:133-154: FP64 evaluation rounded once to FP32 (csrc/unary.cuh),
 // plus the value-ambiguity list and the optional intrinsic bound 2u|y| taken
 // at the largest candidate (never below the reference's).
-__global__ void k_unary(const float* __restrict__ x, float* __restrict__ y, int64_t n, int kind,
+template <int KIND>  // compile-time kind: no per-element switch in the FP64 evaluation
+__global__ void k_unary(const float* __restrict__ x, float* __restrict__ y, int64_t n,
                         void* __restrict__ eps, int eps_f64, double eps_scale,
                         unsigned long long* __restrict__ amb, long long amb_cap) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const UnaryOut o = unary_eval(kind, __ldg(x + i));
+        const UnaryOut o = unary_eval(KIND, __ldg(x + i));
         y[i] = o.y;
         if (eps) {
             const double m = fmax(fabs((double)o.lo), fabs((double)o.hi));
@@ -464,9 +465,18 @@ int nao_unary_fp64(const float* x, float* y, int64_t n, int kind, void* eps, int
     NAO_REQUIRE(kind >= NAO_UN_EXP && kind <= NAO_UN_SILU, "bad unary kind %d", kind);
     NAO_REQUIRE(amb_list == nullptr || amb_cap >= 0, "bad ambiguity list capacity");
     if (n == 0) return NAO_OK;
-    k_unary<<<ew_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        x, y, n, kind, eps, eps_f64, eps_scale,
-        reinterpret_cast<unsigned long long*>(amb_list), (long long)amb_cap);
+    auto* amb = reinterpret_cast<unsigned long long*>(amb_list);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int g = ew_grid(n);
+    switch (kind) {
+        case NAO_UN_EXP: k_unary<NAO_UN_EXP><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        case NAO_UN_LOG: k_unary<NAO_UN_LOG><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        case NAO_UN_SQRT: k_unary<NAO_UN_SQRT><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        case NAO_UN_RSQRT: k_unary<NAO_UN_RSQRT><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        case NAO_UN_TANH: k_unary<NAO_UN_TANH><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        case NAO_UN_GELU: k_unary<NAO_UN_GELU><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+        default: k_unary<NAO_UN_SILU><<<g, 256, 0, st>>>(x, y, n, eps, eps_f64, eps_scale, amb, amb_cap); break;
+    }
     NAO_CHECK_LAUNCH();
     return NAO_OK;
 }

@@ -159,6 +159,10 @@ def main():
             report("mean_bound_f64eps", timeit(lambda: reduce_device("mean", x, -1, model, True),
                                                a.reps), 4 * x.numel() + 8 * shape[0],
                    shape=list(shape))
+    if want("unary"):  # the SiLU of the MLP gate (2048 x 12288)
+        from paper_2510_16028_b200.engine import unary
+        x = torch.randn((S, I), device=dev)
+        report("unary_silu_fp64", timeit(lambda: unary("silu", x), a.reps), 8 * x.numel())
     if want("drift"):
         x = torch.randn((NH, S, S), device=dev)
         report("inject_drift", timeit(lambda: inject_drift(x, 1, 16), a.reps), 8 * x.numel())
