@@ -75,7 +75,8 @@ def run_config(name, steps, warmup, drift_period=16, profile=False, flush_mb=204
     th = ThresholdSet(alpha=3.0, epsilon=1e-12, grid=PERCENTILE_GRID,
                       ops=[OpThresholds(n, 3.0 * a.cpu().numpy(), 3.0 * r.cpu().numpy())
                            for n, (a, r) in env.items()])
-    sv = StreamingVerifier(g, None, thresholds=th, max_lag=4, flush_bytes=flush_mb << 20)
+    sv = StreamingVerifier(g, None, thresholds=th, max_lag=4, flush_bytes=flush_mb << 20,
+                           missing_thresholds="inf")  # empty nodes were not calibrated
 
     def claimed(node, y):
         return drift_claim(node, y, 1, drift_period, fault)
