@@ -366,10 +366,10 @@ def oracle_recheck(node, args, claimed, eps, model=None, profile=None) -> dict:
                 from .bounds import op_bound_device
                 y32, _ = op_bound_device(node, xs, model, profile, eps_f64=None)
                 y32 = y32.contiguous()
-            cap = _lib.BORDER_CAP
+            cap = max(_lib.BORDER_CAP, n_border)  # the API path settles every band element
             border = torch.zeros(1 + cap, dtype=torch.int64, device=y_or.device)
             border[0] = n_border
-            border[1:1 + min(cap, n_border)] = idx[:cap]
+            border[1:1 + n_border] = idx
             rec = new_result_buffer(y_or.device)
             r = torch.zeros(2, dtype=torch.int64, device=y_or.device)
             r[0], r[1] = n_fail, n_border
