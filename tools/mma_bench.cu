@@ -20,7 +20,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, int row_bytes) {
     return d;
 }
 
-template <int KIND, int N>  // KIND 0 = tf32, 1 = f16(bf16)
+template <int KIND, int N>  // KIND 0 = tf32, 1 = f16(bf16), 2 = f16 with A in TMEM (TS)
 __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* cycles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t bar;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -51,9 +51,12 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
                 if (KIND == 0)
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;}"
                                  ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(1));
-                else
+                else if (KIND == 1)
                     asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
                                  ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(1));
+                else  // A operand from TMEM columns 384.. (128 lanes x 8 columns per k16)
+                    asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}"
+                                 ::"r"(tmem), "r"(tmem + 384u), "l"(bd), "r"(idesc), "r"(1));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
             asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @P1 bra D; bra W; D: }" ::"r"(smem_u32(&bar)), "r"(phase));
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(128, 1) k_mma(int iters, unsigned long long* c
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 template <int KIND, int N>
@@ -84,7 +87,7 @@ void run(const char* name) {
     unsigned long long h[148];
     cudaMemcpy(h, d, sms * 8, cudaMemcpyDeviceToHost);
     const double mmas = (double)iters * 16;
-    const double k = KIND == 0 ? 8 : 16;
+    const double k = KIND == 0 ? 8 : 16;  // k per instruction
     const double flops = 2.0 * 128 * N * k * mmas * sms;
     printf("{\"mma\": \"%s\", \"N\": %d, \"cycles_per_mma\": %.1f, \"TFLOP/s\": %.1f, \"err\": \"%s\"}\n", name, N,
            (double)h[0] / mmas, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
@@ -97,5 +100,7 @@ int main() {
     run<0, 256>("tf32");
     run<1, 128>("bf16");
     run<1, 256>("bf16");
+    run<2, 128>("bf16_ts");
+    run<2, 256>("bf16_ts");
     return 0;
 }
