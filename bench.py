@@ -181,6 +181,140 @@ def calibrate_thresholds(g, sv_cls, ids, dev, model, args, start=0, end=None, fr
     return ThresholdSet(alpha=3.0, epsilon=1e-12, grid=PERCENTILE_GRID, ops=ops)
 
 
+def _units(name, a):
+    """Algorithmic units (FLOP or bytes) of one timed C-ABI launch (args a)."""
+    if name == "nao_abs_gemm_bound":
+        return 2.0 * a[4] * a[5] * a[6] * a[7]
+    if name == "nao_abs_gemm_tc":
+        return 2.0 * a[6] * a[9] * a[10] * a[11]
+    if name == "nao_tf32_split":
+        return 12.0 * a[3] * a[4] * a[5]
+    if name == "nao_abs_gemm_tc16":
+        return 2.0 * a[11] * a[14] * a[15] * a[16]
+    if name == "nao_f16_split":  # read 4 B, write 2 x 2 B per element
+        return 8.0 * a[4] * a[5] * a[6]
+    if name in ("nao_softmax_bound", "nao_layernorm_bound"):
+        return 12.0 * a[4] * a[5]
+    if name == "nao_inject_drift":
+        return 8.0 * a[2]
+    if name == "nao_reduce_bound":  # read x, write y + eps (f32/f64) per row
+        return 4.0 * a[4] * a[5] + (4.0 + (8.0 if a[3] else 4.0)) * a[4]
+    if name == "nao_unary_fp64":
+        return 8.0 * a[2]
+    if name in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
+        return float(sum(a[2][i] for i in range(a[0])))
+    if name == "nao_check":
+        return 8.0 * a[2] + (4.0 if a[3] == 0 else 8.0 if a[3] == 1 else 0.0) * a[2]
+    return 0.0
+
+
+def _roofline(timers, t_serial, peaks, sm_mhz, hash_alg):
+    """Roofline of the dominant kernel (largest share of the serial step's
+    event-timed launch time) plus every kernel family's share and rate."""
+    shares = {k: sum(v["ms"]) for k, v in timers.items()}
+    dom = max(shares, key=shares.get) if shares else None
+    roof = None
+    if dom:
+        d = timers[dom]
+        per_launch_ms = sum(d["ms"]) / len(d["ms"])
+        per_launch_units = sum(d["units"]) / len(d["units"])
+        if dom == "nao_abs_gemm_tc":
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
+            tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
+            peak = tf32 / 3.0
+            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
+                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = TF32 dense, / 3 "
+                                   "MMAs per product (3xTF32 split): algorithmic ceiling",
+                    "mma_tflops": round(3 * achieved, 1), "tf32_peak": round(tf32, 1),
+                    "traffic": None}
+        elif dom == "nao_abs_gemm_tc16":
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
+            f16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+            peak = f16 / 3.0
+            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
+                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (timed inside a "
+                                   "second-long step) = FP16 dense, / 3 MMAs per product "
+                                   "(FP16 3-split): algorithmic ceiling",
+                    "mma_tflops": round(3 * achieved, 1), "f16_peak": round(f16, 1),
+                    "traffic": None}
+        elif dom == "nao_abs_gemm_bound":
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
+            peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 SIMT peak (derived, not measured)
+            roof = {"kernel": dom, "bound": "fp32-simt", "achieved": round(achieved, 2),
+                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "derived FP32 FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz "
+                                   "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
+                    "traffic": None}
+        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors") and \
+                hash_alg == "keccak256":
+            # Keccak-f[1600] is integer-ALU bound, not HBM bound: 24 rounds x 180
+            # ALU ops (122 LOP3 + 58 SHF.L.W, cuobjdump) per 136-byte block on a
+            # 64-lane/clk/SM ALU pipe (profiles/r1_keccak_pipe_balance.md)
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
+            try:  # measured: compute-only keccak_f1600 rate (tools/alu_peak.cu)
+                alu = json.load(open(ROOT / "profiles" / "r2_alu_peak.json"))
+                peak = float(alu["keccak_rate_gbs"]) * sm_mhz / 1965.0
+                src = ("measured: profiles/r2_alu_peak.json keccak_rate_gbs (tools/alu_peak.cu, "
+                       "compute-only keccak_f1600 of csrc/hash.cuh on 148 SMs, CUDA events, "
+                       "1965 MHz), scaled to this run's median SM clock")
+            except Exception:
+                peak = 148 * 64 * sm_mhz * 1e6 / (24 * 180 / 136.0) / 1e9
+                src = ("derived integer-ALU roofline of Keccak-256: 148 SM x 64 lanes/clk x SM "
+                       "clock / (24 x 180 ops per 136 B block)")
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
+                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "peak_source": src,
+                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
+        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
+            # SHA-256 is integer-ALU bound too: ~1253 ALU-pipe ops per 64-byte
+            # compression (cuobjdump of k_chunk_leaves<sha256>: 660 SHF + 350 LOP3
+            # + 243 IADD3 per compression; ~130 IMAD go to the FMA pipe)
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
+            peak = 148 * 64 * sm_mhz * 1e6 / (1253 / 64.0) / 1e9
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
+                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "derived integer-ALU roofline of SHA-256: 148 SM x 64 "
+                                   "lanes/clk x SM clock / (1253 ops per 64 B block)",
+                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
+        else:
+            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
+            peak = peaks.get("hbm_gbs", 6650.0)
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
+                    "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks
+                    else "fallback", "traffic": None}
+        # DRAM traffic of the dominant kernel: ratio of measured dram bytes to the
+        # algorithmic unit in one `ncu --set full` capture of this bench command
+        # (profiles/r1_traffic.json), applied to this run's per-launch units
+        try:
+            tr = json.load(open(ROOT / "profiles" / "r2_traffic.json")).get(dom)
+            if tr and "ratio_dram_to_hashed" in tr:
+                roof["traffic"] = round(tr["ratio_dram_to_hashed"] * per_launch_units)
+                roof["traffic_unit"] = "bytes per launch (ncu dram read+write, ratio "
+                roof["traffic_unit"] += f"{tr['ratio_dram_to_hashed']} x hashed bytes)"
+        except Exception:
+            pass
+        roof["share_of_serial_step"] = round(shares[dom] / t_serial, 4)
+        roof["serial_step_ms"] = round(t_serial, 2)
+        roof["kernel_ms_per_step"] = {k: round(v, 2) for k, v in sorted(
+            shares.items(), key=lambda kv: -kv[1])}
+        # algorithmic rate of every timed kernel family (TFLOP/s for the GEMMs,
+        # GB/s otherwise; units as in `units` above)
+        rates = {}
+        for k, v in timers.items():
+            t = sum(v["ms"]) * 1e-3
+            if t > 0 and sum(v["units"]) > 0:
+                flops = k in ("nao_abs_gemm_tc", "nao_abs_gemm_tc16", "nao_abs_gemm_bound")
+                rates[k] = (f"{sum(v['units']) / t / 1e12:.1f} TFLOP/s" if flops
+                            else f"{sum(v['units']) / t / 1e9:.0f} GB/s")
+        roof["kernel_rates"] = rates
+    return roof, shares
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -327,30 +461,7 @@ def run_ours(args):
     # dominant-kernel roofline: CUDA events around every abs-GEMM / commit / check launch
     timers = {}
 
-    def units(name, a):
-        if name == "nao_abs_gemm_bound":
-            return 2.0 * a[4] * a[5] * a[6] * a[7]
-        if name == "nao_abs_gemm_tc":
-            return 2.0 * a[6] * a[9] * a[10] * a[11]
-        if name == "nao_tf32_split":
-            return 12.0 * a[3] * a[4] * a[5]
-        if name == "nao_abs_gemm_tc16":
-            return 2.0 * a[11] * a[14] * a[15] * a[16]
-        if name == "nao_f16_split":  # read 4 B, write 2 x 2 B per element
-            return 8.0 * a[4] * a[5] * a[6]
-        if name in ("nao_softmax_bound", "nao_layernorm_bound"):
-            return 12.0 * a[4] * a[5]
-        if name == "nao_inject_drift":
-            return 8.0 * a[2]
-        if name == "nao_reduce_bound":  # read x, write y + eps (f32/f64) per row
-            return 4.0 * a[4] * a[5] + (4.0 + (8.0 if a[3] else 4.0)) * a[4]
-        if name == "nao_unary_fp64":
-            return 8.0 * a[2]
-        if name in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
-            return float(sum(a[2][i] for i in range(a[0])))
-        if name == "nao_check":
-            return 8.0 * a[2] + (4.0 if a[3] == 0 else 8.0 if a[3] == 1 else 0.0) * a[2]
-        return 0.0
+    units = _units
 
     with ClockSampler(local) as clocks:
         t_ver = timed(verified_step, args.steps)
@@ -437,110 +548,8 @@ def run_ours(args):
         tot_bytes, tot_flops = float(t[0]), float(t[1])
     commit_bytes_per_step = tot_bytes
 
-    # roofline of the dominant kernel (largest share of event-timed launch time)
-    shares = {k: sum(v["ms"]) for k, v in timers.items()}
-    dom = max(shares, key=shares.get) if shares else None
-    roof = None
-    if dom:
-        d = timers[dom]
-        per_launch_ms = sum(d["ms"]) / len(d["ms"])
-        per_launch_units = sum(d["units"]) / len(d["units"])
-        if dom == "nao_abs_gemm_tc":
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
-            tf32 = peaks.get("bf16_tflops", 1590.0) / 2.0
-            peak = tf32 / 3.0
-            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
-                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst) / 2 = TF32 dense, / 3 "
-                                   "MMAs per product (3xTF32 split): algorithmic ceiling",
-                    "mma_tflops": round(3 * achieved, 1), "tf32_peak": round(tf32, 1),
-                    "traffic": None}
-        elif dom == "nao_abs_gemm_tc16":
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
-            f16 = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
-            peak = f16 / 3.0
-            roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 2),
-                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (timed inside a "
-                                   "second-long step) = FP16 dense, / 3 MMAs per product "
-                                   "(FP16 3-split): algorithmic ceiling",
-                    "mma_tflops": round(3 * achieved, 1), "f16_peak": round(f16, 1),
-                    "traffic": None}
-        elif dom == "nao_abs_gemm_bound":
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e12
-            peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 SIMT peak (derived, not measured)
-            roof = {"kernel": dom, "bound": "fp32-simt", "achieved": round(achieved, 2),
-                    "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "derived FP32 FFMA peak 148 SM x 128 lanes x 2 x 1.965 GHz "
-                                   "(MEASURED_PEAKS.json has no FP32 SIMT figure)",
-                    "traffic": None}
-        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors") and \
-                args.hash == "keccak256":
-            # Keccak-f[1600] is integer-ALU bound, not HBM bound: 24 rounds x 180
-            # ALU ops (122 LOP3 + 58 SHF.L.W, cuobjdump) per 136-byte block on a
-            # 64-lane/clk/SM ALU pipe (profiles/r1_keccak_pipe_balance.md)
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
-            sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
-            try:  # measured: compute-only keccak_f1600 rate (tools/alu_peak.cu)
-                alu = json.load(open(ROOT / "profiles" / "r2_alu_peak.json"))
-                peak = float(alu["keccak_rate_gbs"]) * sm_mhz / 1965.0
-                src = ("measured: profiles/r2_alu_peak.json keccak_rate_gbs (tools/alu_peak.cu, "
-                       "compute-only keccak_f1600 of csrc/hash.cuh on 148 SMs, CUDA events, "
-                       "1965 MHz), scaled to this run's median SM clock")
-            except Exception:
-                peak = 148 * 64 * sm_mhz * 1e6 / (24 * 180 / 136.0) / 1e9
-                src = ("derived integer-ALU roofline of Keccak-256: 148 SM x 64 lanes/clk x SM "
-                       "clock / (24 x 180 ops per 136 B block)")
-            hbm = peaks.get("hbm_gbs", 6650.0)
-            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
-                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "peak_source": src,
-                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
-        elif dom in ("nao_merkle_commit_tensors", "nao_commit_check_tensors"):
-            # SHA-256 is integer-ALU bound too: ~1253 ALU-pipe ops per 64-byte
-            # compression (cuobjdump of k_chunk_leaves<sha256>: 660 SHF + 350 LOP3
-            # + 243 IADD3 per compression; ~130 IMAD go to the FMA pipe)
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
-            sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
-            peak = 148 * 64 * sm_mhz * 1e6 / (1253 / 64.0) / 1e9
-            hbm = peaks.get("hbm_gbs", 6650.0)
-            roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 1),
-                    "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "derived integer-ALU roofline of SHA-256: 148 SM x 64 "
-                                   "lanes/clk x SM clock / (1253 ops per 64 B block)",
-                    "hbm_peak": hbm, "hbm_frac": round(achieved / hbm, 4), "traffic": None}
-        else:
-            achieved = per_launch_units / (per_launch_ms * 1e-3) / 1e9
-            peak = peaks.get("hbm_gbs", 6650.0)
-            roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
-                    "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks
-                    else "fallback", "traffic": None}
-        # DRAM traffic of the dominant kernel: ratio of measured dram bytes to the
-        # algorithmic unit in one `ncu --set full` capture of this bench command
-        # (profiles/r1_traffic.json), applied to this run's per-launch units
-        try:
-            tr = json.load(open(ROOT / "profiles" / "r2_traffic.json")).get(dom)
-            if tr and "ratio_dram_to_hashed" in tr:
-                roof["traffic"] = round(tr["ratio_dram_to_hashed"] * per_launch_units)
-                roof["traffic_unit"] = "bytes per launch (ncu dram read+write, ratio "
-                roof["traffic_unit"] += f"{tr['ratio_dram_to_hashed']} x hashed bytes)"
-        except Exception:
-            pass
-        roof["share_of_serial_step"] = round(shares[dom] / t_serial, 4)
-        roof["serial_step_ms"] = round(t_serial, 2)
-        roof["kernel_ms_per_step"] = {k: round(v, 2) for k, v in sorted(
-            shares.items(), key=lambda kv: -kv[1])}
-        # algorithmic rate of every timed kernel family (TFLOP/s for the GEMMs,
-        # GB/s otherwise; units as in `units` above)
-        rates = {}
-        for k, v in timers.items():
-            t = sum(v["ms"]) * 1e-3
-            if t > 0 and sum(v["units"]) > 0:
-                flops = k in ("nao_abs_gemm_tc", "nao_abs_gemm_tc16", "nao_abs_gemm_bound")
-                rates[k] = (f"{sum(v['units']) / t / 1e12:.1f} TFLOP/s" if flops
-                            else f"{sum(v['units']) / t / 1e9:.0f} GB/s")
-        roof["kernel_rates"] = rates
+    roof, shares = _roofline(timers, t_serial, peaks, clocks.summary().get("sm_mhz") or 1965.0,
+                             args.hash)
 
     # the proposer harness's device time: its nao_inject_drift launches (claims of
     # reduction nodes drifted, of the others copied); events around the Python
@@ -739,6 +748,25 @@ def run_config(args):
         host_roots, host_recs = roots.cpu(), recs.cpu()
         e2e_ms += (time.perf_counter() - t0) * 1000.0
     e2e_ms /= args.steps
+    # serial decomposition (not the headline): one eager verified step with the
+    # side streams off, CUDA events around every C-ABI launch
+    timers = {}
+    sv.overlap, keep = False, (sv._s_chk, sv._s_com)
+    sv._s_chk = sv._s_com = None
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    _lib.set_timer(timers, _units, stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sv.run(x, claimed_fn)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    _lib.set_timer(None, None, None)
+    t_serial = e0.elapsed_time(e1)
+    sv.overlap, (sv._s_chk, sv._s_com) = True, keep
+    roof, shares = _roofline(timers, t_serial, _peaks(),
+                             clocks.summary().get("sm_mhz") or 1965.0, args.hash)
+    n_launch = sum(len(v["ms"]) for v in timers.values())
     gc.enable()
     if world > 1:
         t = torch.tensor([e2e_ms], device=coll_dev)
@@ -785,7 +813,8 @@ def run_config(args):
             "e2e": {"value": round(100.0 * (e2e_ms - t_plain) / t_plain, 2), "unit": UNIT,
                     "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(host_roots.numel() + host_recs.numel())},
-            "gpu_launches": None, "roofline": None, "cpu_baseline": None,
+            "proposer_harness_ms": round(shares.get("nao_inject_drift", 0.0), 3),
+            "gpu_launches": n_launch, "roofline": roof, "cpu_baseline": None,
             "clocks": clocks.summary()}
     if args.config == "mlp" and world == 1 and not args.no_cpu:
         res = cpu_mlp_reference(5)

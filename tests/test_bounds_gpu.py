@@ -291,6 +291,23 @@ def test_softmax_many_long_rows(B, shape, f64):
         assert np.all(e <= e_ref * (1 + RTOL) + np.spacing(e_ref.astype(np.float32)) * 2)
 
 
+@pytest.mark.parametrize("shape", [(4096, 2048), (2048, 4096), (300, 100), (8, 30000)])
+def test_softmax_exp_wide_range(B, shape):
+    """z = x - max spread uniformly over [-90, 0] (FP32-normal and FP32-subnormal
+    e values, exp(-inf) = 0): probabilities bit-exact against the oracle
+    (numpy's FP64 exp rounded to FP32) on every row kernel (design G rows,
+    long rows, short-row batches), bound within [ref, ref(1+1e-5)]."""
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    x = -rng.uniform(0.0, 90.0, shape).astype(np.float32)
+    x[:, 0] = 0.0
+    x[1, 1:9] = -np.inf
+    y_ref, e_ref = OB.softmax_bound_parts(x, -1, OB.FpModel())
+    y, e = B.softmax_device(torch.from_numpy(x).cuda(), -1, B.FpModel(), eps_f64=True)
+    assert np.array_equal(y.cpu().numpy().view(np.uint32), y_ref.view(np.uint32))
+    e, ok = e.cpu().numpy(), ~np.isnan(e_ref)
+    assert_bound(e[ok], e_ref[ok], "softmax wide z")
+
+
 @pytest.mark.parametrize("path", TC_PATHS)
 @pytest.mark.parametrize("K", [1, 64, 128, 256])
 def test_abs_gemm_tc_short_k_persistent(B, K, path):
