@@ -1365,7 +1365,11 @@ static int softmax_c(const float* x, float* y, void* eps, int eps_f64, int64_t r
         const int b = e ? atoi(e) : kSmgBudget;
         return b > 0 && b <= kSmgBudget ? b : kSmgBudget;
     }();
-    if (vec && design == 1 && row_bytes <= budget && n < (1 << 30)) {
+    // G stages whole rows in shared memory: below 8 rows per CTA (n > ~2200)
+    // too few sequential folds overlap per SM and design C (e through L2, a
+    // fold thread for every row) is faster (SD-UNet n = 4096 rows: 40.7 vs
+    // 44.8 ms per step)
+    if (vec && design == 1 && 8 * row_bytes <= budget && n < (1 << 30)) {
         int R = (int)(budget / row_bytes);
         if (R > 32) R = 32;
         if (R > 8) R &= ~7;
