@@ -305,20 +305,36 @@ __device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc
         }
     }
     __syncwarp();
-    for (int r = 0; r < 32; r++) {
-        const int64_t m = m0 + quarter * 32 + r;
-        if (m >= g.M) break;
+    // rows in groups of 8: the 16 y loads of a group are issued before any eps
+    // store (C may alias Y as far as the compiler knows, so a row-by-row loop
+    // paid one L2 round trip per row -- ~10 us per tile, the largest part of
+    // the per-tile fixed cost)
+    const int64_t rows_left = g.M - (m0 + quarter * 32);
+    for (int r0 = 0; r0 < 32 && r0 < rows_left; r0 += 8) {
+        float yv[8][2];
 #pragma unroll
-        for (int j = 0; j < 2; j++) {
-            const int64_t n = n0 + half * 64 + 32 * j + lane;
-            if (n < g.N) {
-                double e = stg[r * 65 + 32 * j + lane];
-                const int64_t o = (int64_t)bz * g.sC + m * g.ldc + n;
-                if (g.Y) e = __dadd_rn(e, __dmul_rn(g.u, fabs((double)__ldg(g.Y + o))));
-                if (g.out_f64) static_cast<double*>(g.C)[o] = e;
-                else static_cast<float*>(g.C)[o] = __double2float_ru(e);
+        for (int k = 0; k < 8; k++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                const int64_t m = m0 + quarter * 32 + r0 + k;
+                const int64_t n = n0 + half * 64 + 32 * j + lane;
+                yv[k][j] = (g.Y && r0 + k < rows_left && n < g.N)
+                               ? __ldg(g.Y + (int64_t)bz * g.sC + m * g.ldc + n) : 0.0f;
             }
-        }
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                const int64_t m = m0 + quarter * 32 + r0 + k;
+                const int64_t n = n0 + half * 64 + 32 * j + lane;
+                if (r0 + k < rows_left && n < g.N) {
+                    double e = stg[(r0 + k) * 65 + 32 * j + lane];
+                    const int64_t o = (int64_t)bz * g.sC + m * g.ldc + n;
+                    if (g.Y) e = __dadd_rn(e, __dmul_rn(g.u, fabs((double)yv[k][j])));
+                    if (g.out_f64) static_cast<double*>(g.C)[o] = e;
+                    else static_cast<float*>(g.C)[o] = __double2float_ru(e);
+                }
+            }
     }
 }
 
@@ -677,16 +693,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float* crow = static_cast<float*>(g.C) + (int64_t)bz * g.sC + mq * g.ldc + nb;
             const float* yrow = g.Y ? g.Y + (int64_t)bz * g.sC + mq * g.ldc + nb : nullptr;
             const bool ok0 = nb < g.N, ok1 = nb + 32 < g.N;
-            for (int rr = 0; rr < rows; rr++) {
-                float e0 = stg[rr * 65 + lane], e1 = stg[rr * 65 + 32 + lane];
-                if (yrow) {
-                    if (ok0) e0 = __fmaf_ru(g.uf, fabsf(__ldg(yrow)), e0);
-                    if (ok1) e1 = __fmaf_ru(g.uf, fabsf(__ldg(yrow + 32)), e1);
-                    yrow += g.ldc;
+            for (int r0 = 0; r0 < rows; r0 += 8) {  // y loads of 8 rows before the stores
+                float y0[8], y1[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const bool in = yrow && r0 + k < rows;
+                    y0[k] = in && ok0 ? __ldg(yrow + (int64_t)(r0 + k) * g.ldc) : 0.0f;
+                    y1[k] = in && ok1 ? __ldg(yrow + (int64_t)(r0 + k) * g.ldc + 32) : 0.0f;
                 }
-                if (ok0) crow[0] = e0;
-                if (ok1) crow[32] = e1;
-                crow += g.ldc;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    if (r0 + k >= rows) break;
+                    float e0 = stg[(r0 + k) * 65 + lane], e1 = stg[(r0 + k) * 65 + 32 + lane];
+                    if (yrow) {
+                        e0 = __fmaf_ru(g.uf, fabsf(y0[k]), e0);
+                        e1 = __fmaf_ru(g.uf, fabsf(y1[k]), e1);
+                    }
+                    if (ok0) crow[(int64_t)(r0 + k) * g.ldc] = e0;
+                    if (ok1) crow[(int64_t)(r0 + k) * g.ldc + 32] = e1;
+                }
             }
             __syncwarp();
         }
