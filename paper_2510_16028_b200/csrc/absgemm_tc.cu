@@ -415,6 +415,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        const uint64_t desc0 = make_desc(smem_u32(smem));
         const uint32_t acc1 = tmem + 2 * BN;
         for (int kb = 0; kb < nkb; kb++) {
             const int s = kb % STAGES;
@@ -428,15 +429,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&full[s], ph);
 #endif
             fence_after();
-            const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+            // descriptor of this stage's first operand tile: the start-address field
+            // is (addr >> 4) in the low 14 bits, so offsets within the ring are adds
+            const uint64_t dst = desc0 + (uint64_t)((s * STAGE_BYTES) >> 4);
             const uint32_t acc0 = tmem + buf * BN;
             if (elect_one()) {
 #pragma unroll
                 for (int j = 0; j < BK / 8; j++) {
-                    const uint64_t ahi = make_desc(st + j * 32);
-                    const uint64_t alo = make_desc(st + TILE_BYTES + j * 32);
-                    const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
-                    const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
+                    const uint64_t ahi = dst + (uint64_t)((j * 32) >> 4);
+                    const uint64_t alo = dst + (uint64_t)((TILE_BYTES + j * 32) >> 4);
+                    const uint64_t bhi = dst + (uint64_t)((2 * TILE_BYTES + j * 32) >> 4);
+                    const uint64_t blo = dst + (uint64_t)((3 * TILE_BYTES + j * 32) >> 4);
                     umma_fmt<FMT>(acc0, ahi, bhi, (first && j == 0) ? 0u : 1u);
                     umma_fmt<FMT>(acc1, ahi, blo, (kb == 0 && j == 0) ? 0u : 1u);
                     umma_fmt<FMT>(acc1, alo, bhi, 1u);
@@ -586,6 +589,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        const uint64_t desc0 = make_desc(smem_u32(smem));
         int kg = 0, i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, i++) {
             const int slot = i & 1;
@@ -597,14 +601,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t ph = (kg / shortk::STAGES) & 1;
                 mbar_wait(&full[s], ph);
                 fence_after();
-                const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+                const uint64_t dst = desc0 + (uint64_t)((s * STAGE_BYTES) >> 4);
                 if (elect_one()) {
 #pragma unroll
                     for (int j = 0; j < BK / 8; j++) {
-                        const uint64_t ahi = make_desc(st + j * 32);
-                        const uint64_t alo = make_desc(st + TILE_BYTES + j * 32);
-                        const uint64_t bhi = make_desc(st + 2 * TILE_BYTES + j * 32);
-                        const uint64_t blo = make_desc(st + 3 * TILE_BYTES + j * 32);
+                        const uint64_t ahi = dst + (uint64_t)((j * 32) >> 4);
+                        const uint64_t alo = dst + (uint64_t)((TILE_BYTES + j * 32) >> 4);
+                        const uint64_t bhi = dst + (uint64_t)((2 * TILE_BYTES + j * 32) >> 4);
+                        const uint64_t blo = dst + (uint64_t)((3 * TILE_BYTES + j * 32) >> 4);
                         const uint32_t first = (kb == 0 && j == 0) ? 0u : 1u;
                         umma_fmt<FMT>(acc0, ahi, bhi, first);
                         umma_fmt<FMT>(acc1, ahi, blo, first);
