@@ -174,6 +174,13 @@ def main():
         x = torch.randn((S, I), device=dev)
         report("tf32_split", timeit(lambda: tf32_split(x, S, I, False, False), a.reps),
                12 * x.numel())
+        from paper_2510_16028_b200.bounds import f16_split
+        for shp in ((NH * S, S), (S, H), (S, I)):  # probs (ctx A operand), x, act
+            xs = torch.rand(shp, device=dev)
+            report(f"f16_split_{shp[0]}x{shp[1]}",
+                   timeit(lambda: f16_split(xs, shp[0], shp[1], False, False), a.reps),
+                   8 * xs.numel())
+            del xs
     for path, tag in ((1, "gemm_tc"), (2, "gemm_tc16"), (0, "gemm_ffma")):
         if want(tag):
             shapes = [(S, H, H), (S, H, I), (S, I, H)]
