@@ -338,8 +338,21 @@ __device__ __forceinline__ void tile_epilogue(const TcArgs& g, const EpiAcc& acc
     }
 }
 
+// NAO_TC_REGSPLIT: launched with 128 registers per thread (49152 per CTA) so a
+// commit CTA (128 threads x 128 registers) fits beside it on the SM; the
+// producer / MMA / TMEM-alloc warps give registers back (setmaxnreg.dec 48),
+// the 8 epilogue warps take 168 (the FP64 running sums of their 64 columns).
+#ifndef NAO_TC_REGSPLIT
+#define NAO_TC_REGSPLIT 0
+#endif
+#if NAO_TC_REGSPLIT
+#define NAO_TC_KERNEL_BOUNDS __maxnreg__(128)
+#else
+#define NAO_TC_KERNEL_BOUNDS __launch_bounds__(NUM_THREADS, 1)
+#endif
+
 template <int FMT>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void NAO_TC_KERNEL_BOUNDS
     k_absgemm_tc(const __grid_constant__ CUtensorMap map_ahi,
                  const __grid_constant__ CUtensorMap map_alo,
                  const __grid_constant__ CUtensorMap map_bhi,
@@ -395,8 +408,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     const int nkb = g.nkb;
     constexpr int KBE = FmtK<FMT>::kb;  // k elements per stage
+#if NAO_TC_REGSPLIT
+#define NAO_REG_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 48;")
+#define NAO_REG_INC() asm volatile("setmaxnreg.inc.sync.aligned.u32 168;")
+#else
+#define NAO_REG_DEC()
+#define NAO_REG_INC()
+#endif
 
     if (warp == 0) {
+        NAO_REG_DEC();
         if (lane == 0) {  // ---------------- TMA producer
             const int za = g.a_batched ? bz : 0, zb = g.b_batched ? bz : 0;
             for (int kb = 0; kb < nkb; kb++) {
@@ -415,6 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        NAO_REG_DEC();
         const uint64_t desc0 = make_desc(smem_u32(smem));
         const uint32_t acc1 = tmem + 2 * BN;
         for (int kb = 0; kb < nkb; kb++) {
@@ -452,6 +474,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (elect_one()) umma_commit(acc1_full);
         __syncwarp();
     } else if (warp >= 4) {  // ---------------- epilogue
+        NAO_REG_INC();
         const int ew = warp - 4, quarter = warp & 3, half = ew >> 2;
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
         EpiAcc acc;
@@ -481,6 +504,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t col1 = tmem + lane_addr + 2 * BN + half * 64;
         double* stg = reinterpret_cast<double*>(smem) + ew * (32 * 65);
         tile_epilogue<FMT>(g, acc, col1, stg, lane, quarter, half, m0, n0, bz);
+    } else {  // warps 2, 3 (TMEM allocator, spare)
+        NAO_REG_DEC();
     }
     fence_before();
     __syncthreads();
@@ -1463,6 +1488,10 @@ static int launch_tc(const void* a_hi, const void* a_lo, const int32_t* a_exp, c
         NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc<FMT>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             SMEM_BYTES));
+#if NAO_TC_REGSPLIT  // the full carveout: room for a commit CTA beside the ring
+        NAO_CHECK_CUDA(cudaFuncSetAttribute(k_absgemm_tc<FMT>,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+#endif
         attr_set = true;
     }
     dim3 grid((unsigned)(ceil_div(N, BN) * ceil_div(M, BM)), 1, (unsigned)batch);

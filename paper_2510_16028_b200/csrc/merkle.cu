@@ -964,6 +964,18 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
         const uint32_t mgroups = hash_alg == kKECCAK256 ? ct.chunk_words / MaskGeom<kKECCAK256>::BW + 1
                                                         : (ct.chunk_words + 63) / 64;
         const size_t dsm = (size_t)mgroups * kLeafThreads * 8;
+        static const int carve = [] {  // experiment knob: shared-memory carveout (%)
+            const char* e = getenv("NAO_COMMIT_CARVEOUT");
+            return e ? atoi(e) : -1;
+        }();
+        static bool carve_set = false;
+        if (carve >= 0 && !carve_set) {
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kSHA256>,
+                                                cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kKECCAK256>,
+                                                cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            carve_set = true;
+        }
         if (hash_alg == kSHA256) {
             NAO_CHECK_CUDA(cudaFuncSetAttribute(k_chunk_leaves_check<kSHA256>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));

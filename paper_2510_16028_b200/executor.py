@@ -40,6 +40,7 @@ from .dispute import new_result_buffer
 from .engine import NATIVE, ExecutionError, _batch_view, fma_of, to_device
 from .graph import parse_ref
 
+_EXP_SKIP_COMMIT = os.environ.get("NAO_EXP_SKIP_COMMIT") == "1"
 INF_TAU = np.full(len(PERCENTILE_GRID), np.inf)
 
 
@@ -437,6 +438,11 @@ class StreamingVerifier:
             if self.overlap:
                 s_com.wait_stream(main)
             with torch.cuda.stream(s_com):
+                if _EXP_SKIP_COMMIT:  # timing experiment only: main-stream work alone
+                    st.pending, st.pend_idx, st.pend_bytes = [], [], 0
+                    st.pend_checks, st.pend_keep, st.pend_refine = [], [], []
+                    st.pend_reuse, st.pend_pos = [], {}
+                    return
                 r = commit_tensors(st.pending, self.chunk, self.alg,
                                    checks=st.pend_checks if self.fuse_check else None,
                                    reuse=st.pend_reuse if self.fuse_check else None)

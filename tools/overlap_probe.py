@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--gb", type=float, default=8.0)
     ap.add_argument("--gemms", type=int, default=24)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--gemm", choices=["sgemm", "absgemm"], default="sgemm",
+                    help="main-stream chain: cuBLAS FP32 GEMMs or the FP16-split abs-GEMM bound")
     args = ap.parse_args()
     from paper_2510_16028_b200 import _lib
     from paper_2510_16028_b200.commitments import commit_tensors
@@ -46,9 +48,16 @@ def main():
                              2.0 ** -23, 1.0, _lib.EPS_SCALED_LOCAL, 0, None, 0)
               for i in range(n_t)]
 
+    if args.gemm == "absgemm":
+        from paper_2510_16028_b200.bounds import abs_gemm_bound
+        abs_gemm_bound(x, w, 1e-6, eps_f64=False, path=_lib.GEMM_TC_F16X3, cache_b=True)
+
     def gemms():
         for i in range(args.gemms):
-            torch.matmul(x, w, out=outs[i & 1])
+            if args.gemm == "absgemm":
+                abs_gemm_bound(x, w, 1e-6, eps_f64=False, path=_lib.GEMM_TC_F16X3, cache_b=True)
+            else:
+                torch.matmul(x, w, out=outs[i & 1])
 
     def commit():
         for lo in range(0, n_t, 16):
@@ -89,6 +98,8 @@ def main():
                           "commit_GBps": round(n_t * 64 / 1024 / (b / 1e3), 1),
                           "gemm_TFLOPs": round(args.gemms * 2 * 2048 * 4096 * 12288 / a / 1e9, 1)}
     res["ctas"] = os.environ.get("NAO_COMMIT_CTAS", "default")
+    res["gemm"] = args.gemm
+    res["lib"] = os.environ.get("NAO_LIB_PATH", "default")
     print(json.dumps(res))
 
 
