@@ -187,10 +187,24 @@ typedef struct nao_check_partial {
  * function of the bytes only; the header leaf and the tree are still built).
  * Chunks that differ are hashed.  src = -1: no reuse.  Needs the fused check
  * (checks[i].local).  Sources are processed in an earlier launch. */
+/* mode NAO_REUSE_SAME_OFFSET: an elementwise node whose claimed chunk c is
+ * byte-identical to the source's claimed chunk c (e.g. the lower triangle of
+ * a causal-mask add, x + 0 = x) copies that digest; the equality is verified
+ * word by word on the claimed bytes (block_chunks / repeats unused; same
+ * payload size as the source).  Independently of src, every full chunk of a
+ * checked tensor whose claimed words are all zero (e.g. the masked half of
+ * causal softmax rows) takes the digest of the all-zero chunk (Keccak-256).
+ * row_chunks (0 = none): chunks per row of the tensor's last axis, a divisor
+ * of 128 -- threads of a commit CTA take chunk j of consecutive rows, so
+ * warps meet the same kind of chunk and a warp whose chunks all take a
+ * shortcut leaves the sponge pipe to the other warps. */
+enum nao_reuse_mode { NAO_REUSE_LOCAL_COPY = 0, NAO_REUSE_SAME_OFFSET = 1 };
 typedef struct nao_chunk_reuse {
     int64_t src;
     uint64_t block_chunks;
     uint64_t repeats;
+    int32_t mode;
+    uint32_t row_chunks;
 } nao_chunk_reuse;
 size_t nao_commit_check_accum_bytes(void);
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,

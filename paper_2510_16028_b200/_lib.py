@@ -68,7 +68,11 @@ class CheckDesc(ctypes.Structure):
 class ChunkReuse(ctypes.Structure):
     """nao_chunk_reuse: a data-movement node's chunk digests copied from its source."""
     _fields_ = [("src", ctypes.c_int64), ("block_chunks", ctypes.c_uint64),
-                ("repeats", ctypes.c_uint64)]
+                ("repeats", ctypes.c_uint64), ("mode", ctypes.c_int32),
+                ("row_chunks", ctypes.c_uint32)]
+
+
+REUSE_LOCAL_COPY, REUSE_SAME_OFFSET = 0, 1
 
 
 REFINE_GEMM, REFINE_CONV, REFINE_UNARY = 0, 1, 2

@@ -285,8 +285,10 @@ def commit_tensors(tensors, chunk_bytes: int = DEFAULT_CHUNK_BYTES, alg=SHA256,
     checks: optional list of _lib.CheckDesc (or None entries), one per tensor:
     the acceptance check of tensor i against checks[i].local runs inside the
     same hashing pass (nao_commit_check_tensors).  reuse: optional list of
-    (src, block_chunks, repeats) or None per tensor (nao_chunk_reuse: chunk
-    digests of data-movement nodes copied from their source; roots unchanged)."""
+    (src, block_chunks, repeats[, mode[, row_chunks]]) or None per tensor
+    (nao_chunk_reuse: chunk digests of data-movement nodes -- or, mode
+    REUSE_SAME_OFFSET, of elementwise nodes whose claimed chunk equals the
+    source's -- copied from their source; roots unchanged)."""
     tensors = [_as_payload(t) for t in tensors]
     n = len(tensors)
     if n == 0:

@@ -16,6 +16,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <array>
+#include <map>
+#include <mutex>
 #include "common.cuh"
 #include "check_common.cuh"
 #include "unary.cuh"
@@ -130,6 +133,10 @@ struct CCTable {
     uint64_t reuse_out[kMaxSegs];    // digest index of the source's chunk 0, or ~0 (none)
     uint64_t reuse_block[kMaxSegs];  // chunks per source block
     uint64_t reuse_span[kMaxSegs];   // block_chunks * repeats
+    const uint32_t* reuse_src[kMaxSegs];  // same-offset mode: the source's claimed payload
+    uint32_t row_chunks[kMaxSegs];   // chunk -> thread mapping (0: identity)
+    uint32_t zero_digest[8];         // H(0x00 || zeros(chunk)), valid if zero_ok
+    int zero_ok;
 };
 
 constexpr int kLeafWarps = kLeafThreads / 32;
@@ -345,8 +352,26 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
     // entry always exists), SHA-256 one per 64 words
     const uint32_t groups = ALG == kKECCAK256 ? cw / BW + 1 : (cw + 63) >> 6;
     const uint64_t nchunks = (total_w + cw - 1) / cw;
-    const uint64_t c0 = (vb - tab.block_prefix[s]) * kLeafThreads;
-    const uint64_t c = c0 + threadIdx.x;
+    // chunk of this thread.  Rows of rc > 1 whole chunks: virtual block vl
+    // takes chunk position vl % rc of 128 consecutive rows, so one CTA meets
+    // one kind of chunk (e.g. the all-zero right halves of causal softmax
+    // rows) and a CTA whose chunks all take a digest shortcut ends early.
+    const uint64_t vl = vb - tab.block_prefix[s];
+    const uint32_t rc = tab.row_chunks[s];
+    uint64_t c, cta_words;
+    bool active;
+    if (rc > 1) {
+        const uint64_t nrows = nchunks / rc, r0 = (vl / rc) * kLeafThreads;
+        c = (r0 + threadIdx.x) * rc + vl % rc;
+        active = r0 + threadIdx.x < nrows;
+        cta_words = (nrows - r0 < (uint64_t)kLeafThreads ? nrows - r0 : (uint64_t)kLeafThreads) * cw;
+    } else {
+        const uint64_t c0 = vl * kLeafThreads;
+        c = c0 + threadIdx.x;
+        active = c < nchunks;
+        const uint64_t c1 = c0 + kLeafThreads < nchunks ? c0 + kLeafThreads : nchunks;
+        cta_words = (c1 * cw < total_w ? c1 * cw : total_w) - c0 * cw;
+    }
     int G = 0;
     double epsilon = 0.0;
     if (check) {
@@ -382,37 +407,118 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
         for (uint32_t g = 0; g < groups; g++) s_mask[g * kLeafThreads + threadIdx.x] = 0ull;
         __syncthreads();
     }
-    if (c < nchunks) {
-        const uint64_t off_w = c * cw;
-        const uint32_t nw = (uint32_t)(total_w - off_w < cw ? total_w - off_w : cw);
-        uint32_t dg[8];
-        bool reused = false;
-        if (check && tab.reuse_out[s] != ~0ull) {
-            // data-movement node: claimed chunk == local chunk (word for word,
-            // finite) means the source's chunk digest is this chunk's digest
-            const uint32_t* cp = tab.payload[s] + off_w;
-            const uint32_t* lp = reinterpret_cast<const uint32_t*>(d.local) + off_w;
-            bool eq = true;
-            uint32_t i = 0;
-            for (; i + 4 <= nw; i += 4) {
-                const uint4 a = __ldg(reinterpret_cast<const uint4*>(cp + i));
-                const uint4 b = __ldg(reinterpret_cast<const uint4*>(lp + i));
-                eq &= !(word_needs_check(a.x, b.x) | word_needs_check(a.y, b.y) |
-                        word_needs_check(a.z, b.z) | word_needs_check(a.w, b.w));
-            }
-            for (; i < nw; i++) eq &= !word_needs_check(__ldg(cp + i), __ldg(lp + i));
-            if (eq) {
-                const uint64_t span = tab.reuse_span[s], blk = tab.reuse_block[s];
-                const uint64_t sc = (c / span) * blk + c % blk;
-                const uint4* src = reinterpret_cast<const uint4*>(digests + 8 * (tab.reuse_out[s] + sc));
-                uint4* dst = reinterpret_cast<uint4*>(digests + 8 * (tab.out_index[s] + c));
-                dst[0] = src[0];
-                dst[1] = src[1];
-                reused = true;
-            }
+    const uint64_t off_w = c * cw;
+    const uint32_t nw = active ? (uint32_t)(total_w - off_w < cw ? total_w - off_w : cw) : 0u;
+    bool reused = false;
+    if (active && check && tab.reuse_out[s] != ~0ull && tab.reuse_src[s] == nullptr) {
+        // data-movement node: claimed chunk == local chunk (word for word,
+        // finite) means the source's chunk digest is this chunk's digest
+        const uint32_t* cp = tab.payload[s] + off_w;
+        const uint32_t* lp = reinterpret_cast<const uint32_t*>(d.local) + off_w;
+        bool eq = true;
+        uint32_t i = 0;
+        for (; i + 4 <= nw; i += 4) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(cp + i));
+            const uint4 b = __ldg(reinterpret_cast<const uint4*>(lp + i));
+            eq &= !(word_needs_check(a.x, b.x) | word_needs_check(a.y, b.y) |
+                    word_needs_check(a.z, b.z) | word_needs_check(a.w, b.w));
         }
-        if (reused) {
-        } else if (check) {
+        for (; i < nw; i++) eq &= !word_needs_check(__ldg(cp + i), __ldg(lp + i));
+        if (eq) {
+            const uint64_t span = tab.reuse_span[s], blk = tab.reuse_block[s];
+            const uint64_t sc = (c / span) * blk + c % blk;
+            const uint4* src = reinterpret_cast<const uint4*>(digests + 8 * (tab.reuse_out[s] + sc));
+            uint4* dst = reinterpret_cast<uint4*>(digests + 8 * (tab.out_index[s] + c));
+            dst[0] = src[0];
+            dst[1] = src[1];
+            reused = true;
+        }
+    }
+    if (ALG == kKECCAK256 && check && (tab.reuse_src[s] != nullptr || tab.zero_ok) &&
+        (cw & 3u) == 0u) {
+        // digest shortcut: an all-zero claimed chunk, or (same-offset mode) one
+        // equal to the source's claimed chunk.  Each lane probes its chunk's
+        // first and last 16 bytes; the warp then scans every candidate chunk
+        // together (coalesced 16-byte loads of claimed, local and reference),
+        // setting the owner's check flags at the sponge-block bit positions the
+        // hash pass would use.  Candidates that turn out to differ are hashed.
+        const uint32_t* rbase = tab.reuse_src[s];
+        bool cand = false;
+        if (active && !reused && nw == cw) {
+            const uint32_t* cp = tab.payload[s] + off_w;
+            const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(cp));
+            const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(cp + cw - 4));
+            uint4 b0 = make_uint4(0u, 0u, 0u, 0u), b1 = b0;
+            if (rbase) {
+                b0 = __ldg(reinterpret_cast<const uint4*>(rbase + off_w));
+                b1 = __ldg(reinterpret_cast<const uint4*>(rbase + off_w + cw - 4));
+            }
+            cand = ((a0.x ^ b0.x) | (a0.y ^ b0.y) | (a0.z ^ b0.z) | (a0.w ^ b0.w) |
+                    (a1.x ^ b1.x) | (a1.y ^ b1.y) | (a1.z ^ b1.z) | (a1.w ^ b1.w)) == 0u;
+        }
+        unsigned cm = __ballot_sync(0xffffffffu, cand);
+        while (cm) {
+            const int j = __ffs(cm) - 1;
+            cm &= cm - 1u;
+            const uint64_t joff = __shfl_sync(0xffffffffu, off_w, j);
+            const uint4* cj = reinterpret_cast<const uint4*>(tab.payload[s] + joff);
+            const uint4* lj = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(d.local) + joff);
+            const uint4* rj = rbase ? reinterpret_cast<const uint4*>(rbase + joff) : nullptr;
+            unsigned long long* mj = s_mask + (threadIdx.x & ~31u) + j;
+            uint32_t diff = 0u;
+            const uint32_t nq = cw / 4;
+            for (uint32_t q0 = lane; q0 < nq; q0 += 128) {  // 4 x 3 loads in flight per lane
+                uint4 a[4], y[4], r[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t q = q0 + 32 * u;
+                    a[u] = y[u] = r[u] = make_uint4(0u, 0u, 0u, 0u);
+                    if (q < nq) {
+                        a[u] = __ldg(cj + q);
+                        y[u] = __ldg(lj + q);
+                        if (rj) r[u] = __ldg(rj + q);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t q = q0 + 32 * u;
+                    diff |= (a[u].x ^ r[u].x) | (a[u].y ^ r[u].y) | (a[u].z ^ r[u].z) | (a[u].w ^ r[u].w);
+                    const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+                    const uint32_t yv[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if (q < nq && word_needs_check_f(av[e], yv[e])) {
+                            const uint32_t w = 4 * q + e;
+                            atomicOr(mj + (w / MaskGeom<ALG>::BW) * kLeafThreads,
+                                     1ull << (w % MaskGeom<ALG>::BW));
+                        }
+                }
+            }
+            const bool same = __all_sync(0xffffffffu, diff == 0u);
+            if (lane == j) {
+                if (same) {
+                    uint4* dst = reinterpret_cast<uint4*>(digests + 8 * (tab.out_index[s] + c));
+                    if (rbase) {
+                        const uint4* src = reinterpret_cast<const uint4*>(digests + 8 * (tab.reuse_out[s] + c));
+                        dst[0] = src[0];
+                        dst[1] = src[1];
+                    } else {
+                        dst[0] = make_uint4(tab.zero_digest[0], tab.zero_digest[1],
+                                            tab.zero_digest[2], tab.zero_digest[3]);
+                        dst[1] = make_uint4(tab.zero_digest[4], tab.zero_digest[5],
+                                            tab.zero_digest[6], tab.zero_digest[7]);
+                    }
+                    reused = true;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (active && !reused) {
+        uint32_t dg[8];
+        if (check) {
+            // (re)writes every mask entry of this chunk: stale bits of a failed
+            // shortcut scan are overwritten
             CheckedWords<ALG> ld{tab.payload[s] + off_w,
                                  reinterpret_cast<const uint32_t*>(d.local) + off_w,
                                  s_mask + threadIdx.x};
@@ -422,7 +528,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             GlobalWords ld{tab.payload[s] + off_w};
             hash_tagged_words<ALG>(ld, nw, 0u, dg);
         }
-        if (!reused) store_digest(digests + 8 * (tab.out_index[s] + c), dg);
+        store_digest(digests + 8 * (tab.out_index[s] + c), dg);
     }
     if (!check) return;
     __syncwarp();
@@ -492,9 +598,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             hr += sm.wc[ww][1][threadIdx.x];
         }
         if (threadIdx.x == 0) {  // equal words: bucket 0 of both arrays
-            const uint64_t c1 = c0 + kLeafThreads < nchunks ? c0 + kLeafThreads : nchunks;
-            const uint64_t w1 = c1 * cw < total_w ? c1 * cw : total_w;
-            const unsigned long long eq = (w1 - c0 * cw) - sm.nslow;
+            const unsigned long long eq = cta_words - sm.nslow;
             ha += eq;
             hr += eq;
         }
@@ -505,9 +609,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             unsigned long long mx0 = sm.bmax[0][b], mn0 = sm.bmin_inv[0][b];
             unsigned long long mx1 = sm.bmax[1][b], mn1 = sm.bmin_inv[1][b];
             if (b == 0) {  // the equal words: key 0 in bucket 0 of both arrays
-                const uint64_t c1 = c0 + kLeafThreads < nchunks ? c0 + kLeafThreads : nchunks;
-                const uint64_t w1 = c1 * cw < total_w ? c1 * cw : total_w;
-                if ((w1 - c0 * cw) > sm.nslow) { mn0 = ~0ull; mn1 = ~0ull; }
+                if (cta_words > sm.nslow) { mn0 = ~0ull; mn1 = ~0ull; }
             }
             if (mx0) atomicMax(&acc->bmax[0][b], mx0);
             if (mn0) atomicMax(&acc->bmin_inv[0][b], mn0);
@@ -693,6 +795,56 @@ __global__ void __launch_bounds__(128) k_tree_level(const __grid_constant__ Tree
 
 // ----------------------------------------------------------------- host side
 
+struct ZeroWords {  // an all-zero payload for the sponge
+    __device__ __forceinline__ uint2 v2c(uint32_t, int) const { return make_uint2(0u, 0u); }
+    __device__ __forceinline__ uint32_t wc(uint32_t, int) const { return 0u; }
+    __device__ __forceinline__ void block_end(uint32_t) const {}
+    __device__ __forceinline__ uint4 v4(uint32_t) const { return make_uint4(0u, 0u, 0u, 0u); }
+    __device__ __forceinline__ uint2 v2(uint32_t) const { return make_uint2(0u, 0u); }
+    __device__ __forceinline__ uint32_t w(uint32_t) const { return 0u; }
+};
+
+__global__ void k_zero_chunk_digest(uint32_t cw, uint32_t* out) {
+    uint32_t d[8];
+    hash_tagged_words<kKECCAK256>(ZeroWords{}, cw, 0u, d);
+    for (int i = 0; i < 8; i++) out[i] = d[i];
+}
+
+// H(0x00 || zeros(4 cw)) with Keccak-256, cached per chunk size.  Computed on
+// the device the first time a size is seen on a stream that is not capturing
+// (the eager warm-up run); during a capture an uncached size disables the
+// shortcut for that call (*ok = 0).
+static int zero_chunk_digest(uint32_t cw, uint32_t out[8], int* ok, cudaStream_t st) {
+    static std::mutex mu;
+    static std::map<uint32_t, std::array<uint32_t, 8>> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(cw);
+        if (it != cache.end()) {
+            memcpy(out, it->second.data(), 32);
+            *ok = 1;
+            return NAO_OK;
+        }
+    }
+    *ok = 0;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    NAO_CHECK_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return NAO_OK;
+    uint32_t* dev = nullptr;
+    NAO_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dev), 32, st));
+    k_zero_chunk_digest<<<1, 1, 0, st>>>(cw, dev);
+    NAO_CHECK_LAUNCH();
+    std::array<uint32_t, 8> h{};
+    NAO_CHECK_CUDA(cudaMemcpyAsync(h.data(), dev, 32, cudaMemcpyDeviceToHost, st));
+    NAO_CHECK_CUDA(cudaFreeAsync(dev, st));
+    NAO_CHECK_CUDA(cudaStreamSynchronize(st));
+    std::lock_guard<std::mutex> lk(mu);
+    cache[cw] = h;
+    memcpy(out, h.data(), 32);
+    *ok = 1;
+    return NAO_OK;
+}
+
 static int launch_chunk_leaves(int alg, ChunkTable& tab, uint32_t* digests, cudaStream_t st) {
     uint64_t total = tab.chunk_prefix[tab.n];
     if (total == 0) return NAO_OK;
@@ -861,12 +1013,24 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
     int n_phases = 1;
     for (int64_t i = 0; reuse && i < n_tensors; i++) {
         const nao_chunk_reuse& r = reuse[i];
+        NAO_REQUIRE(r.row_chunks <= 1 || (r.row_chunks <= (uint32_t)kLeafThreads &&
+                                           kLeafThreads % r.row_chunks == 0),
+                    "reuse %lld: row_chunks must divide %d", (long long)i, kLeafThreads);
         if (r.src < 0 || payload_bytes[i] == 0) continue;
         NAO_REQUIRE(r.src < i, "reuse %lld: source %lld must come earlier", (long long)i,
                     (long long)r.src);
         NAO_REQUIRE(checks && checks[i].local, "reuse %lld needs the fused check", (long long)i);
-        NAO_REQUIRE(r.repeats >= 1 && r.block_chunks >= 1, "reuse %lld: bad block", (long long)i);
+        NAO_REQUIRE(r.mode == NAO_REUSE_LOCAL_COPY || r.mode == NAO_REUSE_SAME_OFFSET,
+                    "reuse %lld: bad mode %d", (long long)i, r.mode);
         const uint64_t sb = payload_bytes[r.src];
+        if (r.mode == NAO_REUSE_SAME_OFFSET) {
+            NAO_REQUIRE(payload_bytes[i] == sb,
+                        "reuse %lld: same-offset reuse needs the source's size", (long long)i);
+            phase[i] = phase[r.src] + 1;
+            n_phases = std::max(n_phases, phase[i] + 1);
+            continue;
+        }
+        NAO_REQUIRE(r.repeats >= 1 && r.block_chunks >= 1, "reuse %lld: bad block", (long long)i);
         if (r.repeats == 1)
             NAO_REQUIRE(payload_bytes[i] == sb && r.block_chunks == seg_chunks(sb, chunk_bytes),
                         "reuse %lld: a reshape must have the source's bytes", (long long)i);
@@ -900,6 +1064,14 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
     for (int64_t i = 0; checks && i < n_tensors; i++) any_check |= checks[i].local != nullptr;
     NAO_REQUIRE(!any_check || chunk_bytes / 4 <= (uint64_t)kMaxFusedChunkWords,
                 "the fused check supports chunk_bytes <= %d", 4 * kMaxFusedChunkWords);
+    // digest of the all-zero chunk (Keccak-256 fused check only), computed once
+    // per chunk size on the device outside graph capture
+    uint32_t zero_digest[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int zero_ok = 0;
+    if (any_check && hash_alg == kKECCAK256) {
+        int rc = zero_chunk_digest((uint32_t)(chunk_bytes / 4), zero_digest, &zero_ok, st);
+        if (rc) return rc;
+    }
     std::vector<int64_t> order;  // tensors by phase, canonical order within a phase
     std::vector<int64_t> phase_end;
     for (int ph = 0; ph < n_phases; ph++) {
@@ -940,18 +1112,28 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
             ct.payload[cnt] = static_cast<const uint32_t*>(payloads[i]);
             ct.nbytes[cnt] = payload_bytes[i];
             ct.out_index[cnt] = in_index[i] + 1;
+            // row mapping only where rows are whole chunks (else identity)
+            uint32_t rcs = reuse && reuse[i].row_chunks > 1 ? reuse[i].row_chunks : 0u;
+            if (rcs && payload_bytes[i] % (rcs * chunk_bytes) != 0) rcs = 0u;
+            const int64_t nch = (int64_t)seg_chunks(payload_bytes[i], chunk_bytes);
             ct.block_prefix[cnt + 1] = ct.block_prefix[cnt] +
-                ceil_div((int64_t)seg_chunks(payload_bytes[i], chunk_bytes), kLeafThreads);
+                (rcs ? ceil_div(nch / (int64_t)rcs, kLeafThreads) * rcs : ceil_div(nch, kLeafThreads));
             if (checks && payload_bytes[i] > 0) memcpy(&ct.chk[cnt], &checks[i], sizeof(CheckDesc));
             ct.reuse_out[cnt] = ~0ull;
+            ct.reuse_src[cnt] = nullptr;
+            ct.row_chunks[cnt] = rcs;
             if (phase[i] > 0) {
                 const nao_chunk_reuse& r = reuse[i];
                 ct.reuse_out[cnt] = in_index[r.src] + 1;
                 ct.reuse_block[cnt] = r.block_chunks;
                 ct.reuse_span[cnt] = r.block_chunks * r.repeats;
+                if (r.mode == NAO_REUSE_SAME_OFFSET)
+                    ct.reuse_src[cnt] = static_cast<const uint32_t*>(payloads[r.src]);
             }
         }
         ct.n = cnt;
+        ct.zero_ok = zero_ok;
+        memcpy(ct.zero_digest, zero_digest, sizeof zero_digest);
         b0 = b1;
         uint64_t blocks = ct.block_prefix[cnt];
         if (blocks == 0) continue;

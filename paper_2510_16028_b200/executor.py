@@ -195,6 +195,40 @@ def chunk_reuse(node, xs, pos_of, chunk: int):
     return None
 
 
+# x + c / x - c with c a weight: where c is 0 the claimed output can equal the
+# operand chunk for chunk (a causal-mask add keeps the scores' lower triangle)
+SAME_OFFSET_KINDS = frozenset({"add", "sub"})
+
+
+def row_chunks(y: torch.Tensor, chunk: int) -> int:
+    """Chunks per row of y's last axis when rows are whole chunks and their
+    count divides the commit CTA's 128 chunks, else 0 (nao_chunk_reuse.row_chunks)."""
+    if y.dim() < 2 or y.numel() == 0:
+        return 0
+    rb = int(y.shape[-1]) * 4
+    if rb % chunk:
+        return 0
+    rc = rb // chunk
+    return rc if 1 < rc <= 128 and 128 % rc == 0 else 0
+
+
+def chunk_plan(node, xs, y, pos_of, chunk: int):
+    """nao_chunk_reuse entry of a checked node's claimed tensor, or None:
+    data-movement reuse (chunk_reuse), same-offset reuse for an elementwise
+    node with one same-shaped claimed operand pending in the commit, and the
+    row-chunk thread mapping."""
+    rc = row_chunks(y, chunk)
+    r = chunk_reuse(node, xs, pos_of, chunk) if node.kind in ("reshape", "concat") else None
+    if r is not None:
+        return (r[0], r[1], r[2], _lib.REUSE_LOCAL_COPY, rc)
+    if node.kind in SAME_OFFSET_KINDS and len(node.inputs) == 2:
+        (c0, k0), (c1, _) = parse_ref(node.inputs[0]), parse_ref(node.inputs[1])
+        if (c0 == "node" and c1 == "weight" and k0 in pos_of and y.numel()
+                and tuple(xs[0].shape) == tuple(y.shape)):
+            return (pos_of[k0], -(-y.numel() * 4 // chunk), 1, _lib.REUSE_SAME_OFFSET, rc)
+    return (-1, 0, 0, _lib.REUSE_LOCAL_COPY, rc) if rc else None
+
+
 def run_refine(descs) -> None:
     """One nao_refine_borderline launch on the current stream."""
     if descs:
@@ -563,9 +597,8 @@ class StreamingVerifier:
                     stats.gemm_flops += 2 * y.numel() * xs[1][0].numel()
             del eps, y
             values[node.index] = yc
-            st.pend_reuse.append(chunk_reuse(node, xs, st.pend_pos, self.chunk)
-                                 if desc is not None and node.kind in ("reshape", "concat")
-                                 else None)
+            st.pend_reuse.append(chunk_plan(node, xs, yc, st.pend_pos, self.chunk)
+                                 if desc is not None else None)
             st.pend_pos[node.index] = len(st.pending)
             st.pending.append(yc)
             st.pend_checks.append(desc)

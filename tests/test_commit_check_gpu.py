@@ -272,3 +272,63 @@ def test_chunk_digest_reuse_keeps_roots(chunk):
             assert [x["n_violations"] for x in r] == [0, 1, 1]
         else:
             assert r[0]["n_violations"] == 1 and r[0]["n_nonfinite"] == 1
+
+
+@pytest.mark.parametrize("chunk,width", [(4096, 2048), (512, 512), (4096, 1024)])
+def test_digest_shortcuts_keep_roots_and_records(chunk, width):
+    """Digest shortcuts of the fused commit+check: all-zero claimed chunks take
+    the zero-chunk digest, a causal-mask add (x + mask) copies the digest of
+    the operand's equal chunks (REUSE_SAME_OFFSET), rows of several chunks
+    map one chunk position per warp (row_chunks) -- with claims equal to the
+    local tensors, with a drifted word inside a zero / reused chunk and with a
+    local word that is not zero under a zero claim: roots equal the plain
+    commit and the oracle's, records equal the unshortcut fused check."""
+    from paper_2510_16028_b200 import _lib
+    from paper_2510_16028_b200.commitments import commit_tensors
+    from paper_2510_16028_b200.dispute import CheckRecord
+    from paper_2510_16028_b200.executor import row_chunks
+    rng = np.random.default_rng(11)
+    H, S = 3, 192
+    spec = torch.frombuffer(bytearray(_lib.verdict_spec(GRID, INF, INF, 1e-12)),
+                            dtype=torch.uint8).cuda()
+    scaled = torch.from_numpy((rng.standard_normal((H, S, width)) * 3).astype(np.float32)).cuda()
+    cols = torch.arange(width, device="cuda")
+    rows = torch.arange(S, device="cuda") * (width // S + 1)
+    mask = torch.where(cols[None, :] > rows[:, None], -1e9, 0.0).float()  # causal-style
+    masked = scaled + mask
+    probs = torch.softmax(masked, dim=-1)
+    assert (probs == 0).any() and (masked == scaled).any()
+    rc = row_chunks(masked, chunk)
+    for mode in ("equal", "drift", "local"):
+        c_scaled, c_masked, c_probs = scaled.clone(), masked.clone(), probs.clone()
+        l_masked, l_probs = masked.clone(), probs.clone()
+        if mode == "drift":  # claimed words moved inside shortcut chunks
+            c_masked[0, S - 1, 3] += 1.0          # lower triangle: equals scaled elsewhere
+            c_probs[0, 0, width - 5] = 1e-3       # the zero upper triangle of row 0
+        elif mode == "local":  # local non-zero where the claim is zero
+            l_probs[1, 0, width - 9] = 2.0 ** -40
+        claims = [c_scaled, c_masked, c_probs]
+        locals_ = [scaled, l_masked, l_probs]
+
+        def run(reuse):
+            recs = torch.zeros((3, _lib.CHECK_RESULT_BYTES), dtype=torch.uint8, device="cuda")
+            checks = [_lib.CheckDesc(l.data_ptr(), None, spec.data_ptr(), recs[i].data_ptr(),
+                                     0.0, 1.0, _lib.EPS_ZERO, 0, None, 0)
+                      for i, l in enumerate(locals_)]
+            roots = commit_tensors(claims, chunk, "keccak256", checks=checks, reuse=reuse)
+            torch.cuda.synchronize()
+            return roots, [CheckRecord(recs[i]).host() for i in range(3)]
+
+        nch = -(-masked.numel() * 4 // chunk)
+        got, r_got = run([(-1, 0, 0, 0, rc), (0, nch, 1, _lib.REUSE_SAME_OFFSET, rc),
+                          (-1, 0, 0, 0, rc)])
+        ref, r_ref = run(None)
+        plain = commit_tensors(claims, chunk, "keccak256")
+        torch.cuda.synchronize()
+        assert torch.equal(got, plain) and torch.equal(ref, plain), mode
+        for i, t in enumerate(claims):
+            assert bytes(got[i].cpu().numpy()) == OM.tensor_root(t.cpu().numpy(), chunk,
+                                                                 OM.KECCAK256), (mode, i)
+        assert r_got == r_ref, mode
+        nv = [x["n_violations"] for x in r_got]
+        assert nv == {"equal": [0, 0, 0], "drift": [0, 1, 1], "local": [0, 0, 1]}[mode], (mode, nv)

@@ -85,3 +85,25 @@ def test_chunk_reuse_proposals():
     assert chunk_reuse(_N("concat", ["node:5"] * 2, {"axis": 1}), [y] * 2, pos, 4096) is None
     assert chunk_reuse(_N("concat", ["node:5", "node:6"], {"axis": 1}), [x, x], pos, 4096) is None
     assert chunk_reuse(_N("reshape", ["node:7"]), [x], pos, 4096) is None
+
+
+def test_chunk_plan_proposals():
+    """row_chunks only for rows of whole chunks dividing the CTA's 128; same-offset
+    reuse only for node +/- weight of the output's shape, pending in the commit."""
+    import torch
+    from paper_2510_16028_b200 import _lib
+    from paper_2510_16028_b200.executor import chunk_plan, row_chunks
+    assert row_chunks(torch.empty(4, 2048), 4096) == 2
+    assert row_chunks(torch.empty(4, 1000), 4096) == 0
+    assert row_chunks(torch.empty(4, 3 * 1024), 4096) == 0   # 3 does not divide 128
+    assert row_chunks(torch.empty(2048), 4096) == 0
+    y = torch.empty(2, 64, 2048)
+    pos = {5: 3}
+    assert chunk_plan(_N("add", ["node:5", "weight:mask"]), [y, torch.empty(64, 2048)], y, pos,
+                      4096) == (3, 2 * 64 * 2, 1, _lib.REUSE_SAME_OFFSET, 2)
+    assert chunk_plan(_N("add", ["node:5", "node:6"]), [y, y], y, {5: 3, 6: 4}, 4096) == \
+        (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
+    assert chunk_plan(_N("mul", ["node:5", "weight:w"]), [y, y], y, pos, 4096) == \
+        (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
+    z = torch.empty(2, 64, 1000)
+    assert chunk_plan(_N("add", ["node:7", "weight:w"]), [z, z], z, pos, 4096) is None
