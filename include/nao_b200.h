@@ -198,6 +198,13 @@ typedef struct nao_check_partial {
  * of 128 -- threads of a commit CTA take chunk j of consecutive rows, so
  * warps meet the same kind of chunk and a warp whose chunks all take a
  * shortcut leaves the sponge pipe to the other warps. */
+/* ref_payload / ref_digests / ref_bytes (optional, ref_payload = NULL: none):
+ * a static tensor broadcast over the leading dims (ref_bytes a multiple of
+ * chunk_bytes dividing the payload size) with its chunk digests (ref_digests:
+ * ref_bytes / chunk_bytes digests of 32 bytes, e.g. the leaf digests of its
+ * own commit after the header leaf); a claimed chunk c equal to reference
+ * chunk c mod (ref_bytes / chunk_bytes) takes that digest (the -1e9 fill of
+ * a causal mask add: x + w rounds to w). */
 enum nao_reuse_mode { NAO_REUSE_LOCAL_COPY = 0, NAO_REUSE_SAME_OFFSET = 1 };
 typedef struct nao_chunk_reuse {
     int64_t src;
@@ -205,6 +212,9 @@ typedef struct nao_chunk_reuse {
     uint64_t repeats;
     int32_t mode;
     uint32_t row_chunks;
+    const void* ref_payload;
+    const void* ref_digests;
+    uint64_t ref_bytes;
 } nao_chunk_reuse;
 size_t nao_commit_check_accum_bytes(void);
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,

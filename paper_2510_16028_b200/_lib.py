@@ -69,7 +69,8 @@ class ChunkReuse(ctypes.Structure):
     """nao_chunk_reuse: a data-movement node's chunk digests copied from its source."""
     _fields_ = [("src", ctypes.c_int64), ("block_chunks", ctypes.c_uint64),
                 ("repeats", ctypes.c_uint64), ("mode", ctypes.c_int32),
-                ("row_chunks", ctypes.c_uint32)]
+                ("row_chunks", ctypes.c_uint32), ("ref_payload", ctypes.c_void_p),
+                ("ref_digests", ctypes.c_void_p), ("ref_bytes", ctypes.c_uint64)]
 
 
 REUSE_LOCAL_COPY, REUSE_SAME_OFFSET = 0, 1

@@ -134,7 +134,10 @@ struct CCTable {
     uint64_t reuse_block[kMaxSegs];  // chunks per source block
     uint64_t reuse_span[kMaxSegs];   // block_chunks * repeats
     const uint32_t* reuse_src[kMaxSegs];  // same-offset mode: the source's claimed payload
-    uint32_t row_chunks[kMaxSegs];   // chunk -> thread mapping (0: identity)
+    uint32_t row_chunks[kMaxSegs];   // chunk -> CTA mapping (0: identity)
+    const uint32_t* ref_payload[kMaxSegs];  // broadcast reference tensor, or null
+    const uint32_t* ref_digests[kMaxSegs];  // its chunk digests
+    uint64_t ref_chunks[kMaxSegs];
     uint32_t zero_digest[8];         // H(0x00 || zeros(chunk)), valid if zero_ok
     int zero_ok;
 };
@@ -434,27 +437,48 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             reused = true;
         }
     }
-    if (ALG == kKECCAK256 && check && (tab.reuse_src[s] != nullptr || tab.zero_ok) &&
+    if (ALG == kKECCAK256 && check &&
+        (tab.reuse_src[s] != nullptr || tab.ref_payload[s] != nullptr || tab.zero_ok) &&
         (cw & 3u) == 0u) {
-        // digest shortcut: an all-zero claimed chunk, or (same-offset mode) one
-        // equal to the source's claimed chunk.  Each lane probes its chunk's
-        // first and last 16 bytes; the warp then scans every candidate chunk
-        // together (coalesced 16-byte loads of claimed, local and reference),
-        // setting the owner's check flags at the sponge-block bit positions the
-        // hash pass would use.  Candidates that turn out to differ are hashed.
-        const uint32_t* rbase = tab.reuse_src[s];
+        // digest shortcut: a claimed chunk equal to the same-offset chunk of the
+        // source (REUSE_SAME_OFFSET), to a chunk of the broadcast reference
+        // tensor, or to zeros, takes that chunk's digest.  Each lane probes its
+        // chunk's first and last 16 bytes against the candidates; the warp then
+        // scans every candidate chunk together (coalesced 16-byte loads of
+        // claimed, local and reference), setting the owner's check flags at the
+        // sponge-block bit positions the hash pass would use.  Candidates that
+        // turn out to differ are hashed.
+        const uint32_t* refp = nullptr;  // reference words of this lane's chunk (null: zeros)
+        const uint32_t* digp = nullptr;  // its digest
         bool cand = false;
         if (active && !reused && nw == cw) {
             const uint32_t* cp = tab.payload[s] + off_w;
             const uint4 a0 = __ldg(reinterpret_cast<const uint4*>(cp));
             const uint4 a1 = __ldg(reinterpret_cast<const uint4*>(cp + cw - 4));
-            uint4 b0 = make_uint4(0u, 0u, 0u, 0u), b1 = b0;
-            if (rbase) {
-                b0 = __ldg(reinterpret_cast<const uint4*>(rbase + off_w));
-                b1 = __ldg(reinterpret_cast<const uint4*>(rbase + off_w + cw - 4));
+            auto probe = [&](const uint32_t* r) {
+                const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(r));
+                const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(r + cw - 4));
+                return ((a0.x ^ b0.x) | (a0.y ^ b0.y) | (a0.z ^ b0.z) | (a0.w ^ b0.w) |
+                        (a1.x ^ b1.x) | (a1.y ^ b1.y) | (a1.z ^ b1.z) | (a1.w ^ b1.w)) == 0u;
+            };
+            if (tab.reuse_src[s] != nullptr && probe(tab.reuse_src[s] + off_w)) {
+                cand = true;
+                refp = tab.reuse_src[s] + off_w;
+                digp = digests + 8 * (tab.reuse_out[s] + c);
             }
-            cand = ((a0.x ^ b0.x) | (a0.y ^ b0.y) | (a0.z ^ b0.z) | (a0.w ^ b0.w) |
-                    (a1.x ^ b1.x) | (a1.y ^ b1.y) | (a1.z ^ b1.z) | (a1.w ^ b1.w)) == 0u;
+            if (!cand && tab.ref_payload[s] != nullptr) {
+                const uint64_t rcix = c % tab.ref_chunks[s];
+                if (probe(tab.ref_payload[s] + rcix * cw)) {
+                    cand = true;
+                    refp = tab.ref_payload[s] + rcix * cw;
+                    digp = tab.ref_digests[s] + 8 * rcix;
+                }
+            }
+            if (!cand && tab.zero_ok &&
+                ((a0.x | a0.y | a0.z | a0.w | a1.x | a1.y | a1.z | a1.w) == 0u)) {
+                cand = true;
+                digp = tab.zero_digest;
+            }
         }
         unsigned cm = __ballot_sync(0xffffffffu, cand);
         while (cm) {
@@ -463,7 +487,8 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             const uint64_t joff = __shfl_sync(0xffffffffu, off_w, j);
             const uint4* cj = reinterpret_cast<const uint4*>(tab.payload[s] + joff);
             const uint4* lj = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(d.local) + joff);
-            const uint4* rj = rbase ? reinterpret_cast<const uint4*>(rbase + joff) : nullptr;
+            const uint4* rj = reinterpret_cast<const uint4*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(refp), j));
             unsigned long long* mj = s_mask + (threadIdx.x & ~31u) + j;
             uint32_t diff = 0u;
             const uint32_t nq = cw / 4;
@@ -495,21 +520,11 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
                 }
             }
             const bool same = __all_sync(0xffffffffu, diff == 0u);
-            if (lane == j) {
-                if (same) {
-                    uint4* dst = reinterpret_cast<uint4*>(digests + 8 * (tab.out_index[s] + c));
-                    if (rbase) {
-                        const uint4* src = reinterpret_cast<const uint4*>(digests + 8 * (tab.reuse_out[s] + c));
-                        dst[0] = src[0];
-                        dst[1] = src[1];
-                    } else {
-                        dst[0] = make_uint4(tab.zero_digest[0], tab.zero_digest[1],
-                                            tab.zero_digest[2], tab.zero_digest[3]);
-                        dst[1] = make_uint4(tab.zero_digest[4], tab.zero_digest[5],
-                                            tab.zero_digest[6], tab.zero_digest[7]);
-                    }
-                    reused = true;
-                }
+            if (lane == j && same) {
+                uint32_t* dst = digests + 8 * (tab.out_index[s] + c);
+#pragma unroll
+                for (int k = 0; k < 8; k++) dst[k] = digp[k];
+                reused = true;
             }
             __syncwarp();
         }
@@ -1016,6 +1031,12 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
         NAO_REQUIRE(r.row_chunks <= 1 || (r.row_chunks <= (uint32_t)kLeafThreads &&
                                            kLeafThreads % r.row_chunks == 0),
                     "reuse %lld: row_chunks must divide %d", (long long)i, kLeafThreads);
+        if (r.ref_payload != nullptr)
+            NAO_REQUIRE(r.ref_digests != nullptr && r.ref_bytes > 0 &&
+                            r.ref_bytes % chunk_bytes == 0 && payload_bytes[i] % r.ref_bytes == 0 &&
+                            reinterpret_cast<uintptr_t>(r.ref_payload) % 16 == 0,
+                        "reuse %lld: the reference must be whole chunks dividing the payload",
+                        (long long)i);
         if (r.src < 0 || payload_bytes[i] == 0) continue;
         NAO_REQUIRE(r.src < i, "reuse %lld: source %lld must come earlier", (long long)i,
                     (long long)r.src);
@@ -1122,6 +1143,14 @@ static int commit_tensors_impl(int64_t n_tensors, const void* const* payloads,
             ct.reuse_out[cnt] = ~0ull;
             ct.reuse_src[cnt] = nullptr;
             ct.row_chunks[cnt] = rcs;
+            ct.ref_payload[cnt] = nullptr;
+            ct.ref_digests[cnt] = nullptr;
+            ct.ref_chunks[cnt] = 1;
+            if (reuse && reuse[i].ref_payload != nullptr && payload_bytes[i] > 0) {
+                ct.ref_payload[cnt] = static_cast<const uint32_t*>(reuse[i].ref_payload);
+                ct.ref_digests[cnt] = static_cast<const uint32_t*>(reuse[i].ref_digests);
+                ct.ref_chunks[cnt] = reuse[i].ref_bytes / chunk_bytes;
+            }
             if (phase[i] > 0) {
                 const nao_chunk_reuse& r = reuse[i];
                 ct.reuse_out[cnt] = in_index[r.src] + 1;

@@ -212,20 +212,34 @@ def row_chunks(y: torch.Tensor, chunk: int) -> int:
     return rc if 1 < rc <= 128 and 128 % rc == 0 else 0
 
 
-def chunk_plan(node, xs, y, pos_of, chunk: int):
+def broadcast_ref(w: torch.Tensor, y: torch.Tensor, chunk: int) -> bool:
+    """w broadcasts to y over leading dims only, in whole chunks (a reference
+    tensor for the digest shortcut)."""
+    return (w.dim() >= 1 and w.dtype == torch.float32 and w.is_contiguous() and w.numel() > 0
+            and (w.numel() * 4) % chunk == 0 and y.numel() % w.numel() == 0
+            and tuple(y.shape[y.dim() - w.dim():]) == tuple(w.shape) and w.data_ptr() % 16 == 0)
+
+
+def chunk_plan(node, xs, y, pos_of, chunk: int, ref_digests=None):
     """nao_chunk_reuse entry of a checked node's claimed tensor, or None:
-    data-movement reuse (chunk_reuse), same-offset reuse for an elementwise
-    node with one same-shaped claimed operand pending in the commit, and the
-    row-chunk thread mapping."""
+    data-movement reuse (chunk_reuse); for x + w / x - w (w a weight) the
+    same-offset reuse of x's equal chunks and w as a broadcast reference
+    (ref_digests(w) -> (payload ptr, chunk-digest ptr, bytes), cached by the
+    caller); and the row-chunk mapping."""
     rc = row_chunks(y, chunk)
     r = chunk_reuse(node, xs, pos_of, chunk) if node.kind in ("reshape", "concat") else None
     if r is not None:
         return (r[0], r[1], r[2], _lib.REUSE_LOCAL_COPY, rc)
-    if node.kind in SAME_OFFSET_KINDS and len(node.inputs) == 2:
+    if node.kind in SAME_OFFSET_KINDS and len(node.inputs) == 2 and y.numel():
         (c0, k0), (c1, _) = parse_ref(node.inputs[0]), parse_ref(node.inputs[1])
-        if (c0 == "node" and c1 == "weight" and k0 in pos_of and y.numel()
-                and tuple(xs[0].shape) == tuple(y.shape)):
-            return (pos_of[k0], -(-y.numel() * 4 // chunk), 1, _lib.REUSE_SAME_OFFSET, rc)
+        if c0 == "node" and c1 == "weight" and tuple(xs[0].shape) == tuple(y.shape):
+            src = (pos_of[k0], -(-y.numel() * 4 // chunk), 1, _lib.REUSE_SAME_OFFSET) \
+                if k0 in pos_of else (-1, 0, 0, _lib.REUSE_LOCAL_COPY)
+            ref = (None, None, 0)
+            if ref_digests is not None and broadcast_ref(xs[1], y, chunk):
+                ref = ref_digests(xs[1])
+            if src[0] >= 0 or ref[0] is not None:
+                return src + (rc,) + ref
     return (-1, 0, 0, _lib.REUSE_LOCAL_COPY, rc) if rc else None
 
 
@@ -338,6 +352,7 @@ class StreamingVerifier:
         self._com_events = []
         self._host_events = []  # commit-flush events the host has not waited for
         self.host_lag_bytes = int(float(os.environ.get("NAO_HOST_LAG_GB", "32")) * (1 << 30))
+        self._ref_cache = {}  # (ptr, numel, chunk, alg) -> (weight, its chunk digests)
         # partial: records are combinable nao_check_partial rows (a batch shard of
         # every node; shard.combine_shard_records decides the whole-tensor verdicts)
         self.partial = bool(partial)
@@ -357,6 +372,21 @@ class StreamingVerifier:
         self._s_main = None
 
     # ---------------------------------------------------------- thresholds
+    def _ref_chunk_digests(self, w: torch.Tensor):
+        """(payload ptr, chunk-digest ptr, bytes) of a static broadcast reference
+        tensor (a weight), its chunk digests committed once and cached."""
+        key = (w.data_ptr(), w.numel(), self.chunk, self.alg)
+        hit = self._ref_cache.get(key)
+        if hit is None:
+            if len(self._ref_cache) >= 64:  # weights are static: a handful of masks
+                return (None, None, 0)
+            n = w.numel() * 4 // self.chunk
+            dig = torch.empty((1 + n, 32), dtype=torch.uint8, device=w.device)
+            commit_tensors([w], self.chunk, self.alg, leaf_digests=dig)
+            hit = self._ref_cache[key] = (w, dig)
+        w, dig = hit
+        return (w.data_ptr(), dig.data_ptr() + 32, w.numel() * 4)
+
     def _sync_thresholds(self):
         """Drop the cached taus / device specs when `thresholds` was replaced."""
         if getattr(self, "_spec_for", None) is not self.thresholds:
@@ -597,7 +627,8 @@ class StreamingVerifier:
                     stats.gemm_flops += 2 * y.numel() * xs[1][0].numel()
             del eps, y
             values[node.index] = yc
-            st.pend_reuse.append(chunk_plan(node, xs, yc, st.pend_pos, self.chunk)
+            st.pend_reuse.append(chunk_plan(node, xs, yc, st.pend_pos, self.chunk,
+                                            self._ref_chunk_digests)
                                  if desc is not None else None)
             st.pend_pos[node.index] = len(st.pending)
             st.pending.append(yc)

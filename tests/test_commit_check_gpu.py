@@ -299,11 +299,14 @@ def test_digest_shortcuts_keep_roots_and_records(chunk, width):
     probs = torch.softmax(masked, dim=-1)
     assert (probs == 0).any() and (masked == scaled).any()
     rc = row_chunks(masked, chunk)
+    if width * 4 > chunk:  # rows of several chunks: whole fill chunks exist
+        assert ((masked.view(-1, chunk // 4) == -1e9).all(dim=1)).any()
     for mode in ("equal", "drift", "local"):
         c_scaled, c_masked, c_probs = scaled.clone(), masked.clone(), probs.clone()
         l_masked, l_probs = masked.clone(), probs.clone()
         if mode == "drift":  # claimed words moved inside shortcut chunks
             c_masked[0, S - 1, 3] += 1.0          # lower triangle: equals scaled elsewhere
+            c_masked[2, 0, width - 1] = -1e9 * (1 + 2 ** -20)  # a fill chunk (rc > 1)
             c_probs[0, 0, width - 5] = 1e-3       # the zero upper triangle of row 0
         elif mode == "local":  # local non-zero where the claim is zero
             l_probs[1, 0, width - 9] = 2.0 ** -40
@@ -320,8 +323,14 @@ def test_digest_shortcuts_keep_roots_and_records(chunk, width):
             return roots, [CheckRecord(recs[i]).host() for i in range(3)]
 
         nch = -(-masked.numel() * 4 // chunk)
-        got, r_got = run([(-1, 0, 0, 0, rc), (0, nch, 1, _lib.REUSE_SAME_OFFSET, rc),
+        # the mask as a broadcast reference (its fill chunks: x + -1e9 == -1e9)
+        mdig = torch.empty((1 + mask.numel() * 4 // chunk, 32), dtype=torch.uint8, device="cuda")
+        commit_tensors([mask], chunk, "keccak256", leaf_digests=mdig)
+        ref = (mask.data_ptr(), mdig.data_ptr() + 32, mask.numel() * 4)
+        got, r_got = run([(-1, 0, 0, 0, rc), (0, nch, 1, _lib.REUSE_SAME_OFFSET, rc) + ref,
                           (-1, 0, 0, 0, rc)])
+        got2, r_got2 = run([None, (-1, 0, 0, 0, 0) + ref, None])
+        assert torch.equal(got2, got) and r_got2 == r_got, mode
         ref, r_ref = run(None)
         plain = commit_tensors(claims, chunk, "keccak256")
         torch.cuda.synchronize()
@@ -331,4 +340,4 @@ def test_digest_shortcuts_keep_roots_and_records(chunk, width):
                                                                  OM.KECCAK256), (mode, i)
         assert r_got == r_ref, mode
         nv = [x["n_violations"] for x in r_got]
-        assert nv == {"equal": [0, 0, 0], "drift": [0, 1, 1], "local": [0, 0, 1]}[mode], (mode, nv)
+        assert nv == {"equal": [0, 0, 0], "drift": [0, 2, 1], "local": [0, 0, 1]}[mode], (mode, nv)

@@ -99,8 +99,17 @@ def test_chunk_plan_proposals():
     assert row_chunks(torch.empty(2048), 4096) == 0
     y = torch.empty(2, 64, 2048)
     pos = {5: 3}
-    assert chunk_plan(_N("add", ["node:5", "weight:mask"]), [y, torch.empty(64, 2048)], y, pos,
-                      4096) == (3, 2 * 64 * 2, 1, _lib.REUSE_SAME_OFFSET, 2)
+    m = torch.empty(64, 2048)
+    assert chunk_plan(_N("add", ["node:5", "weight:mask"]), [y, m], y, pos,
+                      4096) == (3, 2 * 64 * 2, 1, _lib.REUSE_SAME_OFFSET, 2, None, None, 0)
+    # the weight as a broadcast reference (digests from the caller's cache)
+    fake = lambda w: (111, 222, w.numel() * 4)  # noqa: E731
+    assert chunk_plan(_N("add", ["node:5", "weight:mask"]), [y, m], y, {}, 4096, fake) == \
+        (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2, 111, 222, 64 * 2048 * 4)
+    assert chunk_plan(_N("add", ["node:5", "weight:b"]), [y, torch.empty(2048)], y, {}, 4096,
+                      fake) == (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2, 111, 222, 2048 * 4)
+    assert chunk_plan(_N("add", ["node:5", "weight:b"]), [y, torch.empty(1000)], y, {}, 4096,
+                      fake) == (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)  # not whole chunks
     assert chunk_plan(_N("add", ["node:5", "node:6"]), [y, y], y, {5: 3, 6: 4}, 4096) == \
         (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
     assert chunk_plan(_N("mul", ["node:5", "weight:w"]), [y, y], y, pos, 4096) == \

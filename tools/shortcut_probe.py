@@ -44,12 +44,17 @@ def main():
               for i, l in enumerate(locals_)]
     rc = row_chunks(probs, 4096)
     nch = probs.numel() * 4 // 4096
+    mdig = torch.empty((1 + mask.numel() * 4 // 4096, 32), dtype=torch.uint8, device="cuda")
+    commit_tensors([mask], 4096, "keccak256", leaf_digests=mdig)
+    ref = (mask.data_ptr(), mdig.data_ptr() + 32, mask.numel() * 4)
     plans = {
         "none": None,
         "rows_only": [(-1, 0, 0, 0, rc)] * 4,
         "shortcuts_identity_map": [None, None, (1, nch, 1, _lib.REUSE_SAME_OFFSET, 0), (-1, 0, 0, 0, 0)],
+        "shortcuts_no_mask_ref": [(-1, 0, 0, 0, rc), (-1, 0, 0, 0, rc),
+                                  (1, nch, 1, _lib.REUSE_SAME_OFFSET, rc), (-1, 0, 0, 0, rc)],
         "shortcuts": [(-1, 0, 0, 0, rc), (-1, 0, 0, 0, rc),
-                      (1, nch, 1, _lib.REUSE_SAME_OFFSET, rc), (-1, 0, 0, 0, rc)],
+                      (1, nch, 1, _lib.REUSE_SAME_OFFSET, rc) + ref, (-1, 0, 0, 0, rc)],
     }
 
     def timed(fn):
@@ -61,7 +66,9 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
-    res = {"zero_chunk_frac_probs": float(
+    res = {"mask_fill_chunk_frac_masked": float(
+        (masked.view(-1, 1024) == -1e9).all(dim=1).float().mean()),
+        "zero_chunk_frac_probs": float(
         (probs.view(-1, 1024) == 0).all(dim=1).float().mean()),
         "masked_eq_scaled_chunk_frac": float(
         (masked.view(-1, 1024) == scaled.view(-1, 1024)).all(dim=1).float().mean())}
