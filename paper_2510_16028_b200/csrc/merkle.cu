@@ -143,6 +143,9 @@ struct CCTable {
 };
 
 constexpr int kLeafWarps = kLeafThreads / 32;
+#ifndef NAO_SCAN_U
+#define NAO_SCAN_U 4  // 16-byte words per lane in flight in the shortcut scan (x3 tensors)
+#endif
 constexpr int kMaxFusedChunkWords = 4096;  // 16 KiB chunks: 64 mask words per thread
 constexpr float kGuard32 = 1.0f / 524288.0f;  // 2^-19 guard of the FP32 relative-key search
 
@@ -492,10 +495,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             unsigned long long* mj = s_mask + (threadIdx.x & ~31u) + j;
             uint32_t diff = 0u;
             const uint32_t nq = cw / 4;
-            for (uint32_t q0 = lane; q0 < nq; q0 += 128) {  // 4 x 3 loads in flight per lane
-                uint4 a[4], y[4], r[4];
+            for (uint32_t q0 = lane; q0 < nq; q0 += 32 * NAO_SCAN_U) {  // U x 3 loads in flight per lane
+                uint4 a[NAO_SCAN_U], y[NAO_SCAN_U], r[NAO_SCAN_U];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < NAO_SCAN_U; u++) {
                     const uint32_t q = q0 + 32 * u;
                     a[u] = y[u] = r[u] = make_uint4(0u, 0u, 0u, 0u);
                     if (q < nq) {
@@ -505,7 +508,7 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < NAO_SCAN_U; u++) {
                     const uint32_t q = q0 + 32 * u;
                     diff |= (a[u].x ^ r[u].x) | (a[u].y ^ r[u].y) | (a[u].z ^ r[u].z) | (a[u].w ^ r[u].w);
                     const uint32_t av[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
