@@ -518,6 +518,19 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True, amb=None):
                                                       torch.float32, device=y.device))
     if kind in SINGLE_ROUNDING_KINDS:
         return y, (("scaled", u) if lazy else scaled_abs(y, u, f64))
+    if kind in GEMM_BOUND_KINDS:
+        return y, gemm_bound_device(node, xs, y, model, profile, f64)
+    raise ValueError(f"no bound template for kind {kind!r}")
+
+
+GEMM_BOUND_KINDS = frozenset({"matmul", "linear", "conv2d"})
+
+
+def gemm_bound_device(node, xs, y, model: FpModel, profile, f64: bool) -> torch.Tensor:
+    """The abs-GEMM bound of a matmul / linear / conv2d node (bounds.py:100-111,
+    209-217) on the current stream, given its inputs and (linear: u|y|) its
+    value -- separable from the value so a caller can run it on another stream."""
+    kind, u = node.kind, model.u
     if kind in ("matmul", "linear"):
         tb = bool(node.attr("transpose_b", 0)) if kind == "matmul" else False
         k_dim = xs[0].shape[-1]
@@ -525,21 +538,19 @@ def op_bound_device(node, xs, model: FpModel, profile, eps_f64=True, amb=None):
         const = model.reduction_const(count)
         static_b = xs[1].dim() == 2  # 2-D right operands are weights in every lowering
         if kind == "matmul":
-            return y, abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64, cache_b=static_b)
-        return y, abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64,
-                                 cache_b=static_b)
-    if kind == "conv2d":
-        # eps[b] = const |W| @ |col_b|^T: the weight is the (cached) A operand and
-        # the patch rows are K-major B rows, so the GEMM writes NCHW directly
-        x, w = xs
-        col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
-                                  int(node.attr("pad", 0)))
-        K = col.shape[-1]
-        count = K if fma_of(profile) else 2 * K - 1
-        eps = abs_gemm_bound(w.reshape(w.shape[0], -1), col, model.reduction_const(count), True,
-                             eps_f64=f64, a_owner=w)
-        return y, eps.reshape(B, w.shape[0], OH, OW)
-    raise ValueError(f"no bound template for kind {kind!r}")
+            return abs_gemm_bound(xs[0], xs[1], const, tb, eps_f64=f64, cache_b=static_b)
+        return abs_gemm_bound(xs[0], xs[1], const, False, y=y, u=u, eps_f64=f64,
+                              cache_b=static_b)
+    # conv2d: eps[b] = const |W| @ |col_b|^T: the weight is the (cached) A operand
+    # and the patch rows are K-major B rows, so the GEMM writes NCHW directly
+    x, w = xs
+    col, (B, OH, OW) = im2col(x, w.shape[-1], int(node.attr("stride", 1)),
+                              int(node.attr("pad", 0)))
+    K = col.shape[-1]
+    count = K if fma_of(profile) else 2 * K - 1
+    eps = abs_gemm_bound(w.reshape(w.shape[0], -1), col, model.reduction_const(count), True,
+                         eps_f64=f64, a_owner=w)
+    return eps.reshape(B, w.shape[0], OH, OW)
 
 
 def im2col(x: torch.Tensor, k: int, stride: int, pad: int):

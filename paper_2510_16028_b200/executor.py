@@ -33,7 +33,8 @@ import torch.nn.functional as F
 
 from . import _lib
 from .bounds import (INTRINSIC_KINDS, ROW_KINDS, FpModel, apply_value, certified_overestimate,
-                     op_bound_device, release_activation_split)
+                     op_bound_device, release_activation_split, apply_value,
+                     gemm_bound_device, GEMM_BOUND_KINDS)
 from .calibration import DEFAULT_EPSILON, PERCENTILE_GRID
 from .commitments import DEFAULT_CHUNK_BYTES, alg_id, commit_tensors, root_of_digests
 from .dispute import new_result_buffer
@@ -230,7 +231,9 @@ def chunk_plan(node, xs, y, pos_of, chunk: int, ref_digests=None):
     r = chunk_reuse(node, xs, pos_of, chunk) if node.kind in ("reshape", "concat") else None
     if r is not None:
         return (r[0], r[1], r[2], _lib.REUSE_LOCAL_COPY, rc)
-    if node.kind in SAME_OFFSET_KINDS and len(node.inputs) == 2 and y.numel():
+    # (only tensors of at least one commit CTA of chunks: the source-first launch
+    # phase a reuse entry adds costs more than it saves on small graphs)
+    if node.kind in SAME_OFFSET_KINDS and len(node.inputs) == 2 and y.numel() * 4 >= 128 * chunk:
         (c0, k0), (c1, _) = parse_ref(node.inputs[0]), parse_ref(node.inputs[1])
         if c0 == "node" and c1 == "weight" and tuple(xs[0].shape) == tuple(y.shape):
             src = (pos_of[k0], -(-y.numel() * 4 // chunk), 1, _lib.REUSE_SAME_OFFSET) \
@@ -369,6 +372,11 @@ class StreamingVerifier:
         self.overlap = bool(overlap)
         self._s_chk = torch.cuda.Stream(self.dev) if overlap else None
         self._s_com = torch.cuda.Stream(self.dev) if overlap else None
+        # abs-GEMM bounds of matmul / linear / conv nodes on their own stream:
+        # the value path (main) runs on while the tensor-core bound fills the
+        # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
+        self.bound_stream = overlap and os.environ.get("NAO_BOUND_STREAM", "1") != "0"
+        self._s_bnd = torch.cuda.Stream(self.dev) if self.bound_stream else None
         self._s_main = None
 
     # ---------------------------------------------------------- thresholds
@@ -477,9 +485,12 @@ class StreamingVerifier:
         s_chk = self._s_chk or main
         s_com = self._s_com or main
         capturing = torch.cuda.is_current_stream_capturing()
+        s_bnd = self._s_bnd if (self.overlap and self._s_bnd is not None) else None
         if self.overlap:  # side streams start after everything already queued on main
             s_chk.wait_stream(main)
             s_com.wait_stream(main)
+        if s_bnd is not None:
+            s_bnd.wait_stream(main)
         with torch.cuda.stream(s_chk):
             ws_chk = _lib.check_accumulator(self.dev)
         chk_ptr = s_chk.cuda_stream
@@ -501,6 +512,8 @@ class StreamingVerifier:
                 return
             if self.overlap:
                 s_com.wait_stream(main)
+            if s_bnd is not None:  # the flush's GEMM bounds
+                s_com.wait_stream(s_bnd)
             with torch.cuda.stream(s_com):
                 if _EXP_SKIP_COMMIT:  # timing experiment only: main-stream work alone
                     st.pending, st.pend_idx, st.pend_bytes = [], [], 0
@@ -558,8 +571,18 @@ class StreamingVerifier:
             i = node.index - start
             border = st.border[i]
             try:
-                y, eps = op_bound_device(node, xs, self.model, self.profile, eps_f64=None,
-                                         amb=border if node.kind in INTRINSIC_KINDS else None)
+                if s_bnd is not None and node.kind in GEMM_BOUND_KINDS:
+                    # value on main, abs-GEMM bound on the bound stream
+                    y = apply_value(node, xs, self.profile)
+                    s_bnd.wait_stream(main)
+                    with torch.cuda.stream(s_bnd):
+                        eps = gemm_bound_device(node, xs, y, self.model, self.profile, False)
+                    for t in xs:
+                        side_use(t, s_bnd)
+                    side_use(y, s_bnd)
+                else:
+                    y, eps = op_bound_device(node, xs, self.model, self.profile, eps_f64=None,
+                                             amb=border if node.kind in INTRINSIC_KINDS else None)
             except (ExecutionError, NotImplementedError):
                 raise
             except Exception as exc:
@@ -581,6 +604,8 @@ class StreamingVerifier:
             if self.trace_writer is not None:
                 self.trace_writer.write(node.index, yc)
             if self.bound_writer is not None:
+                if s_bnd is not None:
+                    main.wait_stream(s_bnd)
                 self.bound_writer.write(node.index, _materialise_eps(eps, y))
             tau_a, tau_r = self._taus(node.name)
             kind, eps_ptr, scale, lo_f, listed = check_band(node, xs, eps)
@@ -604,6 +629,8 @@ class StreamingVerifier:
             elif y.numel():
                 if self.overlap:
                     s_chk.wait_stream(main)
+                    if s_bnd is not None:
+                        s_chk.wait_stream(s_bnd)
                     side_use(y, s_chk)
                     side_use(yc, s_chk)
                     if not isinstance(eps, tuple):
@@ -647,6 +674,8 @@ class StreamingVerifier:
         if self.overlap:
             main.wait_stream(s_chk)
             main.wait_stream(s_com)
+        if s_bnd is not None:
+            main.wait_stream(s_bnd)
         keep.clear()
         release_activation_split()  # the memo must not pin a split past the segment
 

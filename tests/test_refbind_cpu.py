@@ -114,5 +114,8 @@ def test_chunk_plan_proposals():
         (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
     assert chunk_plan(_N("mul", ["node:5", "weight:w"]), [y, y], y, pos, 4096) == \
         (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
+    small = torch.empty(4, 2048)  # below one commit CTA of chunks: no same-offset entry
+    assert chunk_plan(_N("add", ["node:5", "weight:mask"]), [small, torch.empty(2048)], small,
+                      pos, 4096) == (-1, 0, 0, _lib.REUSE_LOCAL_COPY, 2)
     z = torch.empty(2, 64, 1000)
     assert chunk_plan(_N("add", ["node:7", "weight:w"]), [z, z], z, pos, 4096) is None
