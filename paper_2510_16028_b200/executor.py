@@ -572,9 +572,14 @@ class StreamingVerifier:
             border = st.border[i]
             try:
                 if s_bnd is not None and node.kind in GEMM_BOUND_KINDS:
-                    # value on main, abs-GEMM bound on the bound stream
+                    # value on main, abs-GEMM bound on the bound stream (matmul /
+                    # conv: from the inputs alone, concurrently with the value
+                    # GEMM; linear: after it, for the u|y| term)
+                    if node.kind != "linear":
+                        s_bnd.wait_stream(main)
                     y = apply_value(node, xs, self.profile)
-                    s_bnd.wait_stream(main)
+                    if node.kind == "linear":
+                        s_bnd.wait_stream(main)
                     with torch.cuda.stream(s_bnd):
                         eps = gemm_bound_device(node, xs, y, self.model, self.profile, False)
                     for t in xs:
