@@ -702,7 +702,8 @@ def run_config(args):
     stats = NodeStats()
     sv.run(x, claimed_fn, stats=stats)
     torch.cuda.synchronize()
-    seg = args.graphs or 96
+    seg = args.graphs if args.graphs is not None else 96
+    seg = seg or 96
     plain = GraphedRun.record_plain(g, x, dev, 0, None, None, seg_nodes=seg)
     ver = sv.capture(x, claimed_fn, seg_nodes=seg)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -1109,15 +1110,17 @@ def main(argv=None):
                     help="claimed bytes per fused commit launch (StreamingVerifier flush_bytes)")
     ap.add_argument("--separate-check", action="store_true",
                     help="standalone nao_check per node instead of the check fused into commit")
-    ap.add_argument("--graphs", type=int, default=96, metavar="SEG",
-                    help="replay both arms as CUDA graphs of SEG-node segments (default 96: "
-                         "81.1-81.4 %% and e2e alike over six runs; 300: 80.2-80.6 %% at 124 GB "
-                         "peak but one e2e outlier in two runs; >= 1000 runs out of HBM during "
-                         "capture -- side-stream tensors live until the segment joins; "
-                         "0 = eager dispatch: ~1.5 %% faster at best, but the host enqueues "
-                         "only ~7 %% ahead of the GPU and some runs lose the overlap "
-                         "(90-240 %%); graph replay measured 81.1-81.4 %% over six runs)")
+    ap.add_argument("--graphs", type=int, default=None, metavar="SEG",
+                    help="replay both arms as CUDA graphs of SEG-node segments (Qwen default 192, "
+                         "--config default 96 (UNet B=8 memory); Qwen 192: "
+                         "with the abs-GEMM bounds on their own stream, 67.7-68.1 %% over four "
+                         "runs at 116-139 GB peak reserved vs 69.0-69.1 %% at 96; 300: 67.5 %% "
+                         "at 122 GB; >= 1000 runs out of HBM during capture -- side-stream "
+                         "tensors live until the segment joins; 0 = eager dispatch: the host "
+                         "enqueues only ~7 %% ahead of the GPU and some runs lose the overlap)")
     args = ap.parse_args(argv)
+    if args.graphs is None and args.config == "qwen3-8b":
+        args.graphs = 192
     if args.fault_node and args.layers <= int(args.fault_node.split("_")[0][1:] or 0):
         args.fault_node = "l0_down"
     if args.impl == "reference":
