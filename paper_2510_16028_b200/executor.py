@@ -376,7 +376,8 @@ class StreamingVerifier:
         # the value path (main) runs on while the tensor-core bound fills the
         # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
         self.bound_stream = overlap and os.environ.get("NAO_BOUND_STREAM", "1") != "0"
-        self._s_bnd = torch.cuda.Stream(self.dev) if self.bound_stream else None
+        self._s_bnd = (torch.cuda.Stream(self.dev, priority=int(os.environ.get("NAO_BOUND_PRIO", "0")))
+                       if self.bound_stream else None)
         self._s_main = None
 
     # ---------------------------------------------------------- thresholds
