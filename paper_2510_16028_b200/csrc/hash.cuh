@@ -214,6 +214,10 @@ __device__ __forceinline__ Lane lchi(Lane a, Lane b, Lane c) {
     return {a.lo ^ (~b.lo & c.lo), a.hi ^ (~b.hi & c.hi)};
 }
 
+#ifndef NAO_KECCAK_UNROLL
+#define NAO_KECCAK_UNROLL 1
+#endif
+constexpr int kKeccakUnroll = NAO_KECCAK_UNROLL;  // rounds per loop iteration
 // MASK bit j moves rotation j (0..23: rho in the order below, 24..28: theta)
 // to the FMA pipe; bit 31 picks the 32-bit IMAD form over IMAD.WIDE.
 template <uint32_t MASK>
@@ -221,7 +225,7 @@ __device__ __forceinline__ void keccak_f1600_m(uint64_t Aw[25]) {
     Lane A[25];
 #pragma unroll
     for (int i = 0; i < 25; i++) A[i] = {(uint32_t)Aw[i], (uint32_t)(Aw[i] >> 32)};
-#pragma unroll 1
+#pragma unroll kKeccakUnroll
     for (int r = 0; r < 24; r++) {
         const Lane C0 = lxor5(A[0], A[5], A[10], A[15], A[20]);
         const Lane C1 = lxor5(A[1], A[6], A[11], A[16], A[21]);
