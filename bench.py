@@ -376,7 +376,8 @@ def run_ours(args):
     fault = args.fault_node
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
                            chunk_bytes=args.chunk, fuse_check=not args.separate_check,
-                           max_lag=args.max_lag, flush_bytes=args.flush_mb << 20)
+                           max_lag=args.max_lag, flush_bytes=args.flush_mb << 20,
+                           commit_priority=args.main_priority)
 
     no_harness = os.environ.get("NAO_EXP_NO_HARNESS") == "1"  # timing experiment only
 

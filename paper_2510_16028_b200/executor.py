@@ -325,7 +325,8 @@ class StreamingVerifier:
                  hash_alg: str = "keccak256", chunk_bytes: int = DEFAULT_CHUNK_BYTES,
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
                  grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
-                 max_lag: int = 0, partial: bool = False, missing_thresholds: str = "raise"):
+                 max_lag: int = 0, partial: bool = False, missing_thresholds: str = "raise",
+                 commit_priority: int | None = None):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -371,7 +372,13 @@ class StreamingVerifier:
         # pending work pins via record_stream balloons -- measured 2x slower)
         self.overlap = bool(overlap)
         self._s_chk = torch.cuda.Stream(self.dev) if overlap else None
-        self._s_com = torch.cuda.Stream(self.dev) if overlap else None
+        # commit_priority: the commit stream's CUDA priority (lower = higher);
+        # at the caller's main-stream priority the commit takes SMs as soon as
+        # the value path frees them (bench: -1, 66.7-67.1 vs 67.5-67.6 % at 0)
+        if commit_priority is None:
+            commit_priority = int(os.environ.get("NAO_COMMIT_PRIO", "0"))
+        self._s_com = (torch.cuda.Stream(self.dev, priority=int(commit_priority))
+                       if overlap else None)
         # abs-GEMM bounds of matmul / linear / conv nodes on their own stream:
         # the value path (main) runs on while the tensor-core bound fills the
         # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
