@@ -326,7 +326,7 @@ class StreamingVerifier:
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
                  grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
                  max_lag: int = 0, partial: bool = False, missing_thresholds: str = "raise",
-                 commit_priority: int | None = None):
+                 commit_priority: int | None = None, claim_stream: bool = False):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -383,6 +383,10 @@ class StreamingVerifier:
         # the value path (main) runs on while the tensor-core bound fills the
         # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
         self.bound_stream = overlap and os.environ.get("NAO_BOUND_STREAM", "1") != "0"
+        # claim_stream: call claimed_fn on its own stream (a proposer harness
+        # that derives claims from the local values: a node's claim is then
+        # made while independent nodes' values run; consumers wait per node)
+        self._s_clm = torch.cuda.Stream(self.dev) if (overlap and claim_stream) else None
         self._s_bnd = (torch.cuda.Stream(self.dev, priority=int(os.environ.get("NAO_BOUND_PRIO", "0")))
                        if self.bound_stream else None)
         self._s_main = None
@@ -494,11 +498,15 @@ class StreamingVerifier:
         s_com = self._s_com or main
         capturing = torch.cuda.is_current_stream_capturing()
         s_bnd = self._s_bnd if (self.overlap and self._s_bnd is not None) else None
+        s_clm = self._s_clm if (self.overlap and self._s_clm is not None) else None
+        clm_ev = {}  # node index -> event after its claim (claim stream)
         if self.overlap:  # side streams start after everything already queued on main
             s_chk.wait_stream(main)
             s_com.wait_stream(main)
         if s_bnd is not None:
             s_bnd.wait_stream(main)
+        if s_clm is not None:
+            s_clm.wait_stream(main)
         with torch.cuda.stream(s_chk):
             ws_chk = _lib.check_accumulator(self.dev)
         chk_ptr = s_chk.cuda_stream
@@ -522,6 +530,8 @@ class StreamingVerifier:
                 s_com.wait_stream(main)
             if s_bnd is not None:  # the flush's GEMM bounds
                 s_com.wait_stream(s_bnd)
+            if s_clm is not None:  # the flush's claims
+                s_com.wait_stream(s_clm)
             with torch.cuda.stream(s_com):
                 if _EXP_SKIP_COMMIT:  # timing experiment only: main-stream work alone
                     st.pending, st.pend_idx, st.pend_bytes = [], [], 0
@@ -572,6 +582,9 @@ class StreamingVerifier:
                 cat, key = parse_ref(ref)
                 if cat == "node":
                     xs.append(values[key])
+                    ev = clm_ev.pop(key, None) if s_clm is not None else None
+                    if ev is not None:  # this input's claim is made on the claim stream
+                        main.wait_event(ev)
                 elif cat == "input":
                     xs.append(to_device(st.inputs[key], self.dev))
                 else:
@@ -602,7 +615,16 @@ class StreamingVerifier:
                 raise ExecutionError(f"node {node.index} ({node.name!r}, {node.kind}): {exc}",
                                      node_index=node.index, node_name=node.name) from exc
             y = y.contiguous()
-            yc = claimed_fn(node, y)
+            if s_clm is not None:
+                s_clm.wait_stream(main)
+                with torch.cuda.stream(s_clm):
+                    yc = claimed_fn(node, y)
+                ev = torch.cuda.Event()
+                ev.record(s_clm)
+                clm_ev[node.index] = ev
+                side_use(y, s_clm)
+            else:
+                yc = claimed_fn(node, y)
             if not (isinstance(yc, torch.Tensor) and yc.dtype == torch.float32
                     and tuple(yc.shape) == tuple(y.shape) and yc.device == y.device):
                 # the reference raises on a claimed tensor of another shape
@@ -614,7 +636,11 @@ class StreamingVerifier:
                     f"match the recomputed float32 {tuple(y.shape)} on {y.device}",
                     node_index=node.index, node_name=node.name)
             yc = yc.contiguous()
+            if s_clm is not None:
+                side_use(yc, main)  # made on the claim stream, read on main / commit
             if self.trace_writer is not None:
+                if s_clm is not None:
+                    main.wait_stream(s_clm)
                 self.trace_writer.write(node.index, yc)
             if self.bound_writer is not None:
                 if s_bnd is not None:
@@ -689,6 +715,8 @@ class StreamingVerifier:
             main.wait_stream(s_com)
         if s_bnd is not None:
             main.wait_stream(s_bnd)
+        if s_clm is not None:
+            main.wait_stream(s_clm)
         keep.clear()
         release_activation_split()  # the memo must not pin a split past the segment
 

@@ -445,3 +445,40 @@ def test_streaming_conv_in_band_claims_match_oracle():
         else:
             assert rec["n_violations"] == 0, node.name
     assert planted > 0
+
+
+@pytest.mark.parametrize("seg", [7, 1000])
+def test_stream_options_keep_roots_and_records(seg):
+    """The verifier's stream options -- abs-GEMM bounds on their own stream,
+    claims made on a claim stream, the commit stream at another priority --
+    give the serial run's roots and check records, eagerly and replayed as
+    CUDA graphs (segments of `seg` nodes)."""
+    import os
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.executor import StreamingVerifier, drift_claim
+    from paper_2510_16028_b200.lowerings import DecoderShape, build_decoder
+    from paper_2510_16028_b200.tensor import Rng
+    shape = DecoderShape("tiny-qwen", layers=2, hidden=128, heads=4, kv_heads=2, head_dim=32,
+                         inter=256, vocab=500, seq=64)
+    spec = build_decoder(shape, seed=7)
+    g = spec.graph
+    ids = spec.make_inputs(Rng(13))
+
+    def claimed_fn(node, y):
+        return drift_claim(node, y, seed=3, period=4, fault_node="l1_up")
+
+    ref = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256, overlap=False)
+    r0, c0 = ref.run(ids, claimed_fn)
+    r0, c0 = r0.clone(), c0.clone()
+    assert os.environ.get("NAO_BOUND_STREAM", "1") != "0"
+    sv = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256,
+                           claim_stream=True, commit_priority=-1)
+    assert sv._s_bnd is not None and sv._s_clm is not None
+    r1, c1 = sv.run(ids, claimed_fn)
+    torch.cuda.synchronize()
+    assert torch.equal(r1, r0) and torch.equal(c1, c0)
+    gr = sv.capture(ids, claimed_fn, seg_nodes=seg)
+    for _ in range(2):
+        r2, c2 = gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(r2, r0) and torch.equal(c2, c0)
