@@ -377,7 +377,8 @@ def run_ours(args):
     sv = StreamingVerifier(g, model, thresholds=thresholds, hash_alg=args.hash,
                            chunk_bytes=args.chunk, fuse_check=not args.separate_check,
                            max_lag=args.max_lag, flush_bytes=args.flush_mb << 20,
-                           commit_priority=args.main_priority,
+                           commit_priority=(args.main_priority if args.commit_priority is None
+                                            else args.commit_priority),
                            claim_stream=bool(args.claim_stream))
 
     no_harness = os.environ.get("NAO_EXP_NO_HARNESS") == "1"  # timing experiment only
@@ -1110,6 +1111,8 @@ def main(argv=None):
                     help="main waits for commit flush k-LAG (bounded side-stream lag)")
     ap.add_argument("--flush-mb", type=int, default=2048,
                     help="claimed bytes per fused commit launch (StreamingVerifier flush_bytes)")
+    ap.add_argument("--commit-priority", type=int, default=None,
+                    help="CUDA priority of the commit stream (default: --main-priority)")
     ap.add_argument("--claim-stream", type=int, default=0,
                     help="1: the proposer harness makes each node's claim on its own stream "
                          "(consumers wait per node; measured 69.0-69.1 %% vs 67.4-67.8 %% inline); "
