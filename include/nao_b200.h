@@ -217,6 +217,11 @@ typedef struct nao_chunk_reuse {
     uint64_t ref_bytes;
 } nao_chunk_reuse;
 size_t nao_commit_check_accum_bytes(void);
+/* Chunks of nao_commit_check_tensors calls (all streams, since the last reset)
+ * whose digest was copied instead of hashed (chunk-digest reuse and digest
+ * shortcuts): *out = the device counter; reset != 0 zeroes it.  Synchronises
+ * the device (a measurement hook, not for the hot path). */
+int nao_commit_stats(uint64_t* reused_chunks, int reset);
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
                              const uint64_t* payload_bytes, const uint8_t* const* headers,
                              const uint32_t* header_lens, uint64_t chunk_bytes, int hash_alg,

@@ -124,6 +124,7 @@ _SIGS = {
     "nao_verdict_spec_fill": (c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl),
                                       ctypes.POINTER(c_dbl), c_int, c_dbl]),
     "nao_commit_check_accum_bytes": (c_sz, []),
+    "nao_commit_stats": (c_int, [ctypes.POINTER(c_u64), c_int]),
     "nao_commit_check_tensors": (c_int, [c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_u64),
                                          ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_uint32),
                                          c_u64, c_int, ctypes.POINTER(CheckDesc),

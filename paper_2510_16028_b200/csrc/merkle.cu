@@ -143,6 +143,7 @@ struct CCTable {
 };
 
 constexpr int kLeafWarps = kLeafThreads / 32;
+__device__ unsigned long long g_reused_chunks = 0;  // nao_commit_stats
 #ifndef NAO_SCAN_U
 #define NAO_SCAN_U 4  // 16-byte words per lane in flight in the shortcut scan (x3 tensors)
 #endif
@@ -531,6 +532,10 @@ __device__ __forceinline__ void leaf_check_block(const CCTable& tab, uint32_t* _
             }
             __syncwarp();
         }
+    }
+    {  // chunks whose digest was copied (one atomic per warp)
+        const unsigned rb = __ballot_sync(0xffffffffu, active && reused);
+        if (lane == 0 && rb) atomicAdd(&g_reused_chunks, (unsigned long long)__popc(rb));
     }
     if (active && !reused) {
         uint32_t dg[8];
@@ -1223,6 +1228,19 @@ int nao_merkle_commit_tensors(int64_t n_tensors, const void* const* payloads,
 }
 
 size_t nao_commit_check_accum_bytes(void) { return sizeof(CheckAccum) * kMaxSegs; }
+
+int nao_commit_stats(uint64_t* reused_chunks, int reset) {
+    NAO_REQUIRE(reused_chunks != nullptr, "reused_chunks is null");
+    unsigned long long v = 0;
+    NAO_CHECK_CUDA(cudaDeviceSynchronize());
+    NAO_CHECK_CUDA(cudaMemcpyFromSymbol(&v, nao::g_reused_chunks, sizeof v));
+    *reused_chunks = v;
+    if (reset) {
+        const unsigned long long z = 0;
+        NAO_CHECK_CUDA(cudaMemcpyToSymbol(nao::g_reused_chunks, &z, sizeof z));
+    }
+    return NAO_OK;
+}
 
 int nao_commit_check_tensors(int64_t n_tensors, const void* const* payloads,
                              const uint64_t* payload_bytes, const uint8_t* const* headers,
