@@ -356,7 +356,7 @@ class StreamingVerifier:
         self._com_events = []
         self._host_events = []  # commit-flush events the host has not waited for
         self.host_lag_bytes = int(float(os.environ.get("NAO_HOST_LAG_GB", "32")) * (1 << 30))
-        self._ref_cache = {}  # (ptr, numel, chunk, alg) -> (weight, its chunk digests)
+        self._ref_cache = {}  # (ptr, numel, version, chunk, alg) -> (weight, its chunk digests)
         # partial: records are combinable nao_check_partial rows (a batch shard of
         # every node; shard.combine_shard_records decides the whole-tensor verdicts)
         self.partial = bool(partial)
@@ -395,7 +395,9 @@ class StreamingVerifier:
     def _ref_chunk_digests(self, w: torch.Tensor):
         """(payload ptr, chunk-digest ptr, bytes) of a static broadcast reference
         tensor (a weight), its chunk digests committed once and cached."""
-        key = (w.data_ptr(), w.numel(), self.chunk, self.alg)
+        # the version counter keys in-place updates (a stale digest would be
+        # copied for chunks that equal the tensor's new bytes)
+        key = (w.data_ptr(), w.numel(), w._version, self.chunk, self.alg)
         hit = self._ref_cache.get(key)
         if hit is None:
             if len(self._ref_cache) >= 64:  # weights are static: a handful of masks
