@@ -482,3 +482,27 @@ def test_stream_options_keep_roots_and_records(seg):
         r2, c2 = gr.replay()
         torch.cuda.synchronize()
         assert torch.equal(r2, r0) and torch.equal(c2, c0)
+
+
+def test_reference_digest_cache_follows_in_place_updates():
+    """The broadcast-reference digests (causal-mask shortcut) are recommitted
+    after an in-place update of the reference tensor."""
+    from paper_2510_16028_b200.bounds import FpModel
+    from paper_2510_16028_b200.commitments import commit_tensors
+    from paper_2510_16028_b200.executor import StreamingVerifier
+    from paper_2510_16028_b200.lowerings import DecoderShape, build_decoder
+    shape = DecoderShape("tiny-qwen", layers=1, hidden=128, heads=4, kv_heads=2, head_dim=32,
+                         inter=256, vocab=500, seq=64)
+    sv = StreamingVerifier(build_decoder(shape, seed=1).graph, FpModel(), hash_alg="keccak256",
+                           chunk_bytes=4096)
+    w = torch.randn(64, 256, device="cuda")
+    p1 = sv._ref_chunk_digests(w)
+    assert sv._ref_chunk_digests(w) == p1  # cached
+    w.add_(1.0)
+    p2 = sv._ref_chunk_digests(w)
+    assert p2[0] == p1[0] and p2[1] != p1[1]
+    ref = torch.empty((1 + w.numel() * 4 // 4096, 32), dtype=torch.uint8, device="cuda")
+    commit_tensors([w], 4096, "keccak256", leaf_digests=ref)
+    got = [v for v in sv._ref_cache.values() if v[1].data_ptr() + 32 == p2[1]][0][1]
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
