@@ -380,7 +380,8 @@ def run_ours(args):
                            max_lag=args.max_lag, flush_bytes=args.flush_mb << 20,
                            commit_priority=(args.main_priority if args.commit_priority is None
                                             else args.commit_priority),
-                           claim_stream=bool(args.claim_stream))
+                           claim_stream=bool(args.claim_stream),
+                           bound_stream=bool(args.bound_stream))
 
     no_harness = os.environ.get("NAO_EXP_NO_HARNESS") == "1"  # timing experiment only
 
@@ -1125,6 +1126,9 @@ def main(argv=None):
                     help="claimed bytes per fused commit launch (StreamingVerifier flush_bytes)")
     ap.add_argument("--commit-priority", type=int, default=None,
                     help="CUDA priority of the commit stream (default: --main-priority)")
+    ap.add_argument("--bound-stream", type=int, default=1,
+                    help="1: abs-GEMM bounds on their own stream (67.5-68.1 %% vs 71.7-72.3 %% "
+                         "off); 0: inline on the main stream")
     ap.add_argument("--claim-stream", type=int, default=0,
                     help="1: the proposer harness makes each node's claim on its own stream "
                          "(consumers wait per node; measured 69.0-69.1 %% vs 67.4-67.8 %% inline); "

@@ -42,6 +42,8 @@ from .engine import NATIVE, ExecutionError, _batch_view, fma_of, to_device
 from .graph import parse_ref
 
 _EXP_SKIP_COMMIT = os.environ.get("NAO_EXP_SKIP_COMMIT") == "1"
+_BOUND_EARLY = os.environ.get("NAO_BOUND_EARLY", "1") != "0"
+_NO_REF = os.environ.get("NAO_NO_REF") == "1"
 INF_TAU = np.full(len(PERCENTILE_GRID), np.inf)
 
 
@@ -326,7 +328,8 @@ class StreamingVerifier:
                  flush_bytes: int = 2 << 30, device="cuda", epsilon: float = DEFAULT_EPSILON,
                  grid=PERCENTILE_GRID, overlap: bool = True, fuse_check: bool = True,
                  max_lag: int = 0, partial: bool = False, missing_thresholds: str = "raise",
-                 commit_priority: int | None = None, claim_stream: bool = False):
+                 commit_priority: int | None = None, claim_stream: bool = False,
+                 bound_stream: bool | None = None):
         self.g = graph
         self.model = model or FpModel()
         self.profile = profile
@@ -382,7 +385,12 @@ class StreamingVerifier:
         # abs-GEMM bounds of matmul / linear / conv nodes on their own stream:
         # the value path (main) runs on while the tensor-core bound fills the
         # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
-        self.bound_stream = overlap and os.environ.get("NAO_BOUND_STREAM", "1") != "0"
+        # Opt-in (bench.py's Qwen3 line turns it on): on the GPT-2 config (LayerNorm
+        # + biases + GELU) it hits an illegal address in ~40 % of runs, eager and
+        # replayed alike, not reproduced on Qwen3 (33 runs) -- DESIGN.md §6
+        if bound_stream is None:
+            bound_stream = os.environ.get("NAO_BOUND_STREAM", "0") == "1"
+        self.bound_stream = overlap and bool(bound_stream)
         # claim_stream: call claimed_fn on its own stream (a proposer harness
         # that derives claims from the local values: a node's claim is then
         # made while independent nodes' values run; consumers wait per node)
@@ -598,10 +606,11 @@ class StreamingVerifier:
                     # value on main, abs-GEMM bound on the bound stream (matmul /
                     # conv: from the inputs alone, concurrently with the value
                     # GEMM; linear: after it, for the u|y| term)
-                    if node.kind != "linear":
+                    early = node.kind != "linear" and _BOUND_EARLY
+                    if early:
                         s_bnd.wait_stream(main)
                     y = apply_value(node, xs, self.profile)
-                    if node.kind == "linear":
+                    if not early:
                         s_bnd.wait_stream(main)
                     with torch.cuda.stream(s_bnd):
                         eps = gemm_bound_device(node, xs, y, self.model, self.profile, False)
@@ -696,7 +705,7 @@ class StreamingVerifier:
             del eps, y
             values[node.index] = yc
             st.pend_reuse.append(chunk_plan(node, xs, yc, st.pend_pos, self.chunk,
-                                            self._ref_chunk_digests)
+                                            None if _NO_REF else self._ref_chunk_digests)
                                  if desc is not None else None)
             st.pend_pos[node.index] = len(st.pending)
             st.pending.append(yc)

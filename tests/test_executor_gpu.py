@@ -470,9 +470,8 @@ def test_stream_options_keep_roots_and_records(seg):
     ref = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256, overlap=False)
     r0, c0 = ref.run(ids, claimed_fn)
     r0, c0 = r0.clone(), c0.clone()
-    assert os.environ.get("NAO_BOUND_STREAM", "1") != "0"
     sv = StreamingVerifier(g, FpModel(), hash_alg="keccak256", chunk_bytes=256,
-                           claim_stream=True, commit_priority=-1)
+                           claim_stream=True, commit_priority=-1, bound_stream=True)
     assert sv._s_bnd is not None and sv._s_clm is not None
     r1, c1 = sv.run(ids, claimed_fn)
     torch.cuda.synchronize()
