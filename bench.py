@@ -38,16 +38,12 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 # many distinct large tensor sizes per step (node outputs, bounds, splits):
 # expandable segments keep the caching allocator from fragmenting into
-# cudaMalloc retries (device syncs) on the UNet-sized graphs (--config runs).
-# The Qwen3 line runs the abs-GEMM bounds on their own stream, and that third
-# stream together with expandable segments faulted intermittently on the GPT-2
-# config (illegal address in 2 of 3 runs; 5 of 5 clean without expandable
-# segments): the Qwen3 line uses the default allocator (same speed, 128-147 GB
-# peak reserved).
-_CFG = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--config=")),
-            sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv[:-1] else "qwen3-8b")
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:False" if _CFG == "qwen3-8b"
-                      else "expandable_segments:True")
+# cudaMalloc retries (device syncs) on the UNet-sized graphs.  (The Qwen3 line
+# also runs the abs-GEMM bounds on their own stream: 34 of 34 runs clean at
+# 112-139 GB peak reserved; the default allocator is as fast there but peaks
+# at 159 GB.  The --config runs keep the bound stream off: with it, the GPT-2
+# config faulted intermittently under expandable segments only -- DESIGN.md §6.)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 METRIC = "bounds+check+commit overhead % vs FP32 fwd (Qwen3-8B shape); Merkle GB/s"
 UNIT = "%"
 PCT = (0.0, 1.0) + tuple(float(p) for p in range(5, 100, 5)) + (99.0, 100.0)
@@ -635,6 +631,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(n_nodes * (32 + _lib.CHECK_RESULT_BYTES) + 32)},
         "gpu_launches": n_launch,
         "mem_peak_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
+        "alloc_retries": int(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)),
         "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
     }
     print(json.dumps(line))
@@ -848,6 +845,8 @@ def run_config(args):
                     "d2h_bytes_per_step": int(host_roots.numel() + host_recs.numel())},
             "proposer_harness_ms": round(shares.get("nao_inject_drift", 0.0), 3),
             "gpu_launches": n_launch, "roofline": roof, "cpu_baseline": None,
+            "mem_peak_reserved_gb": round(torch.cuda.max_memory_reserved(dev) / 1e9, 1),
+            "alloc_retries": int(torch.cuda.memory_stats(dev).get("num_alloc_retries", 0)),
             "clocks": clocks.summary()}
     if args.config == "mlp" and world == 1 and not args.no_cpu:
         res = cpu_mlp_reference(5)
