@@ -42,8 +42,6 @@ from .engine import NATIVE, ExecutionError, _batch_view, fma_of, to_device
 from .graph import parse_ref
 
 _EXP_SKIP_COMMIT = os.environ.get("NAO_EXP_SKIP_COMMIT") == "1"
-_BOUND_EARLY = os.environ.get("NAO_BOUND_EARLY", "1") != "0"
-_NO_REF = os.environ.get("NAO_NO_REF") == "1"
 INF_TAU = np.full(len(PERCENTILE_GRID), np.inf)
 
 
@@ -606,7 +604,7 @@ class StreamingVerifier:
                     # value on main, abs-GEMM bound on the bound stream (matmul /
                     # conv: from the inputs alone, concurrently with the value
                     # GEMM; linear: after it, for the u|y| term)
-                    early = node.kind != "linear" and _BOUND_EARLY
+                    early = node.kind != "linear"
                     if early:
                         s_bnd.wait_stream(main)
                     y = apply_value(node, xs, self.profile)
@@ -705,7 +703,7 @@ class StreamingVerifier:
             del eps, y
             values[node.index] = yc
             st.pend_reuse.append(chunk_plan(node, xs, yc, st.pend_pos, self.chunk,
-                                            None if _NO_REF else self._ref_chunk_digests)
+                                            self._ref_chunk_digests)
                                  if desc is not None else None)
             st.pend_pos[node.index] = len(st.pending)
             st.pending.append(yc)
