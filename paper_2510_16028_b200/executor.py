@@ -356,6 +356,12 @@ class StreamingVerifier:
         self.max_lag = int(max_lag)
         self._com_events = []
         self._host_events = []  # commit-flush events the host has not waited for
+        # eager runs: tensors a side stream reads stay referenced here until an
+        # event recorded on that stream after the use has completed (a deferred
+        # free instead of Tensor.record_stream: with the expandable-segments
+        # allocator, record_stream'ed blocks of the eager warm-up faulted later
+        # runs of the GPT-2 config -- DESIGN.md §6)
+        self._deferred = []  # [(event, [tensors])]
         self.host_lag_bytes = int(float(os.environ.get("NAO_HOST_LAG_GB", "32")) * (1 << 30))
         self._ref_cache = {}  # (ptr, numel, version, chunk, alg) -> (weight, its chunk digests)
         # partial: records are combinable nao_check_partial rows (a batch shard of
@@ -519,9 +525,11 @@ class StreamingVerifier:
             ws_chk = _lib.check_accumulator(self.dev)
         chk_ptr = s_chk.cuda_stream
         start = st.start
-        # tensors read on a side stream: record_stream when eager; held until
+        # tensors read on a side stream: deferred-freed when eager; held until
         # the segment's join when capturing (a capture cannot record events)
         keep = []
+
+        uses = {}  # eager: side stream -> tensors it read since the last release point
 
         def side_use(t, s):
             if not self.overlap:
@@ -529,7 +537,18 @@ class StreamingVerifier:
             if capturing:
                 keep.append(t)
             else:
-                t.record_stream(s)
+                uses.setdefault(s, []).append(t)
+
+        def defer_uses():
+            """Eager: one event per side stream after its queued uses; drop the
+            references whose events have completed (in order)."""
+            for s, ts in uses.items():
+                ev = torch.cuda.Event()
+                ev.record(s)
+                self._deferred.append((ev, ts))
+            uses.clear()
+            while self._deferred and self._deferred[0][0].query():
+                self._deferred.pop(0)
 
         def flush():
             if not st.pending:
@@ -558,6 +577,7 @@ class StreamingVerifier:
                     st.roots.index_copy_(0, st.all_idx[torch.as_tensor(st.pend_idx)], r)
             for t in st.pending + st.pend_keep:
                 side_use(t, s_com)
+            defer_uses()
             if self.overlap and capturing:
                 keep.append(r)
             if self.overlap and self.max_lag > 0 and not capturing:
@@ -726,6 +746,7 @@ class StreamingVerifier:
             main.wait_stream(s_bnd)
         if s_clm is not None:
             main.wait_stream(s_clm)
+        defer_uses()
         keep.clear()
         release_activation_split()  # the memo must not pin a split past the segment
 
