@@ -272,6 +272,7 @@ class GraphedRun:
         self.pool = torch.cuda.graph_pool_handle()
         self.stream = torch.cuda.Stream(sv.dev)
         torch.cuda.synchronize(sv.dev)
+        sv._deferred.clear()  # every eager use has completed (no event queries in a capture)
         st = sv._begin(inputs, start, end, frontier)
         for lo, hi in _segments(start, st.end, seg_nodes):
             gph = torch.cuda.CUDAGraph()
@@ -389,11 +390,11 @@ class StreamingVerifier:
         # abs-GEMM bounds of matmul / linear / conv nodes on their own stream:
         # the value path (main) runs on while the tensor-core bound fills the
         # SMs the SIMT GEMMs' last waves leave idle; commits wait for it
-        # Opt-in (bench.py's Qwen3 line turns it on): on the GPT-2 config (LayerNorm
-        # + biases + GELU) it hits an illegal address in ~40 % of runs, eager and
-        # replayed alike, not reproduced on Qwen3 (33 runs) -- DESIGN.md §6
+        # (NAO_BOUND_STREAM=0 turns it off.  With Tensor.record_stream for the
+        # eager side-stream reads it faulted intermittently on the GPT-2 config
+        # under expandable segments; the deferred free below fixed that.)
         if bound_stream is None:
-            bound_stream = os.environ.get("NAO_BOUND_STREAM", "0") == "1"
+            bound_stream = os.environ.get("NAO_BOUND_STREAM", "1") != "0"
         self.bound_stream = overlap and bool(bound_stream)
         # claim_stream: call claimed_fn on its own stream (a proposer harness
         # that derives claims from the local values: a node's claim is then
@@ -547,7 +548,7 @@ class StreamingVerifier:
                 ev.record(s)
                 self._deferred.append((ev, ts))
             uses.clear()
-            while self._deferred and self._deferred[0][0].query():
+            while not capturing and self._deferred and self._deferred[0][0].query():
                 self._deferred.pop(0)
 
         def flush():
