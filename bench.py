@@ -38,11 +38,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 # many distinct large tensor sizes per step (node outputs, bounds, splits):
 # expandable segments keep the caching allocator from fragmenting into
-# cudaMalloc retries (device syncs) on the UNet-sized graphs.  (The Qwen3 line
-# also runs the abs-GEMM bounds on their own stream: 34 of 34 runs clean at
-# 112-139 GB peak reserved; the default allocator is as fast there but peaks
-# at 159 GB.  The --config runs keep the bound stream off: with it, the GPT-2
-# config faulted intermittently under expandable segments only -- DESIGN.md §6.)
+# cudaMalloc retries (device syncs) on the UNet-sized graphs.  (With the
+# abs-GEMM bound stream, Tensor.record_stream under expandable segments faulted
+# intermittently on the GPT-2 config; the verifier now defers its eager frees
+# with events instead -- DESIGN.md §6.)
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 METRIC = "bounds+check+commit overhead % vs FP32 fwd (Qwen3-8B shape); Merkle GB/s"
 UNIT = "%"
