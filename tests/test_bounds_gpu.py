@@ -21,6 +21,14 @@ RTOL = 1e-5
 INTRINSIC_TRANSCENDENTAL = {"exp", "log", "tanh", "gelu", "silu"}
 
 
+def _sub32(e_ref):
+    """Slack of an FP32 bound rounded up from the FP64 one: two FP32 spacings,
+    only where e_ref is below FP32's normal range (elsewhere rounding up costs
+    at most 2^-23 relative, inside rtol)."""
+    return np.where(e_ref < np.finfo(np.float32).tiny, 2 * np.spacing(e_ref.astype(np.float32)),
+                    0.0)
+
+
 def assert_bound(eps_gpu, eps_ref, what=""):
     eps_gpu = np.asarray(eps_gpu, dtype=np.float64).reshape(-1)
     eps_ref = np.asarray(eps_ref, dtype=np.float64).reshape(-1)
@@ -288,7 +296,8 @@ def test_softmax_many_long_rows(B, shape, f64):
         assert_bound(e, e_ref, "softmax C f64")
     else:
         assert np.all(e >= e_ref)
-        assert np.all(e <= e_ref * (1 + RTOL) + np.spacing(e_ref.astype(np.float32)) * 2)
+        # FP32 storage rounds up: beyond rtol only below FP32's normal range
+        assert np.all(e <= e_ref * (1 + RTOL) + _sub32(e_ref))
 
 
 @pytest.mark.parametrize("shape", [(4096, 2048), (2048, 4096), (300, 100), (8, 30000)])
@@ -368,7 +377,9 @@ def test_softmax_design_c_parity():
         "        ok = ~np.isnan(e_ref)\n"
         "        assert np.array_equal(np.isnan(e), ~ok)\n"
         "        assert np.all(e[ok] >= e_ref[ok])\n"
-        "        sp = 0 if f64 else 2 * np.spacing(e_ref[ok].astype(np.float32))\n"
+        "        er = e_ref[ok]\n"
+        "        sp = 0 if f64 else np.where(er < np.finfo(np.float32).tiny,\n"
+        "                                    2 * np.spacing(er.astype(np.float32)), 0.0)\n"
         "        assert np.all(e[ok] <= e_ref[ok] * (1 + 1e-5) + sp)\n"
         "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -438,7 +449,7 @@ def test_softmax_full_qwen_scores(B):
     got_y, got_e = flat_y[rows].cpu().numpy(), flat_e[rows].cpu().numpy().astype(np.float64)
     assert np.array_equal(got_y.view(np.uint32), y_ref.view(np.uint32))
     assert np.all(got_e >= e_ref)
-    assert np.all(got_e <= e_ref * (1 + RTOL) + 2 * np.spacing(e_ref.astype(np.float32)))
+    assert np.all(got_e <= e_ref * (1 + RTOL) + _sub32(e_ref))
     perm = torch.from_numpy(rng.permutation(H * S)).cuda()
     yp, ep = B.softmax_device(flat_x[perm].contiguous(), -1, B.FpModel(), eps_f64=False)
     assert torch.equal(yp, flat_y[perm]) and torch.equal(ep, flat_e[perm])
