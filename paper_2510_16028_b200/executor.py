@@ -422,6 +422,14 @@ class StreamingVerifier:
         w, dig = hit
         return (w.data_ptr(), dig.data_ptr() + 32, w.numel() * 4)
 
+    def release(self) -> None:
+        """Wait for the side streams and drop every tensor an eager run kept
+        alive for them (the deferred frees of the last flushes)."""
+        for s in (self._s_chk, self._s_com, self._s_bnd, self._s_clm):
+            if s is not None:
+                s.synchronize()
+        self._deferred.clear()
+
     def _sync_thresholds(self):
         """Drop the cached taus / device specs when `thresholds` was replaced."""
         if getattr(self, "_spec_for", None) is not self.thresholds:
@@ -512,6 +520,9 @@ class StreamingVerifier:
         s_chk = self._s_chk or main
         s_com = self._s_com or main
         capturing = torch.cuda.is_current_stream_capturing()
+        if not capturing:  # references whose side-stream reads have completed
+            while self._deferred and self._deferred[0][0].query():
+                self._deferred.pop(0)
         s_bnd = self._s_bnd if (self.overlap and self._s_bnd is not None) else None
         s_clm = self._s_clm if (self.overlap and self._s_clm is not None) else None
         clm_ev = {}  # node index -> event after its claim (claim stream)

@@ -476,6 +476,8 @@ def test_stream_options_keep_roots_and_records(seg):
     r1, c1 = sv.run(ids, claimed_fn)
     torch.cuda.synchronize()
     assert torch.equal(r1, r0) and torch.equal(c1, c0)
+    sv.release()  # the eager run's deferred frees
+    assert sv._deferred == []
     gr = sv.capture(ids, claimed_fn, seg_nodes=seg)
     for _ in range(2):
         r2, c2 = gr.replay()
